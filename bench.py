@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark of the gSoFa symbolic-factorization hot path on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step = one full symbolic factorization (seed -> traversal -> extraction ->
+supernodes, plus for N > 1 the NCCL count allgather) of the synthetic
+BASELINE config (default C2 = configs[1], 3D 7-point 64^3, ND order).
+value = fill-ins found per second over the whole job (max over ranks of the
+device time); e2e = the same through the public API with host (pinned)
+buffers, uploads and result downloads inside the timed region.
+
+Rank 0 prints ONE JSON line on stdout; diagnostics go to stderr.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import gen  # noqa: E402
+
+METRIC = "symbolic-factorization fill-ins/s"
+UNIT = "fill-ins/s"
+CONFIG_DESC = {
+    "C1": "C1: 2D 5-point 32x32, natural order, p=0.25 dropout (n=1,024)",
+    "C2": "C2: 3D 7-point 64^3, nested-dissection order, p=0.25 dropout (n=262,144)",
+    "C3": "C3: BBMAT-shaped banded+scatter (n=38,744, nnz=1.77M), natural order",
+    "C4": "C4: G3_circuit-shaped ND mesh + hubs (n=1,585,478, nnz=7.66M)",
+    "C5": "C5: 3D 7-point 128^3, nested-dissection order, p=0.25 dropout (n=2,097,152)",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def fills_of_rows(rp, ci, r):
+    """Per-sample fill-in count from oracle rows (for the CPU baselines)."""
+    rows = r["rows"]
+    deg = rp[rows + 1] - rp[rows]
+    # off-diagonal A entries in those rows
+    offd = 0
+    for s in rows:
+        seg = ci[rp[s]:rp[s + 1]]
+        offd += int(np.count_nonzero(seg != s))
+    return int(r["L_rowptr"][-1] + r["U_rowptr"][-1] - rows.size - offd), int(deg.sum())
+
+
+def cpu_oracle_sample(rp, ci, target_s: float, seed: int = 0):
+    """Run the (untuned) oracle on every k-th row, k chosen so the run takes
+    about target_s seconds on this host.  Returns (fills/s, desc, threads)."""
+    import oracle
+    n = rp.size - 1
+    threads = oracle.default_threads()
+    k = max(1, n // 64)
+    probe_rows = np.arange(k // 2, n, k, dtype=np.int64)
+    t = time.perf_counter()
+    oracle.rows(rp, ci, probe_rows, threads)
+    dt = max(time.perf_counter() - t, 1e-3)
+    per_row = dt / probe_rows.size
+    want = int(min(n, max(probe_rows.size, target_s / per_row)))
+    stride = max(1, n // want)
+    rows = np.arange(stride // 2, n, stride, dtype=np.int64)
+    t = time.perf_counter()
+    r = oracle.rows(rp, ci, rows, threads)
+    dt = time.perf_counter() - t
+    r["rows"] = rows
+    fills, _ = fills_of_rows(rp, ci, r)
+    desc = (f"every {stride}-th row ({rows.size} of {n} rows, uniform over the row range), "
+            f"{fills} fill-ins in {dt:.2f} s")
+    return fills / dt, desc, threads, dt
+
+
+def algorithmic_bytes(stats, schedule):
+    """Algorithmic bytes of the traversal kernel:
+    threshold: 12 B per (item, neighbour) pair (4 B colidx + 8 B RMW of the
+    32-source state word of the neighbour) + 24 B per item (8 B pend exchange,
+    8 B rowptr, 8 B list write+read);  FIFO: additionally 8 B per
+    (source, edge) label RMW."""
+    b = 12 * stats["item_edges"] + 24 * stats["frontier_items"]
+    if schedule == "fifo":
+        b += 8 * stats["edge_inspections"]
+    return b
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle as it stands, on host cores (rank 0 only)."""
+    if rank != 0:
+        return 0
+    rp, ci = gen.config(args.config)
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    desc = threads = None
+    for i in range(args.warmup + args.steps):
+        v, desc, threads, dt = cpu_oracle_sample(rp, ci, per_step, seed=i)
+        if i >= args.warmup:
+            vals.append((v, dt))
+    value = statistics.median(v for v, _ in vals)
+    ms = statistics.median(dt for _, dt in vals) * 1e3
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "int32", "data": "synthetic (gen.config, seeded)",
+           "config": {"workload": CONFIG_DESC[args.config], "n": int(rp.size - 1),
+                      "nnz_offdiag": int(ci.size)},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                            "sample": desc},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIG_DESC))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--schedule", default="threshold", choices=["threshold", "fifo"])
+    ap.add_argument("--max-concurrent", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2007_00840_b200 as g
+    from paper_2007_00840_b200 import dist as gd
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    t0 = time.perf_counter()
+    rp, ci = gen.config(args.config)
+    n = rp.size - 1
+    log(f"[rank {rank}] {args.config}: n={n} nnz={ci.size} generated in {time.perf_counter()-t0:.1f}s")
+    chunk = 128
+    bounds = gd.partition(rp, ci, world, chunk) if world > 1 else np.array([0, n], np.int64)
+    rb, re = int(bounds[rank]), int(bounds[rank + 1])
+    d_rp = torch.from_numpy(rp).to(dev)
+    d_ci = torch.from_numpy(ci).to(dev)
+    ctx = g.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def one_step(host=False):
+        kw = dict(ctx=ctx, chunk_size=chunk, schedule=args.schedule,
+                  max_concurrent=args.max_concurrent, stream=stream)
+        src = (h_rp, h_ci) if host else (d_rp, d_ci)
+        res = None
+        if re > rb:
+            res = g.symbolic(*src, row_begin=rb, row_end=re, outputs_on_device=not host, **kw)
+            if host:
+                res.to_numpy()  # results already in host memory; materialise the arrays
+        if world > 1:
+            local_counts = np.zeros(len(gd.COUNT_FIELDS), np.int64)
+            if res is not None:
+                local_counts[:] = [res.nnz_L, res.nnz_U, res.fill_count, res.nsuper,
+                                   res.nnz_A_offdiag, re - rb]
+            counts = gd.allgather_counts(local_counts, device=dev)
+            fills = int(counts[:, 2].sum())
+        else:
+            fills = res.fill_count
+        return res, fills
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        r, fills = one_step()
+        if r is not None:
+            r.free()
+    # ---- timed region (device time, CUDA events on the launch stream)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    step_ms, stats_acc, launches = [], {}, 0
+    fills_step = 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (256 MiB > 126 MB L2), untimed
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r, fills_step = one_step()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            if r is not None:
+                for k, v in r.stats.items():
+                    stats_acc[k] = stats_acc.get(k, 0) + v
+                launches += int(r.stats["kernel_launches"])
+                r.free()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms, float(launches)], dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        tot_ms, launches_all = float(tmax[0]), int(t[1])
+    else:
+        launches_all = launches
+    ms_per_step = tot_ms / args.steps
+    value = fills_step / (ms_per_step / 1e3)
+
+    # ---- e2e through the public API with pinned host buffers
+    h_rp = torch.from_numpy(rp).pin_memory()
+    h_ci = torch.from_numpy(ci).pin_memory()
+    e2e_ms, h2d, d2h = [], 0, 0
+    for i in range(1 + args.e2e_steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        r, fills_e = one_step(host=True)
+        torch.cuda.synchronize(dev)
+        dt = (time.perf_counter() - t) * 1e3
+        if i > 0:
+            e2e_ms.append(dt)
+        if r is not None:
+            h2d = int(rp.nbytes + ci.nbytes)
+            d2h = int(2 * (r.rows + 1) * 8 + 4 * (r.nnz_L + r.nnz_U + r.nsuper + 1))
+            r.free()
+    e2e_step = statistics.median(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_step, float(h2d), float(d2h)], dtype=torch.float64, device=dev)
+        m = t.clone()
+        dist.all_reduce(m[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        e2e_step, h2d, d2h = float(m[0]), int(t[1]), int(t[2])
+
+    # ---- roofline of the dominant kernel (traversal), measured live
+    peak, peak_src = load_peaks()
+    trav_ms = stats_acc.get("ms_traverse", 0.0)
+    alg = algorithmic_bytes(stats_acc, args.schedule) if stats_acc else 0
+    achieved = alg / (trav_ms / 1e3) / 1e9 if trav_ms > 0 else 0.0
+    roofline = {"kernel": "threshold_kernel" if args.schedule == "threshold" else "traverse_kernel",
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_step": alg / args.steps,
+                "kernel_ms_per_step": trav_ms / args.steps,
+                "kernel_share_of_step": (trav_ms / args.steps) / ms_per_step if ms_per_step else None}
+    stats_step = {k: (v / args.steps) for k, v in stats_acc.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, desc, threads, dt = cpu_oracle_sample(rp, ci, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "int32", "data": "synthetic (gen.config, seeded; no datasets)",
+               "config": {"workload": CONFIG_DESC[args.config], "n": n, "nnz_offdiag": int(ci.size),
+                          "fill_ins": fills_step, "schedule": args.schedule,
+                          "parallelism": f"rows split over {world} GPU(s)" if world > 1 else "1 GPU",
+                          "l2": "flushed between timed steps (256 MiB write, untimed)"},
+               "e2e": {"value": fills_step / (e2e_step / 1e3), "unit": UNIT,
+                       "ms_per_step": e2e_step, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+               "gpu_launches": launches_all,
+               "roofline": roofline,
+               "cpu_baseline": cpu,
+               "clocks": clk.summary(),
+               "stats_per_step": stats_step}
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

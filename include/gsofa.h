@@ -1,0 +1,202 @@
+/*
+ * gsofa.h -- C ABI of the B200-native gSoFa symbolic-factorization hot path.
+ *
+ * Problem (PAPER.md = P): "symbolic factorization is used to compute the
+ * locations of the fill-ins for both L and U ... needed to allocate the
+ * compressed sparse data structures for L and U".  For a square
+ * sparsity pattern A with implicitly nonzero diagonal, entry (i,j)
+ * of L+U is nonzero iff A(i,j) != 0 or there is a directed path i -> j in
+ * G(A) whose intermediate vertices are all smaller than min(i,j) (fill-path
+ * theorem, Theorem thm:fill).  The library finds, for every source
+ * row, the L and U patterns with the paper's frontier-driven max-id
+ * relaxation (sec:parallel) run for batches of concurrent sources
+ * on the GPU, then detects T3 supernodes (Definition def:T3) with
+ * the two-phase design.
+ *
+ * Everything here is plain C: pointers and sizes, no C++ or PyTorch types.
+ * All entry points return an int status (0 = GSOFA_OK, negative = error);
+ * on error no output object is produced (*out == NULL) and
+ * gsofa_last_error_detail() describes the cause (thread-local).
+ * There is no CPU fallback: every step of the factorization runs in the
+ * library's sm_100a CUDA kernels; without a usable GPU calls fail with
+ * GSOFA_ECUDA.
+ */
+#ifndef GSOFA_H
+#define GSOFA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSOFA_VERSION 1
+
+/* ---------------------------------------------------------- error codes -- */
+#define GSOFA_OK            0
+#define GSOFA_EINVAL       -1  /* bad argument: n <= 0, NULL pointer, bad opts,
+                                  row_begin >= row_end, row_begin not a multiple
+                                  of chunk_size, max_concurrent not a multiple
+                                  of 32 */
+#define GSOFA_EBADCSR      -2  /* rowptr[0] != 0, rowptr decreasing, column out
+                                  of [0,n), columns not strictly increasing in a
+                                  row, nnz >= 2^31 */
+#define GSOFA_ENOMEM       -3  /* device (or host output) allocation failed */
+#define GSOFA_EINFEASIBLE  -4  /* memory budget below one 32-source group's
+                                  footprint (the paper's "reduce the number of
+                                  concurrent sources" cannot go lower) */
+#define GSOFA_ECUDA        -5  /* any CUDA runtime error (no GPU, launch failure) */
+#define GSOFA_EINTERNAL    -6  /* checked-mode invariant violated */
+
+#define GSOFA_SCHEDULE_THRESHOLD 0
+#define GSOFA_SCHEDULE_FIFO      1
+
+/* -------------------------------------------------------------- options -- */
+typedef struct gsofa_opts {
+  /* chunkSize = user-defined maximum supernode size; a supernode never crosses
+   * a multiple of chunk_size ("chunkSize is identical to the size of the user
+   * defined maximum supernode"; default 128).  >= 1. */
+  int32_t chunk_size;
+  /* #C, the number of concurrent sources per batch.  Multiple of
+   * 32 (one 32-source slot group per warp lane set).  0 = automatic (the
+   * largest batch the memory budget allows, capped at 65536 for the threshold
+   * schedule and 16384 for FIFO). */
+  int32_t max_concurrent;
+  /* memory budget in bytes for the traversal arena.  0 = automatic
+   * (about half of the free device memory). */
+  int64_t mem_budget_bytes;
+  /* 1 = "line 9.5" access order: test the structure before the atomicMin on
+   * maxId.  Result-invariant; default 0 as in the paper. */
+  int32_t fill_first;
+  /* Processing order of the max-id relaxation (result-invariant; DESIGN.md
+   * "Schedules"):
+   *   GSOFA_SCHEDULE_THRESHOLD (0, default): frontier items in increasing
+   *     newMaxId, one CTA per 32-source group ("Dijkstra order"); no
+   *     revisits, no grid-wide barriers.
+   *   GSOFA_SCHEDULE_FIFO (1): the paper's order -- all frontiers of an
+   *     iteration in parallel with revisits, one
+   *     persistent grid-wide kernel per batch with epoch-encoded maxId
+   *     labels. */
+  int32_t schedule;
+  /* source rows [row_begin, row_end); row_end = -1 means n.  row_begin must be
+   * a multiple of chunk_size (so that supernodes, which never cross chunk
+   * boundaries, are identical to those of a whole-matrix run). */
+  int64_t row_begin, row_end;
+  /* CUDA device ordinal used when the call creates its own context. */
+  int32_t device;
+  /* 1: result arrays are device pointers (cudaMalloc'd); 0: host (malloc). */
+  int32_t outputs_on_device;
+  /* cudaStream_t to run on (NULL = the context's own stream). */
+  void *stream;
+} gsofa_opts;
+
+/* ------------------------------------------------------------ statistics -- */
+typedef struct gsofa_stats {
+  int64_t edge_inspections;  /* (source, edge) relaxations performed, incl.
+                                revisits (TEPS numerator) */
+  int64_t frontier_items;    /* (vertex, 32-source group) work items expanded */
+  int64_t item_edges;        /* (item, neighbour) pairs: adjacency entries read,
+                                each touching one 32-source state word */
+  int64_t rounds;            /* frontier levels (iterations) summed over
+                                batches / groups */
+  int64_t thresholds;        /* threshold steps (GSOFA_SCHEDULE_THRESHOLD) */
+  int64_t batches;           /* source batches */
+  int64_t max_batch;         /* largest #C used */
+  int64_t kernel_launches;   /* CUDA kernels launched by this call */
+  double ms_total;           /* device time of the whole call (CUDA events) */
+  double ms_traverse;        /* seed + traversal kernels */
+  double ms_extract;         /* row extraction (count + scan + write) */
+  double ms_supernode;       /* supernode detection */
+  double ms_transfer;        /* host<->device copies inside the call */
+} gsofa_stats;
+
+/* --------------------------------------------------------------- result -- */
+typedef struct gsofa_result {
+  int64_t n, row_begin, row_end;
+  /* CSR over rows [row_begin, row_end) (row i at index i - row_begin);
+   * L strictly lower (unit diagonal implicit), ascending columns */
+  int64_t *L_rowptr;   /* [row_end - row_begin + 1], L_rowptr[0] = 0 */
+  int32_t *L_colidx;   /* [nnz_L] */
+  /* U upper triangle INCLUDING the diagonal (nnz(U(0,:)) = 3 in the worked
+   * example counts the pivot), ascending columns; U(i,:)[0] == i */
+  int64_t *U_rowptr;   /* [row_end - row_begin + 1] */
+  int32_t *U_colidx;   /* [nnz_U] */
+  /* T3 supernodes: leading rows ascending, then the sentinel row_end */
+  int64_t nsuper;
+  int32_t *sn_start;   /* [nsuper + 1] */
+  int64_t nnz_L, nnz_U;
+  int64_t nnz_A_offdiag;  /* off-diagonal nonzeros of A in the rows */
+  int64_t fill_count;     /* nnz_L + (nnz_U - rows) - nnz_A_offdiag */
+  int32_t on_device;      /* 1 if the arrays above are device pointers */
+  int32_t device;
+  gsofa_stats stats;
+} gsofa_result;
+
+typedef struct gsofa_context gsofa_context;
+
+/* Fill *o with the defaults above.  Returns GSOFA_EINVAL if o is NULL. */
+int gsofa_default_opts(gsofa_opts *o);
+
+/* A context owns the device arena (maxId labels, frontier queues and masks,
+ * structure bitmaps: Table tab:complexity, allocated as "a big
+ * chunk of memory"), its stream and the maxId epoch counter
+ * (P:570-574), so that repeated calls neither reallocate nor re-initialise.
+ * mem_budget_bytes = 0: automatic.  Not thread-safe: one context per thread. */
+int gsofa_context_create(int32_t device, int64_t mem_budget_bytes, gsofa_context **ctx);
+void gsofa_context_destroy(gsofa_context *ctx);
+
+/*
+ * gsofa_symbolic -- symbolic LU factorization of the n x n pattern
+ * (rowptr, colidx) for source rows [opts->row_begin, opts->row_end).
+ *
+ *   ctx     context (NULL: a temporary one on opts->device)
+ *   n       order of A (|V| of G(A)), 1 <= n < 2^31
+ *   rowptr  int64[n+1] CSR row pointers, rowptr[0] = 0, nondecreasing
+ *   colidx  int32[rowptr[n]] column indices, strictly increasing per row;
+ *           diagonal entries are accepted and ignored (the diagonal is
+ *           implicit)
+ *   Inputs may be host or device pointers (detected with
+ *   cudaPointerGetAttributes); they are borrowed read-only.
+ *   opts    NULL = defaults
+ *   out     receives a library-allocated result; release with
+ *           gsofa_result_free().  The input must already be ordered
+ *           (fill-reducing ordering is out of scope).
+ */
+int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr,
+                   const int32_t *colidx, const gsofa_opts *opts,
+                   gsofa_result **out);
+
+/* Copies the result arrays into caller-owned buffers (host or device; any
+ * NULL destination is skipped).  Sizes: L_rowptr/U_rowptr rows+1, L_colidx
+ * nnz_L, U_colidx nnz_U, sn_start nsuper+1.  Synchronous.  Lets a binding
+ * move results into its own allocations (e.g. framework tensors). */
+int gsofa_result_copy(const gsofa_result *r, int64_t *L_rowptr, int32_t *L_colidx,
+                      int64_t *U_rowptr, int32_t *U_colidx, int32_t *sn_start);
+
+/* Frees every array of r (host or device) and r itself.  NULL is a no-op. */
+void gsofa_result_free(gsofa_result *r);
+
+/*
+ * gsofa_partition_rows -- split the source rows [0,n) into nparts contiguous
+ * ranges of roughly equal estimated work, for running one range per GPU.
+ * Work grows with the source id; the estimate for row s is the
+ * degree sum over the subtree of s in the elimination tree of the symmetrised
+ * pattern A + A^T (an upper bound of the vertices reachable from s through
+ * smaller vertices; elimination tree).  Range starts are multiples of
+ * `align` (use chunk_size so supernodes never cross ranges).
+ *   bounds: out int64[nparts+1], bounds[0] = 0, bounds[nparts] = n.
+ * Host-only computation (no GPU needed); deterministic, so every rank
+ * computes the same partition.
+ */
+int gsofa_partition_rows(int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                         int32_t nparts, int32_t align, int64_t *bounds);
+
+/* Static strings for an error code; thread-local detail of the last error. */
+const char *gsofa_strerror(int code);
+const char *gsofa_last_error_detail(void);
+int gsofa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSOFA_H */

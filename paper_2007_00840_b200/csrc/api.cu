@@ -1,0 +1,893 @@
+// api.cu -- the C ABI of include/gsofa.h: context/arena management, input
+// upload + validation, batch planning under a memory budget, the per-batch
+// pipeline (seed -> persistent traversal -> extraction), supernode detection
+// and output assembly.  Host code only orchestrates: every step that touches
+// the matrix or the result runs in the kernels of traverse.cu, extract.cu and
+// supernode.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/gsofa.h"
+#include "gsofa_internal.cuh"
+
+namespace gsofa {
+int extract_sub_columns();
+}
+
+namespace {
+
+thread_local char g_detail[512] = "";
+
+void set_detail(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_detail, sizeof g_detail, fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  set_detail("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+  if (e == cudaErrorMemoryAllocation) return GSOFA_ENOMEM;
+  return GSOFA_ECUDA;
+}
+
+#define CK(call)                                        \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) {                            \
+      rc = cuda_fail(e_, #call);                        \
+      goto fail;                                        \
+    }                                                   \
+  } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct gsofa_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t budget = 0;        // requested budget (0 = auto)
+  // arena (one cudaMalloc, carved in fixed regions)
+  char *arena = nullptr;
+  size_t arena_bytes = 0;
+  // arena layout key
+  int64_t key_n = -1;
+  int64_t Cmax = 0, Gmax = 0;
+  int gbits = 0;
+  size_t work_bytes = 0;
+  int work_state = 0;        // WorkState
+  uint32_t *work = nullptr, *is = nullptr;
+  uint32_t *cntL = nullptr, *cntU = nullptr;
+  int64_t *rowL = nullptr, *rowU = nullptr, *totals = nullptr;
+  uint32_t *qcount = nullptr;
+  unsigned long long *stats = nullptr;
+  int *err = nullptr;
+  int64_t nsub = 0;
+  uint32_t floor = 0xFFFFFFFFu;  // lowest maxId value ever written (epoch floor)
+  int max_blocks[2] = {0, 0};
+  // input staging (grow-only)
+  int64_t *in_rowptr = nullptr;
+  int32_t *in_colidx = nullptr, *rowptr32 = nullptr;
+  size_t in_rowptr_cap = 0, in_colidx_cap = 0, rowptr32_cap = 0;
+  int64_t *h_small = nullptr;  // pinned host scratch
+};
+
+namespace {
+
+void release_arena(gsofa_context *c) {
+  if (c->arena) cudaFree(c->arena);
+  c->arena = nullptr;
+  c->arena_bytes = 0;
+  c->key_n = -1;
+}
+
+struct Plan {
+  int64_t Cmax, Gmax;
+  int gbits;
+  size_t work_bytes, is_words, cnt_words;
+  int64_t nsub;
+  size_t total;
+};
+
+size_t small_bytes(int64_t Cmax) {
+  return (size_t)Cmax * 2 * sizeof(int64_t) + 64 + 64 + 64 + 256;
+}
+
+// Traversal working set of a batch of C sources whose labels cover Vb
+// vertices (Table tab:complexity, after bubble removal):
+//   FIFO:      maxId labels C*Vb*4 B + 2 frontier masks + 2 queues (G*Vb words each)
+//   threshold: per 32-source group reached/pend/list0/list1 (Vb words each)
+//              + a threshold bitmap (Vb/32 words)
+size_t work_need(int schedule, int64_t C, int64_t Vb) {
+  const int64_t G = C / 32;
+  if (schedule == GSOFA_SCHEDULE_FIFO) return (size_t)C * Vb * 4 + (size_t)G * Vb * 16;
+  return (size_t)G * gsofa::threshold_ws_words(Vb) * 4;
+}
+
+// FIFO keeps its label region apart from masks/queues so that every label
+// cell only ever holds epoch-encoded values (P:573 requires stale values to
+// decode as "uninitialised").
+size_t fifo_label_bytes(size_t work) { return (size_t)((double)work * 4.0 / 4.5) / 512 * 512; }
+
+bool make_plan(int schedule, int64_t n, int64_t rows, int64_t vb_max, int64_t cmax_req,
+               int64_t budget, Plan &p) {
+  const int64_t sub = gsofa::extract_sub_columns();
+  int64_t Cmax = std::min<int64_t>(cmax_req, round_up(rows, 32));
+  Cmax = std::max<int64_t>(32, round_up(Cmax, 32));
+  for (; Cmax >= 32; Cmax = (Cmax / 2 / 32) * 32) {
+    const int64_t G = Cmax / 32;
+    int gb = 0;
+    while ((int64_t(1) << gb) < G) ++gb;
+    if (schedule == GSOFA_SCHEDULE_FIFO && ((uint64_t)n << gb) > 0xFFFFFFFFull) continue;
+    const int64_t nsub = ceil_div(n, sub);
+    const size_t is_words = (size_t)G * n;
+    const size_t cnt_words = (size_t)G * nsub * 32;
+    const size_t fixed = is_words * 4 + 2 * cnt_words * 4 + small_bytes(Cmax) + 8192;
+    const size_t need_max = work_need(schedule, Cmax, vb_max) + 4096;
+    const size_t need_min = work_need(schedule, 32, vb_max) + 4096;
+    if ((int64_t)(fixed + need_min) > budget) continue;
+    size_t work = std::min<size_t>(need_max, (size_t)budget - fixed);
+    work = (work + 4095) / 4096 * 4096;
+    p.Cmax = Cmax;
+    p.Gmax = G;
+    p.gbits = gb;
+    p.work_bytes = work;
+    p.is_words = is_words;
+    p.cnt_words = cnt_words;
+    p.nsub = nsub;
+    p.total = work + is_words * 4 + 2 * cnt_words * 4 + small_bytes(Cmax) + 4096 + 12 * 256;
+    return true;
+  }
+  return false;
+}
+
+// largest multiple of 32 <= cap whose working set fits `work` bytes
+int64_t fit_batch(int schedule, int64_t n, int64_t s0, int64_t cap, size_t work) {
+  int64_t lo = 0, hi = cap / 32;  // in groups
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    const int64_t C = mid * 32;
+    const int64_t vb = std::min<int64_t>(n, s0 + C);
+    size_t need = work_need(schedule, C, vb);
+    if (schedule == GSOFA_SCHEDULE_FIFO) {
+      const size_t lab = fifo_label_bytes(work);
+      if ((size_t)C * vb * 4 > lab || (size_t)(C / 32) * vb > (work - lab) / 16) need = work + 1;
+    }
+    if (need <= work) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo * 32;
+}
+
+enum WorkState { kWorkZero = 0, kWorkFifo = 1, kWorkDirty = 2 };
+
+int ensure_arena(gsofa_context *c, int64_t n, const Plan &p, cudaStream_t st) {
+  int rc = GSOFA_OK;
+  if (c->arena && c->key_n == n && c->Cmax == p.Cmax && c->work_bytes == p.work_bytes) return rc;
+  release_arena(c);
+  {
+    cudaError_t e = cudaMalloc((void **)&c->arena, p.total);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      c->arena = nullptr;
+      set_detail("arena cudaMalloc(%zu bytes) failed: %s", p.total, cudaGetErrorString(e));
+      return GSOFA_ENOMEM;
+    }
+  }
+  c->arena_bytes = p.total;
+  {
+    char *q = c->arena;
+    auto carve = [&](size_t bytes) {
+      char *r = q;
+      q += (bytes + 255) / 256 * 256;
+      return r;
+    };
+    c->work = (uint32_t *)carve(p.work_bytes);
+    c->is = (uint32_t *)carve(p.is_words * 4);
+    c->cntL = (uint32_t *)carve(p.cnt_words * 4);
+    c->cntU = (uint32_t *)carve(p.cnt_words * 4);
+    c->rowL = (int64_t *)carve(p.Cmax * 8);
+    c->rowU = (int64_t *)carve(p.Cmax * 8);
+    c->totals = (int64_t *)carve(64);
+    c->qcount = (uint32_t *)carve(64);
+    c->stats = (unsigned long long *)carve(64);
+    c->err = (int *)carve(64);
+  }
+  c->key_n = n;
+  c->Cmax = p.Cmax;
+  c->Gmax = p.Gmax;
+  c->gbits = p.gbits;
+  c->work_bytes = p.work_bytes;
+  c->nsub = p.nsub;
+  CK(cudaMemsetAsync(c->work, 0, p.work_bytes, st));
+  CK(cudaMemsetAsync(c->is, 0, p.is_words * 4, st));
+  c->work_state = kWorkZero;
+  c->floor = 0xFFFFFFFFu;
+  return rc;
+fail:
+  release_arena(c);
+  return rc;
+}
+
+// Bring the work region into the state a schedule expects.
+int prepare_work(gsofa_context *c, int schedule, cudaStream_t st) {
+  int rc = GSOFA_OK;
+  if (schedule == GSOFA_SCHEDULE_FIFO) {
+    if (c->work_state != kWorkFifo) {
+      const size_t lab = fifo_label_bytes(c->work_bytes);
+      CK(cudaMemsetAsync(c->work, 0xFF, lab, st));                    // labels: above every epoch
+      CK(cudaMemsetAsync((char *)c->work + lab, 0, c->work_bytes - lab, st));  // masks, queues
+      c->floor = 0xFFFFFFFFu;
+      c->work_state = kWorkFifo;
+    }
+  } else if (c->work_state != kWorkZero) {
+    CK(cudaMemsetAsync(c->work, 0, c->work_bytes, st));
+    c->work_state = kWorkZero;
+  }
+  return rc;
+fail:
+  c->work_state = kWorkDirty;
+  return rc;
+}
+
+template <typename T>
+int grow_device(T **buf, size_t *cap, size_t need, cudaStream_t st) {
+  if (*cap >= need) return GSOFA_OK;
+  size_t nc = std::max(need, *cap * 2);
+  T *nb = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&nb, nc * sizeof(T), st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_detail("output cudaMallocAsync(%zu bytes) failed: %s", nc * sizeof(T), cudaGetErrorString(e));
+    return GSOFA_ENOMEM;
+  }
+  if (*buf) {
+    if (*cap) cudaMemcpyAsync(nb, *buf, *cap * sizeof(T), cudaMemcpyDeviceToDevice, st);
+    cudaFreeAsync(*buf, st);
+  }
+  *buf = nb;
+  *cap = nc;
+  return GSOFA_OK;
+}
+
+int64_t auto_budget(int device) {
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  (void)device;
+  return (int64_t)(fr * 0.5);
+}
+
+}  // namespace
+
+extern "C" {
+
+int gsofa_version(void) { return GSOFA_VERSION; }
+
+const char *gsofa_strerror(int code) {
+  switch (code) {
+    case GSOFA_OK: return "ok";
+    case GSOFA_EINVAL: return "invalid argument";
+    case GSOFA_EBADCSR: return "malformed CSR input";
+    case GSOFA_ENOMEM: return "out of memory";
+    case GSOFA_EINFEASIBLE: return "memory budget below one 32-source group";
+    case GSOFA_ECUDA: return "CUDA error";
+    case GSOFA_EINTERNAL: return "internal invariant violated";
+    default: return "unknown error";
+  }
+}
+
+const char *gsofa_last_error_detail(void) { return g_detail; }
+
+int gsofa_default_opts(gsofa_opts *o) {
+  if (!o) return GSOFA_EINVAL;
+  std::memset(o, 0, sizeof *o);
+  o->chunk_size = 128;
+  o->max_concurrent = 0;
+  o->mem_budget_bytes = 0;
+  o->fill_first = 0;
+  o->row_begin = 0;
+  o->row_end = -1;
+  o->device = 0;
+  o->outputs_on_device = 1;
+  o->stream = nullptr;
+  return GSOFA_OK;
+}
+
+int gsofa_context_create(int32_t device, int64_t mem_budget_bytes, gsofa_context **out) {
+  if (!out) return GSOFA_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    set_detail("no CUDA device available (%s)", cudaGetErrorString(e));
+    return GSOFA_ECUDA;
+  }
+  if (device < 0 || device >= ndev || mem_budget_bytes < 0) {
+    set_detail("bad device %d or budget", device);
+    return GSOFA_EINVAL;
+  }
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  gsofa_context *c = new (std::nothrow) gsofa_context();
+  if (!c) return GSOFA_ENOMEM;
+  c->device = device;
+  c->budget = mem_budget_bytes;
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  e = cudaMallocHost((void **)&c->h_small, 64 * sizeof(int64_t));
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return cuda_fail(e, "cudaMallocHost");
+  }
+  // keep stream-ordered output allocations cached between calls
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  c->max_blocks[0] = gsofa::traverse_max_blocks(device, 0);
+  c->max_blocks[1] = gsofa::traverse_max_blocks(device, 1);
+  if (c->max_blocks[0] <= 0 || c->max_blocks[1] <= 0) {
+    cudaFreeHost(c->h_small);
+    cudaStreamDestroy(c->stream);
+    delete c;
+    set_detail("traversal kernel cannot be made resident (occupancy 0)");
+    return GSOFA_ECUDA;
+  }
+  *out = c;
+  return GSOFA_OK;
+}
+
+void gsofa_context_destroy(gsofa_context *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  release_arena(c);
+  if (c->in_rowptr) cudaFree(c->in_rowptr);
+  if (c->in_colidx) cudaFree(c->in_colidx);
+  if (c->rowptr32) cudaFree(c->rowptr32);
+  if (c->h_small) cudaFreeHost(c->h_small);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int gsofa_result_copy(const gsofa_result *r, int64_t *L_rowptr, int32_t *L_colidx,
+                      int64_t *U_rowptr, int32_t *U_colidx, int32_t *sn_start) {
+  if (!r) {
+    set_detail("result is NULL");
+    return GSOFA_EINVAL;
+  }
+  if (r->on_device) {
+    cudaError_t e = cudaSetDevice(r->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  }
+  const int64_t rows = r->row_end - r->row_begin;
+  struct {
+    void *dst;
+    const void *src;
+    size_t bytes;
+  } cp[5] = {{L_rowptr, r->L_rowptr, (size_t)(rows + 1) * 8},
+             {L_colidx, r->L_colidx, (size_t)r->nnz_L * 4},
+             {U_rowptr, r->U_rowptr, (size_t)(rows + 1) * 8},
+             {U_colidx, r->U_colidx, (size_t)r->nnz_U * 4},
+             {sn_start, r->sn_start, (size_t)(r->nsuper + 1) * 4}};
+  for (auto &c : cp) {
+    if (!c.dst || !c.bytes) continue;
+    if (r->on_device || is_device_ptr(c.dst)) {
+      cudaError_t e = cudaMemcpy(c.dst, c.src, c.bytes, cudaMemcpyDefault);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(result)");
+    } else {
+      std::memcpy(c.dst, c.src, c.bytes);
+    }
+  }
+  return GSOFA_OK;
+}
+
+void gsofa_result_free(gsofa_result *r) {
+  if (!r) return;
+  void *ptrs[5] = {r->L_rowptr, r->L_colidx, r->U_rowptr, r->U_colidx, r->sn_start};
+  if (r->on_device) {
+    cudaSetDevice(r->device);
+    for (void *p : ptrs)
+      if (p) cudaFree(p);
+  } else {
+    for (void *p : ptrs) std::free(p);
+  }
+  std::free(r);
+}
+
+int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                   const gsofa_opts *opts_in, gsofa_result **out) {
+  if (!out) {
+    set_detail("out is NULL");
+    return GSOFA_EINVAL;
+  }
+  *out = nullptr;
+  gsofa_opts o;
+  if (opts_in) o = *opts_in;
+  else gsofa_default_opts(&o);
+  if (n <= 0 || n >= (int64_t(1) << 31) || !rowptr || !colidx) {
+    set_detail("bad n=%lld or NULL input", (long long)n);
+    return GSOFA_EINVAL;
+  }
+  if (o.row_end < 0) o.row_end = n;
+  if (o.chunk_size < 1 || o.row_begin < 0 || o.row_end > n || o.row_begin >= o.row_end ||
+      o.row_begin % o.chunk_size != 0 || o.max_concurrent < 0 || o.max_concurrent % 32 != 0 ||
+      o.mem_budget_bytes < 0 || o.schedule < 0 || o.schedule > 1) {
+    set_detail("bad opts: chunk=%d rows=[%lld,%lld) C=%d budget=%lld", o.chunk_size,
+               (long long)o.row_begin, (long long)o.row_end, o.max_concurrent,
+               (long long)o.mem_budget_bytes);
+    return GSOFA_EINVAL;
+  }
+  bool own_ctx = false;
+  int rc = GSOFA_OK;
+  if (!ctx) {
+    rc = gsofa_context_create(o.device, o.mem_budget_bytes, &ctx);
+    if (rc != GSOFA_OK) return rc;
+    own_ctx = true;
+  }
+  gsofa_context *c = ctx;
+  cudaStream_t st = o.stream ? (cudaStream_t)o.stream : c->stream;
+  gsofa_result *res = nullptr;
+  int64_t *Lrp = nullptr, *Urp = nullptr;
+  int32_t *Lci = nullptr, *Uci = nullptr, *sn = nullptr;
+  size_t Lcap = 0, Ucap = 0;
+  int32_t *sn_scratch = nullptr;
+  void *scan_tmp = nullptr;
+  std::vector<cudaEvent_t> evs;
+  int64_t launches = 0;
+  auto ev = [&]() {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    evs.push_back(e);
+    return (int)evs.size() - 1;
+  };
+  const int64_t rb = o.row_begin, re = o.row_end, rows = re - rb;
+  int64_t nnz = 0;
+  bool in_dev;
+  const int64_t *d_rowptr64;
+  const int32_t *d_colidx;
+  int e_start, e_up, e_sn0, e_sn1, e_end;
+  std::vector<std::pair<int, int>> e_trav, e_ext;
+  int64_t baseL = 0, baseU = 0, nbatches = 0, maxC = 0;
+  Plan plan;
+
+  CK(cudaSetDevice(c->device));
+  e_start = ev();
+  // ---------------------------------------------------- A1: residency
+  in_dev = is_device_ptr(rowptr);
+  if (in_dev != is_device_ptr(colidx) && n > 0) {
+    // mixed is allowed only if colidx is empty-ish; require same kind
+    set_detail("rowptr and colidx must both be host or both be device pointers");
+    rc = GSOFA_EINVAL;
+    goto fail;
+  }
+  if (in_dev) {
+    CK(cudaMemcpyAsync(c->h_small, rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    nnz = c->h_small[0];
+  } else {
+    nnz = rowptr[n];
+  }
+  if (nnz < 0 || nnz >= (int64_t(1) << 31)) {
+    set_detail("nnz=%lld out of range [0, 2^31)", (long long)nnz);
+    rc = GSOFA_EBADCSR;
+    goto fail;
+  }
+  if (in_dev) {
+    d_rowptr64 = rowptr;
+    d_colidx = colidx;
+  } else {
+    if ((rc = grow_device(&c->in_rowptr, &c->in_rowptr_cap, (size_t)n + 1, st)) != GSOFA_OK) goto fail;
+    if ((rc = grow_device(&c->in_colidx, &c->in_colidx_cap, (size_t)std::max<int64_t>(nnz, 1), st)) != GSOFA_OK) goto fail;
+    CK(cudaMemcpyAsync(c->in_rowptr, rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    if (nnz) CK(cudaMemcpyAsync(c->in_colidx, colidx, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    d_rowptr64 = c->in_rowptr;
+    d_colidx = c->in_colidx;
+  }
+  e_up = ev();
+  if ((rc = grow_device(&c->rowptr32, &c->rowptr32_cap, (size_t)n + 1, st)) != GSOFA_OK) goto fail;
+  // ---------------------------------------------------- plan + arena
+  {
+    const int64_t cmax_req =
+        o.max_concurrent ? o.max_concurrent : (o.schedule == GSOFA_SCHEDULE_FIFO ? 16384 : 65536);
+    int64_t budget = o.mem_budget_bytes ? o.mem_budget_bytes : c->budget;
+    if (!budget) budget = auto_budget(c->device) + (int64_t)c->arena_bytes;
+    const int64_t vb_max = std::min<int64_t>(n, re + 32);
+    if (!make_plan(o.schedule, n, rows, vb_max, cmax_req, budget, plan)) {
+      set_detail("budget %lld B cannot hold one 32-source group for n=%lld", (long long)budget,
+                 (long long)n);
+      rc = GSOFA_EINFEASIBLE;
+      goto fail;
+    }
+  }
+  if ((rc = ensure_arena(c, n, plan, st)) != GSOFA_OK) goto fail;
+  if ((rc = prepare_work(c, o.schedule, st)) != GSOFA_OK) goto fail;
+  // validate (GSOFA_EBADCSR) and narrow row pointers to int32
+  CK(cudaMemsetAsync(c->err, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(c->stats, 0, 8 * sizeof(unsigned long long), st));
+  CK(gsofa::launch_validate(d_rowptr64, d_colidx, n, nnz, c->rowptr32, c->err, st));
+  ++launches;
+  CK(cudaMemcpyAsync(c->h_small, c->err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (*(int *)c->h_small) {
+    const int f = *(int *)c->h_small;
+    set_detail("CSR check failed:%s%s%s", (f & 1) ? " bad rowptr" : "",
+               (f & 2) ? " column out of range" : "", (f & 4) ? " columns not strictly increasing" : "");
+    rc = GSOFA_EBADCSR;
+    goto fail;
+  }
+  // ---------------------------------------------------- outputs
+  {
+    cudaError_t e1 = cudaMallocAsync((void **)&Lrp, (rows + 1) * sizeof(int64_t), st);
+    cudaError_t e2 = cudaMallocAsync((void **)&Urp, (rows + 1) * sizeof(int64_t), st);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      cudaGetLastError();
+      set_detail("output row pointer allocation failed");
+      rc = GSOFA_ENOMEM;
+      goto fail;
+    }
+    CK(cudaMemsetAsync(Lrp, 0, sizeof(int64_t), st));
+    CK(cudaMemsetAsync(Urp, 0, sizeof(int64_t), st));
+    const size_t guess = (size_t)std::max<int64_t>(1024, 4 * (nnz + n) * rows / n);
+    if ((rc = grow_device(&Lci, &Lcap, guess, st)) != GSOFA_OK) goto fail;
+    if ((rc = grow_device(&Uci, &Ucap, guess, st)) != GSOFA_OK) goto fail;
+  }
+  // ---------------------------------------------------- batches
+  for (int64_t s0 = rb; s0 < re;) {
+    // #C for this batch: the largest multiple of 32 whose bubble-removed
+    // working set fits the work region ("dynamic space allocation",
+    // P:768-778; "reduce the number of concurrent sources")
+    const int64_t C = fit_batch(o.schedule, n, s0, std::min<int64_t>(c->Cmax, round_up(re - s0, 32)),
+                                c->work_bytes);
+    if (C < 32) {
+      set_detail("work region too small for a 32-source group at s0=%lld", (long long)s0);
+      rc = GSOFA_EINFEASIBLE;
+      goto fail;
+    }
+    const int64_t G = C / 32;
+    const int64_t vb = std::min<int64_t>(n, s0 + C);
+    const int32_t s_end = (int32_t)std::min<int64_t>(re, s0 + C);
+    const int et0 = ev();
+    if (o.schedule == GSOFA_SCHEDULE_FIFO) {
+      // epoch: a fresh value range below every value written so far
+      if (c->floor < (uint32_t)(n + 2) + 1u) {
+        CK(cudaMemsetAsync(c->work, 0xFF, fifo_label_bytes(c->work_bytes), st));
+        c->floor = 0xFFFFFFFFu;
+      }
+      const uint32_t base = c->floor - (uint32_t)(n + 2);
+      c->floor = base;
+      // masks and queues at FIXED offsets (capacity Q words each): a mask
+      // array must never land on memory a previous batch used as a queue
+      const size_t lab_b = fifo_label_bytes(c->work_bytes);
+      const size_t Q = (c->work_bytes - lab_b) / 16;
+      uint32_t *fmq = (uint32_t *)((char *)c->work + lab_b);
+      gsofa::BatchParams bp;
+      bp.rowptr = c->rowptr32;
+      bp.colidx = d_colidx;
+      bp.n = (int32_t)n;
+      bp.s0 = (int32_t)s0;
+      bp.s_end = s_end;
+      bp.G = (int32_t)G;
+      bp.gbits = c->gbits;
+      bp.Vb = (int32_t)vb;
+      bp.base = base;
+      bp.lab = c->work;
+      bp.fm0 = fmq;
+      bp.fm1 = fmq + Q;
+      bp.q0 = fmq + 2 * Q;
+      bp.q1 = fmq + 3 * Q;
+      bp.qcount = c->qcount;
+      bp.is = c->is;
+      bp.stats = c->stats;
+      CK(cudaMemsetAsync(c->qcount, 0, 3 * sizeof(uint32_t), st));
+      CK(gsofa::launch_seed(bp, st));
+      CK(gsofa::launch_traverse(bp, o.fill_first ? 1 : 0, c->max_blocks[o.fill_first ? 1 : 0], st));
+      launches += 2;
+    } else {
+      gsofa::ThrParams tp;
+      tp.rowptr = c->rowptr32;
+      tp.colidx = d_colidx;
+      tp.n = (int32_t)n;
+      tp.s0 = (int32_t)s0;
+      tp.s_end = s_end;
+      tp.G = (int32_t)G;
+      tp.Vb = (int32_t)vb;
+      tp.ws = c->work;
+      tp.ws_words = gsofa::threshold_ws_words(vb);
+      tp.is = c->is;
+      tp.stats = c->stats;
+      CK(gsofa::launch_threshold(tp, st));
+      ++launches;
+    }
+    const int et1 = ev();
+    e_trav.push_back({et0, et1});
+
+    gsofa::ExtractParams ep;
+    ep.is_ro = c->is;
+    ep.is = c->is;
+    ep.n = (int32_t)n;
+    ep.s0 = (int32_t)s0;
+    ep.s_end = s_end;
+    ep.G = (int32_t)G;
+    ep.nchunks = (int32_t)c->nsub;
+    ep.cntL = c->cntL;
+    ep.cntU = c->cntU;
+    ep.rowL = c->rowL;
+    ep.rowU = c->rowU;
+    ep.totals = c->totals;
+    ep.L_rowptr = Lrp;
+    ep.U_rowptr = Urp;
+    ep.row_begin = (int32_t)rb;
+    ep.baseL = baseL;
+    ep.baseU = baseU;
+    ep.L_out = nullptr;
+    ep.U_out = nullptr;
+    CK(gsofa::launch_extract_count(ep, st));
+    CK(gsofa::launch_extract_scan(ep, st));
+    launches += 3;
+    CK(cudaMemcpyAsync(c->h_small, c->totals, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    {
+      const int64_t tL = c->h_small[0], tU = c->h_small[1];
+      if ((rc = grow_device(&Lci, &Lcap, (size_t)(baseL + tL), st)) != GSOFA_OK) goto fail;
+      if ((rc = grow_device(&Uci, &Ucap, (size_t)(baseU + tU), st)) != GSOFA_OK) goto fail;
+      ep.L_out = Lci;
+      ep.U_out = Uci;
+      CK(gsofa::launch_extract_write(ep, st));
+      ++launches;
+      baseL += tL;
+      baseU += tU;
+    }
+    e_ext.push_back({et1, ev()});
+    ++nbatches;
+    maxC = std::max(maxC, C);
+    s0 += C;
+  }
+  // ---------------------------------------------------- supernodes (A8)
+  e_sn0 = ev();
+  {
+    const size_t tmpb = gsofa::scan_tmp_bytes(rows);
+    cudaError_t e1 = cudaMallocAsync((void **)&sn_scratch, (size_t)rows * 3 * sizeof(int32_t) + 64, st);
+    cudaError_t e2 = cudaMallocAsync(&scan_tmp, tmpb, st);
+    cudaError_t e3 = cudaMallocAsync((void **)&sn, (size_t)(rows + 1) * sizeof(int32_t), st);
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+      cudaGetLastError();
+      set_detail("supernode scratch allocation failed");
+      rc = GSOFA_ENOMEM;
+      goto fail;
+    }
+    int32_t *flags = sn_scratch;                 // [2 rows]: Phase-I bits, leaders
+    int32_t *pos = sn_scratch + 2 * rows;        // [rows]
+    int32_t *total = (int32_t *)c->totals + 4;   // scratch int
+    CK(gsofa::launch_supernode_flags(Lrp, Lci, Urp, (int32_t)rb, (int32_t)re, o.chunk_size, flags, st));
+    CK(gsofa::scan_exclusive_i32(flags + rows, pos, rows, total, scan_tmp, tmpb, st));
+    CK(gsofa::launch_supernode_scatter(flags + rows, pos, (int32_t)rb, (int32_t)re, total, sn, st));
+    launches += 4;
+    unsigned long long *offd = c->stats + 5;
+    CK(gsofa::launch_count_offdiag(c->rowptr32, d_colidx, (int32_t)rb, (int32_t)re, offd, st));
+    ++launches;
+  }
+  e_sn1 = ev();
+  // ---------------------------------------------------- result
+  res = (gsofa_result *)std::calloc(1, sizeof(gsofa_result));
+  if (!res) {
+    rc = GSOFA_ENOMEM;
+    goto fail;
+  }
+  CK(cudaMemcpyAsync(c->h_small, c->stats, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->h_small + 8, (int32_t *)c->totals + 4, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  {
+    const unsigned long long *hs = (const unsigned long long *)c->h_small;
+    res->n = n;
+    res->row_begin = rb;
+    res->row_end = re;
+    res->nnz_L = baseL;
+    res->nnz_U = baseU;
+    res->nsuper = *(int32_t *)(c->h_small + 8);
+    res->nnz_A_offdiag = (int64_t)hs[5];
+    res->fill_count = baseL + (baseU - rows) - res->nnz_A_offdiag;
+    res->device = c->device;
+    res->stats.frontier_items = (int64_t)hs[0];
+    res->stats.edge_inspections = (int64_t)hs[1];
+    res->stats.rounds = (int64_t)hs[2];
+    res->stats.thresholds = (int64_t)hs[3];
+    res->stats.item_edges = (int64_t)hs[4];
+    res->stats.batches = nbatches;
+    res->stats.max_batch = maxC;
+    res->stats.kernel_launches = launches;
+  }
+  if (o.outputs_on_device) {
+    res->on_device = 1;
+    res->L_rowptr = Lrp;
+    res->U_rowptr = Urp;
+    res->L_colidx = Lci;
+    res->U_colidx = Uci;
+    res->sn_start = sn;
+    Lrp = Urp = nullptr;
+    Lci = Uci = sn = nullptr;
+  } else {
+    res->on_device = 0;
+    const size_t nl = (size_t)res->nnz_L, nu = (size_t)res->nnz_U, ns = (size_t)res->nsuper + 1;
+    res->L_rowptr = (int64_t *)std::malloc((rows + 1) * sizeof(int64_t));
+    res->U_rowptr = (int64_t *)std::malloc((rows + 1) * sizeof(int64_t));
+    res->L_colidx = (int32_t *)std::malloc(std::max<size_t>(nl, 1) * sizeof(int32_t));
+    res->U_colidx = (int32_t *)std::malloc(std::max<size_t>(nu, 1) * sizeof(int32_t));
+    res->sn_start = (int32_t *)std::malloc(ns * sizeof(int32_t));
+    if (!res->L_rowptr || !res->U_rowptr || !res->L_colidx || !res->U_colidx || !res->sn_start) {
+      set_detail("host output allocation failed");
+      rc = GSOFA_ENOMEM;
+      goto fail;
+    }
+    const int eh0 = ev();
+    CK(cudaMemcpyAsync(res->L_rowptr, Lrp, (rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(res->U_rowptr, Urp, (rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (nl) CK(cudaMemcpyAsync(res->L_colidx, Lci, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    if (nu) CK(cudaMemcpyAsync(res->U_colidx, Uci, nu * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(res->sn_start, sn, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    const int eh1 = ev();
+    CK(cudaStreamSynchronize(st));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, evs[eh0], evs[eh1]);
+    res->stats.ms_transfer += ms;
+  }
+  e_end = ev();
+  CK(cudaStreamSynchronize(st));
+  {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, evs[e_start], evs[e_end]);
+    res->stats.ms_total = ms;
+    if (!in_dev) {
+      cudaEventElapsedTime(&ms, evs[e_start], evs[e_up]);
+      res->stats.ms_transfer += ms;
+    }
+    for (auto &p : e_trav) {
+      cudaEventElapsedTime(&ms, evs[p.first], evs[p.second]);
+      res->stats.ms_traverse += ms;
+    }
+    for (auto &p : e_ext) {
+      cudaEventElapsedTime(&ms, evs[p.first], evs[p.second]);
+      res->stats.ms_extract += ms;
+    }
+    cudaEventElapsedTime(&ms, evs[e_sn0], evs[e_sn1]);
+    res->stats.ms_supernode = ms;
+  }
+  if (sn_scratch) cudaFreeAsync(sn_scratch, st);
+  if (scan_tmp) cudaFreeAsync(scan_tmp, st);
+  if (Lrp) cudaFreeAsync(Lrp, st);
+  if (Urp) cudaFreeAsync(Urp, st);
+  if (Lci) cudaFreeAsync(Lci, st);
+  if (Uci) cudaFreeAsync(Uci, st);
+  if (sn) cudaFreeAsync(sn, st);
+  cudaStreamSynchronize(st);
+  for (auto e : evs) cudaEventDestroy(e);
+  if (own_ctx) gsofa_context_destroy(c);
+  *out = res;
+  return GSOFA_OK;
+
+fail:
+  cudaStreamSynchronize(st);
+  cudaGetLastError();
+  if (sn_scratch) cudaFree(sn_scratch);
+  if (scan_tmp) cudaFree(scan_tmp);
+  if (Lrp) cudaFree(Lrp);
+  if (Urp) cudaFree(Urp);
+  if (Lci) cudaFree(Lci);
+  if (Uci) cudaFree(Uci);
+  if (sn) cudaFree(sn);
+  if (res) {
+    if (!res->on_device) {
+      std::free(res->L_rowptr);
+      std::free(res->U_rowptr);
+      std::free(res->L_colidx);
+      std::free(res->U_colidx);
+      std::free(res->sn_start);
+    }
+    std::free(res);
+  }
+  for (auto e : evs) cudaEventDestroy(e);
+  // a failed batch may leave masks/bitmaps dirty: force re-initialisation
+  release_arena(c);
+  if (own_ctx) gsofa_context_destroy(c);
+  return rc;
+}
+
+// ------------------------------------------------------------ partitioning
+int gsofa_partition_rows(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t nparts,
+                         int32_t align, int64_t *bounds) {
+  if (n <= 0 || !rowptr || !colidx || nparts < 1 || align < 1 || !bounds) {
+    set_detail("bad arguments to gsofa_partition_rows");
+    return GSOFA_EINVAL;
+  }
+  if (is_device_ptr(rowptr) || is_device_ptr(colidx)) {
+    set_detail("gsofa_partition_rows takes host pointers");
+    return GSOFA_EINVAL;
+  }
+  const int64_t nnz = rowptr[n];
+  // transpose pattern (for the symmetrised A + A^T)
+  std::vector<int64_t> tp(n + 1, 0);
+  std::vector<int32_t> ti(std::max<int64_t>(nnz, 1));
+  for (int64_t e = 0; e < nnz; ++e) {
+    const int32_t cix = colidx[e];
+    if (cix < 0 || cix >= n) {
+      set_detail("column out of range");
+      return GSOFA_EBADCSR;
+    }
+    ++tp[cix + 1];
+  }
+  for (int64_t i = 0; i < n; ++i) tp[i + 1] += tp[i];
+  {
+    std::vector<int64_t> cur(tp.begin(), tp.end() - 1);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) ti[cur[colidx[e]]++] = (int32_t)i;
+  }
+  // elimination tree of A + A^T (Liu, with path compression)
+  std::vector<int32_t> parent(n, -1), anc(n, -1);
+  auto visit = [&](int32_t i, int32_t k) {
+    int32_t r = k;
+    while (anc[r] != -1 && anc[r] != i) {
+      const int32_t t = anc[r];
+      anc[r] = i;
+      r = t;
+    }
+    if (anc[r] == -1) {
+      anc[r] = i;
+      parent[r] = i;
+    }
+  };
+  for (int32_t i = 0; i < n; ++i) {
+    for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e)
+      if (colidx[e] < i) visit(i, colidx[e]);
+    for (int64_t e = tp[i]; e < tp[i + 1]; ++e)
+      if (ti[e] < i) visit(i, ti[e]);
+  }
+  // work(s) ~ sum of out-degrees over the subtree of s (vertices reachable from
+  // s through smaller ids are inside it; work grows with s)
+  std::vector<double> w(n);
+  for (int64_t v = 0; v < n; ++v) w[v] = 1.0 + (double)(rowptr[v + 1] - rowptr[v]);
+  for (int64_t v = 0; v < n; ++v)
+    if (parent[v] >= 0) w[parent[v]] += w[v];
+  std::vector<double> pre(n + 1, 0.0);
+  for (int64_t v = 0; v < n; ++v) pre[v + 1] = pre[v] + w[v];
+  bounds[0] = 0;
+  for (int32_t p = 1; p < nparts; ++p) {
+    const double target = pre[n] * p / nparts;
+    int64_t s = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
+    s = std::min<int64_t>(n, std::max<int64_t>(bounds[p - 1], (s + align / 2) / align * align));
+    bounds[p] = s;
+  }
+  bounds[nparts] = n;
+  return GSOFA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// gsofa_internal.cuh -- shared declarations of the CUDA path (sm_100a only).
+//
+// Device data layout for one batch of C = 32*G concurrent sources
+// [s0, s0 + C):
+//
+//   lab [G][Vb][32] uint32  maxId labels, Vb = min(n, s0 + C): bubble removal
+//                           at batch granularity.  Lane k of slot
+//                           group g is source s0 + 32g + k, so one warp's 32
+//                           labels of a vertex are one 128-byte line.
+//                           Epoch-encoded: enc(m) = base + m + 1,
+//                           m in [-1, n]; values from older epochs are larger
+//                           than any current value and decode as "infinity".
+//   fm  [2][G][Vb] uint32   frontier masks (bit k: (vertex, source k) is in the
+//                           frontier of the current / next iteration); they
+//                           replace frontierQueue+tracker (Table 2)
+//   queue [2][cap] uint32   compacted (vertex << gbits | g) work items, one per
+//                           (vertex, group) with a nonzero mask
+//   is  [G][n] uint32       in-structure bitmaps: bit k of is[g][v] set iff
+//                           (s0 + 32g + k, v) is an off-diagonal entry of L+U
+//                           (the paper's fill(:))
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gsofa {
+
+constexpr int kWarp = 32;
+constexpr int kTraverseThreads = 512;   // 16 warps
+
+struct BatchParams {
+  const int32_t *rowptr;   // [n+1] (device, int32 offsets)
+  const int32_t *colidx;   // [nnz]
+  int32_t n;
+  int32_t s0;              // first source of the batch
+  int32_t s_end;           // one past the last valid source (<= row_end)
+  int32_t G;               // slot groups (C = 32 G)
+  int32_t gbits;           // bits for g in a queue item
+  int32_t Vb;              // label rows per group
+  uint32_t base;           // epoch base: enc(m) = base + m + 1
+  uint32_t *lab;           // [G][Vb][32]
+  uint32_t *fm0, *fm1;     // [G][Vb]
+  uint32_t *q0, *q1;       // queues
+  uint32_t *qcount;        // [3] rotating item counters
+  uint32_t *is;            // [G][n]
+  unsigned long long *stats;  // [4]: items, edge inspections, rounds, pushes
+};
+
+// ---------------------------------------------------------------- kernels
+// traverse.cu
+cudaError_t launch_seed(const BatchParams &p, cudaStream_t st);
+cudaError_t launch_traverse(const BatchParams &p, int fill_first, int grid_blocks,
+                            cudaStream_t st);
+int traverse_max_blocks(int device, int fill_first);
+
+// threshold.cu (default schedule: increasing newMaxId, one CTA per group)
+struct ThrParams {
+  const int32_t *rowptr;
+  const int32_t *colidx;
+  int32_t n, s0, s_end, G, Vb;
+  uint32_t *ws;            // [G][ws_words] per-group workspace
+  size_t ws_words;
+  uint32_t *is;            // [G][n]
+  unsigned long long *stats;  // [4]: items, edge inspections, levels, thresholds
+};
+size_t threshold_ws_words(int64_t Vb);
+cudaError_t launch_threshold(const ThrParams &p, cudaStream_t st);
+
+// extract.cu
+struct ExtractParams {
+  const uint32_t *is_ro;
+  uint32_t *is;
+  int32_t n, s0, s_end, G, nchunks;  // nchunks = ceil(n / extract_sub_columns())
+  uint32_t *cntL, *cntU;     // [G][nchunks][32] counts, then exclusive prefixes
+  int64_t *rowL, *rowU;      // [C] row start offsets (relative to the batch)
+  int64_t *totals;           // [2] batch totals (L, U incl. diagonal)
+  int64_t *L_rowptr, *U_rowptr;  // global output row pointers (row_begin based)
+  int32_t row_begin;
+  int64_t baseL, baseU;      // global offsets of the batch's first row
+  int32_t *L_out, *U_out;    // global colidx arrays
+};
+cudaError_t launch_extract_count(const ExtractParams &e, cudaStream_t st);
+cudaError_t launch_extract_scan(const ExtractParams &e, cudaStream_t st);
+cudaError_t launch_extract_write(const ExtractParams &e, cudaStream_t st);
+int extract_sub_columns();  // columns per extraction warp unit
+
+// supernode.cu + utilities
+cudaError_t launch_validate(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
+                            int64_t nnz, int32_t *rowptr32, int *err_flag, cudaStream_t st);
+cudaError_t launch_count_offdiag(const int32_t *rowptr, const int32_t *colidx, int32_t r0,
+                                 int32_t r1, unsigned long long *out, cudaStream_t st);
+cudaError_t launch_supernode_flags(const int64_t *L_rowptr, const int32_t *L_colidx,
+                                   const int64_t *U_rowptr, int32_t row_begin, int32_t row_end,
+                                   int32_t chunk, int32_t *flags, cudaStream_t st);
+// exclusive scan of int32 flags (count) into int32 positions; total -> *total
+cudaError_t scan_exclusive_i32(const int32_t *in, int32_t *out, int64_t count, int32_t *total,
+                               void *tmp, size_t tmp_bytes, cudaStream_t st);
+size_t scan_tmp_bytes(int64_t count);
+cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, int32_t row_begin,
+                                     int32_t row_end, const int32_t *total, int32_t *sn_start,
+                                     cudaStream_t st);
+
+// ------------------------------------------------------------- helpers
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace gsofa

@@ -1,0 +1,242 @@
+// supernode.cu -- T3 supernode detection (Definition def:T3) with the
+// paper's two-phase SIMT design, plus input validation, the
+// off-diagonal count of A and a device-wide exclusive scan.
+//
+// Phase I (one thread per row): bit[s] = nnz(U(s,:)) == nnz(U(s-1,:)) - 1 and
+//   s is not a chunk start (chunks of chunk_size rows never share a supernode,
+//   P:640).  Rows with bit 0 are the Phase-I leaders ("queue" of P:609).
+// Phase II (one thread per Phase-I leader): the leader r grows through the
+//   following run of bit-1 rows while L(s, r) != 0 (binary search in the sorted
+//   row s of L); a rejected row becomes a new leader and growth continues from
+//   it ("continue this process until no supernode grows").  Runs
+//   between Phase-I leaders are independent, which is the parallelism the
+//   paper's first phase exposes.
+#include "gsofa_internal.cuh"
+
+namespace gsofa {
+
+namespace {
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+__global__ void validate_kernel(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
+                                int64_t nnz, int32_t *rowptr32, int *err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  const int64_t a = rowptr64[i];
+  rowptr32[i] = (int32_t)a;
+  if (i == 0 && a != 0) atomicOr(err, 1);
+  if (i == n) {
+    if (a != nnz) atomicOr(err, 1);
+    return;
+  }
+  const int64_t b = rowptr64[i + 1];
+  if (b < a || a < 0 || b > nnz) {
+    atomicOr(err, 1);
+    return;
+  }
+  int32_t prev = -1;
+  for (int64_t e = a; e < b; ++e) {
+    const int32_t c = colidx[e];
+    if (c < 0 || c >= n) atomicOr(err, 2);
+    if (c <= prev) atomicOr(err, 4);
+    prev = c;
+  }
+}
+
+__global__ void offdiag_kernel(const int32_t *rowptr, const int32_t *colidx, int32_t r0,
+                               int32_t r1, unsigned long long *out) {
+  __shared__ unsigned long long ws[32];
+  const int i = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long c = 0;
+  if (i < r1) {
+    const int a = rowptr[i], b = rowptr[i + 1];
+    c = (unsigned long long)(b - a);
+    for (int e = a; e < b; ++e) c -= (colidx[e] == i);
+  }
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    atomicAdd(out, t);
+  }
+}
+
+__device__ __forceinline__ bool row_contains(const int32_t *cols, int64_t a, int64_t b,
+                                             int32_t key) {
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    const int32_t v = cols[m];
+    if (v == key) return true;
+    if (v < key) a = m + 1;
+    else b = m;
+  }
+  return false;
+}
+
+// Phase I: flags[s] = 1 (Phase-I leader, bit 0) or 0 (bit 1)
+__global__ void sn_phase1_kernel(const int64_t *U_rowptr, int32_t row_begin, int32_t row_end,
+                                 int32_t chunk, int32_t *bit) {
+  const int32_t s = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= row_end) return;
+  const int k = s - row_begin;
+  int b = 0;
+  if (s != row_begin && s % chunk != 0) {
+    const int64_t nu = U_rowptr[k + 1] - U_rowptr[k];
+    const int64_t np = U_rowptr[k] - U_rowptr[k - 1];
+    b = (nu == np - 1);
+  }
+  bit[k] = b;
+}
+
+// Phase II: each Phase-I leader grows through its run of bit-1 rows
+__global__ void sn_phase2_kernel(const int64_t *L_rowptr, const int32_t *L_colidx,
+                                 int32_t row_begin, int32_t row_end, const int32_t *bit,
+                                 int32_t *leader) {
+  const int32_t s = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= row_end) return;
+  const int k = s - row_begin;
+  if (bit[k]) return;  // not a Phase-I leader
+  leader[k] = 1;
+  int32_t r = s;
+  for (int32_t t = s + 1; t < row_end && bit[t - row_begin]; ++t) {
+    const int kt = t - row_begin;
+    if (row_contains(L_colidx, L_rowptr[kt], L_rowptr[kt + 1], r)) {
+      leader[kt] = 0;  // joins the supernode led by r (Def. def:T3 (ii))
+    } else {
+      leader[kt] = 1;  // rejected: starts a new supernode
+      r = t;
+    }
+  }
+}
+
+__global__ void sn_scatter_kernel(const int32_t *flags, const int32_t *pos, int32_t row_begin,
+                                  int32_t row_end, const int32_t *total, int32_t *sn_start) {
+  const int32_t s = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s == row_begin) sn_start[*total] = row_end;  // sentinel
+  if (s >= row_end) return;
+  const int k = s - row_begin;
+  if (flags[k]) sn_start[pos[k]] = s;
+}
+
+// ---- exclusive scan (int32), 4096 items per block, recursive on block sums
+constexpr int kScanThreads = 1024, kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads) scan_tile_kernel(const int32_t *in, int32_t *out,
+                                                                 int64_t count, int32_t *sums) {
+  __shared__ int32_t ws[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)tid * kScanItems;
+  int32_t v[kScanItems];
+  int32_t t = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = (base + i < count) ? in[base + i] : 0;
+    t += v[i];
+  }
+  int32_t x = t;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int32_t y = __shfl_up_sync(kFull, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) ws[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int32_t z = ws[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t y = __shfl_up_sync(kFull, z, d);
+      if (lane >= d) z += y;
+    }
+    ws[lane] = z;
+  }
+  __syncthreads();
+  int32_t run = x - t + (wid ? ws[wid - 1] : 0);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < count) out[base + i] = run;
+    run += v[i];
+  }
+  if (tid == kScanThreads - 1) sums[blockIdx.x] = run;
+}
+
+__global__ void scan_add_kernel(int32_t *out, int64_t count, const int32_t *offs) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] += offs[i / kScanTile];
+}
+
+cudaError_t scan_rec(const int32_t *in, int32_t *out, int64_t count, int32_t *total, int32_t *tmp,
+                     cudaStream_t st) {
+  const int64_t nb = (count + kScanTile - 1) / kScanTile;
+  int32_t *sums = tmp, *sums_scan = tmp + nb;
+  scan_tile_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, count, sums);
+  if (nb == 1) {
+    cudaMemcpyAsync(total, sums, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+    return cudaGetLastError();
+  }
+  cudaError_t e = scan_rec(sums, sums_scan, nb, total, tmp + 2 * nb, st);
+  if (e != cudaSuccess) return e;
+  scan_add_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(out, count, sums_scan);
+  return cudaGetLastError();
+}
+}  // namespace
+
+size_t scan_tmp_bytes(int64_t count) {
+  size_t tot = 0;
+  int64_t c = count;
+  do {
+    const int64_t nb = (c + kScanTile - 1) / kScanTile;
+    tot += 2 * (size_t)nb;
+    c = nb;
+  } while (c > 1);
+  return (tot + 16) * sizeof(int32_t);
+}
+
+cudaError_t scan_exclusive_i32(const int32_t *in, int32_t *out, int64_t count, int32_t *total,
+                               void *tmp, size_t tmp_bytes, cudaStream_t st) {
+  if (count <= 0) return cudaMemsetAsync(total, 0, sizeof(int32_t), st);
+  if (tmp_bytes < scan_tmp_bytes(count)) return cudaErrorInvalidValue;
+  return scan_rec(in, out, count, total, (int32_t *)tmp, st);
+}
+
+cudaError_t launch_validate(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
+                            int64_t nnz, int32_t *rowptr32, int *err_flag, cudaStream_t st) {
+  validate_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(rowptr64, colidx, n, nnz,
+                                                                   rowptr32, err_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_offdiag(const int32_t *rowptr, const int32_t *colidx, int32_t r0,
+                                 int32_t r1, unsigned long long *out, cudaStream_t st) {
+  if (r1 <= r0) return cudaSuccess;
+  offdiag_kernel<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, st>>>(rowptr, colidx, r0, r1, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_supernode_flags(const int64_t *L_rowptr, const int32_t *L_colidx,
+                                   const int64_t *U_rowptr, int32_t row_begin, int32_t row_end,
+                                   int32_t chunk, int32_t *flags, cudaStream_t st) {
+  // flags has room for 2 * rows: [0, rows) = Phase-I bits, [rows, 2 rows) = leaders
+  const int32_t rows = row_end - row_begin;
+  if (rows <= 0) return cudaSuccess;
+  const unsigned nb = (unsigned)((rows + 255) / 256);
+  sn_phase1_kernel<<<nb, 256, 0, st>>>(U_rowptr, row_begin, row_end, chunk, flags);
+  sn_phase2_kernel<<<nb, 256, 0, st>>>(L_rowptr, L_colidx, row_begin, row_end, flags,
+                                       flags + rows);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, int32_t row_begin,
+                                     int32_t row_end, const int32_t *total, int32_t *sn_start,
+                                     cudaStream_t st) {
+  const int32_t rows = row_end - row_begin;
+  sn_scatter_kernel<<<(unsigned)((rows + 255) / 256 + 1), 256, 0, st>>>(flags, pos, row_begin,
+                                                                        row_end, total, sn_start);
+  return cudaGetLastError();
+}
+
+}  // namespace gsofa

@@ -1,0 +1,114 @@
+"""Multi-GPU layer: one process per GPU (torch.distributed), graph replicated,
+source rows split into contiguous work-balanced ranges.
+
+Rows are independent given the static G(A); only supernode detection
+couples consecutive rows.  Ranges start at multiples of
+chunk_size, and supernodes never cross a chunk boundary (chunkSize = maximum
+supernode size), so every rank's supernodes are final and there is no
+supernode-boundary exchange to make.  The one collective on the path is the
+final allgather of per-rank counts (nnz_L, nnz_U, fill, nsuper, nnz_A_offdiag),
+from which each rank derives the global CSR offsets of its slice -- a few
+dozen bytes per rank over NCCL (NVLink/NVSwitch on a B200 box).
+
+The partition comes from gsofa_partition_rows (host C++ in libgsofa.so):
+equal shares of an elimination-tree work estimate.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+COUNT_FIELDS = ("nnz_L", "nnz_U", "fill_count", "nsuper", "nnz_A_offdiag", "rows")
+
+
+@dataclass
+class RankSlice:
+    rank: int
+    world: int
+    row_begin: int
+    row_end: int
+    counts: np.ndarray        # [world, len(COUNT_FIELDS)] int64, all ranks
+    L_base: int               # global offset of this slice in L_colidx
+    U_base: int               # global offset of this slice in U_colidx
+    sn_base: int              # global index of this slice's first supernode
+    result: object = None     # local Result (None if the range is empty)
+
+    @property
+    def totals(self):
+        t = self.counts.sum(axis=0)
+        return dict(zip(COUNT_FIELDS, (int(x) for x in t)))
+
+
+def partition(rowptr, colidx, world: int, chunk_size: int = 128, partition_fn=None):
+    """Contiguous row ranges, one per rank, starting at multiples of chunk_size."""
+    if partition_fn is None:
+        from . import partition_rows as partition_fn
+    return partition_fn(rowptr, colidx, world, chunk_size)
+
+
+def global_offsets(counts: np.ndarray, rank: int):
+    """Exclusive prefix over ranks of the gathered counts -> (L_base, U_base, sn_base)."""
+    before = counts[:rank].sum(axis=0) if rank else np.zeros(counts.shape[1], np.int64)
+    return int(before[0]), int(before[1]), int(before[3])
+
+
+def allgather_counts(local: np.ndarray, group=None, device=None) -> np.ndarray:
+    """all_gather of a small int64 vector (NCCL on GPU tensors, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = torch.as_tensor(local, dtype=torch.int64)
+    if device is not None:
+        t = t.to(device)
+    out = torch.empty(world * t.numel(), dtype=torch.int64, device=t.device)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return out.cpu().numpy().reshape(world, -1)
+
+
+def symbolic_distributed(rowptr, colidx, bounds, *, rank: int, compute_fn=None,
+                         group=None, device=None, **kw) -> RankSlice:
+    """Run this rank's row range and exchange counts.
+
+    compute_fn(rowptr, colidx, row_begin=..., row_end=..., **kw) -> object with
+    nnz_L, nnz_U, fill_count, nsuper, nnz_A_offdiag (default: the CUDA
+    library's :func:`symbolic`).  Tests inject the CPU oracle here to check the
+    host logic with the gloo backend; the product path always uses the GPU.
+    """
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if compute_fn is None:
+        from . import symbolic as compute_fn
+    rb, re = int(bounds[rank]), int(bounds[rank + 1])
+    res = None
+    local = np.zeros(len(COUNT_FIELDS), np.int64)
+    if re > rb:
+        res = compute_fn(rowptr, colidx, row_begin=rb, row_end=re, **kw)
+        local[:] = [res.nnz_L, res.nnz_U, res.fill_count, res.nsuper, res.nnz_A_offdiag, re - rb]
+    counts = allgather_counts(local, group=group, device=device)
+    assert counts.shape == (world, len(COUNT_FIELDS))
+    L_base, U_base, sn_base = global_offsets(counts, rank)
+    return RankSlice(rank, world, rb, re, counts, L_base, U_base, sn_base, res)
+
+
+def assemble(slices_arrays, n: int):
+    """Concatenate per-rank host arrays into the global result (verification
+    helper; not on the timed path).  slices_arrays: list over ranks of dicts
+    with L_rowptr, L_colidx, U_rowptr, U_colidx, sn_start (local, row-range
+    based) -- empty ranges may be None."""
+    Lp, Li, Up, Ui, sn = [np.zeros(1, np.int64)], [], [np.zeros(1, np.int64)], [], []
+    lb = ub = 0
+    for a in slices_arrays:
+        if a is None:
+            continue
+        Lp.append(a["L_rowptr"][1:] + lb)
+        Up.append(a["U_rowptr"][1:] + ub)
+        Li.append(a["L_colidx"])
+        Ui.append(a["U_colidx"])
+        sn.append(a["sn_start"][:-1])
+        lb += int(a["L_rowptr"][-1])
+        ub += int(a["U_rowptr"][-1])
+    sn.append(np.array([n], np.int32))
+    return dict(L_rowptr=np.concatenate(Lp), L_colidx=np.concatenate(Li).astype(np.int32),
+                U_rowptr=np.concatenate(Up), U_colidx=np.concatenate(Ui).astype(np.int32),
+                sn_start=np.concatenate(sn).astype(np.int32))

@@ -1,0 +1,218 @@
+"""GPU parity: the CUDA path (through the C-ABI, libgsofa.so) against the CPU
+oracle (oracle/), element by element, on seeded synthetic inputs.
+
+Bar: bit-exact -- L/U column indices and row pointers,
+supernode starts and fill counts are integers; there are no floating-point
+decisions.  Full-size configs that the oracle cannot finish in seconds are
+checked on sampled rows (the oracle computes rows one by one), and the
+supernode partition is checked by running the oracle's Def. def:T3 scan on
+the GPU's own L/U rows plus the Def. def:T3 properties.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+g = pytest.importorskip("paper_2007_00840_b200")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = g.Context(0)
+    yield c
+    c.close()
+
+
+def run(rp, ci, ctx=None, **kw):
+    r = g.symbolic(rp, ci, ctx=ctx, **kw)
+    a = dict(r.to_numpy())
+    a.update(nnz_L=r.nnz_L, nnz_U=r.nnz_U, nsuper=r.nsuper, fill_count=r.fill_count,
+             nnz_A_offdiag=r.nnz_A_offdiag, stats=r.stats, row_begin=r.row_begin,
+             row_end=r.row_end)
+    r.free()
+    return a
+
+
+def assert_full_equal(got, want):
+    for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start"):
+        assert got[k].dtype == want[k].dtype, k
+        assert np.array_equal(got[k], want[k]), k
+    for k in ("nnz_L", "nnz_U", "nsuper", "fill_count", "nnz_A_offdiag"):
+        assert got[k] == want[k], k
+
+
+def assert_rows_equal(got, rp, ci, rows, nthreads=None):
+    """Sampled-row parity: the oracle computes the listed rows one by one."""
+    want = oracle.rows(rp, ci, rows, nthreads)
+    rb = got["row_begin"]
+    for t, s in enumerate(rows):
+        k = s - rb
+        gl = got["L_colidx"][got["L_rowptr"][k]:got["L_rowptr"][k + 1]]
+        gu = got["U_colidx"][got["U_rowptr"][k]:got["U_rowptr"][k + 1]]
+        wl = want["L_colidx"][want["L_rowptr"][t]:want["L_rowptr"][t + 1]]
+        wu = want["U_colidx"][want["U_rowptr"][t]:want["U_rowptr"][t + 1]]
+        assert np.array_equal(gl, wl), f"L row {s}"
+        assert np.array_equal(gu, wu), f"U row {s}"
+
+
+def assert_supernodes_consistent(got, chunk=128):
+    """Oracle's greedy Def. def:T3 scan on the GPU's rows == GPU sn_start."""
+    sn = oracle.supernodes(got["row_begin"], got["L_rowptr"], got["L_colidx"], got["U_rowptr"], chunk)
+    assert np.array_equal(sn, got["sn_start"])
+    assert got["nsuper"] == sn.size - 1
+
+
+def sample_rows(n, rb=0, re=None, k=160, top=96, seed=0):
+    re = n if re is None else re
+    rng = np.random.default_rng(seed)
+    rows = set(rng.integers(rb, re, size=k).tolist())
+    rows |= set(range(max(rb, re - top), re))
+    rows |= {rb, re - 1}
+    return np.array(sorted(rows), dtype=np.int64)
+
+
+# ------------------------------------------------------------ small / exact --
+
+@pytest.mark.parametrize("schedule", ["threshold", "fifo"])
+def test_paper_example(ctx, schedule):
+    rp, ci = gen.paper_example()
+    assert_full_equal(run(rp, ci, ctx, schedule=schedule), oracle.symbolic(rp, ci))
+
+
+@pytest.mark.parametrize("schedule", ["threshold", "fifo"])
+@pytest.mark.parametrize("seed", range(40))
+def test_random_graphs(ctx, seed, schedule):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 300))
+    rp, ci = gen.random_graph(n, float(rng.uniform(0.005, 0.2)), seed=100 + seed)
+    chunk = int(rng.choice([1, 3, 16, 128]))
+    got = run(rp, ci, ctx, chunk_size=chunk, fill_first=bool(seed & 1),
+              max_concurrent=int(rng.choice([0, 32, 64])), schedule=schedule)
+    assert_full_equal(got, oracle.symbolic(rp, ci, chunk_size=chunk))
+
+
+@pytest.mark.parametrize("name,scale", [("C1", None), ("C2", 12), ("C2", 24), ("C3", 3000),
+                                        ("C4", 60), ("C5", 16)])
+def test_config_shapes_full(ctx, name, scale):
+    rp, ci = gen.config(name, scale)
+    want = oracle.symbolic(rp, ci)
+    for kw in (dict(), dict(max_concurrent=32), dict(schedule="fifo"),
+               dict(schedule="fifo", fill_first=True, max_concurrent=96)):
+        assert_full_equal(run(rp, ci, ctx, **kw), want)
+
+
+@pytest.mark.parametrize("schedule", ["threshold", "fifo"])
+def test_C3_full(ctx, schedule):
+    rp, ci = gen.config("C3")
+    got = run(rp, ci, ctx, schedule=schedule)
+    assert_full_equal(got, oracle.symbolic(rp, ci))
+
+
+# ------------------------------------------------------ options / boundary --
+
+def test_row_ranges_and_devices(ctx):
+    torch = pytest.importorskip("torch")
+    rp, ci = gen.config("C5", 14)
+    n = rp.size - 1
+    full = oracle.symbolic(rp, ci)
+    # device inputs, device outputs
+    got = run(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(), ctx, outputs_on_device=True)
+    assert_full_equal(got, full)
+    # chunk-aligned row ranges reproduce the slices of the full result
+    for rb, re in [(0, 128), (128, 1280), (1280, n)]:
+        part = run(rp, ci, ctx, row_begin=rb, row_end=re)
+        want = oracle.symbolic(rp, ci, row_begin=rb, row_end=re)
+        assert_full_equal(part, want)
+
+
+def test_input_diagonal_ignored(ctx):
+    rp, ci = gen.random_graph(200, 0.03, seed=5)
+    n = rp.size - 1
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    key = np.unique(np.concatenate([rows * n + ci, np.arange(n) * n + np.arange(n)]))
+    rp2 = np.concatenate([[0], np.cumsum(np.bincount(key // n, minlength=n))]).astype(np.int64)
+    ci2 = (key % n).astype(np.int32)
+    assert_full_equal(run(rp2, ci2, ctx), oracle.symbolic(rp, ci))
+
+
+def test_empty_and_tiny(ctx):
+    for n in (1, 2, 33):
+        rp = np.zeros(n + 1, np.int64)
+        ci = np.zeros(0, np.int32)
+        got = run(rp, ci, ctx)
+        assert got["nnz_L"] == 0 and got["nnz_U"] == n and got["fill_count"] == 0
+        assert np.array_equal(got["U_colidx"], np.arange(n, dtype=np.int32))
+
+
+@pytest.mark.parametrize("schedule", ["threshold", "fifo"])
+def test_budget_batches_and_epoch_wrap(ctx, schedule):
+    """n = 2^24 with structure on the first 9,600 vertices and 32-source
+    batches: 300 batches of epoch width n+2 wrap the 32-bit maxId range
+    (floor(2^32 / (n+2)) = 255 epochs), forcing the re-initialisation path of
+    P:573-574.  Output must not change."""
+    n_act, n = 9600, 1 << 24
+    rp0, ci0 = gen.random_graph(400, 0.01, seed=3)
+    rows = []
+    cols = []
+    rng = np.random.default_rng(4)
+    src = rng.integers(0, n_act, size=60000)
+    dst = np.clip(src + rng.integers(-300, 300, size=src.size), 0, n_act - 1)
+    rp, ci = gen.csr_from_edges(n, src, dst)
+    got = run(rp, ci, ctx, row_end=n_act, max_concurrent=32, schedule=schedule)
+    assert got["stats"]["batches"] == n_act // 32
+    want = oracle.symbolic(rp, ci, row_end=n_act)
+    assert_full_equal(got, want)
+
+
+@pytest.mark.parametrize("schedule", ["threshold", "fifo"])
+def test_tight_budget_same_result(schedule):
+    rp, ci = gen.config("C2", 20)
+    want = oracle.symbolic(rp, ci)
+    with g.Context(0, mem_budget_bytes=24 << 20) as c:
+        got = run(rp, ci, c, schedule=schedule)
+    assert got["stats"]["batches"] > 1
+    assert_full_equal(got, want)
+
+
+def test_errors():
+    rp, ci = gen.random_graph(50, 0.1, seed=1)
+    bad = ci.copy()
+    bad[3] = 1000
+    with pytest.raises(g.GsofaError) as e:
+        g.symbolic(rp, bad)
+    assert e.value.code == -2
+    unsorted = ci.copy()
+    unsorted[rp[10]:rp[11]] = unsorted[rp[10]:rp[11]][::-1]
+    if rp[11] - rp[10] > 1:
+        with pytest.raises(g.GsofaError) as e:
+            g.symbolic(rp, unsorted)
+        assert e.value.code == -2
+    with pytest.raises(g.GsofaError) as e:
+        g.symbolic(rp, ci, row_begin=5)
+    assert e.value.code == -1
+    with pytest.raises(g.GsofaError) as e:
+        g.symbolic(rp, ci, max_concurrent=33)
+    assert e.value.code == -1
+    with pytest.raises(g.GsofaError) as e:
+        g.symbolic(rp, ci, mem_budget_bytes=1024)
+    assert e.value.code == -4
+    with pytest.raises(KeyError):
+        g.symbolic(rp, ci, schedule="bogus")
+
+
+# --------------------------------------------------- full BASELINE configs --
+
+@pytest.mark.parametrize("name", ["C2", "C4", "C5"])
+def test_full_config_sampled(ctx, name):
+    rp, ci = gen.config(name)
+    n = rp.size - 1
+    got = run(rp, ci, ctx)
+    # counts and shapes
+    assert got["L_rowptr"][-1] == got["nnz_L"] and got["U_rowptr"][-1] == got["nnz_U"]
+    assert got["fill_count"] == got["nnz_L"] + got["nnz_U"] - n - got["nnz_A_offdiag"]
+    assert got["nnz_A_offdiag"] == ci.size
+    assert_rows_equal(got, rp, ci, sample_rows(n, k=96, top=32 if name == "C5" else 64))
+    assert_supernodes_consistent(got)
