@@ -74,8 +74,12 @@ struct gsofa_context {
   int64_t key_n = -1;
   int64_t Cmax = 0, Gmax = 0;
   int gbits = 0;
-  size_t work_bytes = 0;
+  size_t work_bytes = 0, is_words = 0;
   int work_state = 0;        // WorkState
+  uint64_t layout_sig = 0;   // streaming slot layout of the last call (Vmax, ws_words)
+  int stream_blocks = 0;     // resident CTAs of the streaming kernel
+  int32_t *stage = nullptr;  // staging area for streamed rows (grow-only)
+  size_t stage_cap = 0;
   uint32_t *work = nullptr, *is = nullptr;
   uint32_t *cntL = nullptr, *cntU = nullptr;
   int64_t *rowL = nullptr, *rowU = nullptr, *totals = nullptr;
@@ -107,6 +111,9 @@ struct Plan {
   size_t work_bytes, is_words, cnt_words;
   int64_t nsub;
   size_t total;
+  // streaming (threshold) schedule
+  int64_t slots = 0, Vmax = 0;
+  size_t ws_words = 0, slot_is_words = 0;
 };
 
 size_t small_bytes(int64_t Cmax) {
@@ -121,7 +128,7 @@ size_t small_bytes(int64_t Cmax) {
 size_t work_need(int schedule, int64_t C, int64_t Vb) {
   const int64_t G = C / 32;
   if (schedule == GSOFA_SCHEDULE_FIFO) return (size_t)C * Vb * 4 + (size_t)G * Vb * 16;
-  return (size_t)G * gsofa::threshold_ws_words(Vb) * 4;
+  return (size_t)G * gsofa::stream_ws_words(Vb) * 4;
 }
 
 // FIFO keeps its label region apart from masks/queues so that every label
@@ -161,6 +168,36 @@ bool make_plan(int schedule, int64_t n, int64_t rows, int64_t vb_max, int64_t cm
   return false;
 }
 
+// Streaming schedule: one workspace slot per resident CTA, each slot holding
+// one 32-source group at a time: reached/pend/lists over Vmax vertices (bubble
+// removal: no maxId state above the largest source) plus an n-word
+// structure bitmap.  The number of slots is what the budget allows
+// ("reduce the number of concurrent sources"), at most the resident
+// CTA count and the number of groups.
+bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int64_t max_resident,
+                      Plan &p) {
+  const size_t ws = gsofa::stream_ws_words(Vmax), isw = gsofa::stream_is_words(n);
+  const size_t per_slot = (ws + isw) * 4;
+  const size_t fixed = small_bytes(32) + 8192;
+  if (budget <= (int64_t)(fixed + per_slot)) return false;
+  int64_t slots = (int64_t)(((size_t)budget - fixed) / per_slot);
+  slots = std::min<int64_t>(slots, std::min<int64_t>(max_resident, ceil_div(rows, 32)));
+  if (slots < 1) return false;
+  p.Cmax = 32;
+  p.Gmax = 1;
+  p.gbits = 0;
+  p.slots = slots;
+  p.Vmax = Vmax;
+  p.ws_words = ws;
+  p.slot_is_words = isw;
+  p.work_bytes = (size_t)slots * ws * 4;
+  p.is_words = (size_t)slots * isw;
+  p.cnt_words = 0;
+  p.nsub = 0;
+  p.total = p.work_bytes + p.is_words * 4 + small_bytes(32) + 4096 + 12 * 256;
+  return true;
+}
+
 // largest multiple of 32 <= cap whose working set fits `work` bytes
 int64_t fit_batch(int schedule, int64_t n, int64_t s0, int64_t cap, size_t work) {
   int64_t lo = 0, hi = cap / 32;  // in groups
@@ -183,7 +220,9 @@ enum WorkState { kWorkZero = 0, kWorkFifo = 1, kWorkDirty = 2 };
 
 int ensure_arena(gsofa_context *c, int64_t n, const Plan &p, cudaStream_t st) {
   int rc = GSOFA_OK;
-  if (c->arena && c->key_n == n && c->Cmax == p.Cmax && c->work_bytes == p.work_bytes) return rc;
+  if (c->arena && c->key_n == n && c->Cmax == p.Cmax && c->work_bytes == p.work_bytes &&
+      c->is_words == p.is_words)
+    return rc;
   release_arena(c);
   {
     cudaError_t e = cudaMalloc((void **)&c->arena, p.total);
@@ -218,7 +257,9 @@ int ensure_arena(gsofa_context *c, int64_t n, const Plan &p, cudaStream_t st) {
   c->Gmax = p.Gmax;
   c->gbits = p.gbits;
   c->work_bytes = p.work_bytes;
+  c->is_words = p.is_words;
   c->nsub = p.nsub;
+  c->layout_sig = 0;
   CK(cudaMemsetAsync(c->work, 0, p.work_bytes, st));
   CK(cudaMemsetAsync(c->is, 0, p.is_words * 4, st));
   c->work_state = kWorkZero;
@@ -353,9 +394,10 @@ int gsofa_context_create(int32_t device, int64_t mem_budget_bytes, gsofa_context
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
+  c->stream_blocks = gsofa::stream_max_blocks(device);
   c->max_blocks[0] = gsofa::traverse_max_blocks(device, 0);
   c->max_blocks[1] = gsofa::traverse_max_blocks(device, 1);
-  if (c->max_blocks[0] <= 0 || c->max_blocks[1] <= 0) {
+  if (c->max_blocks[0] <= 0 || c->max_blocks[1] <= 0 || c->stream_blocks <= 0) {
     cudaFreeHost(c->h_small);
     cudaStreamDestroy(c->stream);
     delete c;
@@ -374,6 +416,7 @@ void gsofa_context_destroy(gsofa_context *c) {
   if (c->in_rowptr) cudaFree(c->in_rowptr);
   if (c->in_colidx) cudaFree(c->in_colidx);
   if (c->rowptr32) cudaFree(c->rowptr32);
+  if (c->stage) cudaFree(c->stage);
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -462,6 +505,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   size_t Lcap = 0, Ucap = 0;
   int32_t *sn_scratch = nullptr;
   void *scan_tmp = nullptr;
+  void *stream_scratch = nullptr;
   std::vector<cudaEvent_t> evs;
   int64_t launches = 0;
   auto ev = [&]() {
@@ -523,7 +567,11 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     int64_t budget = o.mem_budget_bytes ? o.mem_budget_bytes : c->budget;
     if (!budget) budget = auto_budget(c->device) + (int64_t)c->arena_bytes;
     const int64_t vb_max = std::min<int64_t>(n, re + 32);
-    if (!make_plan(o.schedule, n, rows, vb_max, cmax_req, budget, plan)) {
+    const bool ok = o.schedule == GSOFA_SCHEDULE_FIFO
+                        ? make_plan(o.schedule, n, rows, vb_max, cmax_req, budget, plan)
+                        : make_plan_stream(n, rows, std::min<int64_t>(n, re), budget,
+                                           c->stream_blocks, plan);
+    if (!ok) {
       set_detail("budget %lld B cannot hold one 32-source group for n=%lld", (long long)budget,
                  (long long)n);
       rc = GSOFA_EINFEASIBLE;
@@ -531,6 +579,13 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     }
   }
   if ((rc = ensure_arena(c, n, plan, st)) != GSOFA_OK) goto fail;
+  if (o.schedule != GSOFA_SCHEDULE_FIFO) {
+    // the slot layout (Vmax, ws_words) moved: list garbage could now sit
+    // under state words, so start from an all-zero work region
+    const uint64_t sig = ((uint64_t)plan.Vmax << 32) ^ (uint64_t)plan.ws_words;
+    if (c->layout_sig != sig && c->work_state == kWorkZero && c->layout_sig != 0) c->work_state = kWorkDirty;
+    c->layout_sig = sig;
+  }
   if ((rc = prepare_work(c, o.schedule, st)) != GSOFA_OK) goto fail;
   // validate (GSOFA_EBADCSR) and narrow row pointers to int32
   CK(cudaMemsetAsync(c->err, 0, sizeof(int), st));
@@ -558,12 +613,134 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     }
     CK(cudaMemsetAsync(Lrp, 0, sizeof(int64_t), st));
     CK(cudaMemsetAsync(Urp, 0, sizeof(int64_t), st));
-    const size_t guess = (size_t)std::max<int64_t>(1024, 4 * (nnz + n) * rows / n);
-    if ((rc = grow_device(&Lci, &Lcap, guess, st)) != GSOFA_OK) goto fail;
-    if ((rc = grow_device(&Uci, &Ucap, guess, st)) != GSOFA_OK) goto fail;
+    if (o.schedule == GSOFA_SCHEDULE_FIFO) {
+      const size_t guess = (size_t)std::max<int64_t>(1024, 4 * (nnz + n) * rows / n);
+      if ((rc = grow_device(&Lci, &Lcap, guess, st)) != GSOFA_OK) goto fail;
+      if ((rc = grow_device(&Uci, &Ucap, guess, st)) != GSOFA_OK) goto fail;
+    }
   }
-  // ---------------------------------------------------- batches
-  for (int64_t s0 = rb; s0 < re;) {
+  if (o.schedule != GSOFA_SCHEDULE_FIFO) {
+    // ---------------------------------------------- streaming threshold schedule
+    const int64_t ngroups = ceil_div(rows, 32);
+    int64_t *row_off = nullptr;
+    int32_t *row_nL = nullptr, *row_nU = nullptr, *failed = nullptr, *grp = nullptr;
+    {
+      cudaError_t e1 = cudaMallocAsync((void **)&stream_scratch,
+                                       (size_t)rows * 16 + (size_t)ngroups * 8 + 256, st);
+      if (e1 != cudaSuccess) {
+        cudaGetLastError();
+        set_detail("row scratch allocation failed");
+        rc = GSOFA_ENOMEM;
+        goto fail;
+      }
+      char *q = (char *)stream_scratch;
+      row_off = (int64_t *)q;
+      row_nL = (int32_t *)(q + (size_t)rows * 8);
+      row_nU = row_nL + rows;
+      failed = row_nU + rows;
+      grp = failed + ngroups;
+    }
+    if (c->stage_cap == 0) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      const size_t want = std::max<size_t>((size_t)1 << 24, (size_t)(fr * 0.3) / 4);
+      if ((rc = grow_device(&c->stage, &c->stage_cap, want, st)) != GSOFA_OK) goto fail;
+    }
+    unsigned int *group_ctr = c->qcount;
+    int32_t *nfailed = (int32_t *)(c->qcount + 1);
+    unsigned long long *cursor = (unsigned long long *)c->totals;
+    unsigned long long *failed_need = cursor + 1;
+    CK(cudaMemsetAsync(c->qcount, 0, 16, st));
+    CK(cudaMemsetAsync(c->totals, 0, 16, st));
+    gsofa::StreamParams sp;
+    sp.rowptr = c->rowptr32;
+    sp.colidx = d_colidx;
+    sp.n = (int32_t)n;
+    sp.row_begin = (int32_t)rb;
+    sp.row_end = (int32_t)re;
+    sp.ngroups = (int32_t)ngroups;
+    sp.Vmax = (int32_t)plan.Vmax;
+    sp.ws = c->work;
+    sp.ws_words = plan.ws_words;
+    sp.is = c->is;
+    sp.is_words = plan.slot_is_words;
+    sp.group_ctr = group_ctr;
+    sp.group_list = nullptr;
+    sp.list_len = 0;
+    sp.stage = c->stage;
+    sp.stage_cap = c->stage_cap;
+    sp.stage_cursor = cursor;
+    sp.row_off = row_off;
+    sp.row_nL = row_nL;
+    sp.row_nU = row_nU;
+    sp.failed = failed;
+    sp.nfailed = nfailed;
+    sp.failed_need = failed_need;
+    sp.stats = c->stats;
+    int64_t grid = std::min<int64_t>(plan.slots, ngroups);
+    for (int pass = 0;; ++pass) {
+      const int et0 = ev();
+      CK(gsofa::launch_stream(sp, (int)grid, st));
+      ++launches;
+      e_trav.push_back({et0, ev()});
+      CK(cudaMemcpyAsync(c->h_small, c->totals, 16, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(c->h_small + 2, c->qcount, 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      const unsigned long long used = (unsigned long long)c->h_small[0];
+      const unsigned long long need = (unsigned long long)c->h_small[1];
+      const int nf = (int)((uint32_t)(c->h_small[2] >> 32));
+      if (nf == 0) break;
+      if (pass > 4) {
+        set_detail("staging retries did not converge");
+        rc = GSOFA_EINTERNAL;
+        goto fail;
+      }
+      // rows of nf groups did not fit: grow the staging area (keeping what is
+      // there) and re-run just those groups
+      if ((rc = grow_device(&c->stage, &c->stage_cap, (size_t)(used + need + (need >> 3) + 1024),
+                            st)) != GSOFA_OK)
+        goto fail;
+      CK(cudaMemcpyAsync(grp, failed, (size_t)nf * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemsetAsync(c->qcount, 0, 8, st));
+      CK(cudaMemsetAsync(failed_need, 0, 8, st));
+      sp.stage = c->stage;
+      sp.stage_cap = c->stage_cap;
+      sp.group_list = grp;
+      sp.list_len = nf;
+      grid = std::min<int64_t>(plan.slots, nf);
+    }
+    // row pointers (int64: C5 has > 2^31 entries) and the final CSR gather
+    {
+      const int ex0 = ev();
+      const size_t tmpb = gsofa::scan_tmp_bytes(rows);
+      cudaError_t e1 = cudaMallocAsync(&scan_tmp, tmpb, st);
+      if (e1 != cudaSuccess) {
+        cudaGetLastError();
+        set_detail("scan scratch allocation failed");
+        rc = GSOFA_ENOMEM;
+        goto fail;
+      }
+      CK(gsofa::scan_exclusive_i32_i64(row_nL, Lrp, rows, Lrp + rows, scan_tmp, tmpb, st));
+      CK(gsofa::scan_exclusive_i32_i64(row_nU, Urp, rows, Urp + rows, scan_tmp, tmpb, st));
+      launches += 4;
+      CK(cudaMemcpyAsync(c->h_small, Lrp + rows, 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(c->h_small + 1, Urp + rows, 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      baseL = c->h_small[0];
+      baseU = c->h_small[1];
+      if ((rc = grow_device(&Lci, &Lcap, (size_t)std::max<int64_t>(baseL, 1), st)) != GSOFA_OK) goto fail;
+      if ((rc = grow_device(&Uci, &Ucap, (size_t)std::max<int64_t>(baseU, 1), st)) != GSOFA_OK) goto fail;
+      CK(gsofa::launch_gather(c->stage, row_off, row_nL, Lrp, Urp, (int)rows, Lci, Uci, st));
+      ++launches;
+      e_ext.push_back({ex0, ev()});
+      cudaFreeAsync(scan_tmp, st);
+      scan_tmp = nullptr;
+    }
+    nbatches = 1;
+    maxC = 32 * std::min<int64_t>(plan.slots, ngroups);
+  }
+  // ---------------------------------------------------- batches (FIFO)
+  for (int64_t s0 = rb; o.schedule == GSOFA_SCHEDULE_FIFO && s0 < re;) {
     // #C for this batch: the largest multiple of 32 whose bubble-removed
     // working set fits the work region ("dynamic space allocation",
     // P:768-778; "reduce the number of concurrent sources")
@@ -613,21 +790,6 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       CK(gsofa::launch_seed(bp, st));
       CK(gsofa::launch_traverse(bp, o.fill_first ? 1 : 0, c->max_blocks[o.fill_first ? 1 : 0], st));
       launches += 2;
-    } else {
-      gsofa::ThrParams tp;
-      tp.rowptr = c->rowptr32;
-      tp.colidx = d_colidx;
-      tp.n = (int32_t)n;
-      tp.s0 = (int32_t)s0;
-      tp.s_end = s_end;
-      tp.G = (int32_t)G;
-      tp.Vb = (int32_t)vb;
-      tp.ws = c->work;
-      tp.ws_words = gsofa::threshold_ws_words(vb);
-      tp.is = c->is;
-      tp.stats = c->stats;
-      CK(gsofa::launch_threshold(tp, st));
-      ++launches;
     }
     const int et1 = ev();
     e_trav.push_back({et0, et1});
@@ -784,6 +946,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   }
   if (sn_scratch) cudaFreeAsync(sn_scratch, st);
   if (scan_tmp) cudaFreeAsync(scan_tmp, st);
+  if (stream_scratch) cudaFreeAsync(stream_scratch, st);
   if (Lrp) cudaFreeAsync(Lrp, st);
   if (Urp) cudaFreeAsync(Urp, st);
   if (Lci) cudaFreeAsync(Lci, st);
@@ -800,6 +963,7 @@ fail:
   cudaGetLastError();
   if (sn_scratch) cudaFree(sn_scratch);
   if (scan_tmp) cudaFree(scan_tmp);
+  if (stream_scratch) cudaFree(stream_scratch);
   if (Lrp) cudaFree(Lrp);
   if (Urp) cudaFree(Urp);
   if (Lci) cudaFree(Lci);

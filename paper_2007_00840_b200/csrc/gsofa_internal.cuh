@@ -52,18 +52,36 @@ cudaError_t launch_traverse(const BatchParams &p, int fill_first, int grid_block
                             cudaStream_t st);
 int traverse_max_blocks(int device, int fill_first);
 
-// threshold.cu (default schedule: increasing newMaxId, one CTA per group)
-struct ThrParams {
+// threshold.cu (default schedule: increasing newMaxId, persistent streaming
+// kernel, one 32-source group at a time per CTA)
+struct StreamParams {
   const int32_t *rowptr;
   const int32_t *colidx;
-  int32_t n, s0, s_end, G, Vb;
-  uint32_t *ws;            // [G][ws_words] per-group workspace
+  int32_t n, row_begin, row_end, ngroups, Vmax;
+  uint32_t *ws;              // [slots][ws_words]
   size_t ws_words;
-  uint32_t *is;            // [G][n]
-  unsigned long long *stats;  // [4]: items, edge inspections, levels, thresholds
+  uint32_t *is;              // [slots][is_words]: is[n] | isum[n/1024]
+  size_t is_words;
+  unsigned int *group_ctr;   // next group (global counter)
+  const int32_t *group_list; // optional explicit group ids (retry pass)
+  int32_t list_len;
+  int32_t *stage;            // staged rows: [L entries | diag | U entries]
+  unsigned long long stage_cap;
+  unsigned long long *stage_cursor;
+  int64_t *row_off;          // [rows] staging offset (-1: not staged)
+  int32_t *row_nL, *row_nU;  // [rows] counts (nU includes the diagonal)
+  int32_t *failed;           // groups whose rows did not fit the staging area
+  int32_t *nfailed;
+  unsigned long long *failed_need;
+  unsigned long long *stats; // items, edges, levels, thresholds, pairs
 };
-size_t threshold_ws_words(int64_t Vb);
-cudaError_t launch_threshold(const ThrParams &p, cudaStream_t st);
+size_t stream_ws_words(int64_t Vmax);
+size_t stream_is_words(int64_t n);
+int stream_max_blocks(int device);
+cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st);
+cudaError_t launch_gather(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,
+                          const int64_t *L_rowptr, const int64_t *U_rowptr, int rows,
+                          int32_t *L_out, int32_t *U_out, cudaStream_t st);
 
 // extract.cu
 struct ExtractParams {
@@ -91,10 +109,12 @@ cudaError_t launch_count_offdiag(const int32_t *rowptr, const int32_t *colidx, i
 cudaError_t launch_supernode_flags(const int64_t *L_rowptr, const int32_t *L_colidx,
                                    const int64_t *U_rowptr, int32_t row_begin, int32_t row_end,
                                    int32_t chunk, int32_t *flags, cudaStream_t st);
-// exclusive scan of int32 flags (count) into int32 positions; total -> *total
+// exclusive scans (int32 -> int32 / int32 -> int64); total -> *total
 cudaError_t scan_exclusive_i32(const int32_t *in, int32_t *out, int64_t count, int32_t *total,
                                void *tmp, size_t tmp_bytes, cudaStream_t st);
-size_t scan_tmp_bytes(int64_t count);
+cudaError_t scan_exclusive_i32_i64(const int32_t *in, int64_t *out, int64_t count, int64_t *total,
+                                   void *tmp, size_t tmp_bytes, cudaStream_t st);
+size_t scan_tmp_bytes(int64_t count);  // enough for either scan
 cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, int32_t row_begin,
                                      int32_t row_end, const int32_t *total, int32_t *sn_start,
                                      cudaStream_t st);

@@ -121,41 +121,42 @@ __global__ void sn_scatter_kernel(const int32_t *flags, const int32_t *pos, int3
   if (flags[k]) sn_start[pos[k]] = s;
 }
 
-// ---- exclusive scan (int32), 4096 items per block, recursive on block sums
+// ---- exclusive scan, 4096 items per block, recursive on block sums
 constexpr int kScanThreads = 1024, kScanItems = 4;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-__global__ void __launch_bounds__(kScanThreads) scan_tile_kernel(const int32_t *in, int32_t *out,
-                                                                 int64_t count, int32_t *sums) {
-  __shared__ int32_t ws[32];
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(kScanThreads) scan_tile_kernel(const Tin *in, Tout *out,
+                                                                 int64_t count, Tout *sums) {
+  __shared__ Tout ws[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)tid * kScanItems;
-  int32_t v[kScanItems];
-  int32_t t = 0;
+  Tout v[kScanItems];
+  Tout t = 0;
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
-    v[i] = (base + i < count) ? in[base + i] : 0;
+    v[i] = (base + i < count) ? (Tout)in[base + i] : (Tout)0;
     t += v[i];
   }
-  int32_t x = t;
+  Tout x = t;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    const int32_t y = __shfl_up_sync(kFull, x, d);
+    const Tout y = __shfl_up_sync(kFull, x, d);
     if (lane >= d) x += y;
   }
   if (lane == 31) ws[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    int32_t z = ws[lane];
+    Tout z = ws[lane];
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const int32_t y = __shfl_up_sync(kFull, z, d);
+      const Tout y = __shfl_up_sync(kFull, z, d);
       if (lane >= d) z += y;
     }
     ws[lane] = z;
   }
   __syncthreads();
-  int32_t run = x - t + (wid ? ws[wid - 1] : 0);
+  Tout run = x - t + (wid ? ws[wid - 1] : (Tout)0);
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     if (base + i < count) out[base + i] = run;
@@ -164,23 +165,25 @@ __global__ void __launch_bounds__(kScanThreads) scan_tile_kernel(const int32_t *
   if (tid == kScanThreads - 1) sums[blockIdx.x] = run;
 }
 
-__global__ void scan_add_kernel(int32_t *out, int64_t count, const int32_t *offs) {
+template <typename T>
+__global__ void scan_add_kernel(T *out, int64_t count, const T *offs) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) out[i] += offs[i / kScanTile];
 }
 
-cudaError_t scan_rec(const int32_t *in, int32_t *out, int64_t count, int32_t *total, int32_t *tmp,
+template <typename Tin, typename Tout>
+cudaError_t scan_rec(const Tin *in, Tout *out, int64_t count, Tout *total, Tout *tmp,
                      cudaStream_t st) {
   const int64_t nb = (count + kScanTile - 1) / kScanTile;
-  int32_t *sums = tmp, *sums_scan = tmp + nb;
-  scan_tile_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, count, sums);
+  Tout *sums = tmp, *sums_scan = tmp + nb;
+  scan_tile_kernel<Tin, Tout><<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, count, sums);
   if (nb == 1) {
-    cudaMemcpyAsync(total, sums, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(total, sums, sizeof(Tout), cudaMemcpyDeviceToDevice, st);
     return cudaGetLastError();
   }
-  cudaError_t e = scan_rec(sums, sums_scan, nb, total, tmp + 2 * nb, st);
+  cudaError_t e = scan_rec<Tout, Tout>(sums, sums_scan, nb, total, tmp + 2 * nb, st);
   if (e != cudaSuccess) return e;
-  scan_add_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(out, count, sums_scan);
+  scan_add_kernel<Tout><<<(unsigned)((count + 255) / 256), 256, 0, st>>>(out, count, sums_scan);
   return cudaGetLastError();
 }
 }  // namespace
@@ -193,14 +196,21 @@ size_t scan_tmp_bytes(int64_t count) {
     tot += 2 * (size_t)nb;
     c = nb;
   } while (c > 1);
-  return (tot + 16) * sizeof(int32_t);
+  return (tot + 16) * sizeof(int64_t);
 }
 
 cudaError_t scan_exclusive_i32(const int32_t *in, int32_t *out, int64_t count, int32_t *total,
                                void *tmp, size_t tmp_bytes, cudaStream_t st) {
   if (count <= 0) return cudaMemsetAsync(total, 0, sizeof(int32_t), st);
   if (tmp_bytes < scan_tmp_bytes(count)) return cudaErrorInvalidValue;
-  return scan_rec(in, out, count, total, (int32_t *)tmp, st);
+  return scan_rec<int32_t, int32_t>(in, out, count, total, (int32_t *)tmp, st);
+}
+
+cudaError_t scan_exclusive_i32_i64(const int32_t *in, int64_t *out, int64_t count, int64_t *total,
+                                   void *tmp, size_t tmp_bytes, cudaStream_t st) {
+  if (count <= 0) return cudaMemsetAsync(total, 0, sizeof(int64_t), st);
+  if (tmp_bytes < scan_tmp_bytes(count)) return cudaErrorInvalidValue;
+  return scan_rec<int32_t, int64_t>(in, out, count, total, (int64_t *)tmp, st);
 }
 
 cudaError_t launch_validate(const int64_t *rowptr64, const int32_t *colidx, int64_t n,

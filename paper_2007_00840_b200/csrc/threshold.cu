@@ -1,40 +1,44 @@
 // threshold.cu -- the max-id relaxation (PAPER.md sec:parallel)
-// scheduled in increasing newMaxId order, one CTA per 32-source slot group.
+// scheduled in increasing newMaxId order, as ONE persistent streaming kernel:
+// each CTA owns a workspace slot and repeatedly takes the next 32-source
+// group (heaviest -- highest row ids -- first), traverses it,
+// extracts its 32 rows into a staging area and resets what it touched.
 //
-// Schedule: the paper relaxes all frontiers in
-// parallel and accepts revisits; fill2 processes thresholds one
-// at a time in increasing order and never revisits.  The relaxation is
-// confluent (any order reaches the same maxId fixpoint), so the order is a
-// scheduling choice.  On B200 the fine-grained parallelism comes from 32
-// sources per warp lane set and from thousands of independent slot groups,
-// not from relaxing one source out of order, so this kernel processes, per
-// group, the frontier items in increasing newMaxId = T ("Dijkstra order",
-// P:1038):
+// Schedule: the relaxation is confluent, so the order is a
+// scheduling choice.  Per group, frontier items are processed in increasing
+// newMaxId = T ("Dijkstra order"):
 //   * thresholds T are the vertices that entered the structure (direct
-//     neighbours get maxId = -1, R3, so newMaxId = max(-1, w) = w; fills get
-//     maxId < w so newMaxId = w), visited in increasing id via a bitmap scan;
-//   * the frontier of T is closed level by level (CTA barriers, no grid
-//     barriers): every vertex w < T it reaches gets maxId = T and continues
-//     with newMaxId = T; a vertex w > T (w < src) reached with T < w is a new
-//     fill (R4) and a future threshold; w > src is an entry of U.
-// In this order atomicMin(maxId(w), T) succeeds at most once per (source, w)
-// -- the first T that reaches w is its final maxId -- so the 32 labels of a
-// vertex collapse to one 32-bit "reached" mask and revisits vanish.
+//     neighbours get maxId -1 (R3), so newMaxId = max(-1, w) = w; fills get
+//     maxId < w so newMaxId = w);
+//   * the frontier of T is closed level by level with CTA barriers: every
+//     vertex w < T it reaches gets maxId = T and continues with newMaxId = T;
+//     a vertex T < w < src reached with T < w is a new fill (R4) and a later
+//     threshold; w > src is an entry of U.
+// In this order atomicMin(maxId(w), T) succeeds at most once per (source, w),
+// so the 32 labels of a vertex collapse to one 32-bit "reached" mask and
+// there are no revisits.
 //
-// Per group workspace (uint32 words): reached[Vb] | pend[Vb] | thr[Vb/32] |
-// list0[Vb] | list1[Vb];  is[g][n] is the in-structure bitmap of extract.cu.
+// Workspace slot (uint32 words, fixed layout per launch):
+//   state[2*Vmax]  reached | pend interleaved per vertex (one 32 B sector)
+//   thr[Vmax/32]   threshold bitmap          rsum[Vmax/1024] touched lines
+//   list0[Vmax], list1[Vmax]                 frontier lists of a closure
+//   is[n]          in-structure bits          isum[n/1024]   touched lines
+// All of it is zero between groups; a group clears only the 32-vertex lines
+// recorded in rsum/isum (first-touch tracking), never the whole slot.
+#include <climits>
+
 #include "gsofa_internal.cuh"
 
 namespace gsofa {
 
 namespace {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
-constexpr int kThrWarps = 4;
-constexpr int kThrThreads = kThrWarps * 32;
+constexpr int kWarps = 4;
+constexpr int kThreads = kWarps * 32;
 
 // lanes k (sources s0g + k) with source > w, resp. source < w
 __device__ __forceinline__ uint32_t lanes_above(int w, int s0g) {
-  const int d = w - s0g;  // lane index of w
+  const int d = w - s0g;
   if (d < 0) return kFull;
   if (d >= 31) return 0u;
   return kFull << (d + 1);
@@ -46,215 +50,427 @@ __device__ __forceinline__ uint32_t lanes_below(int w, int s0g) {
   return kFull >> (32 - d);
 }
 
-__global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThrParams p) {
-  const int g = blockIdx.x;
-  const int s0g = p.s0 + 32 * g;
-  if (s0g >= p.s_end) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nsrc = min(32, p.s_end - s0g);
-  const int Vb = p.Vb;
-  const int tbw = (Vb + 31) >> 5;
-  uint32_t *reached = p.ws + (size_t)g * p.ws_words;
-  uint32_t *pend = reached + Vb;
-  uint32_t *thr = pend + Vb;
-  uint32_t *list0 = thr + tbw;
-  uint32_t *list1 = list0 + Vb;
-  uint32_t *isg = p.is + (size_t)g * p.n;
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int j = 16 >> i;
+    const uint32_t m = masks[i];
+    const uint32_t y = __shfl_xor_sync(kFull, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
+
+struct Slot {
+  uint32_t *state, *thr, *rsum, *list0, *list1, *is, *isum;
+};
+
+// mark the 32-vertex line of v in a touched-line summary (returning atomic:
+// the summary is read by other warps of this CTA after a barrier)
+__device__ __forceinline__ uint32_t touch(uint32_t *sum, int v) {
+  return atomicOr(sum + (v >> 10), 1u << ((v >> 5) & 31));
+}
+
+// next set bit of thr strictly above T (warp-cooperative), INT_MAX if none
+__device__ __forceinline__ int scan_next(const uint32_t *thr, int tbw, int T, int lane) {
+  const int start = T + 1;
+  int wi = start >> 5;
+  bool first = true;
+  while (wi < tbw) {
+    const int idx = wi + lane;
+    uint32_t x = idx < tbw ? __ldcg(thr + idx) : 0u;
+    if (first && lane == 0) x &= kFull << (start & 31);
+    const uint32_t b = __ballot_sync(kFull, x != 0u);
+    if (b) {
+      const int l = __ffs(b) - 1;
+      const uint32_t xl = __shfl_sync(kFull, x, l);
+      return ((wi + l) << 5) + __ffs(xl) - 1;
+    }
+    wi += 32;
+    first = false;
+  }
+  return INT_MAX;
+}
+
+struct Counters {
+  unsigned long long items, edges, pairs, levels, steps;
+  uint32_t sink;
+};
+
+// Expand up to 32 frontier items (one per lane; u < 0 = none) of the closure
+// of threshold T.  Every item's newMaxId is T.  Pushes closure members into
+// `nq` (count *nqn), records new fills in thr / *minfill.
+__device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, int s0g, int T,
+                                       int u, uint32_t *nq, int *nqn, int *minfill, int lane,
+                                       Counters &c) {
   const int32_t *__restrict__ rowptr = p.rowptr;
   const int32_t *__restrict__ colidx = p.colidx;
-
-  __shared__ int s_T;
-  __shared__ int s_qn[2];
-  unsigned long long st_items = 0, st_edges = 0, st_pairs = 0, st_steps = 0, st_levels = 0;
-  // XOR of atomic return values: consuming them forces the returning form
-  // (ATOMG, the warp waits for completion at L2) instead of REDG.
-  uint32_t sink = 0u;
-
-  // ---- seed: out-neighbours of each source are in the
-  // structure; the smaller ones are reached with maxId -1 -> thresholds
-  for (int k = warp; k < nsrc; k += kThrWarps) {
-    const int s = s0g + k;
-    const uint32_t bit = 1u << k;
-    const int beg = rowptr[s], end = rowptr[s + 1];
-    for (int j = beg + lane; j < end; j += 32) {
-      const int w = colidx[j];
-      if (w == s) continue;
-      atomicOr(isg + w, bit);
-      if (w < s) {
-        sink ^= atomicOr(reached + w, bit) ^ atomicOr(pend + w, bit) ^
-                atomicOr(thr + (w >> 5), 1u << (w & 31));  // returning: see below
-      }
+  int beg = 0, deg = 0;
+  uint32_t mask = 0u;
+  if (u >= 0) {
+    mask = atomicExch(sl.state + 2 * u + 1, 0u);  // lanes that expand u (pend)
+    if (mask) {
+      beg = __ldg(rowptr + u);
+      deg = __ldg(rowptr + u + 1) - beg;
     }
   }
-  __syncthreads();
+  c.items += mask != 0u;
+  c.pairs += (unsigned long long)deg;
+  c.edges += (unsigned long long)__popc(mask) * (unsigned long long)deg;
+  // load-balanced expansion of the (item, neighbour) pairs over the lanes
+  int incl = deg;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const int total = __shfl_sync(kFull, incl, 31);
+  if (total == 0) return;
+  const int excl = incl - deg;
+  for (int f0 = 0; f0 < total; f0 += 32) {
+    const int f = f0 + lane;
+    int o = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const int cand = o + step;
+      const int e = __shfl_sync(kFull, excl, cand & 31);
+      if (cand < 32 && e <= f) o = cand;
+    }
+    const int ob = __shfl_sync(kFull, beg, o);
+    const int oe = __shfl_sync(kFull, excl, o);
+    const uint32_t om = __shfl_sync(kFull, mask, o);
+    bool push = false;
+    int w = 0;
+    if (f < total) {
+      w = __ldg(colidx + ob + (f - oe));
+      const uint32_t um = om & lanes_below(w, s0g);  // sources < w: U entry
+      const uint32_t lm = om & lanes_above(w, s0g);  // sources > w: maxId(w)
+      if (um && atomicOr(sl.is + w, um) == 0u) c.sink ^= touch(sl.isum, w);
+      if (lm) {
+        // atomicMin(maxId(w), T) succeeds exactly for the lanes that have not
+        // reached w yet (line 10)
+        const uint32_t old = atomicOr(sl.state + 2 * w, lm);
+        const uint32_t nw = lm & ~old;
+        if (old == 0u) c.sink ^= touch(sl.rsum, w);
+        if (nw) {
+          if (w > T) {
+            // newMaxId T < w: (src, w) is a fill of L (R4); w proposes
+            // newMaxId = w later, as a threshold
+            if (atomicOr(sl.is + w, nw) == 0u) c.sink ^= touch(sl.isum, w);
+            c.sink ^= atomicOr(sl.state + 2 * w + 1, nw) ^
+                      atomicOr(sl.thr + (w >> 5), 1u << (w & 31));
+            atomicMin(minfill, w);
+          } else {
+            // w < T: maxId(w) = T, not in the structure: continue with T
+            push = atomicOr(sl.state + 2 * w + 1, nw) == 0u;
+          }
+        }
+      }
+    }
+    const uint32_t pb = __ballot_sync(kFull, push);
+    if (pb) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(nqn, __popc(pb));
+      base = __shfl_sync(kFull, base, 0);
+      if (push) nq[base + __popc(pb & lanemask_lt())] = (uint32_t)w;
+    }
+  }
+}
 
-  int T = -1;
-  int scan_word = 0;  // thr words below scan_word are known empty
-  int max_list = 1;   // largest list length used (cleared at the end)
+__device__ __forceinline__ void split_masks(int d, uint32_t &lm, uint32_t &um) {
+  lm = d <= 0 ? 0u : (d >= 32 ? kFull : ((1u << d) - 1u));
+  um = d < 0 ? kFull : (d >= 31 ? 0u : (kFull << (d + 1)));
+}
+
+__global__ void __launch_bounds__(kThreads) stream_kernel(StreamParams p) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  const int n = p.n, Vmax = p.Vmax;
+  const int tbw_max = (Vmax + 31) >> 5;
+  const int rsw = (Vmax + 1023) >> 10;
+  const int isw = (n + 1023) >> 10;
+  Slot sl;
+  sl.state = p.ws + (size_t)blockIdx.x * p.ws_words;
+  sl.thr = sl.state + 2 * (size_t)Vmax;
+  sl.rsum = sl.thr + tbw_max;
+  sl.list0 = sl.rsum + rsw;
+  sl.list1 = sl.list0 + Vmax;
+  sl.is = p.is + (size_t)blockIdx.x * p.is_words;
+  sl.isum = sl.is + n;
+
+  __shared__ int s_g, s_qn[2], s_scan[3], s_minfill[3];
+  __shared__ uint32_t s_cnt[kWarps][2][32];
+  __shared__ long long s_rowoff[32];
+  __shared__ int s_nL[32];
+  __shared__ int s_ok;
+  Counters c = {0, 0, 0, 0, 0, 0u};
+
   for (;;) {
-    // ---- next threshold: smallest set bit of thr above T (warp 0)
-    if (warp == 0) {
-      int nt = -1;
-      const int start = T + 1;
-      int wi = max(scan_word, start >> 5);
-      bool first = true;
-      while (wi < tbw) {
-        const int idx = wi + lane;
-        uint32_t x = idx < tbw ? __ldcg(thr + idx) : 0u;
-        if (first && idx == (start >> 5)) x &= kFull << (start & 31);
-        const uint32_t b = __ballot_sync(kFull, x != 0u);
-        if (b) {
-          const int l = __ffs(b) - 1;
-          const uint32_t xl = __shfl_sync(kFull, x, l);
-          nt = ((wi + l) << 5) + __ffs(xl) - 1;
-          wi += l;
-          break;
-        }
-        wi += 32;
-        first = false;
-      }
-      if (lane == 0) {
-        s_T = nt;
-        if (nt >= 0) {
-          list0[0] = (uint32_t)nt;
-          s_qn[0] = 1;
-          s_qn[1] = 0;
-        }
-      }
-      scan_word = wi;
+    if (tid == 0) {
+      const int j = (int)atomicAdd(p.group_ctr, 1u);
+      const int total = p.group_list ? p.list_len : p.ngroups;
+      s_g = j < total ? (p.group_list ? p.group_list[j] : p.ngroups - 1 - j) : -1;
+      s_qn[0] = s_qn[1] = 0;
+      for (int i = 0; i < 3; ++i) s_scan[i] = s_minfill[i] = INT_MAX;
     }
     __syncthreads();
-    T = s_T;
-    if (T < 0) break;
-    ++st_steps;
-    // ---- close the frontier of T level by level (every item has newMaxId T)
-    for (int lvl = 0;; ++lvl) {
-      const int cur = lvl & 1, nxt = cur ^ 1;
-      const uint32_t *cq = cur ? list1 : list0;
-      uint32_t *nq = cur ? list0 : list1;
-      const int qn = s_qn[cur];
-      max_list = max(max_list, qn);
+    const int g = s_g;
+    if (g < 0) break;
+    const int s0g = p.row_begin + 32 * g;
+    const int nsrc = min(32, p.row_end - s0g);
+    const int Vb = min(n, s0g + nsrc);  // maxId only below the largest source
+    const int tbw = (Vb + 31) >> 5;
+
+    // ---- seed: out-neighbours of each source are in the
+    // structure; the smaller ones are reached with maxId -1 -> thresholds
+    for (int k = warp; k < nsrc; k += kWarps) {
+      const int s = s0g + k;
+      const uint32_t bit = 1u << k;
+      const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
+      for (int j = beg + lane; j < end; j += 32) {
+        const int w = __ldg(p.colidx + j);
+        if (w == s) continue;
+        if (atomicOr(sl.is + w, bit) == 0u) c.sink ^= touch(sl.isum, w);
+        if (w < s) {
+          if (atomicOr(sl.state + 2 * w, bit) == 0u) c.sink ^= touch(sl.rsum, w);
+          c.sink ^= atomicOr(sl.state + 2 * w + 1, bit) ^
+                    atomicOr(sl.thr + (w >> 5), 1u << (w & 31));
+        }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int t0 = scan_next(sl.thr, tbw, -1, lane);
+      if (lane == 0) s_scan[0] = t0;
+    }
+    __syncthreads();
+
+    // ---- thresholds in increasing order
+    for (int step = 0;; ++step) {
+      const int cur3 = step % 3, nx3 = (step + 1) % 3;
+      const int T = min(s_scan[cur3], s_minfill[cur3]);
+      if (T == INT_MAX) break;
+      c.steps += 1;
+      __syncthreads();  // all threads are done with the previous step's s_qn / T
+      if (tid == 0) {
+        s_scan[(step + 2) % 3] = INT_MAX;
+        s_minfill[(step + 2) % 3] = INT_MAX;
+      }
+      // level 0: warp 0 expands T itself; warp 1 finds the next threshold
+      // above T in parallel (new fills of this step go to s_minfill[nx3])
+      if (warp == 0) {
+        expand(p, sl, s0g, T, lane == 0 ? T : -1, sl.list1, &s_qn[1], &s_minfill[nx3], lane, c);
+      } else if (warp == 1) {
+        const int nt = scan_next(sl.thr, tbw, T, lane);
+        if (lane == 0) s_scan[nx3] = nt;
+      }
       __syncthreads();
-      if (threadIdx.x == 0) s_qn[cur] = 0;
-      ++st_levels;
-      for (int b0 = warp * 32; b0 < qn; b0 += kThrThreads) {
-        const int cnt = min(32, qn - b0);
-        int u = 0, beg = 0, deg = 0;
-        uint32_t mask = 0u;
-        if (lane < cnt) {
-          u = (int)cq[b0 + lane];
-          mask = atomicExch(pend + u, 0u);  // lanes that expand u with newMaxId T
-          if (mask) {
-            beg = rowptr[u];
-            deg = rowptr[u + 1] - beg;
-          }
+      c.levels += 1;
+      // closure levels: every item has newMaxId T
+      for (int lvl = 1;; ++lvl) {
+        const int cur = lvl & 1, nxt = cur ^ 1;
+        const int qn = s_qn[cur];
+        if (qn == 0) break;
+        const uint32_t *cq = cur ? sl.list1 : sl.list0;
+        uint32_t *nq = cur ? sl.list0 : sl.list1;
+        __syncthreads();
+        if (tid == 0) s_qn[cur] = 0;
+        c.levels += 1;
+        for (int b0 = warp * 32; b0 < qn; b0 += kThreads) {
+          const int u = (b0 + lane < qn) ? (int)cq[b0 + lane] : -1;
+          expand(p, sl, s0g, T, u, nq, &s_qn[nxt], &s_minfill[nx3], lane, c);
         }
-        // load-balanced expansion of the (item, neighbour) pairs over lanes
-        int incl = deg;
+        __syncthreads();
+      }
+    }
+
+    // ---- extraction of the group's rows (touched IS lines, ascending)
+    // warp w owns isum words [w*q, (w+1)*q): its lines are ascending and all
+    // of them precede warp w+1's, so per-warp counts give the write offsets
+    const int q = (isw + kWarps - 1) / kWarps;
+    const int wa = min(isw, warp * q), wb = min(isw, wa + q);
+    const int s_lane = s0g + lane;
+    uint32_t cl = 0, cu = 0;
+    for (int i = wa; i < wb; ++i) {
+      uint32_t x = __ldcg(sl.isum + i);
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1u;
+        const int v0 = ((i << 5) + b) << 5;
+        const uint32_t word = (v0 + lane < n) ? __ldcg(sl.is + v0 + lane) : 0u;
+        const uint32_t y = transpose32(word, lane);
+        uint32_t lm, um;
+        split_masks(s_lane - v0, lm, um);
+        cl += __popc(y & lm);
+        cu += __popc(y & um);
+      }
+    }
+    s_cnt[warp][0][lane] = cl;
+    s_cnt[warp][1][lane] = cu;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t nl = 0, nu = 0;
+      for (int w2 = 0; w2 < kWarps; ++w2) {
+        nl += s_cnt[w2][0][lane];
+        nu += s_cnt[w2][1][lane];
+      }
+      const bool valid = lane < nsrc;
+      if (valid) nu += 1;  // the diagonal
+      const long long sz = valid ? (long long)nl + nu : 0;
+      long long inc = sz;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int y = __shfl_up_sync(kFull, incl, d);
-          if (lane >= d) incl += y;
+      for (int d = 1; d < 32; d <<= 1) {
+        const long long y = __shfl_up_sync(kFull, inc, d);
+        if (lane >= d) inc += y;
+      }
+      const long long tot = __shfl_sync(kFull, inc, 31);
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(p.stage_cursor, (unsigned long long)tot);
+      base = __shfl_sync(kFull, base, 0);
+      const bool ok = base + (unsigned long long)tot <= p.stage_cap;
+      if (valid) {
+        const long long off = (long long)base + inc - sz;
+        s_rowoff[lane] = off;
+        s_nL[lane] = (int)nl;
+        const int r = s_lane - p.row_begin;
+        p.row_off[r] = ok ? off : -1;
+        p.row_nL[r] = (int)nl;
+        p.row_nU[r] = (int)nu;
+        if (ok) p.stage[off + nl] = s_lane;  // U(s,:) starts with the diagonal
+      }
+      if (lane == 0) {
+        s_ok = ok;
+        if (!ok) {
+          p.failed[atomicAdd(p.nfailed, 1)] = g;
+          atomicAdd(p.failed_need, (unsigned long long)tot);
         }
-        const int total = __shfl_sync(kFull, incl, 31);
-        const int excl = incl - deg;
-        st_items += mask != 0u;
-        st_pairs += (unsigned long long)deg;
-        st_edges += (unsigned long long)__popc(mask) * (unsigned long long)deg;
-        for (int f0 = 0; f0 < total; f0 += 32) {
-          const int f = f0 + lane;
-          int o = 0;
-#pragma unroll
-          for (int step = 16; step >= 1; step >>= 1) {
-            const int cand = o + step;
-            const int e = __shfl_sync(kFull, excl, cand & 31);
-            if (cand < 32 && e <= f) o = cand;
-          }
-          const int ob = __shfl_sync(kFull, beg, o);
-          const int oe = __shfl_sync(kFull, excl, o);
-          const uint32_t om = __shfl_sync(kFull, mask, o);
-          bool push = false;
-          int w = 0;
-          if (f < total) {
-            w = __ldg(colidx + ob + (f - oe));
-            const uint32_t um = om & lanes_below(w, s0g);   // sources < w: U entry
-            const uint32_t lm = om & lanes_above(w, s0g);   // sources > w: maxId(w)
-            if (um) atomicOr(isg + w, um);
-            if (lm) {
-              // atomicMin(maxId(w), T) succeeds exactly for the lanes that
-              // have not reached w yet (line 10)
-              const uint32_t nw = lm & ~atomicOr(reached + w, lm);
-              if (nw) {
-                if (w > T) {
-                  // newMaxId T < w: (src, w) is a fill of L (R4); w proposes
-                  // newMaxId = w later, as a threshold.  pend/thr are read by
-                  // other warps after the next barrier, so these are returning
-                  // atomics whose results are consumed here (a fire-and-forget
-                  // RED may still be in flight to L2 when the barrier opens).
-                  atomicOr(isg + w, nw);
-                  sink ^= atomicOr(pend + w, nw) ^ atomicOr(thr + (w >> 5), 1u << (w & 31));
-                } else {
-                  // w < T: maxId(w) = T, not in the structure, continue with T
-                  push = atomicOr(pend + w, nw) == 0u;
-                }
-              }
+      }
+    }
+    __syncthreads();
+    {
+      const bool ok = s_ok;
+      long long pl = 0, pu = 0;
+      for (int w2 = 0; w2 < warp; ++w2) {
+        pl += s_cnt[w2][0][lane];
+        pu += s_cnt[w2][1][lane];
+      }
+      const bool valid = lane < nsrc;
+      int32_t *Lp = p.stage + (valid && ok ? s_rowoff[lane] + pl : 0);
+      int32_t *Up = p.stage + (valid && ok ? s_rowoff[lane] + s_nL[lane] + 1 + pu : 0);
+      for (int i = wa; i < wb; ++i) {
+        uint32_t x = __ldcg(sl.isum + i);
+        if (!x) continue;
+        if (lane == 0) sl.isum[i] = 0u;
+        while (x) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1u;
+          const int v0 = ((i << 5) + b) << 5;
+          const uint32_t word = (v0 + lane < n) ? __ldcg(sl.is + v0 + lane) : 0u;
+          if (v0 + lane < n) sl.is[v0 + lane] = 0u;
+          const uint32_t y = transpose32(word, lane);
+          if (ok) {
+            uint32_t lm, um;
+            split_masks(s_lane - v0, lm, um);
+            uint32_t yl = y & lm, yu = y & um;
+            while (yl) {
+              *Lp++ = v0 + __ffs(yl) - 1;
+              yl &= yl - 1u;
             }
-          }
-          const uint32_t pb = __ballot_sync(kFull, push);
-          if (pb) {
-            int base = 0;
-            if (lane == 0) base = atomicAdd(&s_qn[nxt], __popc(pb));
-            base = __shfl_sync(kFull, base, 0);
-            if (push) nq[base + __popc(pb & lanemask_lt())] = (uint32_t)w;
+            while (yu) {
+              *Up++ = v0 + __ffs(yu) - 1;
+              yu &= yu - 1u;
+            }
           }
         }
       }
-      __syncthreads();
-      if (s_qn[nxt] == 0) break;
     }
-  }
-  // ---- reset the workspace: the next batch may lay groups out differently
-  // (Vb changes), so every word this group wrote must be zero again --
-  // reached and thr here, the used prefix of both lists, pend is already 0
-  {
-    for (int i = threadIdx.x; i < max_list; i += kThrThreads) {
-      list0[i] = 0u;
-      list1[i] = 0u;
+    // ---- reset the touched state lines (reached; pend is already 0) and thr
+    {
+      const int qr = (rsw + kWarps - 1) / kWarps;
+      const int ra = min(rsw, warp * qr), rb = min(rsw, ra + qr);
+      for (int i = ra; i < rb; ++i) {
+        uint32_t x = __ldcg(sl.rsum + i);
+        if (!x) continue;
+        if (lane == 0) sl.rsum[i] = 0u;
+        while (x) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1u;
+          const int line = (i << 5) + b;
+          reinterpret_cast<uint2 *>(sl.state)[(line << 5) + lane] = make_uint2(0u, 0u);
+          if (lane == 0) sl.thr[line] = 0u;
+        }
+      }
     }
-    uint4 *r4 = reinterpret_cast<uint4 *>(reached);
-    const int n4 = Vb >> 2;
-    for (int i = threadIdx.x; i < n4; i += kThrThreads) r4[i] = make_uint4(0u, 0u, 0u, 0u);
-    for (int i = (n4 << 2) + threadIdx.x; i < Vb; i += kThrThreads) reached[i] = 0u;
-    for (int i = threadIdx.x; i < tbw; i += kThrThreads) thr[i] = 0u;
+    // the clears above are plain stores; the next group's atomics on the same
+    // words are performed at L2, so make the stores globally visible first
+    __threadfence();
+    __syncthreads();
   }
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) {
-    st_items += __shfl_xor_sync(kFull, st_items, d);
-    st_edges += __shfl_xor_sync(kFull, st_edges, d);
-    st_pairs += __shfl_xor_sync(kFull, st_pairs, d);
+    c.items += __shfl_xor_sync(kFull, c.items, d);
+    c.edges += __shfl_xor_sync(kFull, c.edges, d);
+    c.pairs += __shfl_xor_sync(kFull, c.pairs, d);
   }
   if (lane == 0) {
-    atomicAdd(p.stats + 0, st_items);
-    atomicAdd(p.stats + 1, st_edges);
-    atomicAdd(p.stats + 4, st_pairs);
+    atomicAdd(p.stats + 0, c.items);
+    atomicAdd(p.stats + 1, c.edges);
+    atomicAdd(p.stats + 4, c.pairs);
   }
-  if (p.n < 0) p.stats[7] = sink;  // never true; keeps `sink` alive
-  if (threadIdx.x == 0) {
-    atomicAdd(p.stats + 2, st_levels);
-    atomicAdd(p.stats + 3, st_steps);
+  if (tid == 0) {
+    atomicAdd(p.stats + 2, c.levels);
+    atomicAdd(p.stats + 3, c.steps);
   }
+  if (p.n < 0) p.stats[7] = c.sink;  // never true; keeps the returning atomics
+}
+
+// copies each staged row into the final CSR arrays (warp per row)
+__global__ void gather_kernel(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,
+                              const int64_t *L_rowptr, const int64_t *U_rowptr, int rows,
+                              int32_t *L_out, int32_t *U_out) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int64_t off = row_off[r];
+  const int nl = row_nL[r];
+  const int64_t lo = L_rowptr[r], uo = U_rowptr[r];
+  const int nu = (int)(U_rowptr[r + 1] - uo);
+  for (int i = lane; i < nl; i += 32) L_out[lo + i] = stage[off + i];
+  for (int i = lane; i < nu; i += 32) U_out[uo + i] = stage[off + nl + i];
 }
 }  // namespace
 
-size_t threshold_ws_words(int64_t Vb) {
-  // reached + pend + list0 + list1 + thr, padded to 16 bytes
-  const size_t w = 4 * (size_t)Vb + (size_t)((Vb + 31) / 32);
-  return (w + 3) / 4 * 4;
+size_t stream_ws_words(int64_t Vmax) {
+  const size_t w = 2 * (size_t)Vmax + (size_t)((Vmax + 31) / 32) + (size_t)((Vmax + 1023) / 1024) +
+                   2 * (size_t)Vmax;
+  return (w + 7) / 8 * 8;
 }
 
-cudaError_t launch_threshold(const ThrParams &p, cudaStream_t st) {
-  if (p.s_end <= p.s0) return cudaSuccess;
-  threshold_kernel<<<p.G, kThrThreads, 0, st>>>(p);
+size_t stream_is_words(int64_t n) {
+  const size_t w = (size_t)n + (size_t)((n + 1023) / 1024);
+  return (w + 7) / 8 * 8;
+}
+
+int stream_max_blocks(int device) {
+  int sms = 0, per = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_kernel, kThreads, 0) != cudaSuccess)
+    return 0;
+  return sms * per;
+}
+
+cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st) {
+  if (grid <= 0) return cudaSuccess;
+  stream_kernel<<<grid, kThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,
+                          const int64_t *L_rowptr, const int64_t *U_rowptr, int rows,
+                          int32_t *L_out, int32_t *U_out, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  gather_kernel<<<(rows + 7) / 8, 256, 0, st>>>(stage, row_off, row_nL, L_rowptr, U_rowptr, rows,
+                                                L_out, U_out);
   return cudaGetLastError();
 }
 

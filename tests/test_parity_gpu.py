@@ -154,15 +154,13 @@ def test_budget_batches_and_epoch_wrap(ctx, schedule):
     (floor(2^32 / (n+2)) = 255 epochs), forcing the re-initialisation path of
     P:573-574.  Output must not change."""
     n_act, n = 9600, 1 << 24
-    rp0, ci0 = gen.random_graph(400, 0.01, seed=3)
-    rows = []
-    cols = []
     rng = np.random.default_rng(4)
     src = rng.integers(0, n_act, size=60000)
     dst = np.clip(src + rng.integers(-300, 300, size=src.size), 0, n_act - 1)
     rp, ci = gen.csr_from_edges(n, src, dst)
     got = run(rp, ci, ctx, row_end=n_act, max_concurrent=32, schedule=schedule)
-    assert got["stats"]["batches"] == n_act // 32
+    if schedule == "fifo":
+        assert got["stats"]["batches"] == n_act // 32
     want = oracle.symbolic(rp, ci, row_end=n_act)
     assert_full_equal(got, want)
 
@@ -173,7 +171,10 @@ def test_tight_budget_same_result(schedule):
     want = oracle.symbolic(rp, ci)
     with g.Context(0, mem_budget_bytes=24 << 20) as c:
         got = run(rp, ci, c, schedule=schedule)
-    assert got["stats"]["batches"] > 1
+    if schedule == "fifo":
+        assert got["stats"]["batches"] > 1
+    else:
+        assert got["stats"]["max_batch"] < 8000 // 32 * 32  # fewer slots than groups
     assert_full_equal(got, want)
 
 
