@@ -66,6 +66,7 @@ bool is_device_ptr(const void *p) {
 struct gsofa_context {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // heavy-group kernel runs here, concurrently
   int64_t budget = 0;        // requested budget (0 = auto)
   // arena (one cudaMalloc, carved in fixed regions)
   char *arena = nullptr;
@@ -112,7 +113,7 @@ struct Plan {
   int64_t nsub;
   size_t total;
   // streaming (threshold) schedule
-  int64_t slots = 0, Vmax = 0;
+  int64_t slots = 0, heavy = 0, light = 0, Vmax = 0;
   size_t ws_words = 0, slot_is_words = 0;
 };
 
@@ -174,19 +175,38 @@ bool make_plan(int schedule, int64_t n, int64_t rows, int64_t vb_max, int64_t cm
 // structure bitmap.  The number of slots is what the budget allows
 // ("reduce the number of concurrent sources"), at most the resident
 // CTA count and the number of groups.
-bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int64_t max_resident,
-                      Plan &p) {
+bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int device, Plan &p) {
+  if (gsofa::stream_smem_bytes(Vmax) > 200 * 1024) return false;
   const size_t ws = gsofa::stream_ws_words(Vmax), isw = gsofa::stream_is_words(n);
   const size_t per_slot = (ws + isw) * 4;
   const size_t fixed = small_bytes(32) + 8192;
   if (budget <= (int64_t)(fixed + per_slot)) return false;
-  int64_t slots = (int64_t)(((size_t)budget - fixed) / per_slot);
-  slots = std::min<int64_t>(slots, std::min<int64_t>(max_resident, ceil_div(rows, 32)));
-  if (slots < 1) return false;
+  const int64_t max_slots = (int64_t)(((size_t)budget - fixed) / per_slot);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int64_t ngroups = ceil_div(rows, 32);
+  const int64_t res_light = gsofa::stream_max_blocks(device, Vmax, 0);
+  const int64_t res_heavy = gsofa::stream_max_blocks(device, Vmax, 1);
+  if (res_light < 1) return false;
+  // one heavy CTA per SM (16 warps) for the heaviest groups, light CTAs in
+  // the remaining residency; both bounded by the memory budget
+  int64_t heavy = std::min<int64_t>(std::min<int64_t>(sms, res_heavy), ngroups);
+  if (const char *e = std::getenv("GSOFA_HEAVY_CTAS")) heavy = std::min<int64_t>(heavy, atoll(e));
+  heavy = std::max<int64_t>(0, std::min<int64_t>(heavy, max_slots / 2));
+  int64_t light = res_light - gsofa::stream_heavy_ratio() * heavy;
+  light = std::max<int64_t>(0, std::min<int64_t>(light, std::min<int64_t>(max_slots - heavy, ngroups)));
+  if (heavy + light < 1) {
+    light = std::min<int64_t>(1, max_slots);
+    heavy = 0;
+  }
+  if (heavy + light < 1) return false;
+  const int64_t slots = heavy + light;
   p.Cmax = 32;
   p.Gmax = 1;
   p.gbits = 0;
   p.slots = slots;
+  p.heavy = heavy;
+  p.light = light;
   p.Vmax = Vmax;
   p.ws_words = ws;
   p.slot_is_words = isw;
@@ -382,6 +402,12 @@ int gsofa_context_create(int32_t device, int64_t mem_budget_bytes, gsofa_context
     delete c;
     return cuda_fail(e, "cudaStreamCreate");
   }
+  e = cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
   e = cudaMallocHost((void **)&c->h_small, 64 * sizeof(int64_t));
   if (e != cudaSuccess) {
     cudaStreamDestroy(c->stream);
@@ -394,7 +420,7 @@ int gsofa_context_create(int32_t device, int64_t mem_budget_bytes, gsofa_context
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  c->stream_blocks = gsofa::stream_max_blocks(device);
+  c->stream_blocks = gsofa::stream_max_blocks(device, 1 << 20, 0);
   c->max_blocks[0] = gsofa::traverse_max_blocks(device, 0);
   c->max_blocks[1] = gsofa::traverse_max_blocks(device, 1);
   if (c->max_blocks[0] <= 0 || c->max_blocks[1] <= 0 || c->stream_blocks <= 0) {
@@ -419,6 +445,7 @@ void gsofa_context_destroy(gsofa_context *c) {
   if (c->stage) cudaFree(c->stage);
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
   delete c;
 }
 
@@ -569,8 +596,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     const int64_t vb_max = std::min<int64_t>(n, re + 32);
     const bool ok = o.schedule == GSOFA_SCHEDULE_FIFO
                         ? make_plan(o.schedule, n, rows, vb_max, cmax_req, budget, plan)
-                        : make_plan_stream(n, rows, std::min<int64_t>(n, re), budget,
-                                           c->stream_blocks, plan);
+                        : make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device,
+                                           plan);
     if (!ok) {
       set_detail("budget %lld B cannot hold one 32-source group for n=%lld", (long long)budget,
                  (long long)n);
@@ -650,7 +677,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     int32_t *nfailed = (int32_t *)(c->qcount + 1);
     unsigned long long *cursor = (unsigned long long *)c->totals;
     unsigned long long *failed_need = cursor + 1;
-    CK(cudaMemsetAsync(c->qcount, 0, 16, st));
+    CK(cudaMemsetAsync(c->qcount, 0, 16, st));  // group_ctr, nfailed, ctr_heavy
     CK(cudaMemsetAsync(c->totals, 0, 16, st));
     gsofa::StreamParams sp;
     sp.rowptr = c->rowptr32;
@@ -677,11 +704,45 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.nfailed = nfailed;
     sp.failed_need = failed_need;
     sp.stats = c->stats;
-    int64_t grid = std::min<int64_t>(plan.slots, ngroups);
+    sp.group_trace = nullptr;
+    const char *trace_path = std::getenv("GSOFA_GROUP_TRACE");  // dev: per-group trace dump
+    if (trace_path) {
+      if (cudaMallocAsync((void **)&sp.group_trace, (size_t)ngroups * 64, st) != cudaSuccess) {
+        cudaGetLastError();
+        sp.group_trace = nullptr;
+      } else {
+        cudaMemsetAsync(sp.group_trace, 0, (size_t)ngroups * 64, st);
+      }
+    }
+    sp.ctr_heavy = c->qcount + 2;
+    sp.n_heavy = 0;
+    if (plan.heavy > 0) {
+      int64_t nh = std::min<int64_t>(ngroups, 2 * plan.heavy);
+      if (const char *e = std::getenv("GSOFA_HEAVY_GROUPS")) nh = std::min<int64_t>(ngroups, atoll(e));
+      sp.n_heavy = (int32_t)nh;
+    }
+    int64_t grid = plan.light;
     for (int pass = 0;; ++pass) {
       const int et0 = ev();
-      CK(gsofa::launch_stream(sp, (int)grid, st));
-      ++launches;
+      if (pass == 0 && plan.heavy > 0 && sp.n_heavy > 0) {
+        // heavy kernel (16-warp CTAs, slots [0, heavy)) on the second stream,
+        // light kernel (4-warp CTAs, slots [heavy, slots)) on this one
+        cudaEvent_t ea, eb;
+        CK(cudaEventCreateWithFlags(&ea, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&eb, cudaEventDisableTiming));
+        CK(cudaEventRecord(ea, st));
+        CK(cudaStreamWaitEvent(c->stream2, ea, 0));
+        CK(gsofa::launch_stream(sp, (int)plan.heavy, 1, 0, c->stream2));
+        CK(cudaEventRecord(eb, c->stream2));
+        CK(gsofa::launch_stream(sp, (int)grid, 0, (int)plan.heavy, st));
+        CK(cudaStreamWaitEvent(st, eb, 0));
+        cudaEventDestroy(ea);
+        cudaEventDestroy(eb);
+        launches += 2;
+      } else {
+        CK(gsofa::launch_stream(sp, (int)std::max<int64_t>(grid, 1), 0, 0, st));
+        ++launches;
+      }
       e_trav.push_back({et0, ev()});
       CK(cudaMemcpyAsync(c->h_small, c->totals, 16, cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(c->h_small + 2, c->qcount, 8, cudaMemcpyDeviceToHost, st));
@@ -708,6 +769,17 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       sp.group_list = grp;
       sp.list_len = nf;
       grid = std::min<int64_t>(plan.slots, nf);
+      sp.n_heavy = 0;
+    }
+    if (sp.group_trace) {
+      std::vector<long long> h((size_t)ngroups * 8);
+      cudaMemcpyAsync(h.data(), sp.group_trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      if (FILE *f = std::fopen(trace_path, "wb")) {
+        std::fwrite(h.data(), 8, h.size(), f);
+        std::fclose(f);
+      }
+      cudaFreeAsync(sp.group_trace, st);
     }
     // row pointers (int64: C5 has > 2^31 entries) and the final CSR gather
     {
@@ -737,7 +809,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       scan_tmp = nullptr;
     }
     nbatches = 1;
-    maxC = 32 * std::min<int64_t>(plan.slots, ngroups);
+    maxC = 32 * std::min<int64_t>(plan.slots, ngroups);  // concurrent sources
   }
   // ---------------------------------------------------- batches (FIFO)
   for (int64_t s0 = rb; o.schedule == GSOFA_SCHEDULE_FIFO && s0 < re;) {

@@ -33,8 +33,8 @@ namespace gsofa {
 
 namespace {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
-constexpr int kWarps = 4;
-constexpr int kThreads = kWarps * 32;
+constexpr int kLightWarps = 4;   // CTA of the light kernel (most groups)
+constexpr int kHeavyWarps = 16;  // CTA of the heavy kernel (the heaviest groups)
 
 // lanes k (sources s0g + k) with source > w, resp. source < w
 __device__ __forceinline__ uint32_t lanes_above(int w, int s0g) {
@@ -64,31 +64,35 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 
 struct Slot {
   uint32_t *state, *thr, *rsum, *list0, *list1, *is, *isum;
+  uint32_t *tsum;  // shared memory
 };
 
-// mark the 32-vertex line of v in a touched-line summary (returning atomic:
-// the summary is read by other warps of this CTA after a barrier)
-__device__ __forceinline__ uint32_t touch(uint32_t *sum, int v) {
-  return atomicOr(sum + (v >> 10), 1u << ((v >> 5) & 31));
-}
-
-// next set bit of thr strictly above T (warp-cooperative), INT_MAX if none
-__device__ __forceinline__ int scan_next(const uint32_t *thr, int tbw, int T, int lane) {
+// Next set bit of thr strictly above T (warp-cooperative), INT_MAX if none.
+// tsum (shared memory) has one bit per thr word that is nonzero, so the scan
+// touches at most two thr words however far the next threshold is.
+__device__ __forceinline__ int scan_next(const uint32_t *thr, const uint32_t *tsum, int tbw, int T,
+                                         int lane) {
   const int start = T + 1;
-  int wi = start >> 5;
-  bool first = true;
-  while (wi < tbw) {
-    const int idx = wi + lane;
-    uint32_t x = idx < tbw ? __ldcg(thr + idx) : 0u;
-    if (first && lane == 0) x &= kFull << (start & 31);
-    const uint32_t b = __ballot_sync(kFull, x != 0u);
+  const int wi = start >> 5;
+  if (wi >= tbw) return INT_MAX;
+  uint32_t x = 0u;
+  if (lane == 0) x = __ldcg(thr + wi) & (kFull << (start & 31));
+  x = __shfl_sync(kFull, x, 0);
+  if (x) return (wi << 5) + __ffs(x) - 1;
+  const int nw = wi + 1;  // first thr word to look for
+  const int tsw = (tbw + 31) >> 5;
+  for (int si = nw >> 5; si < tsw; si += 32) {
+    const int idx = si + lane;
+    uint32_t y = idx < tsw ? tsum[idx] : 0u;
+    if (si == (nw >> 5) && lane == 0) y &= kFull << (nw & 31);
+    const uint32_t b = __ballot_sync(kFull, y != 0u);
     if (b) {
       const int l = __ffs(b) - 1;
-      const uint32_t xl = __shfl_sync(kFull, x, l);
-      return ((wi + l) << 5) + __ffs(xl) - 1;
+      const uint32_t yl = __shfl_sync(kFull, y, l);
+      const int word = ((si + l) << 5) + __ffs(yl) - 1;
+      const uint32_t z = __ldcg(thr + word);
+      return (word << 5) + __ffs(z) - 1;
     }
-    wi += 32;
-    first = false;
   }
   return INT_MAX;
 }
@@ -98,9 +102,20 @@ struct Counters {
   uint32_t sink;
 };
 
+// release this thread's fire-and-forget reductions (REDs) before a barrier:
+// after fence + bar.sync every thread of the CTA observes them
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+constexpr int kBatch = 4;  // 32-pair batches whose atomics a warp keeps in flight
+
 // Expand up to 32 frontier items (one per lane; u < 0 = none) of the closure
 // of threshold T.  Every item's newMaxId is T.  Pushes closure members into
-// `nq` (count *nqn), records new fills in thr / *minfill.
+// `nq` (count *nqn), records new fills in thr / tsum / *minfill.
+// Only two atomics per (item, neighbour) pair return a value the warp waits
+// for: the reached mask of w (line 10 of fig:alg) and, for w < T, the
+// pend mask (enqueue test); both are issued for kBatch*32 pairs before any
+// result is used.  Every other update is a RED, published by fence_gpu()
+// before the next barrier.
 __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, int s0g, int T,
                                        int u, uint32_t *nq, int *nqn, int *minfill, int lane,
                                        Counters &c) {
@@ -109,11 +124,10 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
   int beg = 0, deg = 0;
   uint32_t mask = 0u;
   if (u >= 0) {
+    beg = __ldg(rowptr + u);
+    deg = __ldg(rowptr + u + 1) - beg;
     mask = atomicExch(sl.state + 2 * u + 1, 0u);  // lanes that expand u (pend)
-    if (mask) {
-      beg = __ldg(rowptr + u);
-      deg = __ldg(rowptr + u + 1) - beg;
-    }
+    if (!mask) deg = 0;
   }
   c.items += mask != 0u;
   c.pairs += (unsigned long long)deg;
@@ -128,53 +142,69 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
   const int total = __shfl_sync(kFull, incl, 31);
   if (total == 0) return;
   const int excl = incl - deg;
-  for (int f0 = 0; f0 < total; f0 += 32) {
-    const int f = f0 + lane;
-    int o = 0;
+  for (int f0 = 0; f0 < total; f0 += 32 * kBatch) {
+    int w[kBatch];
+    uint32_t lm[kBatch], ro[kBatch], io[kBatch];
 #pragma unroll
-    for (int step = 16; step >= 1; step >>= 1) {
-      const int cand = o + step;
-      const int e = __shfl_sync(kFull, excl, cand & 31);
-      if (cand < 32 && e <= f) o = cand;
+    for (int k = 0; k < kBatch; ++k) {
+      const int f = f0 + 32 * k + lane;
+      int o = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int cand = o + step;
+        const int e = __shfl_sync(kFull, excl, cand & 31);
+        if (cand < 32 && e <= f) o = cand;
+      }
+      const int ob = __shfl_sync(kFull, beg, o);
+      const int oe = __shfl_sync(kFull, excl, o);
+      const uint32_t om = __shfl_sync(kFull, mask, o);
+      w[k] = f < total ? __ldg(colidx + ob + (f - oe)) : 0;
+      const uint32_t um = f < total ? om & lanes_below(w[k], s0g) : 0u;  // U entries
+      lm[k] = f < total ? om & lanes_above(w[k], s0g) : 0u;             // maxId(w)
+      // atomicMin(maxId(w), T) succeeds exactly for the lanes that have not
+      // reached w yet (line 10); IS first-touch is detected from its
+      // old value.  Both are issued now and consumed below.
+      ro[k] = lm[k] ? atomicOr(sl.state + 2 * w[k], lm[k]) : kFull;
+      io[k] = um ? atomicOr(sl.is + w[k], um) : kFull;
     }
-    const int ob = __shfl_sync(kFull, beg, o);
-    const int oe = __shfl_sync(kFull, excl, o);
-    const uint32_t om = __shfl_sync(kFull, mask, o);
-    bool push = false;
-    int w = 0;
-    if (f < total) {
-      w = __ldg(colidx + ob + (f - oe));
-      const uint32_t um = om & lanes_below(w, s0g);  // sources < w: U entry
-      const uint32_t lm = om & lanes_above(w, s0g);  // sources > w: maxId(w)
-      if (um && atomicOr(sl.is + w, um) == 0u) c.sink ^= touch(sl.isum, w);
-      if (lm) {
-        // atomicMin(maxId(w), T) succeeds exactly for the lanes that have not
-        // reached w yet (line 10)
-        const uint32_t old = atomicOr(sl.state + 2 * w, lm);
-        const uint32_t nw = lm & ~old;
-        if (old == 0u) c.sink ^= touch(sl.rsum, w);
-        if (nw) {
-          if (w > T) {
-            // newMaxId T < w: (src, w) is a fill of L (R4); w proposes
-            // newMaxId = w later, as a threshold
-            if (atomicOr(sl.is + w, nw) == 0u) c.sink ^= touch(sl.isum, w);
-            c.sink ^= atomicOr(sl.state + 2 * w + 1, nw) ^
-                      atomicOr(sl.thr + (w >> 5), 1u << (w & 31));
-            atomicMin(minfill, w);
-          } else {
-            // w < T: maxId(w) = T, not in the structure: continue with T
-            push = atomicOr(sl.state + 2 * w + 1, nw) == 0u;
-          }
+    bool push[kBatch];
+    uint32_t po[kBatch];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+      if (io[k] == 0u) atomicOr(sl.isum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));  // RED
+      if (ro[k] == 0u) atomicOr(sl.rsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));  // RED
+      const uint32_t nw = lm[k] & ~ro[k];
+      push[k] = false;
+      po[k] = kFull;
+      if (nw) {
+        if (w[k] > T) {
+          // newMaxId T < w: (src, w) is a fill of L (R4); w proposes newMaxId
+          // = w later, as a threshold
+          atomicOr(sl.is + w[k], nw);                                           // RED
+          atomicOr(sl.isum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));          // RED
+          atomicOr(sl.state + 2 * w[k] + 1, nw);                                // RED
+          atomicOr(sl.thr + (w[k] >> 5), 1u << (w[k] & 31));                    // RED
+          atomicOr(sl.tsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));          // smem
+          atomicMin(minfill, w[k]);                                             // smem
+        } else {
+          // w < T: maxId(w) = T, not in the structure: continue with T
+          po[k] = atomicOr(sl.state + 2 * w[k] + 1, nw);
+          push[k] = true;
         }
       }
     }
-    const uint32_t pb = __ballot_sync(kFull, push);
-    if (pb) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(nqn, __popc(pb));
-      base = __shfl_sync(kFull, base, 0);
-      if (push) nq[base + __popc(pb & lanemask_lt())] = (uint32_t)w;
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+      const bool ps = push[k] && po[k] == 0u;
+      const uint32_t pb = __ballot_sync(kFull, ps);
+      if (pb) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(nqn, __popc(pb));
+        base = __shfl_sync(kFull, base, 0);
+        if (ps) nq[base + __popc(pb & lanemask_lt())] = (uint32_t)w[k];
+      }
     }
+    if (f0 + 32 * kBatch >= total) break;
   }
 }
 
@@ -183,20 +213,26 @@ __device__ __forceinline__ void split_masks(int d, uint32_t &lm, uint32_t &um) {
   um = d < 0 ? kFull : (d >= 31 ? 0u : (kFull << (d + 1)));
 }
 
-__global__ void __launch_bounds__(kThreads) stream_kernel(StreamParams p) {
+template <int kWarps>
+__global__ void __launch_bounds__(kWarps * 32, kWarps == kLightWarps ? 8 : 2)
+    stream_kernel(StreamParams p, int slot_base, int heavy) {
+  constexpr int kThreads = kWarps * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   const int n = p.n, Vmax = p.Vmax;
   const int tbw_max = (Vmax + 31) >> 5;
   const int rsw = (Vmax + 1023) >> 10;
   const int isw = (n + 1023) >> 10;
   Slot sl;
-  sl.state = p.ws + (size_t)blockIdx.x * p.ws_words;
+  const size_t slot = (size_t)slot_base + blockIdx.x;
+  sl.state = p.ws + slot * p.ws_words;
   sl.thr = sl.state + 2 * (size_t)Vmax;
   sl.rsum = sl.thr + tbw_max;
   sl.list0 = sl.rsum + rsw;
   sl.list1 = sl.list0 + Vmax;
-  sl.is = p.is + (size_t)blockIdx.x * p.is_words;
+  sl.is = p.is + slot * p.is_words;
   sl.isum = sl.is + n;
+  extern __shared__ uint32_t s_tsum[];  // [(tbw_max + 31) / 32]
+  sl.tsum = s_tsum;
 
   __shared__ int s_g, s_qn[2], s_scan[3], s_minfill[3];
   __shared__ uint32_t s_cnt[kWarps][2][32];
@@ -207,19 +243,38 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamParams p) {
 
   for (;;) {
     if (tid == 0) {
-      const int j = (int)atomicAdd(p.group_ctr, 1u);
-      const int total = p.group_list ? p.list_len : p.ngroups;
-      s_g = j < total ? (p.group_list ? p.group_list[j] : p.ngroups - 1 - j) : -1;
+      // heaviest first: group ngroups-1-j is the j-th taken; the heavy kernel
+      // owns the first n_heavy of them, then helps with the rest
+      int gg = -1;
+      if (p.group_list) {
+        const int j = (int)atomicAdd(p.group_ctr, 1u);
+        if (j < p.list_len) gg = p.group_list[j];
+      } else {
+        if (heavy) {
+          const int j = (int)atomicAdd(p.ctr_heavy, 1u);
+          if (j < p.n_heavy) gg = p.ngroups - 1 - j;
+        }
+        if (gg < 0) {
+          const int j = (int)atomicAdd(p.group_ctr, 1u) + p.n_heavy;
+          if (j < p.ngroups) gg = p.ngroups - 1 - j;
+        }
+      }
+      s_g = gg;
       s_qn[0] = s_qn[1] = 0;
       for (int i = 0; i < 3; ++i) s_scan[i] = s_minfill[i] = INT_MAX;
     }
     __syncthreads();
     const int g = s_g;
     if (g < 0) break;
+    const long long t_start = clock64();
+    const unsigned long long st0 = c.steps, lv0 = c.levels, it0 = c.items, pr0 = c.pairs;
+    long long t_trav = 0, t_ext = 0;
     const int s0g = p.row_begin + 32 * g;
     const int nsrc = min(32, p.row_end - s0g);
     const int Vb = min(n, s0g + nsrc);  // maxId only below the largest source
     const int tbw = (Vb + 31) >> 5;
+    for (int i = tid; i < ((tbw + 31) >> 5); i += kThreads) s_tsum[i] = 0u;
+    __syncthreads();
 
     // ---- seed: out-neighbours of each source are in the
     // structure; the smaller ones are reached with maxId -1 -> thresholds
@@ -230,17 +285,21 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamParams p) {
       for (int j = beg + lane; j < end; j += 32) {
         const int w = __ldg(p.colidx + j);
         if (w == s) continue;
-        if (atomicOr(sl.is + w, bit) == 0u) c.sink ^= touch(sl.isum, w);
+        atomicOr(sl.is + w, bit);                                     // RED
+        atomicOr(sl.isum + (w >> 10), 1u << ((w >> 5) & 31));       // RED
         if (w < s) {
-          if (atomicOr(sl.state + 2 * w, bit) == 0u) c.sink ^= touch(sl.rsum, w);
-          c.sink ^= atomicOr(sl.state + 2 * w + 1, bit) ^
-                    atomicOr(sl.thr + (w >> 5), 1u << (w & 31));
+          atomicOr(sl.state + 2 * w, bit);                            // RED
+          atomicOr(sl.rsum + (w >> 10), 1u << ((w >> 5) & 31));       // RED
+          atomicOr(sl.state + 2 * w + 1, bit);                        // RED
+          atomicOr(sl.thr + (w >> 5), 1u << (w & 31));                // RED
+          atomicOr(sl.tsum + (w >> 10), 1u << ((w >> 5) & 31));       // smem
         }
       }
     }
+    fence_gpu();
     __syncthreads();
     if (warp == 0) {
-      const int t0 = scan_next(sl.thr, tbw, -1, lane);
+      const int t0 = scan_next(sl.thr, sl.tsum, tbw, -1, lane);
       if (lane == 0) s_scan[0] = t0;
     }
     __syncthreads();
@@ -261,16 +320,21 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamParams p) {
       if (warp == 0) {
         expand(p, sl, s0g, T, lane == 0 ? T : -1, sl.list1, &s_qn[1], &s_minfill[nx3], lane, c);
       } else if (warp == 1) {
-        const int nt = scan_next(sl.thr, tbw, T, lane);
+        const int nt = scan_next(sl.thr, sl.tsum, tbw, T, lane);
         if (lane == 0) s_scan[nx3] = nt;
       }
       __syncthreads();
       c.levels += 1;
-      // closure levels: every item has newMaxId T
+      // closure levels: every item has newMaxId T.  Levels only consume
+      // returning atomics (reached, pend pushes); the REDs of this step
+      // (fill pend / thr / is) are published before the next step's barrier.
       for (int lvl = 1;; ++lvl) {
         const int cur = lvl & 1, nxt = cur ^ 1;
         const int qn = s_qn[cur];
-        if (qn == 0) break;
+        if (qn == 0) {
+          fence_gpu();
+          break;
+        }
         const uint32_t *cq = cur ? sl.list1 : sl.list0;
         uint32_t *nq = cur ? sl.list0 : sl.list1;
         __syncthreads();
@@ -284,6 +348,8 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamParams p) {
       }
     }
 
+    __syncthreads();  // every thread's REDs were fenced at its last closure end
+    t_trav = clock64();
     // ---- extraction of the group's rows (touched IS lines, ascending)
     // warp w owns isum words [w*q, (w+1)*q): its lines are ascending and all
     // of them precede warp w+1's, so per-warp counts give the write offsets
@@ -384,6 +450,7 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamParams p) {
         }
       }
     }
+    t_ext = clock64();
     // ---- reset the touched state lines (reached; pend is already 0) and thr
     {
       const int qr = (rsw + kWarps - 1) / kWarps;
@@ -404,6 +471,19 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamParams p) {
     // the clears above are plain stores; the next group's atomics on the same
     // words are performed at L2, so make the stores globally visible first
     __threadfence();
+    if (p.group_trace && lane == 0) {
+      long long *t = p.group_trace + 8 * (size_t)g;
+      // per-warp item / pair counts are summed over the warps' lane 0
+      atomicAdd((unsigned long long *)&t[2], (unsigned long long)(c.items - it0));
+      atomicAdd((unsigned long long *)&t[6], (unsigned long long)(c.pairs - pr0));
+      if (warp == 0) {
+        t[0] = (long long)(c.steps - st0);
+        t[1] = (long long)(c.levels - lv0);
+        t[3] = clock64() - t_start;
+        t[4] = t_trav - t_start;
+        t[5] = t_ext - t_trav;
+      }
+    }
     __syncthreads();
   }
 #pragma unroll
@@ -451,17 +531,48 @@ size_t stream_is_words(int64_t n) {
   return (w + 7) / 8 * 8;
 }
 
-int stream_max_blocks(int device) {
+size_t stream_smem_bytes(int64_t Vmax) {
+  return (size_t)((((Vmax + 31) / 32) + 31) / 32) * 4;
+}
+
+template <int W>
+int max_blocks_t(int device, int64_t Vmax) {
   int sms = 0, per = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_kernel, kThreads, 0) != cudaSuccess)
+  const size_t smem = stream_smem_bytes(Vmax);
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(stream_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+    return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_kernel<W>, W * 32, smem) != cudaSuccess)
     return 0;
   return sms * per;
 }
 
-cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st) {
+int stream_max_blocks(int device, int64_t Vmax, int heavy) {
+  return heavy ? max_blocks_t<kHeavyWarps>(device, Vmax) : max_blocks_t<kLightWarps>(device, Vmax);
+}
+
+int stream_heavy_ratio() { return kHeavyWarps / kLightWarps; }
+
+cudaError_t launch_stream(const StreamParams &p, int grid, int heavy, int slot_base, cudaStream_t st) {
   if (grid <= 0) return cudaSuccess;
-  stream_kernel<<<grid, kThreads, 0, st>>>(p);
+  const size_t smem = stream_smem_bytes(p.Vmax);
+  if (heavy) {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(stream_kernel<kHeavyWarps>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    stream_kernel<kHeavyWarps><<<grid, kHeavyWarps * 32, smem, st>>>(p, slot_base, 1);
+  } else {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(stream_kernel<kLightWarps>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    stream_kernel<kLightWarps><<<grid, kLightWarps * 32, smem, st>>>(p, slot_base, 0);
+  }
   return cudaGetLastError();
 }
 
