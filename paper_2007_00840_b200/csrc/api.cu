@@ -114,7 +114,7 @@ struct Plan {
   size_t total;
   // streaming (threshold) schedule
   int64_t slots = 0, heavy = 0, light = 0, Vmax = 0;
-  size_t ws_words = 0, slot_is_words = 0;
+  size_t ws_words = 0, slot_is_words = 0, hws_words = 0;
 };
 
 size_t small_bytes(int64_t Cmax) {
@@ -175,43 +175,47 @@ bool make_plan(int schedule, int64_t n, int64_t rows, int64_t vb_max, int64_t cm
 // structure bitmap.  The number of slots is what the budget allows
 // ("reduce the number of concurrent sources"), at most the resident
 // CTA count and the number of groups.
+// Streaming schedule: one workspace slot per resident CTA.  Lockstep slots
+// (4-warp CTAs, one 32-source group at a time, shared frontier items) and
+// solo slots (32-warp CTAs, one warp per source, for the heavy groups the
+// lockstep kernel hands over).  No maxId state above the largest source
+// (bubble removal).  Slot counts follow the residency of both kernels
+// sharing the SMs and the memory budget ("reduce the number of concurrent
+// sources").
 bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int device, Plan &p) {
   if (gsofa::stream_smem_bytes(Vmax) > 200 * 1024) return false;
   const size_t ws = gsofa::stream_ws_words(Vmax), isw = gsofa::stream_is_words(n);
-  const size_t per_slot = (ws + isw) * 4;
+  const size_t hws = gsofa::solo_ws_words(Vmax);
+  const size_t per_light = (ws + isw) * 4, per_heavy = (hws + isw) * 4;
   const size_t fixed = small_bytes(32) + 8192;
-  if (budget <= (int64_t)(fixed + per_slot)) return false;
-  const int64_t max_slots = (int64_t)(((size_t)budget - fixed) / per_slot);
+  if (budget <= (int64_t)(fixed + per_light)) return false;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const int64_t ngroups = ceil_div(rows, 32);
   const int64_t res_light = gsofa::stream_max_blocks(device, Vmax, 0);
   const int64_t res_heavy = gsofa::stream_max_blocks(device, Vmax, 1);
   if (res_light < 1) return false;
-  // one heavy CTA per SM (16 warps) for the heaviest groups, light CTAs in
-  // the remaining residency; both bounded by the memory budget
+  // one solo CTA per SM (half of its warps); lockstep CTAs fill the rest
   int64_t heavy = std::min<int64_t>(std::min<int64_t>(sms, res_heavy), ngroups);
-  if (const char *e = std::getenv("GSOFA_HEAVY_CTAS")) heavy = std::min<int64_t>(heavy, atoll(e));
-  heavy = std::max<int64_t>(0, std::min<int64_t>(heavy, max_slots / 2));
-  int64_t light = res_light - gsofa::stream_heavy_ratio() * heavy;
-  light = std::max<int64_t>(0, std::min<int64_t>(light, std::min<int64_t>(max_slots - heavy, ngroups)));
-  if (heavy + light < 1) {
-    light = std::min<int64_t>(1, max_slots);
-    heavy = 0;
-  }
-  if (heavy + light < 1) return false;
-  const int64_t slots = heavy + light;
+  if (const char *e = std::getenv("GSOFA_SOLO_CTAS")) heavy = std::min<int64_t>(heavy, atoll(e));
+  heavy = std::max<int64_t>(0, std::min<int64_t>(heavy, (int64_t)(((size_t)budget - fixed) / 2 / per_heavy)));
+  int64_t light = heavy > 0 ? (int64_t)sms * gsofa::stream_light_per_sm_with_solo(device, Vmax) : res_light;
+  light = std::min<int64_t>(light, res_light);
+  light = std::min<int64_t>(light, (int64_t)(((size_t)budget - fixed - heavy * per_heavy) / per_light));
+  light = std::max<int64_t>(1, std::min<int64_t>(light, ngroups));
+  if ((size_t)light * per_light + (size_t)heavy * per_heavy + fixed > (size_t)budget) return false;
   p.Cmax = 32;
   p.Gmax = 1;
   p.gbits = 0;
-  p.slots = slots;
+  p.slots = light + heavy;
   p.heavy = heavy;
   p.light = light;
   p.Vmax = Vmax;
   p.ws_words = ws;
+  p.hws_words = hws;
   p.slot_is_words = isw;
-  p.work_bytes = (size_t)slots * ws * 4;
-  p.is_words = (size_t)slots * isw;
+  p.work_bytes = (size_t)light * ws * 4 + (size_t)heavy * hws * 4;
+  p.is_words = (size_t)(light + heavy) * isw;
   p.cnt_words = 0;
   p.nsub = 0;
   p.total = p.work_bytes + p.is_words * 4 + small_bytes(32) + 4096 + 12 * 256;
@@ -609,7 +613,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   if (o.schedule != GSOFA_SCHEDULE_FIFO) {
     // the slot layout (Vmax, ws_words) moved: list garbage could now sit
     // under state words, so start from an all-zero work region
-    const uint64_t sig = ((uint64_t)plan.Vmax << 32) ^ (uint64_t)plan.ws_words;
+    const uint64_t sig = ((uint64_t)plan.Vmax << 32) ^ (uint64_t)plan.ws_words ^
+                         ((uint64_t)plan.light << 48) ^ ((uint64_t)plan.heavy << 40);
     if (c->layout_sig != sig && c->work_state == kWorkZero && c->layout_sig != 0) c->work_state = kWorkDirty;
     c->layout_sig = sig;
   }
@@ -651,9 +656,10 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     const int64_t ngroups = ceil_div(rows, 32);
     int64_t *row_off = nullptr;
     int32_t *row_nL = nullptr, *row_nU = nullptr, *failed = nullptr, *grp = nullptr;
+    int32_t *hq = nullptr, *hq_ready = nullptr;
     {
       cudaError_t e1 = cudaMallocAsync((void **)&stream_scratch,
-                                       (size_t)rows * 16 + (size_t)ngroups * 8 + 256, st);
+                                       (size_t)rows * 16 + (size_t)ngroups * 16 + 256, st);
       if (e1 != cudaSuccess) {
         cudaGetLastError();
         set_detail("row scratch allocation failed");
@@ -666,6 +672,9 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       row_nU = row_nL + rows;
       failed = row_nU + rows;
       grp = failed + ngroups;
+      hq = grp + ngroups;
+      hq_ready = hq + ngroups;
+      CK(cudaMemsetAsync(hq_ready, 0, (size_t)ngroups * 4, st));
     }
     if (c->stage_cap == 0) {
       size_t fr = 0, tot = 0;
@@ -677,7 +686,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     int32_t *nfailed = (int32_t *)(c->qcount + 1);
     unsigned long long *cursor = (unsigned long long *)c->totals;
     unsigned long long *failed_need = cursor + 1;
-    CK(cudaMemsetAsync(c->qcount, 0, 16, st));  // group_ctr, nfailed, ctr_heavy
+    // qcount: [0] group_ctr, [1] nfailed, [2] hq_head, [3] hq_tail, [4] done
+    CK(cudaMemsetAsync(c->qcount, 0, 32, st));
     CK(cudaMemsetAsync(c->totals, 0, 16, st));
     gsofa::StreamParams sp;
     sp.rowptr = c->rowptr32;
@@ -705,6 +715,11 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.failed_need = failed_need;
     sp.stats = c->stats;
     sp.group_trace = nullptr;
+    sp.debug = nullptr;
+    if (std::getenv("GSOFA_CHECK_CLEAN")) {
+      cudaMallocAsync((void **)&sp.debug, 256, st);
+      cudaMemsetAsync(sp.debug, 0, 256, st);
+    }
     const char *trace_path = std::getenv("GSOFA_GROUP_TRACE");  // dev: per-group trace dump
     if (trace_path) {
       if (cudaMallocAsync((void **)&sp.group_trace, (size_t)ngroups * 64, st) != cudaSuccess) {
@@ -714,33 +729,42 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
         cudaMemsetAsync(sp.group_trace, 0, (size_t)ngroups * 64, st);
       }
     }
-    sp.ctr_heavy = c->qcount + 2;
-    sp.n_heavy = 0;
+    sp.hq = hq;
+    sp.hq_ready = hq_ready;
+    sp.hq_head = c->qcount + 2;
+    sp.hq_tail = c->qcount + 3;
+    sp.done = c->qcount + 4;
+    sp.hws = c->work + (size_t)plan.light * plan.ws_words;
+    sp.hws_words = plan.hws_words;
+    sp.light_slots = (int32_t)plan.light;
+    sp.abort_cycles = 0;
     if (plan.heavy > 0) {
-      int64_t nh = std::min<int64_t>(ngroups, 2 * plan.heavy);
-      if (const char *e = std::getenv("GSOFA_HEAVY_GROUPS")) nh = std::min<int64_t>(ngroups, atoll(e));
-      sp.n_heavy = (int32_t)nh;
+      double ms = 5.0;
+      if (const char *e = std::getenv("GSOFA_ABORT_MS")) ms = atof(e);
+      int khz = 0;
+      cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, c->device);
+      sp.abort_cycles = (long long)(ms * (double)khz);
     }
     int64_t grid = plan.light;
     for (int pass = 0;; ++pass) {
       const int et0 = ev();
-      if (pass == 0 && plan.heavy > 0 && sp.n_heavy > 0) {
-        // heavy kernel (16-warp CTAs, slots [0, heavy)) on the second stream,
-        // light kernel (4-warp CTAs, slots [heavy, slots)) on this one
+      if (pass == 0 && plan.heavy > 0) {
+        // solo kernel (32-warp CTAs) on the second stream, concurrently with
+        // the lockstep kernel; it serves the heavy queue until all are done
         cudaEvent_t ea, eb;
         CK(cudaEventCreateWithFlags(&ea, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&eb, cudaEventDisableTiming));
         CK(cudaEventRecord(ea, st));
         CK(cudaStreamWaitEvent(c->stream2, ea, 0));
-        CK(gsofa::launch_stream(sp, (int)plan.heavy, 1, 0, c->stream2));
+        CK(gsofa::launch_solo(sp, (int)plan.heavy, c->stream2));
         CK(cudaEventRecord(eb, c->stream2));
-        CK(gsofa::launch_stream(sp, (int)grid, 0, (int)plan.heavy, st));
+        CK(gsofa::launch_stream(sp, (int)grid, st));
         CK(cudaStreamWaitEvent(st, eb, 0));
         cudaEventDestroy(ea);
         cudaEventDestroy(eb);
         launches += 2;
       } else {
-        CK(gsofa::launch_stream(sp, (int)std::max<int64_t>(grid, 1), 0, 0, st));
+        CK(gsofa::launch_stream(sp, (int)std::max<int64_t>(grid, 1), st));
         ++launches;
       }
       e_trav.push_back({et0, ev()});
@@ -768,8 +792,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       sp.stage_cap = c->stage_cap;
       sp.group_list = grp;
       sp.list_len = nf;
-      grid = std::min<int64_t>(plan.slots, nf);
-      sp.n_heavy = 0;
+      grid = std::min<int64_t>(plan.light, nf);
+      sp.abort_cycles = 0;  // retries run on the lockstep kernel alone
     }
     if (sp.group_trace) {
       std::vector<long long> h((size_t)ngroups * 8);
@@ -780,6 +804,51 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
         std::fclose(f);
       }
       cudaFreeAsync(sp.group_trace, st);
+    }
+    if (std::getenv("GSOFA_CHECK_CLEAN")) {
+      // dev: every state word must be zero again after the traversal
+      // (lists / queues excepted); report the first offenders per array
+      cudaStreamSynchronize(st);
+      std::vector<uint32_t> hw(c->work_bytes / 4), hi(c->is_words);
+      cudaMemcpy(hw.data(), c->work, c->work_bytes, cudaMemcpyDeviceToHost);
+      cudaMemcpy(hi.data(), c->is, c->is_words * 4, cudaMemcpyDeviceToHost);
+      const size_t Vm = plan.Vmax, tbw = (Vm + 31) / 32, tsw = (tbw + 31) / 32, rsw = (Vm + 1023) / 1024;
+      int reported = 0;
+      for (int64_t sl = 0; sl < plan.light && reported < 8; ++sl) {
+        const uint32_t *b = hw.data() + sl * plan.ws_words;
+        for (size_t i = 0; i < 2 * Vm + tbw + rsw && reported < 8; ++i)
+          if (b[i]) {
+            std::fprintf(stderr, "[dirty] light slot %lld word %zu (%s) = %08x\n", (long long)sl, i,
+                         i < 2 * Vm ? "state" : (i < 2 * Vm + tbw ? "thr" : "rsum"), b[i]);
+            ++reported;
+          }
+      }
+      for (int64_t sl = 0; sl < plan.heavy && reported < 16; ++sl) {
+        const uint32_t *b = hw.data() + plan.light * plan.ws_words + sl * plan.hws_words;
+        const size_t rs0 = (Vm + 3) & ~(size_t)3, th0 = rs0 + ((rsw + 3) & ~(size_t)3);
+        const size_t ts0 = th0 + 32 * tbw, q0 = ts0 + 32 * tsw;
+        for (size_t i = 0; i < q0 && reported < 16; ++i)
+          if (b[i]) {
+            std::fprintf(stderr, "[dirty] solo slot %lld word %zu (%s) = %08x\n", (long long)sl, i,
+                         i < rs0 ? "reached" : (i < th0 ? "rsum" : (i < ts0 ? "thr" : "tsum")), b[i]);
+            ++reported;
+          }
+      }
+      for (size_t i = 0; i < hi.size() && reported < 24; ++i)
+        if (hi[i]) {
+          std::fprintf(stderr, "[dirty] is slot %zu word %zu = %08x\n", i / plan.slot_is_words,
+                       i % plan.slot_is_words, hi[i]);
+          ++reported;
+        }
+      std::fprintf(stderr, "[dirty] check done, %d reported\n", reported);
+      if (sp.debug) {
+        int hd[33];
+        cudaMemcpy(hd, sp.debug, sizeof hd, cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "[solo-check] %d groups left reached bits\n", hd[0]);
+        for (int i = 0; i < std::min(hd[0], 8); ++i)
+          std::fprintf(stderr, "  g=%d vertex=%d val=%08x kind/cta=%d\n", hd[1 + 4 * i],
+                       hd[2 + 4 * i], hd[3 + 4 * i], hd[4 + 4 * i]);
+      }
     }
     // row pointers (int64: C5 has > 2^31 entries) and the final CSR gather
     {

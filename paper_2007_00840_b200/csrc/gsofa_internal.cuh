@@ -62,9 +62,17 @@ struct StreamParams {
   size_t ws_words;
   uint32_t *is;              // [slots][is_words]: is[n] | isum[n/1024]
   size_t is_words;
-  unsigned int *group_ctr;   // next light group (global counter)
-  unsigned int *ctr_heavy;   // next heavy group
-  int32_t n_heavy;           // the first n_heavy groups (heaviest) go to the heavy kernel
+  unsigned int *group_ctr;   // next fresh group (global counter, heaviest first)
+  // heavy path: groups abandoned by the lockstep kernel after abort_cycles
+  // are queued for the solo kernel (one warp per source)
+  long long abort_cycles;    // 0: never abandon
+  int32_t *hq;               // [ngroups] queued group ids
+  unsigned int *hq_head, *hq_tail;
+  int32_t *hq_ready;         // [ngroups] publication flags
+  unsigned int *done;        // groups completed (both kernels)
+  uint32_t *hws;             // [heavy slots][hws_words] solo workspaces
+  size_t hws_words;
+  int32_t light_slots;       // is[] slots [0, light_slots) lockstep, then solo
   const int32_t *group_list; // optional explicit group ids (retry pass)
   int32_t list_len;
   int32_t *stage;            // staged rows: [L entries | diag | U entries]
@@ -76,14 +84,18 @@ struct StreamParams {
   int32_t *nfailed;
   unsigned long long *failed_need;
   unsigned long long *stats; // items, edges, levels, thresholds, pairs
-  long long *group_trace;    // optional [ngroups][4]: steps, levels, items, cycles
+  long long *group_trace;    // optional [ngroups][8]: steps, levels, items, cycles, ...
+  int *debug;                // optional dev checks
 };
 size_t stream_ws_words(int64_t Vmax);
 size_t stream_is_words(int64_t n);
 int stream_max_blocks(int device, int64_t Vmax, int heavy);
-int stream_heavy_ratio();  // warps of a heavy CTA / warps of a light CTA
+int stream_heavy_ratio();  // warps of a solo CTA / warps of a lockstep CTA
+size_t solo_ws_words(int64_t Vmax);
+int stream_light_per_sm_with_solo(int device, int64_t Vmax);
 size_t stream_smem_bytes(int64_t Vmax);  // dynamic smem: threshold-word summary
-cudaError_t launch_stream(const StreamParams &p, int grid, int heavy, int slot_base, cudaStream_t st);
+cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st);
+cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st);
 cudaError_t launch_gather(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,
                           const int64_t *L_rowptr, const int64_t *U_rowptr, int rows,
                           int32_t *L_out, int32_t *U_out, cudaStream_t st);

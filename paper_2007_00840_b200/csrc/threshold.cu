@@ -25,6 +25,7 @@
 //   is[n]          in-structure bits          isum[n/1024]   touched lines
 // All of it is zero between groups; a group clears only the 32-vertex lines
 // recorded in rsum/isum (first-touch tracking), never the whole slot.
+#include <algorithm>
 #include <climits>
 
 #include "gsofa_internal.cuh"
@@ -33,8 +34,8 @@ namespace gsofa {
 
 namespace {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
-constexpr int kLightWarps = 4;   // CTA of the light kernel (most groups)
-constexpr int kHeavyWarps = 16;  // CTA of the heavy kernel (the heaviest groups)
+constexpr int kLightWarps = 4;   // lockstep CTA: 32 sources share frontier items
+constexpr int kSoloWarps = 32;   // solo CTA: one warp per source (heavy groups)
 
 // lanes k (sources s0g + k) with source > w, resp. source < w
 __device__ __forceinline__ uint32_t lanes_above(int w, int s0g) {
@@ -60,6 +61,11 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
     x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
   }
   return x;
+}
+
+__device__ __forceinline__ void split_masks(int d, uint32_t &lm, uint32_t &um) {
+  lm = d <= 0 ? 0u : (d >= 32 ? kFull : ((1u << d) - 1u));
+  um = d < 0 ? kFull : (d >= 31 ? 0u : (kFull << (d + 1)));
 }
 
 struct Slot {
@@ -208,14 +214,124 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
   }
 }
 
-__device__ __forceinline__ void split_masks(int d, uint32_t &lm, uint32_t &um) {
-  lm = d <= 0 ? 0u : (d >= 32 ? kFull : ((1u << d) - 1u));
-  um = d < 0 ? kFull : (d >= 31 ? 0u : (kFull << (d + 1)));
+
+// Extraction of a group's rows from its in-structure bitmap (touched lines
+// only, ascending), staging reservation (one atomic per group) and write-out;
+// zeroes the bitmap lines it reads.  All kWarps warps of the CTA take part.
+// warp w owns isum words [w*q, (w+1)*q): its lines are ascending and all of
+// them precede warp w+1's, so per-warp counts give the write offsets.
+template <int kWarps>
+__device__ __forceinline__ void stage_rows(const StreamParams &p, uint32_t *is, uint32_t *isum,
+                                           int s0g, int nsrc, int g, int lane, int warp,
+                                           uint32_t (*s_cnt)[2][32], long long *s_rowoff,
+                                           int *s_nL, int *s_ok, bool write) {
+  const int n = p.n;
+  const int isw = (n + 1023) >> 10;
+  const int q = (isw + kWarps - 1) / kWarps;
+  const int wa = min(isw, warp * q), wb = min(isw, wa + q);
+  const int s_lane = s0g + lane;
+  if (write) {
+    uint32_t cl = 0, cu = 0;
+    for (int i = wa; i < wb; ++i) {
+      uint32_t x = __ldcg(isum + i);
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1u;
+        const int v0 = ((i << 5) + b) << 5;
+        const uint32_t word = (v0 + lane < n) ? __ldcg(is + v0 + lane) : 0u;
+        const uint32_t y = transpose32(word, lane);
+        uint32_t lm, um;
+        split_masks(s_lane - v0, lm, um);
+        cl += __popc(y & lm);
+        cu += __popc(y & um);
+      }
+    }
+    s_cnt[warp][0][lane] = cl;
+    s_cnt[warp][1][lane] = cu;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t nl = 0, nu = 0;
+      for (int w2 = 0; w2 < kWarps; ++w2) {
+        nl += s_cnt[w2][0][lane];
+        nu += s_cnt[w2][1][lane];
+      }
+      const bool valid = lane < nsrc;
+      if (valid) nu += 1;  // the diagonal (P:313)
+      const long long sz = valid ? (long long)nl + nu : 0;
+      long long inc = sz;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const long long y = __shfl_up_sync(kFull, inc, d);
+        if (lane >= d) inc += y;
+      }
+      const long long tot = __shfl_sync(kFull, inc, 31);
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(p.stage_cursor, (unsigned long long)tot);
+      base = __shfl_sync(kFull, base, 0);
+      const bool ok = base + (unsigned long long)tot <= p.stage_cap;
+      if (valid) {
+        const long long off = (long long)base + inc - sz;
+        s_rowoff[lane] = off;
+        s_nL[lane] = (int)nl;
+        const int r = s_lane - p.row_begin;
+        p.row_off[r] = ok ? off : -1;
+        p.row_nL[r] = (int)nl;
+        p.row_nU[r] = (int)nu;
+        if (ok) p.stage[off + nl] = s_lane;  // U(s,:) starts with the diagonal
+      }
+      if (lane == 0) {
+        *s_ok = ok;
+        if (!ok) {
+          p.failed[atomicAdd(p.nfailed, 1)] = g;
+          atomicAdd(p.failed_need, (unsigned long long)tot);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const bool ok = write && *s_ok;
+  long long pl = 0, pu = 0;
+  if (ok)
+    for (int w2 = 0; w2 < warp; ++w2) {
+      pl += s_cnt[w2][0][lane];
+      pu += s_cnt[w2][1][lane];
+    }
+  const bool valid = lane < nsrc;
+  int32_t *Lp = p.stage + (valid && ok ? s_rowoff[lane] + pl : 0);
+  int32_t *Up = p.stage + (valid && ok ? s_rowoff[lane] + s_nL[lane] + 1 + pu : 0);
+  for (int i = wa; i < wb; ++i) {
+    uint32_t x = __ldcg(isum + i);
+    if (!x) continue;
+    if (lane == 0) isum[i] = 0u;
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1u;
+      const int v0 = ((i << 5) + b) << 5;
+      const uint32_t word = (v0 + lane < n) ? __ldcg(is + v0 + lane) : 0u;
+      if (v0 + lane < n) is[v0 + lane] = 0u;
+      if (ok) {
+        const uint32_t y = transpose32(word, lane);
+        uint32_t lm, um;
+        split_masks(s_lane - v0, lm, um);
+        uint32_t yl = y & lm, yu = y & um;
+        while (yl) {
+          *Lp++ = v0 + __ffs(yl) - 1;
+          yl &= yl - 1u;
+        }
+        while (yu) {
+          *Up++ = v0 + __ffs(yu) - 1;
+          yu &= yu - 1u;
+        }
+      }
+    }
+  }
 }
 
-template <int kWarps>
-__global__ void __launch_bounds__(kWarps * 32, kWarps == kLightWarps ? 8 : 2)
-    stream_kernel(StreamParams p, int slot_base, int heavy) {
+// Lockstep kernel: the 32 sources of a group share frontier items (one bit
+// each); a group that runs longer than p.abort_cycles is abandoned -- its
+// slot is cleaned -- and handed to the solo kernel through the heavy queue.
+__global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParams p) {
+  constexpr int kWarps = kLightWarps;
   constexpr int kThreads = kWarps * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   const int n = p.n, Vmax = p.Vmax;
@@ -223,7 +339,7 @@ __global__ void __launch_bounds__(kWarps * 32, kWarps == kLightWarps ? 8 : 2)
   const int rsw = (Vmax + 1023) >> 10;
   const int isw = (n + 1023) >> 10;
   Slot sl;
-  const size_t slot = (size_t)slot_base + blockIdx.x;
+  const size_t slot = blockIdx.x;
   sl.state = p.ws + slot * p.ws_words;
   sl.thr = sl.state + 2 * (size_t)Vmax;
   sl.rsum = sl.thr + tbw_max;
@@ -238,28 +354,22 @@ __global__ void __launch_bounds__(kWarps * 32, kWarps == kLightWarps ? 8 : 2)
   __shared__ uint32_t s_cnt[kWarps][2][32];
   __shared__ long long s_rowoff[32];
   __shared__ int s_nL[32];
-  __shared__ int s_ok;
+  __shared__ int s_ok, s_abort;
   Counters c = {0, 0, 0, 0, 0, 0u};
 
   for (;;) {
     if (tid == 0) {
-      // heaviest first: group ngroups-1-j is the j-th taken; the heavy kernel
-      // owns the first n_heavy of them, then helps with the rest
+      // heaviest first: group ngroups-1-j is the j-th taken (work grows
+      // with the source id)
       int gg = -1;
+      const int j = (int)atomicAdd(p.group_ctr, 1u);
       if (p.group_list) {
-        const int j = (int)atomicAdd(p.group_ctr, 1u);
         if (j < p.list_len) gg = p.group_list[j];
-      } else {
-        if (heavy) {
-          const int j = (int)atomicAdd(p.ctr_heavy, 1u);
-          if (j < p.n_heavy) gg = p.ngroups - 1 - j;
-        }
-        if (gg < 0) {
-          const int j = (int)atomicAdd(p.group_ctr, 1u) + p.n_heavy;
-          if (j < p.ngroups) gg = p.ngroups - 1 - j;
-        }
+      } else if (j < p.ngroups) {
+        gg = p.ngroups - 1 - j;
       }
       s_g = gg;
+      s_abort = 0;
       s_qn[0] = s_qn[1] = 0;
       for (int i = 0; i < 3; ++i) s_scan[i] = s_minfill[i] = INT_MAX;
     }
@@ -310,7 +420,9 @@ __global__ void __launch_bounds__(kWarps * 32, kWarps == kLightWarps ? 8 : 2)
       const int T = min(s_scan[cur3], s_minfill[cur3]);
       if (T == INT_MAX) break;
       c.steps += 1;
+      if (tid == 0) s_abort = p.abort_cycles > 0 && clock64() - t_start > p.abort_cycles;
       __syncthreads();  // all threads are done with the previous step's s_qn / T
+      if (s_abort) break;
       if (tid == 0) {
         s_scan[(step + 2) % 3] = INT_MAX;
         s_minfill[(step + 2) % 3] = INT_MAX;
@@ -349,108 +461,12 @@ __global__ void __launch_bounds__(kWarps * 32, kWarps == kLightWarps ? 8 : 2)
     }
 
     __syncthreads();  // every thread's REDs were fenced at its last closure end
+    const bool aborted = s_abort;
     t_trav = clock64();
-    // ---- extraction of the group's rows (touched IS lines, ascending)
-    // warp w owns isum words [w*q, (w+1)*q): its lines are ascending and all
-    // of them precede warp w+1's, so per-warp counts give the write offsets
-    const int q = (isw + kWarps - 1) / kWarps;
-    const int wa = min(isw, warp * q), wb = min(isw, wa + q);
-    const int s_lane = s0g + lane;
-    uint32_t cl = 0, cu = 0;
-    for (int i = wa; i < wb; ++i) {
-      uint32_t x = __ldcg(sl.isum + i);
-      while (x) {
-        const int b = __ffs(x) - 1;
-        x &= x - 1u;
-        const int v0 = ((i << 5) + b) << 5;
-        const uint32_t word = (v0 + lane < n) ? __ldcg(sl.is + v0 + lane) : 0u;
-        const uint32_t y = transpose32(word, lane);
-        uint32_t lm, um;
-        split_masks(s_lane - v0, lm, um);
-        cl += __popc(y & lm);
-        cu += __popc(y & um);
-      }
-    }
-    s_cnt[warp][0][lane] = cl;
-    s_cnt[warp][1][lane] = cu;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t nl = 0, nu = 0;
-      for (int w2 = 0; w2 < kWarps; ++w2) {
-        nl += s_cnt[w2][0][lane];
-        nu += s_cnt[w2][1][lane];
-      }
-      const bool valid = lane < nsrc;
-      if (valid) nu += 1;  // the diagonal (P:313)
-      const long long sz = valid ? (long long)nl + nu : 0;
-      long long inc = sz;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const long long y = __shfl_up_sync(kFull, inc, d);
-        if (lane >= d) inc += y;
-      }
-      const long long tot = __shfl_sync(kFull, inc, 31);
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(p.stage_cursor, (unsigned long long)tot);
-      base = __shfl_sync(kFull, base, 0);
-      const bool ok = base + (unsigned long long)tot <= p.stage_cap;
-      if (valid) {
-        const long long off = (long long)base + inc - sz;
-        s_rowoff[lane] = off;
-        s_nL[lane] = (int)nl;
-        const int r = s_lane - p.row_begin;
-        p.row_off[r] = ok ? off : -1;
-        p.row_nL[r] = (int)nl;
-        p.row_nU[r] = (int)nu;
-        if (ok) p.stage[off + nl] = s_lane;  // U(s,:) starts with the diagonal
-      }
-      if (lane == 0) {
-        s_ok = ok;
-        if (!ok) {
-          p.failed[atomicAdd(p.nfailed, 1)] = g;
-          atomicAdd(p.failed_need, (unsigned long long)tot);
-        }
-      }
-    }
-    __syncthreads();
-    {
-      const bool ok = s_ok;
-      long long pl = 0, pu = 0;
-      for (int w2 = 0; w2 < warp; ++w2) {
-        pl += s_cnt[w2][0][lane];
-        pu += s_cnt[w2][1][lane];
-      }
-      const bool valid = lane < nsrc;
-      int32_t *Lp = p.stage + (valid && ok ? s_rowoff[lane] + pl : 0);
-      int32_t *Up = p.stage + (valid && ok ? s_rowoff[lane] + s_nL[lane] + 1 + pu : 0);
-      for (int i = wa; i < wb; ++i) {
-        uint32_t x = __ldcg(sl.isum + i);
-        if (!x) continue;
-        if (lane == 0) sl.isum[i] = 0u;
-        while (x) {
-          const int b = __ffs(x) - 1;
-          x &= x - 1u;
-          const int v0 = ((i << 5) + b) << 5;
-          const uint32_t word = (v0 + lane < n) ? __ldcg(sl.is + v0 + lane) : 0u;
-          if (v0 + lane < n) sl.is[v0 + lane] = 0u;
-          const uint32_t y = transpose32(word, lane);
-          if (ok) {
-            uint32_t lm, um;
-            split_masks(s_lane - v0, lm, um);
-            uint32_t yl = y & lm, yu = y & um;
-            while (yl) {
-              *Lp++ = v0 + __ffs(yl) - 1;
-              yl &= yl - 1u;
-            }
-            while (yu) {
-              *Up++ = v0 + __ffs(yu) - 1;
-              yu &= yu - 1u;
-            }
-          }
-        }
-      }
-    }
+    stage_rows<kWarps>(p, sl.is, sl.isum, s0g, nsrc, g, lane, warp, s_cnt, s_rowoff, s_nL, &s_ok,
+                       !aborted);
     t_ext = clock64();
+    __syncthreads();  // extraction done in every warp before the reset below
     // ---- reset the touched state lines (reached; pend is already 0) and thr
     {
       const int qr = (rsw + kWarps - 1) / kWarps;
@@ -471,18 +487,30 @@ __global__ void __launch_bounds__(kWarps * 32, kWarps == kLightWarps ? 8 : 2)
     // the clears above are plain stores; the next group's atomics on the same
     // words are performed at L2, so make the stores globally visible first
     __threadfence();
-    if (p.group_trace && lane == 0) {
-      long long *t = p.group_trace + 8 * (size_t)g;
-      // per-warp item / pair counts are summed over the warps' lane 0
-      atomicAdd((unsigned long long *)&t[2], (unsigned long long)(c.items - it0));
-      atomicAdd((unsigned long long *)&t[6], (unsigned long long)(c.pairs - pr0));
-      if (warp == 0) {
-        t[0] = (long long)(c.steps - st0);
-        t[1] = (long long)(c.levels - lv0);
-        t[3] = clock64() - t_start;
-        t[4] = t_trav - t_start;
-        t[5] = t_ext - t_trav;
+    if (aborted) {
+      // hand the group to the solo kernel (it restarts from the seed)
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned idx = atomicAdd(p.hq_tail, 1u);
+        p.hq[idx] = g;
+        __threadfence();
+        atomicExch(p.hq_ready + idx, 1);
       }
+    } else {
+      if (p.group_trace && lane == 0) {
+        long long *t = p.group_trace + 8 * (size_t)g;
+        atomicAdd((unsigned long long *)&t[2], (unsigned long long)(c.items - it0));
+        atomicAdd((unsigned long long *)&t[6], (unsigned long long)(c.pairs - pr0));
+        if (warp == 0) {
+          t[0] = (long long)(c.steps - st0);
+          t[1] = (long long)(c.levels - lv0);
+          t[3] = clock64() - t_start;
+          t[4] = t_trav - t_start;
+          t[5] = t_ext - t_trav;
+          t[7] = 0;  // lockstep kernel
+        }
+      }
+      if (tid == 0) atomicAdd(p.done, 1u);
     }
     __syncthreads();
   }
@@ -502,6 +530,305 @@ __global__ void __launch_bounds__(kWarps * 32, kWarps == kLightWarps ? 8 : 2)
     atomicAdd(p.stats + 3, c.steps);
   }
   if (p.n < 0) p.stats[7] = c.sink;  // never true; keeps the returning atomics
+}
+
+// ---------------------------------------------------------------- solo kernel
+// Heavy groups (rows of top separators, hub rows): their 32 sources share
+// almost no frontier items in threshold order, so lockstep only makes every
+// source wait for the union of all thresholds.  Here warp k runs source
+// s0g + k on its own: its own threshold bitmap + summary (global), its own
+// append-only closure queue (tail in a register), no CTA barriers during the
+// traversal.  The reached and in-structure words are still shared (bit k).
+constexpr int kSoloBatch = 2;
+
+struct SoloSlot {
+  uint32_t *reached, *rsum, *thr, *tsum, *queue, *is, *isum;
+};
+
+__device__ __forceinline__ int solo_scan_next(const uint32_t *thr, const uint32_t *tsum, int tbw,
+                                              int T, int lane) {
+  const int start = T + 1;
+  const int wi = start >> 5;
+  if (wi >= tbw) return INT_MAX;
+  uint32_t x = 0u;
+  if (lane == 0) x = __ldcg(thr + wi) & (kFull << (start & 31));
+  x = __shfl_sync(kFull, x, 0);
+  if (x) return (wi << 5) + __ffs(x) - 1;
+  const int nw = wi + 1;
+  const int tsw = (tbw + 31) >> 5;
+  for (int si = nw >> 5; si < tsw; si += 32) {
+    const int idx = si + lane;
+    uint32_t y = idx < tsw ? __ldcg(tsum + idx) : 0u;
+    if (si == (nw >> 5) && lane == 0) y &= kFull << (nw & 31);
+    const uint32_t b = __ballot_sync(kFull, y != 0u);
+    if (b) {
+      const int l = __ffs(b) - 1;
+      const uint32_t yl = __shfl_sync(kFull, y, l);
+      const int word = ((si + l) << 5) + __ffs(yl) - 1;
+      const uint32_t z = __ldcg(thr + word);
+      return (word << 5) + __ffs(z) - 1;
+    }
+  }
+  return INT_MAX;
+}
+
+// one source, one warp: expand the items u (one per lane, -1 = none) of the
+// closure of T; closure members are appended to q at `tail` (warp-uniform)
+__device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
+                                            uint32_t *thr, uint32_t *tsum, uint32_t *q, int &tail,
+                                            int s, uint32_t bit, int T, int u, int lane,
+                                            Counters &c) {
+  int beg = 0, deg = 0;
+  if (u >= 0) {
+    beg = __ldg(p.rowptr + u);
+    deg = __ldg(p.rowptr + u + 1) - beg;
+  }
+  c.items += u >= 0;
+  c.pairs += (unsigned long long)deg;
+  c.edges += (unsigned long long)deg;
+  int incl = deg;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const int total = __shfl_sync(kFull, incl, 31);
+  const int excl = incl - deg;
+  for (int f0 = 0; f0 < total; f0 += 32 * kSoloBatch) {
+    int w[kSoloBatch];
+    uint32_t ro[kSoloBatch], io[kSoloBatch];
+#pragma unroll
+    for (int k = 0; k < kSoloBatch; ++k) {
+      const int f = f0 + 32 * k + lane;
+      int o = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int cand = o + step;
+        const int e = __shfl_sync(kFull, excl, cand & 31);
+        if (cand < 32 && e <= f) o = cand;
+      }
+      const int ob = __shfl_sync(kFull, beg, o);
+      const int oe = __shfl_sync(kFull, excl, o);
+      w[k] = f < total ? __ldg(p.colidx + ob + (f - oe)) : s;
+      // w > s: entry of U; w < s: atomicMin(maxId(w), T) = first reach
+      ro[k] = w[k] < s ? atomicOr(sl.reached + w[k], bit) : bit;
+      io[k] = w[k] > s ? atomicOr(sl.is + w[k], bit) : kFull;
+    }
+    bool push[kSoloBatch];
+#pragma unroll
+    for (int k = 0; k < kSoloBatch; ++k) {
+      push[k] = false;
+      if (io[k] == 0u) atomicOr(sl.isum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));  // RED
+      if (!(ro[k] & bit)) {
+        if (ro[k] == 0u) atomicOr(sl.rsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));  // RED
+        if (w[k] > T) {
+          // fill of L(s,:) (R4); w becomes a threshold of this source
+          atomicOr(sl.is + w[k], bit);                                                // RED
+          atomicOr(sl.isum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));                 // RED
+          const uint32_t t = atomicOr(thr + (w[k] >> 5), 1u << (w[k] & 31));
+          if (t == 0u) c.sink ^= atomicOr(tsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));
+          c.sink ^= t;
+        } else {
+          push[k] = true;  // maxId(w) = T, not in the structure: continue with T
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kSoloBatch; ++k) {
+      const uint32_t pb = __ballot_sync(kFull, push[k]);
+      if (push[k]) q[tail + __popc(pb & lanemask_lt())] = (uint32_t)w[k];
+      tail += __popc(pb);
+    }
+  }
+}
+
+__device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s, int k,
+                                            int lane, Counters &c) {
+  const uint32_t bit = 1u << k;
+  const int tbw_max = (p.Vmax + 31) >> 5;
+  const int tsw_max = (tbw_max + 31) >> 5;
+  uint32_t *thr = sl.thr + (size_t)k * tbw_max;
+  uint32_t *tsum = sl.tsum + (size_t)k * tsw_max;
+  uint32_t *q = sl.queue + (size_t)k * p.Vmax;
+  const int tbw = (s + 31) >> 5;  // thresholds are < s
+  // seed
+  const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
+  for (int j = beg + lane; j < end; j += 32) {
+    const int w = __ldg(p.colidx + j);
+    if (w == s) continue;
+    atomicOr(sl.is + w, bit);                                  // RED
+    atomicOr(sl.isum + (w >> 10), 1u << ((w >> 5) & 31));      // RED
+    if (w < s) {
+      if (atomicOr(sl.reached + w, bit) == 0u) atomicOr(sl.rsum + (w >> 10), 1u << ((w >> 5) & 31));
+      const uint32_t t = atomicOr(thr + (w >> 5), 1u << (w & 31));
+      if (t == 0u) c.sink ^= atomicOr(tsum + (w >> 10), 1u << ((w >> 5) & 31));
+      c.sink ^= t;
+    }
+  }
+  __syncwarp();
+  int T = -1;
+  for (;;) {
+    T = solo_scan_next(thr, tsum, tbw, T, lane);
+    if (T == INT_MAX) break;
+    c.steps += 1;
+    int head = 0, tail = 0;
+    int u = lane == 0 ? T : -1;
+    for (;;) {
+      c.levels += 1;
+      solo_expand(p, sl, thr, tsum, q, tail, s, bit, T, u, lane, c);
+      __syncwarp();
+      if (head >= tail) break;
+      const int cnt = min(32, tail - head);
+      u = lane < cnt ? (int)q[head + lane] : -1;
+      head += cnt;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSoloWarps * 32, 2) solo_kernel(StreamParams p) {
+  constexpr int kWarps = kSoloWarps;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  const int n = p.n, Vmax = p.Vmax;
+  const int tbw_max = (Vmax + 31) >> 5;
+  const int tsw_max = (tbw_max + 31) >> 5;
+  const int rsw = (Vmax + 1023) >> 10;
+  SoloSlot sl;
+  uint32_t *base = p.hws + (size_t)blockIdx.x * p.hws_words;
+  sl.reached = base;
+  sl.rsum = sl.reached + ((Vmax + 3) & ~3);
+  sl.thr = sl.rsum + ((rsw + 3) & ~3);
+  sl.tsum = sl.thr + (size_t)32 * tbw_max;
+  sl.queue = sl.tsum + (size_t)32 * tsw_max;
+  sl.is = p.is + ((size_t)p.light_slots + blockIdx.x) * p.is_words;
+  sl.isum = sl.is + n;
+
+  __shared__ int s_g;
+  __shared__ uint32_t s_cnt[kWarps][2][32];
+  __shared__ long long s_rowoff[32];
+  __shared__ int s_nL[32];
+  __shared__ int s_ok;
+  Counters c = {0, 0, 0, 0, 0, 0u};
+
+  for (;;) {
+    if (tid == 0) {
+      // queued heavy groups first, then fresh groups (heaviest first); exit
+      // once every group is done
+      int gg = -1;
+      for (;;) {
+        const unsigned h = *(volatile unsigned *)p.hq_head;
+        const unsigned t = *(volatile unsigned *)p.hq_tail;
+        if (h < t) {
+          if (atomicCAS(p.hq_head, h, h + 1) == h) {
+            while (*(volatile int *)(p.hq_ready + h) == 0) __nanosleep(200);
+            gg = *(volatile int *)(p.hq + h);
+            break;
+          }
+          continue;
+        }
+        if (*(volatile unsigned *)p.group_ctr < (unsigned)p.ngroups) {
+          const int j = (int)atomicAdd(p.group_ctr, 1u);
+          if (j < p.ngroups) {
+            gg = p.ngroups - 1 - j;
+            break;
+          }
+        }
+        if (*(volatile unsigned *)p.done >= (unsigned)p.ngroups) break;
+        __nanosleep(1000);
+      }
+      s_g = gg;
+    }
+    __syncthreads();
+    const int g = s_g;
+    if (g < 0) break;
+    const long long t_start = clock64();
+    const unsigned long long st0 = c.steps, lv0 = c.levels, it0 = c.items, pr0 = c.pairs;
+    const int s0g = p.row_begin + 32 * g;
+    const int nsrc = min(32, p.row_end - s0g);
+    if (warp < nsrc) solo_source(p, sl, s0g + warp, warp, lane, c);
+    fence_gpu();
+    __syncthreads();
+    if (p.debug && warp == 0) {
+      for (int i = lane; i < Vmax; i += 32) {
+        const uint32_t v = __ldcg(sl.reached + i);
+        if (v && !((__ldcg(sl.rsum + (i >> 10)) >> ((i >> 5) & 31)) & 1)) {
+          const int slot_i = atomicAdd(p.debug, 1);
+          if (slot_i < 8) {
+            p.debug[1 + 4 * slot_i] = g;
+            p.debug[2 + 4 * slot_i] = i;
+            p.debug[3 + 4 * slot_i] = (int)v;
+            p.debug[4 + 4 * slot_i] = 2000 + (int)blockIdx.x;  // missing rsum bit
+          }
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    const long long t_trav = clock64();
+    stage_rows<kWarps>(p, sl.is, sl.isum, s0g, nsrc, g, lane, warp, s_cnt, s_rowoff, s_nL, &s_ok,
+                       true);
+    const long long t_ext = clock64();
+    __syncthreads();  // extraction done in every warp before the reset below
+    // reset the touched lines: reached, and every source's thr word / tsum word
+    for (int i = warp; i < rsw; i += kWarps) {
+      uint32_t x = __ldcg(sl.rsum + i);
+      if (!x) continue;
+      if (lane == 0) sl.rsum[i] = 0u;
+      sl.tsum[(size_t)lane * tsw_max + i] = 0u;  // summary word of lines [32i, 32i+32)
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1u;
+        const int line = (i << 5) + b;
+        sl.reached[(line << 5) + lane] = 0u;
+        sl.thr[(size_t)lane * tbw_max + line] = 0u;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (p.debug && warp == 0) {
+      for (int i = lane; i < Vmax; i += 32)
+        if (__ldcg(sl.reached + i)) {
+          const int slot_i = atomicAdd(p.debug, 1);
+          if (slot_i < 8) {
+            p.debug[1 + 4 * slot_i] = g;
+            p.debug[2 + 4 * slot_i] = i;
+            p.debug[3 + 4 * slot_i] = (int)__ldcg(sl.reached + i);
+            p.debug[4 + 4 * slot_i] = 3000 + (int)blockIdx.x;  // left after the reset
+          }
+          break;
+        }
+    }
+    if (p.group_trace && lane == 0) {
+      long long *tr = p.group_trace + 8 * (size_t)g;
+      atomicAdd((unsigned long long *)&tr[2], (unsigned long long)(c.items - it0));
+      atomicAdd((unsigned long long *)&tr[6], (unsigned long long)(c.pairs - pr0));
+      atomicMax((unsigned long long *)&tr[0], (unsigned long long)(c.steps - st0));
+      atomicMax((unsigned long long *)&tr[1], (unsigned long long)(c.levels - lv0));
+      if (warp == 0) {
+        tr[3] = clock64() - t_start;
+        tr[4] = t_trav - t_start;
+        tr[5] = t_ext - t_trav;
+        tr[7] = 1;  // solo kernel
+      }
+    }
+    if (tid == 0) atomicAdd(p.done, 1u);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    c.items += __shfl_xor_sync(kFull, c.items, d);
+    c.edges += __shfl_xor_sync(kFull, c.edges, d);
+    c.pairs += __shfl_xor_sync(kFull, c.pairs, d);
+    c.levels += __shfl_xor_sync(kFull, c.levels, d);
+    c.steps += __shfl_xor_sync(kFull, c.steps, d);
+  }
+  if (lane == 0) {
+    atomicAdd(p.stats + 0, c.items);
+    atomicAdd(p.stats + 1, c.edges);
+    atomicAdd(p.stats + 4, c.pairs);
+    atomicAdd(p.stats + 2, c.levels / 32);  // every lane counted the warp's levels
+    atomicAdd(p.stats + 3, c.steps / 32);
+  }
+  if (p.n < 0) p.stats[7] = c.sink;
 }
 
 // copies each staged row into the final CSR arrays (warp per row)
@@ -535,44 +862,69 @@ size_t stream_smem_bytes(int64_t Vmax) {
   return (size_t)((((Vmax + 31) / 32) + 31) / 32) * 4;
 }
 
-template <int W>
-int max_blocks_t(int device, int64_t Vmax) {
+int stream_max_blocks(int device, int64_t Vmax, int heavy) {
   int sms = 0, per = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
-  const size_t smem = stream_smem_bytes(Vmax);
-  if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(stream_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess)
-    return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_kernel<W>, W * 32, smem) != cudaSuccess)
-    return 0;
+  cudaError_t e;
+  if (heavy) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solo_kernel, kSoloWarps * 32, 0);
+  } else {
+    const size_t smem = stream_smem_bytes(Vmax);
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+      return 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_kernel, kLightWarps * 32, smem);
+  }
+  if (e != cudaSuccess) return 0;
   return sms * per;
 }
 
-int stream_max_blocks(int device, int64_t Vmax, int heavy) {
-  return heavy ? max_blocks_t<kHeavyWarps>(device, Vmax) : max_blocks_t<kLightWarps>(device, Vmax);
+int stream_heavy_ratio() { return kSoloWarps / kLightWarps; }
+
+// lockstep CTAs that still fit on an SM next to one solo CTA
+int stream_light_per_sm_with_solo(int device, int64_t Vmax) {
+  cudaFuncAttributes fs, fl;
+  if (cudaFuncGetAttributes(&fs, solo_kernel) != cudaSuccess ||
+      cudaFuncGetAttributes(&fl, stream_kernel) != cudaSuccess)
+    return 0;
+  int regs = 0, warps = 0, smem_sm = 0;
+  cudaDeviceGetAttribute(&regs, cudaDevAttrMaxRegistersPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&warps, cudaDevAttrMaxThreadsPerMultiProcessor, device);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  warps /= 32;
+  const int solo_regs = ((fs.numRegs * 32 + 255) / 256 * 256) * kSoloWarps;
+  const int light_regs = ((fl.numRegs * 32 + 255) / 256 * 256) * kLightWarps;
+  const int by_regs = (regs - solo_regs) / light_regs;
+  const int by_warps = (warps - kSoloWarps) / kLightWarps;
+  const size_t light_smem = fl.sharedSizeBytes + stream_smem_bytes(Vmax) + 1024;
+  const int by_smem = (int)((smem_sm - fs.sharedSizeBytes - 1024) / light_smem);
+  return std::max(0, std::min(std::min(by_regs, by_warps), by_smem));
 }
 
-int stream_heavy_ratio() { return kHeavyWarps / kLightWarps; }
+size_t solo_ws_words(int64_t Vmax) {
+  const size_t tbw = (size_t)((Vmax + 31) / 32), tsw = (tbw + 31) / 32;
+  const size_t rsw = (size_t)((Vmax + 1023) / 1024);
+  const size_t w = (((size_t)Vmax + 3) & ~(size_t)3) + ((rsw + 3) & ~(size_t)3) + 32 * tbw +
+                   32 * tsw + 32 * (size_t)Vmax;
+  return (w + 7) / 8 * 8;
+}
 
-cudaError_t launch_stream(const StreamParams &p, int grid, int heavy, int slot_base, cudaStream_t st) {
+cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st) {
   if (grid <= 0) return cudaSuccess;
   const size_t smem = stream_smem_bytes(p.Vmax);
-  if (heavy) {
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(stream_kernel<kHeavyWarps>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-    }
-    stream_kernel<kHeavyWarps><<<grid, kHeavyWarps * 32, smem, st>>>(p, slot_base, 1);
-  } else {
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(stream_kernel<kLightWarps>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-    }
-    stream_kernel<kLightWarps><<<grid, kLightWarps * 32, smem, st>>>(p, slot_base, 0);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
   }
+  stream_kernel<<<grid, kLightWarps * 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st) {
+  if (grid <= 0) return cudaSuccess;
+  solo_kernel<<<grid, kSoloWarps * 32, 0, st>>>(p);
   return cudaGetLastError();
 }
 

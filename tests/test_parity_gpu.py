@@ -36,12 +36,14 @@ def run(rp, ci, ctx=None, **kw):
     return a
 
 
-def assert_full_equal(got, want):
+def assert_full_equal(got, want, tag=""):
     for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start"):
         assert got[k].dtype == want[k].dtype, k
-        assert np.array_equal(got[k], want[k]), k
+        if not np.array_equal(got[k], want[k]):
+            bad = np.nonzero(got[k][:min(got[k].size, want[k].size)] != want[k][:min(got[k].size, want[k].size)])[0]
+            raise AssertionError(f"{tag} {k} differs (sizes {got[k].size}/{want[k].size}, first at {bad[:5]})")
     for k in ("nnz_L", "nnz_U", "nsuper", "fill_count", "nnz_A_offdiag"):
-        assert got[k] == want[k], k
+        assert got[k] == want[k], (tag, k)
 
 
 def assert_rows_equal(got, rp, ci, rows, nthreads=None):
@@ -101,7 +103,7 @@ def test_config_shapes_full(ctx, name, scale):
     want = oracle.symbolic(rp, ci)
     for kw in (dict(), dict(max_concurrent=32), dict(schedule="fifo"),
                dict(schedule="fifo", fill_first=True, max_concurrent=96)):
-        assert_full_equal(run(rp, ci, ctx, **kw), want)
+        assert_full_equal(run(rp, ci, ctx, **kw), want, tag=f"{name}-{scale} {kw}")
 
 
 @pytest.mark.parametrize("schedule", ["threshold", "fifo"])
@@ -217,3 +219,21 @@ def test_full_config_sampled(ctx, name):
     assert got["nnz_A_offdiag"] == ci.size
     assert_rows_equal(got, rp, ci, sample_rows(n, k=96, top=32 if name == "C5" else 64))
     assert_supernodes_consistent(got)
+
+
+# ------------------------------------------- schedule paths of the streaming
+# kernel: lockstep-only, every group handed to the solo kernel, and repeated
+# calls on one context (the workspace must be left clean by every group)
+
+@pytest.mark.parametrize("mode", ["default", "lockstep_only", "all_solo"])
+def test_stream_paths_repeated(mode, monkeypatch):
+    if mode == "lockstep_only":
+        monkeypatch.setenv("GSOFA_SOLO_CTAS", "0")
+    if mode == "all_solo":
+        monkeypatch.setenv("GSOFA_ABORT_MS", "0.00001")
+    cases = [gen.config("C4", 60), gen.config("C5", 14), gen.config("C3", 2000)]
+    wants = [oracle.symbolic(rp, ci) for rp, ci in cases]
+    with g.Context(0) as c:
+        for rep in range(3):
+            for (rp, ci), want in zip(cases, wants):
+                assert_full_equal(run(rp, ci, c), want, tag=f"{mode} rep {rep} n={rp.size - 1}")
