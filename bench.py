@@ -114,23 +114,21 @@ def fills_of_rows(rp, ci, r):
 
 
 def cpu_oracle_sample(rp, ci, target_s: float, seed: int = 0):
-    """Run the (untuned) oracle on every k-th row, k chosen so the run takes
-    about target_s seconds on this host.  Returns (fills/s, desc, threads)."""
+    """Run the (untuned) oracle on every k-th row of the workload, halving k
+    until one run takes at least ~target_s/2 seconds on this host (or all rows
+    are covered).  Returns (fill-ins/s, description, threads, seconds)."""
     import oracle
     n = rp.size - 1
     threads = oracle.default_threads()
-    k = max(1, n // 64)
-    probe_rows = np.arange(k // 2, n, k, dtype=np.int64)
-    t = time.perf_counter()
-    oracle.rows(rp, ci, probe_rows, threads)
-    dt = max(time.perf_counter() - t, 1e-3)
-    per_row = dt / probe_rows.size
-    want = int(min(n, max(probe_rows.size, target_s / per_row)))
-    stride = max(1, n // want)
-    rows = np.arange(stride // 2, n, stride, dtype=np.int64)
-    t = time.perf_counter()
-    r = oracle.rows(rp, ci, rows, threads)
-    dt = time.perf_counter() - t
+    stride = max(1, n // 256)
+    while True:
+        rows = np.arange(stride // 2, n, stride, dtype=np.int64)
+        t = time.perf_counter()
+        r = oracle.rows(rp, ci, rows, threads)
+        dt = time.perf_counter() - t
+        if dt >= target_s / 2 or stride == 1:
+            break
+        stride = max(1, int(stride / max(2.0, min(16.0, target_s / 2 / max(dt, 1e-3)))))
     r["rows"] = rows
     fills, _ = fills_of_rows(rp, ci, r)
     desc = (f"every {stride}-th row ({rows.size} of {n} rows, uniform over the row range), "
@@ -231,7 +229,8 @@ def main():
         if re > rb:
             res = g.symbolic(*src, row_begin=rb, row_end=re, outputs_on_device=not host, **kw)
             if host:
-                res.to_numpy()  # results already in host memory; materialise the arrays
+                arrs = res.to_numpy(copy=False)  # the CSR arrays, in (pinned) host memory
+                assert arrs["L_rowptr"].size == res.rows + 1
         if world > 1:
             local_counts = np.zeros(len(gd.COUNT_FIELDS), np.int64)
             if res is not None:

@@ -172,7 +172,17 @@ class Result:
                     U_rowptr=(self.rows + 1, np.int64), U_colidx=(self.nnz_U, np.int32),
                     sn_start=(self.nsuper + 1, np.int32))
 
-    def to_numpy(self):
+    def to_numpy(self, copy: bool = True):
+        """Arrays as numpy.  Host results with copy=False are zero-copy views
+        of the library's (pinned) storage, valid until :meth:`free`."""
+        if not self.on_device and not copy:
+            r = self._p.contents
+            views = {}
+            for k, (sz, dt) in self._sizes().items():
+                ptr = getattr(r, k)
+                views[k] = (np.ctypeslib.as_array(ptr, shape=(max(sz, 1),))[:sz] if sz
+                            else np.empty(0, dt))
+            return views
         if self._arrays is None:
             out = {k: np.empty(sz, dt) for k, (sz, dt) in self._sizes().items()}
             self._copy(out)

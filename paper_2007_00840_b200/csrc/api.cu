@@ -62,6 +62,28 @@ bool is_device_ptr(const void *p) {
 
 }  // namespace
 
+// Pinned host block for host-side results, shared by a context (its pool)
+// and by the results that point into it; freed when the last owner lets go.
+struct HostBlock {
+  char *p = nullptr;
+  size_t cap = 0;
+  int refs = 0;
+  bool in_use = false;  // handed to a live result
+};
+
+void host_block_release(HostBlock *b) {
+  if (b && --b->refs == 0) {
+    if (b->p) cudaFreeHost(b->p);
+    delete b;
+  }
+}
+
+// a result and its bookkeeping; the public struct is the first member
+struct ResultImpl {
+  gsofa_result r;
+  HostBlock *block;  // pinned host storage of the arrays (host results)
+};
+
 // ------------------------------------------------------------------ context
 struct gsofa_context {
   int device = 0;
@@ -95,6 +117,7 @@ struct gsofa_context {
   int32_t *in_colidx = nullptr, *rowptr32 = nullptr;
   size_t in_rowptr_cap = 0, in_colidx_cap = 0, rowptr32_cap = 0;
   int64_t *h_small = nullptr;  // pinned host scratch
+  HostBlock *hpool = nullptr;  // pinned storage reused by host-side results
 };
 
 namespace {
@@ -448,6 +471,7 @@ void gsofa_context_destroy(gsofa_context *c) {
   if (c->rowptr32) cudaFree(c->rowptr32);
   if (c->stage) cudaFree(c->stage);
   if (c->h_small) cudaFreeHost(c->h_small);
+  host_block_release(c->hpool);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->stream2) cudaStreamDestroy(c->stream2);
   delete c;
@@ -487,15 +511,19 @@ int gsofa_result_copy(const gsofa_result *r, int64_t *L_rowptr, int32_t *L_colid
 
 void gsofa_result_free(gsofa_result *r) {
   if (!r) return;
+  ResultImpl *impl = reinterpret_cast<ResultImpl *>(r);
   void *ptrs[5] = {r->L_rowptr, r->L_colidx, r->U_rowptr, r->U_colidx, r->sn_start};
   if (r->on_device) {
     cudaSetDevice(r->device);
     for (void *p : ptrs)
       if (p) cudaFree(p);
+  } else if (impl->block) {
+    impl->block->in_use = false;
+    host_block_release(impl->block);
   } else {
     for (void *p : ptrs) std::free(p);
   }
-  std::free(r);
+  std::free(impl);
 }
 
 int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const int32_t *colidx,
@@ -1002,7 +1030,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   }
   e_sn1 = ev();
   // ---------------------------------------------------- result
-  res = (gsofa_result *)std::calloc(1, sizeof(gsofa_result));
+  res = (gsofa_result *)std::calloc(1, sizeof(ResultImpl));
   if (!res) {
     rc = GSOFA_ENOMEM;
     goto fail;
@@ -1042,15 +1070,48 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   } else {
     res->on_device = 0;
     const size_t nl = (size_t)res->nnz_L, nu = (size_t)res->nnz_U, ns = (size_t)res->nsuper + 1;
-    res->L_rowptr = (int64_t *)std::malloc((rows + 1) * sizeof(int64_t));
-    res->U_rowptr = (int64_t *)std::malloc((rows + 1) * sizeof(int64_t));
-    res->L_colidx = (int32_t *)std::malloc(std::max<size_t>(nl, 1) * sizeof(int32_t));
-    res->U_colidx = (int32_t *)std::malloc(std::max<size_t>(nu, 1) * sizeof(int32_t));
-    res->sn_start = (int32_t *)std::malloc(ns * sizeof(int32_t));
-    if (!res->L_rowptr || !res->U_rowptr || !res->L_colidx || !res->U_colidx || !res->sn_start) {
-      set_detail("host output allocation failed");
-      rc = GSOFA_ENOMEM;
-      goto fail;
+    // pinned host storage (fast D2H), reused from the context pool when the
+    // previous host result has been freed
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t need = al((rows + 1) * 8) * 2 + al(std::max<size_t>(nl, 1) * 4) +
+                        al(std::max<size_t>(nu, 1) * 4) + al(ns * 4);
+    HostBlock *blk = c->hpool;
+    if (!blk || blk->in_use || blk->cap < need) {
+      if (blk && !blk->in_use) {  // too small: drop it
+        host_block_release(blk);
+        c->hpool = blk = nullptr;
+      }
+      HostBlock *nb = new (std::nothrow) HostBlock();
+      if (!nb || cudaMallocHost((void **)&nb->p, need + need / 8) != cudaSuccess) {
+        cudaGetLastError();
+        delete nb;
+        set_detail("pinned host output allocation failed");
+        rc = GSOFA_ENOMEM;
+        goto fail;
+      }
+      nb->cap = need + need / 8;
+      nb->refs = 1;  // the result's reference
+      if (!c->hpool) {
+        c->hpool = nb;
+        nb->refs = 2;  // + the pool's
+      }
+      blk = nb;
+    } else {
+      blk->refs += 1;
+    }
+    blk->in_use = true;
+    reinterpret_cast<ResultImpl *>(res)->block = blk;
+    {
+      char *q = blk->p;
+      res->L_rowptr = (int64_t *)q;
+      q += al((rows + 1) * 8);
+      res->U_rowptr = (int64_t *)q;
+      q += al((rows + 1) * 8);
+      res->L_colidx = (int32_t *)q;
+      q += al(std::max<size_t>(nl, 1) * 4);
+      res->U_colidx = (int32_t *)q;
+      q += al(std::max<size_t>(nu, 1) * 4);
+      res->sn_start = (int32_t *)q;
     }
     const int eh0 = ev();
     CK(cudaMemcpyAsync(res->L_rowptr, Lrp, (rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -1111,12 +1172,10 @@ fail:
   if (Uci) cudaFree(Uci);
   if (sn) cudaFree(sn);
   if (res) {
-    if (!res->on_device) {
-      std::free(res->L_rowptr);
-      std::free(res->U_rowptr);
-      std::free(res->L_colidx);
-      std::free(res->U_colidx);
-      std::free(res->sn_start);
+    ResultImpl *impl = reinterpret_cast<ResultImpl *>(res);
+    if (impl->block) {
+      impl->block->in_use = false;
+      host_block_release(impl->block);
     }
     std::free(res);
   }
