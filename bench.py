@@ -202,11 +202,22 @@ def main():
     import paper_2007_00840_b200 as g
     from paper_2007_00840_b200 import dist as gd
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    shared = world > ndev  # dev smoke test: several ranks on one GPU
+    dev_index = local % ndev
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    coll_dev = dev
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            # NCCL needs one GPU per rank; for a single-GPU smoke test of the
+            # multi-rank path the count allgather goes over gloo instead
+            dist.init_process_group("gloo")
+            coll_dev = None
+            log(f"[rank {rank}] {world} ranks share {ndev} GPU(s): gloo collectives (smoke test only)")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     t0 = time.perf_counter()
     rp, ci = gen.config(args.config)
@@ -217,7 +228,7 @@ def main():
     rb, re = int(bounds[rank]), int(bounds[rank + 1])
     d_rp = torch.from_numpy(rp).to(dev)
     d_ci = torch.from_numpy(ci).to(dev)
-    ctx = g.Context(local)
+    ctx = g.Context(dev_index)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -236,7 +247,7 @@ def main():
             if res is not None:
                 local_counts[:] = [res.nnz_L, res.nnz_U, res.fill_count, res.nsuper,
                                    res.nnz_A_offdiag, re - rb]
-            counts = gd.allgather_counts(local_counts, device=dev)
+            counts = gd.allgather_counts(local_counts, device=coll_dev)
             fills = int(counts[:, 2].sum())
         else:
             fills = res.fill_count
@@ -253,7 +264,7 @@ def main():
     torch.cuda.synchronize(dev)
     step_ms, stats_acc, launches = [], {}, 0
     fills_step = 0
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (256 MiB > 126 MB L2), untimed
             e0 = torch.cuda.Event(enable_timing=True)
@@ -273,7 +284,7 @@ def main():
         dist.barrier()
     tot_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([tot_ms, float(launches)], dtype=torch.float64, device=dev)
+        t = torch.tensor([tot_ms, float(launches)], dtype=torch.float64, device=coll_dev or "cpu")
         tmax = t.clone()
         dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
         dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
@@ -303,7 +314,8 @@ def main():
             r.free()
     e2e_step = statistics.median(e2e_ms)
     if world > 1:
-        t = torch.tensor([e2e_step, float(h2d), float(d2h)], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_step, float(h2d), float(d2h)], dtype=torch.float64,
+                         device=coll_dev or "cpu")
         m = t.clone()
         dist.all_reduce(m[:1], op=dist.ReduceOp.MAX)
         dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
@@ -333,6 +345,7 @@ def main():
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                "dtype": "int32", "data": "synthetic (gen.config, seeded; no datasets)",
                "config": {"workload": CONFIG_DESC[args.config], "n": n, "nnz_offdiag": int(ci.size),
+                          "row_ranges": [int(b) for b in bounds],
                           "fill_ins": fills_step, "schedule": args.schedule,
                           "parallelism": f"rows split over {world} GPU(s)" if world > 1 else "1 GPU",
                           "l2": "flushed between timed steps (256 MiB write, untimed)"},

@@ -218,11 +218,15 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
   const int64_t res_light = gsofa::stream_max_blocks(device, Vmax, 0);
   const int64_t res_heavy = gsofa::stream_max_blocks(device, Vmax, 1);
   if (res_light < 1) return false;
-  // one solo CTA per SM (half of its warps); lockstep CTAs fill the rest
-  int64_t heavy = std::min<int64_t>(std::min<int64_t>(sms, res_heavy), ngroups);
+  // solo CTAs: one per SM is resident next to the lockstep CTAs from the
+  // start; a second wave becomes resident as lockstep CTAs finish and joins
+  // the heavy queue (the grid is deliberately larger than the first wave)
+  int64_t heavy = std::min<int64_t>(2 * (int64_t)sms, ngroups);
+  (void)res_heavy;
   if (const char *e = std::getenv("GSOFA_SOLO_CTAS")) heavy = std::min<int64_t>(heavy, atoll(e));
   heavy = std::max<int64_t>(0, std::min<int64_t>(heavy, (int64_t)(((size_t)budget - fixed) / 2 / per_heavy)));
   int64_t light = heavy > 0 ? (int64_t)sms * gsofa::stream_light_per_sm_with_solo(device, Vmax) : res_light;
+  if (res_heavy < 1) heavy = 0;
   light = std::min<int64_t>(light, res_light);
   light = std::min<int64_t>(light, (int64_t)(((size_t)budget - fixed - heavy * per_heavy) / per_light));
   light = std::max<int64_t>(1, std::min<int64_t>(light, ngroups));
@@ -783,10 +787,10 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
         CK(cudaEventCreateWithFlags(&ea, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&eb, cudaEventDisableTiming));
         CK(cudaEventRecord(ea, st));
+        CK(gsofa::launch_stream(sp, (int)grid, st));  // lockstep CTAs first
         CK(cudaStreamWaitEvent(c->stream2, ea, 0));
         CK(gsofa::launch_solo(sp, (int)plan.heavy, c->stream2));
         CK(cudaEventRecord(eb, c->stream2));
-        CK(gsofa::launch_stream(sp, (int)grid, st));
         CK(cudaStreamWaitEvent(st, eb, 0));
         cudaEventDestroy(ea);
         cudaEventDestroy(eb);
@@ -853,12 +857,12 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       }
       for (int64_t sl = 0; sl < plan.heavy && reported < 16; ++sl) {
         const uint32_t *b = hw.data() + plan.light * plan.ws_words + sl * plan.hws_words;
-        const size_t rs0 = (Vm + 3) & ~(size_t)3, th0 = rs0 + ((rsw + 3) & ~(size_t)3);
+        const size_t rs0 = 2 * ((Vm + 3) & ~(size_t)3), th0 = rs0 + ((rsw + 3) & ~(size_t)3);
         const size_t ts0 = th0 + 32 * tbw, q0 = ts0 + 32 * tsw;
         for (size_t i = 0; i < q0 && reported < 16; ++i)
           if (b[i]) {
             std::fprintf(stderr, "[dirty] solo slot %lld word %zu (%s) = %08x\n", (long long)sl, i,
-                         i < rs0 ? "reached" : (i < th0 ? "rsum" : (i < ts0 ? "thr" : "tsum")), b[i]);
+                         i < rs0 ? "reached/pend" : (i < th0 ? "rsum" : (i < ts0 ? "thr" : "tsum")), b[i]);
             ++reported;
           }
       }

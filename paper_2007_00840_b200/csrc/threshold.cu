@@ -541,8 +541,16 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
 // traversal.  The reached and in-structure words are still shared (bit k).
 constexpr int kSoloBatch = 2;
 
+// closure ring capacity per source: a power of two, at most 64k entries
+__host__ __device__ inline int solo_ring(int64_t Vmax) {
+  int r = 1024;
+  while (r < 65536 && r < Vmax) r <<= 1;
+  return r;
+}
+
 struct SoloSlot {
-  uint32_t *reached, *rsum, *thr, *tsum, *queue, *is, *isum;
+  uint32_t *reached, *pend, *rsum, *thr, *tsum, *queue, *is, *isum;
+  int qmask;  // ring capacity - 1 (power of two)
 };
 
 __device__ __forceinline__ int solo_scan_next(const uint32_t *thr, const uint32_t *tsum, int tbw,
@@ -575,9 +583,9 @@ __device__ __forceinline__ int solo_scan_next(const uint32_t *thr, const uint32_
 // one source, one warp: expand the items u (one per lane, -1 = none) of the
 // closure of T; closure members are appended to q at `tail` (warp-uniform)
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
-                                            uint32_t *thr, uint32_t *tsum, uint32_t *q, int &tail,
-                                            int s, uint32_t bit, int T, int u, int lane,
-                                            Counters &c) {
+                                            uint32_t *thr, uint32_t *tsum, uint32_t *q, int head,
+                                            int &tail, bool &spilled, int s, uint32_t bit, int T,
+                                            int u, int lane, Counters &c) {
   int beg = 0, deg = 0;
   if (u >= 0) {
     beg = __ldg(p.rowptr + u);
@@ -635,9 +643,18 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
     }
 #pragma unroll
     for (int k = 0; k < kSoloBatch; ++k) {
+      // ring of closure items; when it is full the item is parked in pend
+      // (bit k) and picked up by a rescan once the ring drains
       const uint32_t pb = __ballot_sync(kFull, push[k]);
-      if (push[k]) q[tail + __popc(pb & lanemask_lt())] = (uint32_t)w[k];
-      tail += __popc(pb);
+      const int pos = tail + __popc(pb & lanemask_lt());
+      const bool fits = pos - head <= sl.qmask;
+      if (push[k]) {
+        if (fits) q[pos & sl.qmask] = (uint32_t)w[k];
+        else c.sink ^= atomicOr(sl.pend + w[k], bit);
+      }
+      const uint32_t fb = __ballot_sync(kFull, push[k] && fits);
+      tail += __popc(fb);
+      spilled |= __ballot_sync(kFull, push[k] && !fits) != 0u;
     }
   }
 }
@@ -649,7 +666,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
   const int tsw_max = (tbw_max + 31) >> 5;
   uint32_t *thr = sl.thr + (size_t)k * tbw_max;
   uint32_t *tsum = sl.tsum + (size_t)k * tsw_max;
-  uint32_t *q = sl.queue + (size_t)k * p.Vmax;
+  uint32_t *q = sl.queue + (size_t)k * (sl.qmask + 1);
   const int tbw = (s + 31) >> 5;  // thresholds are < s
   // seed
   const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
@@ -672,14 +689,38 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
     if (T == INT_MAX) break;
     c.steps += 1;
     int head = 0, tail = 0;
+    bool spilled = false;
     int u = lane == 0 ? T : -1;
     for (;;) {
       c.levels += 1;
-      solo_expand(p, sl, thr, tsum, q, tail, s, bit, T, u, lane, c);
+      solo_expand(p, sl, thr, tsum, q, head, tail, spilled, s, bit, T, u, lane, c);
       __syncwarp();
+      if (head >= tail && spilled) {
+        // the ring overflowed during this closure: move parked items (pend
+        // bit k, all below T) back into the ring, as many as fit
+        spilled = false;
+        for (int b0 = 0; b0 < T; b0 += 32) {
+          const int v = b0 + lane;
+          const bool has = v < T && (__ldcg(sl.pend + v) & bit);
+          const uint32_t hb = __ballot_sync(kFull, has);
+          if (!hb) continue;
+          const int pos = tail + __popc(hb & lanemask_lt());
+          const bool fits = pos - head <= sl.qmask;
+          if (has && fits) {
+            c.sink ^= atomicAnd(sl.pend + v, ~bit);
+            q[pos & sl.qmask] = (uint32_t)v;
+          }
+          tail += __popc(__ballot_sync(kFull, has && fits));
+          if (__ballot_sync(kFull, has && !fits)) {
+            spilled = true;  // still more parked: rescan after this batch drains
+            break;
+          }
+        }
+        __syncwarp();
+      }
       if (head >= tail) break;
       const int cnt = min(32, tail - head);
-      u = lane < cnt ? (int)q[head + lane] : -1;
+      u = lane < cnt ? (int)q[(head + lane) & sl.qmask] : -1;
       head += cnt;
     }
   }
@@ -695,7 +736,9 @@ __global__ void __launch_bounds__(kSoloWarps * 32, 2) solo_kernel(StreamParams p
   SoloSlot sl;
   uint32_t *base = p.hws + (size_t)blockIdx.x * p.hws_words;
   sl.reached = base;
-  sl.rsum = sl.reached + ((Vmax + 3) & ~3);
+  sl.pend = sl.reached + ((Vmax + 3) & ~3);
+  sl.rsum = sl.pend + ((Vmax + 3) & ~3);
+  sl.qmask = solo_ring(Vmax) - 1;
   sl.thr = sl.rsum + ((rsw + 3) & ~3);
   sl.tsum = sl.thr + (size_t)32 * tbw_max;
   sl.queue = sl.tsum + (size_t)32 * tsw_max;
@@ -905,8 +948,8 @@ int stream_light_per_sm_with_solo(int device, int64_t Vmax) {
 size_t solo_ws_words(int64_t Vmax) {
   const size_t tbw = (size_t)((Vmax + 31) / 32), tsw = (tbw + 31) / 32;
   const size_t rsw = (size_t)((Vmax + 1023) / 1024);
-  const size_t w = (((size_t)Vmax + 3) & ~(size_t)3) + ((rsw + 3) & ~(size_t)3) + 32 * tbw +
-                   32 * tsw + 32 * (size_t)Vmax;
+  const size_t w = 2 * (((size_t)Vmax + 3) & ~(size_t)3) + ((rsw + 3) & ~(size_t)3) + 32 * tbw +
+                   32 * tsw + 32 * (size_t)solo_ring(Vmax);
   return (w + 7) / 8 * 8;
 }
 
