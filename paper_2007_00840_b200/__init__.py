@@ -74,10 +74,11 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("GSOFA_LIB", LIB_PATH)  # dev: A/B a variant build
+    if not os.path.exists(path):
         raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
                           "(nvcc -gencode arch=compute_100a,code=sm_100a)")
-    lib = ctypes.CDLL(LIB_PATH)
+    lib = ctypes.CDLL(path)
     lib.gsofa_default_opts.argtypes = [_P(Opts)]
     lib.gsofa_context_create.argtypes = [_I32, _I64, _P(ctypes.c_void_p)]
     lib.gsofa_context_destroy.argtypes = [ctypes.c_void_p]
