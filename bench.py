@@ -326,9 +326,19 @@ def main():
     trav_ms = stats_acc.get("ms_traverse", 0.0)
     alg = algorithmic_bytes(stats_acc, args.schedule) if stats_acc else 0
     achieved = alg / (trav_ms / 1e3) / 1e9 if trav_ms > 0 else 0.0
-    roofline = {"kernel": "threshold_kernel" if args.schedule == "threshold" else "traverse_kernel",
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        ent = tj.get(f"{args.config}/{args.schedule}")
+        if ent:
+            traffic = {"dram_bytes_per_launch": ent["dram_bytes"], "kernel": ent["kernel"],
+                       "source": ent["source"]}
+    except Exception:
+        pass
+    roofline = {"kernel": ("solo_kernel+stream_kernel" if args.schedule == "threshold"
+                           else "traverse_kernel"),
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_step": alg / args.steps,
                 "kernel_ms_per_step": trav_ms / args.steps,
                 "kernel_share_of_step": (trav_ms / args.steps) / ms_per_step if ms_per_step else None}
