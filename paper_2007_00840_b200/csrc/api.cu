@@ -215,7 +215,8 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const int64_t ngroups = ceil_div(rows, 32);
-  const int64_t res_light = gsofa::stream_max_blocks(device, Vmax, 0);
+  const int64_t wpc = gsofa::stream_warps_per_cta();  // lockstep slots (warps) per CTA
+  const int64_t res_light = gsofa::stream_max_blocks(device, Vmax, 0) * wpc;
   const int64_t res_heavy = gsofa::stream_max_blocks(device, Vmax, 1);
   if (res_light < 1) return false;
   // solo CTAs: one per SM is resident next to the lockstep CTAs from the
@@ -225,9 +226,11 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
   (void)res_heavy;
   if (const char *e = std::getenv("GSOFA_SOLO_CTAS")) heavy = std::min<int64_t>(heavy, atoll(e));
   heavy = std::max<int64_t>(0, std::min<int64_t>(heavy, (int64_t)(((size_t)budget - fixed) / 2 / per_heavy)));
-  int64_t light = heavy > 0 ? (int64_t)sms * gsofa::stream_light_per_sm_with_solo(device, Vmax) : res_light;
+  int64_t light = heavy > 0 ? (int64_t)sms * gsofa::stream_light_per_sm_with_solo(device, Vmax) * wpc
+                            : res_light;
   if (res_heavy < 1) heavy = 0;
   light = std::min<int64_t>(light, res_light);
+  if (const char *e = std::getenv("GSOFA_LIGHT_CTAS")) light = std::min<int64_t>(light, atoll(e));
   light = std::min<int64_t>(light, (int64_t)(((size_t)budget - fixed - heavy * per_heavy) / per_light));
   light = std::max<int64_t>(1, std::min<int64_t>(light, ngroups));
   if ((size_t)light * per_light + (size_t)heavy * per_heavy + fixed > (size_t)budget) return false;
@@ -734,6 +737,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.is = c->is;
     sp.is_words = plan.slot_is_words;
     sp.group_ctr = group_ctr;
+    sp.solo_ctr = c->qcount + 5;
+    sp.solo_top = 0;
     sp.group_list = nullptr;
     sp.list_len = 0;
     sp.stage = c->stage;
@@ -748,6 +753,12 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.stats = c->stats;
     sp.group_trace = nullptr;
     sp.debug = nullptr;
+    sp.prof = nullptr;
+    const char *prof_path = std::getenv("GSOFA_PROF");  // dev: cycle accounting (-DGSOFA_PROF builds)
+    if (prof_path && cudaMallocAsync((void **)&sp.prof, 16 * 8, st) == cudaSuccess)
+      cudaMemsetAsync(sp.prof, 0, 16 * 8, st);
+    else
+      cudaGetLastError();
     if (std::getenv("GSOFA_CHECK_CLEAN")) {
       cudaMallocAsync((void **)&sp.debug, 256, st);
       cudaMemsetAsync(sp.debug, 0, 256, st);
@@ -771,6 +782,13 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.light_slots = (int32_t)plan.light;
     sp.abort_cycles = 0;
     if (plan.heavy > 0) {
+      // the heaviest groups (top separator / hub rows) start on
+      // the solo kernel: one per first-wave solo CTA (one per SM)
+      int sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      int64_t top = std::min<int64_t>(plan.heavy, sms);
+      if (const char *e = std::getenv("GSOFA_SOLO_TOP")) top = std::min<int64_t>(plan.heavy, atoll(e));
+      sp.solo_top = (int32_t)std::min<int64_t>(top, ngroups);
       double ms = 5.0;
       if (const char *e = std::getenv("GSOFA_ABORT_MS")) ms = atof(e);
       int khz = 0;
@@ -787,7 +805,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
         CK(cudaEventCreateWithFlags(&ea, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&eb, cudaEventDisableTiming));
         CK(cudaEventRecord(ea, st));
-        CK(gsofa::launch_stream(sp, (int)grid, st));  // lockstep CTAs first
+        CK(gsofa::launch_stream(sp, (int)ceil_div(grid, gsofa::stream_warps_per_cta()), st));  // lockstep first
         CK(cudaStreamWaitEvent(c->stream2, ea, 0));
         CK(gsofa::launch_solo(sp, (int)plan.heavy, c->stream2));
         CK(cudaEventRecord(eb, c->stream2));
@@ -796,7 +814,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
         cudaEventDestroy(eb);
         launches += 2;
       } else {
-        CK(gsofa::launch_stream(sp, (int)std::max<int64_t>(grid, 1), st));
+        CK(gsofa::launch_stream(sp, (int)ceil_div(std::max<int64_t>(grid, 1), gsofa::stream_warps_per_cta()),
+                                st));
         ++launches;
       }
       e_trav.push_back({et0, ev()});
@@ -826,6 +845,17 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       sp.list_len = nf;
       grid = std::min<int64_t>(plan.light, nf);
       sp.abort_cycles = 0;  // retries run on the lockstep kernel alone
+      sp.solo_top = 0;
+    }
+    if (sp.prof) {
+      unsigned long long h[16];
+      cudaMemcpyAsync(h, sp.prof, sizeof h, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      if (FILE *f = std::fopen(prof_path, "ab")) {
+        std::fwrite(h, 8, 16, f);
+        std::fclose(f);
+      }
+      cudaFreeAsync(sp.prof, st);
     }
     if (sp.group_trace) {
       std::vector<long long> h((size_t)ngroups * 8);

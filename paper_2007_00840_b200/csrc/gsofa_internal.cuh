@@ -63,6 +63,8 @@ struct StreamParams {
   uint32_t *is;              // [slots][is_words]: is[n] | isum[n/1024]
   size_t is_words;
   unsigned int *group_ctr;   // next fresh group (global counter, heaviest first)
+  unsigned int *solo_ctr;    // next of the solo_top heaviest groups (solo kernel only)
+  int32_t solo_top;          // groups ngroups-solo_top.. start on the solo kernel
   // heavy path: groups abandoned by the lockstep kernel after abort_cycles
   // are queued for the solo kernel (one warp per source)
   long long abort_cycles;    // 0: never abandon
@@ -86,11 +88,13 @@ struct StreamParams {
   unsigned long long *stats; // items, edges, levels, thresholds, pairs
   long long *group_trace;    // optional [ngroups][8]: steps, levels, items, cycles, ...
   int *debug;                // optional dev checks
+  unsigned long long *prof;  // optional [16] solo-kernel cycle accounting (GSOFA_PROF builds)
 };
 size_t stream_ws_words(int64_t Vmax);
 size_t stream_is_words(int64_t n);
 int stream_max_blocks(int device, int64_t Vmax, int heavy);
 int stream_heavy_ratio();  // warps of a solo CTA / warps of a lockstep CTA
+int stream_warps_per_cta();  // lockstep slots (one group per warp) per CTA
 size_t solo_ws_words(int64_t Vmax);
 int stream_light_per_sm_with_solo(int device, int64_t Vmax);
 size_t stream_smem_bytes(int64_t Vmax);  // dynamic smem: threshold-word summary

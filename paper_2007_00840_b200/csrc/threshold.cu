@@ -220,7 +220,7 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
 // zeroes the bitmap lines it reads.  All kWarps warps of the CTA take part.
 // warp w owns isum words [w*q, (w+1)*q): its lines are ascending and all of
 // them precede warp w+1's, so per-warp counts give the write offsets.
-template <int kWarps>
+template <int kWarps, bool kWarpOnly = false>
 __device__ __forceinline__ void stage_rows(const StreamParams &p, uint32_t *is, uint32_t *isum,
                                            int s0g, int nsrc, int g, int lane, int warp,
                                            uint32_t (*s_cnt)[2][32], long long *s_rowoff,
@@ -248,7 +248,7 @@ __device__ __forceinline__ void stage_rows(const StreamParams &p, uint32_t *is, 
     }
     s_cnt[warp][0][lane] = cl;
     s_cnt[warp][1][lane] = cu;
-    __syncthreads();
+    if (kWarpOnly) __syncwarp(); else __syncthreads();
     if (warp == 0) {
       uint32_t nl = 0, nu = 0;
       for (int w2 = 0; w2 < kWarps; ++w2) {
@@ -287,7 +287,7 @@ __device__ __forceinline__ void stage_rows(const StreamParams &p, uint32_t *is, 
         }
       }
     }
-    __syncthreads();
+    if (kWarpOnly) __syncwarp(); else __syncthreads();
   }
   const bool ok = write && *s_ok;
   long long pl = 0, pu = 0;
@@ -365,8 +365,8 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
       const int j = (int)atomicAdd(p.group_ctr, 1u);
       if (p.group_list) {
         if (j < p.list_len) gg = p.group_list[j];
-      } else if (j < p.ngroups) {
-        gg = p.ngroups - 1 - j;
+      } else if (j < p.ngroups - p.solo_top) {
+        gg = p.ngroups - p.solo_top - 1 - j;  // the top solo_top go to the solo kernel
       }
       s_g = gg;
       s_abort = 0;
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
     __syncthreads();  // every thread's REDs were fenced at its last closure end
     const bool aborted = s_abort;
     t_trav = clock64();
-    stage_rows<kWarps>(p, sl.is, sl.isum, s0g, nsrc, g, lane, warp, s_cnt, s_rowoff, s_nL, &s_ok,
+    stage_rows<kWarps, false>(p, sl.is, sl.isum, s0g, nsrc, g, lane, warp, s_cnt, s_rowoff, s_nL, &s_ok,
                        !aborted);
     t_ext = clock64();
     __syncthreads();  // extraction done in every warp before the reset below
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
 // s0g + k on its own: its own threshold bitmap + summary (global), its own
 // append-only closure queue (tail in a register), no CTA barriers during the
 // traversal.  The reached and in-structure words are still shared (bit k).
-constexpr int kSoloBatch = 2;
+constexpr int kSoloBatch = 1;
 
 // closure ring capacity per source: a power of two, at most 64k entries
 __host__ __device__ inline int solo_ring(int64_t Vmax) {
@@ -580,20 +580,45 @@ __device__ __forceinline__ int solo_scan_next(const uint32_t *thr, const uint32_
   return INT_MAX;
 }
 
-// one source, one warp: expand the items u (one per lane, -1 = none) of the
-// closure of T; closure members are appended to q at `tail` (warp-uniform)
+// Per-warp shared memory of the solo kernel.
+//   win[32]   a window of 32 words (1024 vertices) of this source's threshold
+//             bitmap, starting at word wb: thresholds found while the window
+//             covers them are set here with shared-memory atomics, so finding
+//             the next threshold costs no global round trip; thresholds beyond
+//             the window go to the global bitmap + summary (REDs), published
+//             by one fence when the window moves on
+//   q*[kSoloQ] closure worklist: (w, rowptr[w], rowptr[w+1]); the row
+//             pointers were loaded together with the atomic that reached w,
+//             so expanding w needs one dependent load (colidx) and one atomic
+//             round trip per level.  Overflow goes to the global ring (vertex
+//             only), then to the pend bitmap.
+constexpr int kSoloQ = 64;
+struct SoloWarpSmem {
+  uint32_t win[32];
+  int qw[kSoloQ], qb[kSoloQ], qe[kSoloQ];
+};
+
+// per-thread counters of the solo kernel, 32-bit, flushed after every group
+struct SoloCounters {
+  uint32_t items, pairs, levels, steps, sink;
+};
+
+struct SoloQueue {
+  int sh, st;      // shared-memory worklist head / tail (warp-uniform)
+  int gh, gt;      // global ring head / tail
+  bool spilled;    // items parked in pend (bit k)
+};
+
+// one source, one warp: expand the items u (one per lane, -1 = none; beg/end
+// = its adjacency range) of the closure of T
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
-                                            uint32_t *thr, uint32_t *tsum, uint32_t *q, int head,
-                                            int &tail, bool &spilled, int s, uint32_t bit, int T,
-                                            int u, int lane, Counters &c) {
-  int beg = 0, deg = 0;
-  if (u >= 0) {
-    beg = __ldg(p.rowptr + u);
-    deg = __ldg(p.rowptr + u + 1) - beg;
-  }
+                                            uint32_t *thr, uint32_t *tsum, uint32_t *q,
+                                            SoloWarpSmem &sw, int wb, SoloQueue &Q, int s,
+                                            uint32_t bit, int T, int u, int beg, int end, int lane,
+                                            SoloCounters &c) {
+  const int deg = u >= 0 ? end - beg : 0;
   c.items += u >= 0;
-  c.pairs += (unsigned long long)deg;
-  c.edges += (unsigned long long)deg;
+  c.pairs += (uint32_t)deg;
   int incl = deg;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -603,7 +628,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
   const int total = __shfl_sync(kFull, incl, 31);
   const int excl = incl - deg;
   for (int f0 = 0; f0 < total; f0 += 32 * kSoloBatch) {
-    int w[kSoloBatch];
+    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch];
     uint32_t ro[kSoloBatch], io[kSoloBatch];
 #pragma unroll
     for (int k = 0; k < kSoloBatch; ++k) {
@@ -621,6 +646,12 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       // w > s: entry of U; w < s: atomicMin(maxId(w), T) = first reach
       ro[k] = w[k] < s ? atomicOr(sl.reached + w[k], bit) : bit;
       io[k] = w[k] > s ? atomicOr(sl.is + w[k], bit) : kFull;
+      // w < T may join the closure: its row pointers travel with the atomic
+      rb[k] = re[k] = 0;
+      if (w[k] < T) {
+        rb[k] = __ldg(p.rowptr + w[k]);
+        re[k] = __ldg(p.rowptr + w[k] + 1);
+      }
     }
     bool push[kSoloBatch];
 #pragma unroll
@@ -633,9 +664,13 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
           // fill of L(s,:) (R4); w becomes a threshold of this source
           atomicOr(sl.is + w[k], bit);                                                // RED
           atomicOr(sl.isum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));                 // RED
-          const uint32_t t = atomicOr(thr + (w[k] >> 5), 1u << (w[k] & 31));
-          if (t == 0u) c.sink ^= atomicOr(tsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));
-          c.sink ^= t;
+          const int d = (w[k] >> 5) - wb;
+          if (d < 32) {
+            atomicOr(&sw.win[d], 1u << (w[k] & 31));  // smem (d >= 0: w > T >= 32 wb)
+          } else {
+            atomicOr(thr + (w[k] >> 5), 1u << (w[k] & 31));                            // RED
+            atomicOr(tsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));                   // RED
+          }
         } else {
           push[k] = true;  // maxId(w) = T, not in the structure: continue with T
         }
@@ -643,24 +678,68 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
     }
 #pragma unroll
     for (int k = 0; k < kSoloBatch; ++k) {
-      // ring of closure items; when it is full the item is parked in pend
-      // (bit k) and picked up by a rescan once the ring drains
+      // shared worklist first, then the global ring, then park in pend
       const uint32_t pb = __ballot_sync(kFull, push[k]);
-      const int pos = tail + __popc(pb & lanemask_lt());
-      const bool fits = pos - head <= sl.qmask;
-      if (push[k]) {
-        if (fits) q[pos & sl.qmask] = (uint32_t)w[k];
-        else c.sink ^= atomicOr(sl.pend + w[k], bit);
+      if (!pb) continue;
+      const int pos = Q.st + __popc(pb & lanemask_lt());
+      const bool in_s = pos - Q.sh < kSoloQ;
+      if (push[k] && in_s) {
+        const int i = pos & (kSoloQ - 1);
+        sw.qw[i] = w[k];
+        sw.qb[i] = rb[k];
+        sw.qe[i] = re[k];
       }
-      const uint32_t fb = __ballot_sync(kFull, push[k] && fits);
-      tail += __popc(fb);
-      spilled |= __ballot_sync(kFull, push[k] && !fits) != 0u;
+      const uint32_t sb = __ballot_sync(kFull, push[k] && in_s);
+      Q.st += __popc(sb);
+      const uint32_t gb = pb & ~sb;
+      if (gb) {
+        const int gpos = Q.gt + __popc(gb & lanemask_lt());
+        const bool in_g = gpos - Q.gh <= sl.qmask;
+        if (push[k] && !in_s) {
+          if (in_g) q[gpos & sl.qmask] = (uint32_t)w[k];
+          else c.sink ^= atomicOr(sl.pend + w[k], bit);
+        }
+        Q.gt += __popc(__ballot_sync(kFull, push[k] && !in_s && in_g));
+        Q.spilled |= __ballot_sync(kFull, push[k] && !in_s && !in_g) != 0u;
+      }
     }
   }
 }
 
+// Next threshold of the source above T.  Inside the window: shared memory
+// only.  Past it: publish this warp's global threshold REDs, scan the global
+// bitmap (summary-guided) and load a new window at the found threshold.
+__device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const uint32_t *tsum,
+                                                   int tbw, int T, int &wb, SoloWarpSmem &sw,
+                                                   int lane) {
+  if (wb >= 0) {
+    const int d0 = (T + 1) >> 5;  // first candidate word
+    const int rel = d0 - wb;
+    if (rel < 32) {
+      uint32_t x = lane >= rel ? sw.win[lane] : 0u;
+      if (lane == rel) x &= kFull << ((T + 1) & 31);
+      const uint32_t b = __ballot_sync(kFull, x != 0u);
+      if (b) {
+        const int l = __ffs(b) - 1;
+        const uint32_t xl = __shfl_sync(kFull, x, l);
+        return ((wb + l) << 5) + __ffs(xl) - 1;
+      }
+    }
+    T = max(T, ((wb + 32) << 5) - 1);  // the window holds nothing more
+  }
+  fence_gpu();  // this warp's global threshold REDs are visible to the scan
+  __syncwarp();
+  const int t = solo_scan_next(thr, tsum, tbw, T, lane);
+  if (t == INT_MAX) return INT_MAX;
+  wb = t >> 5;
+  __syncwarp();
+  sw.win[lane] = wb + lane < tbw ? __ldcg(thr + wb + lane) : 0u;
+  __syncwarp();
+  return t;
+}
+
 __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s, int k,
-                                            int lane, Counters &c) {
+                                            int lane, SoloCounters &c, SoloWarpSmem &sw) {
   const uint32_t bit = 1u << k;
   const int tbw_max = (p.Vmax + 31) >> 5;
   const int tsw_max = (tbw_max + 31) >> 5;
@@ -677,53 +756,107 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
     atomicOr(sl.isum + (w >> 10), 1u << ((w >> 5) & 31));      // RED
     if (w < s) {
       if (atomicOr(sl.reached + w, bit) == 0u) atomicOr(sl.rsum + (w >> 10), 1u << ((w >> 5) & 31));
-      const uint32_t t = atomicOr(thr + (w >> 5), 1u << (w & 31));
-      if (t == 0u) c.sink ^= atomicOr(tsum + (w >> 10), 1u << ((w >> 5) & 31));
-      c.sink ^= t;
+      atomicOr(thr + (w >> 5), 1u << (w & 31));               // RED
+      atomicOr(tsum + (w >> 10), 1u << ((w >> 5) & 31));      // RED
     }
   }
   __syncwarp();
+  int wb = -1;  // no window yet
   int T = -1;
+#ifdef GSOFA_PROF
+  // [0] next-threshold cycles [1] window misses [2] step-start cycles (rowptr of T)
+  // [3] expand cycles [4] worklist cycles [5] levels [6] steps [7] ring/pend levels
+  unsigned long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t0 = clock64();
+#define PROF_MARK(i) do { const long long t1 = clock64(); pr[i] += t1 - t0; t0 = t1; } while (0)
+#else
+#define PROF_MARK(i) do {} while (0)
+#endif
   for (;;) {
-    T = solo_scan_next(thr, tsum, tbw, T, lane);
+#ifdef GSOFA_PROF
+    const int wb_old = wb;
+#endif
+    T = solo_next_threshold(thr, tsum, tbw, T, wb, sw, lane);
+#ifdef GSOFA_PROF
+    pr[1] += wb != wb_old;
+    pr[6] += 1;
+#endif
+    PROF_MARK(0);
     if (T == INT_MAX) break;
     c.steps += 1;
-    int head = 0, tail = 0;
-    bool spilled = false;
-    int u = lane == 0 ? T : -1;
+    SoloQueue Q = {0, 0, 0, 0, false};
+    int u = -1, ub = 0, ue = 0;
+    if (lane == 0) {
+      u = T;
+      ub = __ldg(p.rowptr + T);
+      ue = __ldg(p.rowptr + T + 1);
+    }
+    PROF_MARK(2);
     for (;;) {
       c.levels += 1;
-      solo_expand(p, sl, thr, tsum, q, head, tail, spilled, s, bit, T, u, lane, c);
+      solo_expand(p, sl, thr, tsum, q, sw, wb, Q, s, bit, T, u, ub, ue, lane, c);
       __syncwarp();
-      if (head >= tail && spilled) {
+#ifdef GSOFA_PROF
+      pr[5] += 1;
+      if (u >= 0) c.sink ^= (uint32_t)ub;  // wait for the expand's results
+#endif
+      PROF_MARK(3);
+      if (Q.sh < Q.st) {
+        const int cnt = min(32, Q.st - Q.sh);
+        u = -1;
+        if (lane < cnt) {
+          const int i = (Q.sh + lane) & (kSoloQ - 1);
+          u = sw.qw[i];
+          ub = sw.qb[i];
+          ue = sw.qe[i];
+        }
+        Q.sh += cnt;
+        __syncwarp();
+        PROF_MARK(4);
+        continue;
+      }
+#ifdef GSOFA_PROF
+      pr[7] += Q.gh < Q.gt || Q.spilled;
+#endif
+      if (Q.gh >= Q.gt && Q.spilled) {
         // the ring overflowed during this closure: move parked items (pend
         // bit k, all below T) back into the ring, as many as fit
-        spilled = false;
+        Q.spilled = false;
         for (int b0 = 0; b0 < T; b0 += 32) {
           const int v = b0 + lane;
           const bool has = v < T && (__ldcg(sl.pend + v) & bit);
           const uint32_t hb = __ballot_sync(kFull, has);
           if (!hb) continue;
-          const int pos = tail + __popc(hb & lanemask_lt());
-          const bool fits = pos - head <= sl.qmask;
+          const int pos = Q.gt + __popc(hb & lanemask_lt());
+          const bool fits = pos - Q.gh <= sl.qmask;
           if (has && fits) {
             c.sink ^= atomicAnd(sl.pend + v, ~bit);
             q[pos & sl.qmask] = (uint32_t)v;
           }
-          tail += __popc(__ballot_sync(kFull, has && fits));
+          Q.gt += __popc(__ballot_sync(kFull, has && fits));
           if (__ballot_sync(kFull, has && !fits)) {
-            spilled = true;  // still more parked: rescan after this batch drains
+            Q.spilled = true;  // still more parked: rescan after this batch drains
             break;
           }
         }
         __syncwarp();
       }
-      if (head >= tail) break;
-      const int cnt = min(32, tail - head);
-      u = lane < cnt ? (int)q[(head + lane) & sl.qmask] : -1;
-      head += cnt;
+      if (Q.gh >= Q.gt) break;
+      const int cnt = min(32, Q.gt - Q.gh);
+      u = lane < cnt ? (int)q[(Q.gh + lane) & sl.qmask] : -1;
+      Q.gh += cnt;
+      if (u >= 0) {
+        ub = __ldg(p.rowptr + u);
+        ue = __ldg(p.rowptr + u + 1);
+      }
+      PROF_MARK(4);
     }
   }
+#ifdef GSOFA_PROF
+  if (lane == 0 && p.prof)
+    for (int i = 0; i < 8; ++i) atomicAdd(p.prof + i, pr[i]);
+#endif
+#undef PROF_MARK
 }
 
 __global__ void __launch_bounds__(kSoloWarps * 32, 2) solo_kernel(StreamParams p) {
@@ -746,18 +879,25 @@ __global__ void __launch_bounds__(kSoloWarps * 32, 2) solo_kernel(StreamParams p
   sl.isum = sl.is + n;
 
   __shared__ int s_g;
+  __shared__ SoloWarpSmem s_sw[kWarps];
   __shared__ uint32_t s_cnt[kWarps][2][32];
   __shared__ long long s_rowoff[32];
   __shared__ int s_nL[32];
   __shared__ int s_ok;
-  Counters c = {0, 0, 0, 0, 0, 0u};
+  SoloCounters c = {0u, 0u, 0u, 0u, 0u};
+  uint32_t sink = 0u;
 
   for (;;) {
     if (tid == 0) {
       // queued heavy groups first, then fresh groups (heaviest first); exit
       // once every group is done
       int gg = -1;
-      for (;;) {
+      // the solo_top heaviest groups are reserved for this kernel
+      if (*(volatile unsigned *)p.solo_ctr < (unsigned)p.solo_top) {
+        const int j = (int)atomicAdd(p.solo_ctr, 1u);
+        if (j < p.solo_top) gg = p.ngroups - 1 - j;
+      }
+      for (; gg < 0;) {
         const unsigned h = *(volatile unsigned *)p.hq_head;
         const unsigned t = *(volatile unsigned *)p.hq_tail;
         if (h < t) {
@@ -768,10 +908,11 @@ __global__ void __launch_bounds__(kSoloWarps * 32, 2) solo_kernel(StreamParams p
           }
           continue;
         }
-        if (*(volatile unsigned *)p.group_ctr < (unsigned)p.ngroups) {
+        const int nfresh = p.ngroups - p.solo_top;
+        if (*(volatile unsigned *)p.group_ctr < (unsigned)nfresh) {
           const int j = (int)atomicAdd(p.group_ctr, 1u);
-          if (j < p.ngroups) {
-            gg = p.ngroups - 1 - j;
+          if (j < nfresh) {
+            gg = nfresh - 1 - j;
             break;
           }
         }
@@ -784,10 +925,9 @@ __global__ void __launch_bounds__(kSoloWarps * 32, 2) solo_kernel(StreamParams p
     const int g = s_g;
     if (g < 0) break;
     const long long t_start = clock64();
-    const unsigned long long st0 = c.steps, lv0 = c.levels, it0 = c.items, pr0 = c.pairs;
     const int s0g = p.row_begin + 32 * g;
     const int nsrc = min(32, p.row_end - s0g);
-    if (warp < nsrc) solo_source(p, sl, s0g + warp, warp, lane, c);
+    if (warp < nsrc) solo_source(p, sl, s0g + warp, warp, lane, c, s_sw[warp]);
     fence_gpu();
     __syncthreads();
     if (p.debug && warp == 0) {
@@ -840,39 +980,43 @@ __global__ void __launch_bounds__(kSoloWarps * 32, 2) solo_kernel(StreamParams p
           break;
         }
     }
-    if (p.group_trace && lane == 0) {
-      long long *tr = p.group_trace + 8 * (size_t)g;
-      atomicAdd((unsigned long long *)&tr[2], (unsigned long long)(c.items - it0));
-      atomicAdd((unsigned long long *)&tr[6], (unsigned long long)(c.pairs - pr0));
-      atomicMax((unsigned long long *)&tr[0], (unsigned long long)(c.steps - st0));
-      atomicMax((unsigned long long *)&tr[1], (unsigned long long)(c.levels - lv0));
-      if (warp == 0) {
-        tr[3] = clock64() - t_start;
-        tr[4] = t_trav - t_start;
-        tr[5] = t_ext - t_trav;
-        tr[7] = 1;  // solo kernel
+    {
+      // flush this group's counters (warp sums; levels/steps are warp-uniform)
+      uint32_t it = c.items, pr = c.pairs;
+#pragma unroll
+      for (int d = 16; d >= 1; d >>= 1) {
+        it += __shfl_xor_sync(kFull, it, d);
+        pr += __shfl_xor_sync(kFull, pr, d);
       }
+      if (lane == 0) {
+        atomicAdd(p.stats + 0, (unsigned long long)it);
+        atomicAdd(p.stats + 1, (unsigned long long)pr);  // solo: one source per item
+        atomicAdd(p.stats + 4, (unsigned long long)pr);
+        atomicAdd(p.stats + 2, (unsigned long long)c.levels);
+        atomicAdd(p.stats + 3, (unsigned long long)c.steps);
+        if (p.group_trace) {
+          long long *tr = p.group_trace + 8 * (size_t)g;
+          atomicAdd((unsigned long long *)&tr[2], (unsigned long long)it);
+          atomicAdd((unsigned long long *)&tr[6], (unsigned long long)pr);
+          atomicMax((unsigned long long *)&tr[0], (unsigned long long)c.steps);
+          atomicMax((unsigned long long *)&tr[1], (unsigned long long)c.levels);
+          if (warp == 0) {
+            tr[3] = clock64() - t_start;
+            tr[4] = t_trav - t_start;
+            tr[5] = t_ext - t_trav;
+            tr[7] = 1;  // solo kernel
+          }
+        }
+      }
+      sink ^= c.sink;
+      c = {0u, 0u, 0u, 0u, 0u};
     }
     if (tid == 0) atomicAdd(p.done, 1u);
     __syncthreads();
   }
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) {
-    c.items += __shfl_xor_sync(kFull, c.items, d);
-    c.edges += __shfl_xor_sync(kFull, c.edges, d);
-    c.pairs += __shfl_xor_sync(kFull, c.pairs, d);
-    c.levels += __shfl_xor_sync(kFull, c.levels, d);
-    c.steps += __shfl_xor_sync(kFull, c.steps, d);
-  }
-  if (lane == 0) {
-    atomicAdd(p.stats + 0, c.items);
-    atomicAdd(p.stats + 1, c.edges);
-    atomicAdd(p.stats + 4, c.pairs);
-    atomicAdd(p.stats + 2, c.levels / 32);  // every lane counted the warp's levels
-    atomicAdd(p.stats + 3, c.steps / 32);
-  }
-  if (p.n < 0) p.stats[7] = c.sink;
+  if (p.n < 0) p.stats[7] = sink;
 }
+
 
 // copies each staged row into the final CSR arrays (warp per row)
 __global__ void gather_kernel(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,
@@ -924,6 +1068,8 @@ int stream_max_blocks(int device, int64_t Vmax, int heavy) {
 }
 
 int stream_heavy_ratio() { return kSoloWarps / kLightWarps; }
+
+int stream_warps_per_cta() { return 1; }  // slots are CTAs
 
 // lockstep CTAs that still fit on an SM next to one solo CTA
 int stream_light_per_sm_with_solo(int device, int64_t Vmax) {
