@@ -224,7 +224,9 @@ def main():
     n = rp.size - 1
     log(f"[rank {rank}] {args.config}: n={n} nnz={ci.size} generated in {time.perf_counter()-t0:.1f}s")
     chunk = 128
-    bounds = gd.partition(rp, ci, world, chunk) if world > 1 else np.array([0, n], np.int64)
+    # row-granular ranges of equal estimated work; supernodes are stitched
+    # across range boundaries by the tail chain (gsofa_supernode_stitch)
+    bounds = gd.partition(rp, ci, world) if world > 1 else np.array([0, n], np.int64)
     rb, re = int(bounds[rank]), int(bounds[rank + 1])
     d_rp = torch.from_numpy(rp).to(dev)
     d_ci = torch.from_numpy(ci).to(dev)
@@ -236,21 +238,17 @@ def main():
         kw = dict(ctx=ctx, chunk_size=chunk, schedule=args.schedule,
                   max_concurrent=args.max_concurrent, stream=stream)
         src = (h_rp, h_ci) if host else (d_rp, d_ci)
-        res = None
-        if re > rb:
-            res = g.symbolic(*src, row_begin=rb, row_end=re, outputs_on_device=not host, **kw)
-            if host:
-                arrs = res.to_numpy(copy=False)  # the CSR arrays, in (pinned) host memory
-                assert arrs["L_rowptr"].size == res.rows + 1
         if world > 1:
-            local_counts = np.zeros(len(gd.COUNT_FIELDS), np.int64)
-            if res is not None:
-                local_counts[:] = [res.nnz_L, res.nnz_U, res.fill_count, res.nsuper,
-                                   res.nnz_A_offdiag, re - rb]
-            counts = gd.allgather_counts(local_counts, device=coll_dev)
-            fills = int(counts[:, 2].sum())
+            # this rank's range, supernode-boundary chain, count allgather
+            sl = gd.symbolic_distributed(*src, bounds, rank=rank, device=coll_dev,
+                                         outputs_on_device=not host, **kw)
+            res, fills = sl.result, sl.totals["fill_count"]
         else:
+            res = g.symbolic(*src, row_begin=rb, row_end=re, outputs_on_device=not host, **kw)
             fills = res.fill_count
+        if host and res is not None:
+            arrs = res.to_numpy(copy=False)  # the CSR arrays, in (pinned) host memory
+            assert arrs["L_rowptr"].size == res.rows + 1
         return res, fills
 
     # ---- warm-up

@@ -35,9 +35,9 @@ extern "C" {
 /* ---------------------------------------------------------- error codes -- */
 #define GSOFA_OK            0
 #define GSOFA_EINVAL       -1  /* bad argument: n <= 0, NULL pointer, bad opts,
-                                  row_begin >= row_end, row_begin not a multiple
-                                  of chunk_size, max_concurrent not a multiple
-                                  of 32 */
+                                  row_begin >= row_end, max_concurrent not a
+                                  multiple of 32, a stitch tail that does not
+                                  end at row_begin - 1 */
 #define GSOFA_EBADCSR      -2  /* rowptr[0] != 0, rowptr decreasing, column out
                                   of [0,n), columns not strictly increasing in a
                                   row, nnz >= 2^31 */
@@ -78,9 +78,12 @@ typedef struct gsofa_opts {
    *     persistent grid-wide kernel per batch with epoch-encoded maxId
    *     labels. */
   int32_t schedule;
-  /* source rows [row_begin, row_end); row_end = -1 means n.  row_begin must be
-   * a multiple of chunk_size (so that supernodes, which never cross chunk
-   * boundaries, are identical to those of a whole-matrix run). */
+  /* source rows [row_begin, row_end); row_end = -1 means n.  Any row_begin:
+   * if it is not a multiple of chunk_size, the supernodes of the head rows
+   * [row_begin, next multiple of chunk_size) are provisional (computed as if
+   * row_begin started a block) until gsofa_supernode_stitch() is given the
+   * predecessor range's tail; supernodes never cross a multiple of
+   * chunk_size, so all later blocks are final. */
   int64_t row_begin, row_end;
   /* CUDA device ordinal used when the call creates its own context. */
   int32_t device;
@@ -166,6 +169,35 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr,
                    const int32_t *colidx, const gsofa_opts *opts,
                    gsofa_result **out);
 
+/* Tail record of a row range, exchanged between neighbouring ranges (the
+ * multi-GPU supernode-boundary exchange): the range's last row, its nnz(U)
+ * (diagonal included, R6) and the leading row of the supernode containing it. */
+typedef struct gsofa_tail {
+  int64_t row;
+  int64_t nnzU;
+  int64_t leader;
+} gsofa_tail;
+
+/*
+ * gsofa_supernode_stitch -- supernode continuity across row ranges
+ * (Definition def:T3; chunk rule P:640).
+ *   r     a result of gsofa_symbolic over [row_begin, row_end); modified in
+ *         place: sn_start / nsuper of the head rows [row_begin, next multiple
+ *         of chunk_size) are recomputed by the greedy Def. def:T3 scan
+ *         starting from *prev (row s joins the block of leader r iff
+ *         nnz(U(s,:)) = nnz(U(s-1,:)) - 1 and L(s, r) != 0).  Blocks after
+ *         that chunk boundary are unchanged.  The scan runs in a CUDA kernel
+ *         (host results are read through their pinned mapping).
+ *   prev  tail of the range ending at row_begin - 1 (else GSOFA_EINVAL);
+ *         NULL: row_begin truly starts a block (e.g. row_begin = 0), nothing
+ *         changes.
+ *   out   if not NULL, receives this range's tail (after stitching), to be
+ *         passed to the next range.
+ * Ranges must be stitched in increasing order.  Synchronous; a few hundred
+ * bytes move.  Errors: GSOFA_EINVAL, GSOFA_ECUDA (r is left unchanged).
+ */
+int gsofa_supernode_stitch(gsofa_result *r, const gsofa_tail *prev, gsofa_tail *out);
+
 /* Copies the result arrays into caller-owned buffers (host or device; any
  * NULL destination is skipped).  Sizes: L_rowptr/U_rowptr rows+1, L_colidx
  * nnz_L, U_colidx nnz_U, sn_start nsuper+1.  Synchronous.  Lets a binding
@@ -183,7 +215,9 @@ void gsofa_result_free(gsofa_result *r);
  * degree sum over the subtree of s in the elimination tree of the symmetrised
  * pattern A + A^T (an upper bound of the vertices reachable from s through
  * smaller vertices; elimination tree).  Range starts are multiples of
- * `align` (use chunk_size so supernodes never cross ranges).
+ * `align` (1 = row-granular, the default of the multi-GPU layer, which then
+ * stitches supernodes across ranges with gsofa_supernode_stitch; chunk_size
+ * makes every range start a block).
  *   bounds: out int64[nparts+1], bounds[0] = 0, bounds[nparts] = n.
  * Host-only computation (no GPU needed); deterministic, so every rank
  * computes the same partition.

@@ -19,14 +19,14 @@ import numpy as np
 
 from .build import LIB_PATH, build  # noqa: F401
 
-__all__ = ["Context", "Result", "symbolic", "partition_rows", "load", "GsofaError",
+__all__ = ["Context", "Result", "Tail", "symbolic", "partition_rows", "load", "GsofaError",
            "EXPORTED_SYMBOLS", "build", "LIB_PATH"]
 
 EXPORTED_SYMBOLS = [
     "gsofa_default_opts", "gsofa_context_create", "gsofa_context_destroy",
     "gsofa_symbolic", "gsofa_result_copy", "gsofa_result_free",
     "gsofa_partition_rows", "gsofa_strerror", "gsofa_last_error_detail",
-    "gsofa_version",
+    "gsofa_version", "gsofa_supernode_stitch",
 ]
 
 _I64, _I32 = ctypes.c_int64, ctypes.c_int32
@@ -57,6 +57,14 @@ class CResult(ctypes.Structure):
                 ("nnz_L", _I64), ("nnz_U", _I64), ("nnz_A_offdiag", _I64),
                 ("fill_count", _I64), ("on_device", _I32), ("device", _I32),
                 ("stats", Stats)]
+
+
+class Tail(ctypes.Structure):
+    """gsofa_tail: last row of a range, its nnz(U) and the leader of its block."""
+    _fields_ = [("row", _I64), ("nnzU", _I64), ("leader", _I64)]
+
+    def as_tuple(self):
+        return (self.row, self.nnzU, self.leader)
 
 
 class GsofaError(RuntimeError):
@@ -90,6 +98,7 @@ def load():
     lib.gsofa_result_free.restype = None
     lib.gsofa_partition_rows.argtypes = [_I64, ctypes.c_void_p, ctypes.c_void_p, _I32, _I32,
                                          ctypes.c_void_p]
+    lib.gsofa_supernode_stitch.argtypes = [_P(CResult), ctypes.c_void_p, ctypes.c_void_p]
     lib.gsofa_strerror.restype = ctypes.c_char_p
     lib.gsofa_strerror.argtypes = [ctypes.c_int]
     lib.gsofa_last_error_detail.restype = ctypes.c_char_p
@@ -206,6 +215,19 @@ class Result:
         _check(load().gsofa_result_copy(self._p, *[ctypes.c_void_p(p) if p else None for p in ptrs]),
                "gsofa_result_copy")
 
+    def stitch(self, prev=None) -> Tail:
+        """gsofa_supernode_stitch: fix the head supernodes of this range from
+        the predecessor's tail (a Tail, a (row, nnzU, leader) tuple, or None
+        when row_begin starts a block); returns this range's tail."""
+        if prev is not None and not isinstance(prev, Tail):
+            prev = Tail(*[int(x) for x in prev])
+        out = Tail()
+        _check(load().gsofa_supernode_stitch(self._p, ctypes.byref(prev) if prev is not None else None,
+                                             ctypes.byref(out)), "gsofa_supernode_stitch")
+        self.nsuper = self._p.contents.nsuper
+        self._arrays = None
+        return out
+
     def __getitem__(self, k):
         return self.to_numpy()[k]
 
@@ -255,9 +277,9 @@ def symbolic(rowptr, colidx, *, ctx: Context | None = None, chunk_size: int = 12
     return Result(out)
 
 
-def partition_rows(rowptr, colidx, nparts: int, align: int = 128) -> np.ndarray:
+def partition_rows(rowptr, colidx, nparts: int, align: int = 1) -> np.ndarray:
     """gsofa_partition_rows: contiguous, align-multiple row ranges of equal
-    estimated work (host computation)."""
+    estimated work (host computation); align=1: row-granular."""
     lib = load()
     rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
     colidx = np.ascontiguousarray(colidx, dtype=np.int32)

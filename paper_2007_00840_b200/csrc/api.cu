@@ -82,6 +82,7 @@ void host_block_release(HostBlock *b) {
 struct ResultImpl {
   gsofa_result r;
   HostBlock *block;  // pinned host storage of the arrays (host results)
+  int32_t chunk_size;  // of the call (supernode stitch); sn_start has room for rows+1
 };
 
 // ------------------------------------------------------------------ context
@@ -533,6 +534,70 @@ void gsofa_result_free(gsofa_result *r) {
   std::free(impl);
 }
 
+int gsofa_supernode_stitch(gsofa_result *r, const gsofa_tail *prev, gsofa_tail *out) {
+  if (!r) {
+    set_detail("result is NULL");
+    return GSOFA_EINVAL;
+  }
+  ResultImpl *impl = reinterpret_cast<ResultImpl *>(r);
+  const int64_t rb = r->row_begin, re = r->row_end, rows = re - rb;
+  const int32_t chunk = impl->chunk_size;
+  if (prev && (prev->row != rb - 1 || prev->leader < 0 || prev->leader > prev->row || prev->nnzU < 1)) {
+    set_detail("stitch tail {row %lld, nnzU %lld, leader %lld} does not precede row_begin %lld",
+               (long long)prev->row, (long long)prev->nnzU, (long long)prev->leader, (long long)rb);
+    return GSOFA_EINVAL;
+  }
+  cudaError_t e = cudaSetDevice(r->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  if (prev && rb % chunk != 0) {
+    // provisional head blocks [rb, he): re-scan from the predecessor's tail
+    const int64_t he = std::min<int64_t>(re, (rb / chunk + 1) * chunk);
+    int32_t *d_out = nullptr;
+    if ((e = cudaMalloc((void **)&d_out, (size_t)(chunk + 2) * 4)) != cudaSuccess)
+      return cuda_fail(e, "cudaMalloc(stitch)");
+    std::vector<int32_t> h((size_t)chunk + 2);
+    e = gsofa::launch_supernode_stitch(r->U_rowptr, r->L_rowptr, r->L_colidx, (int32_t)rb,
+                                       (int32_t)he, prev->nnzU, (int32_t)prev->leader, r->sn_start,
+                                       r->nsuper, d_out, nullptr);
+    if (e == cudaSuccess) e = cudaMemcpy(h.data(), d_out, h.size() * 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      cudaFree(d_out);
+      return cuda_fail(e, "supernode stitch");
+    }
+    const int64_t nc = h[0], oc = h[1], tail = r->nsuper + 1 - oc;  // tail incl. the sentinel
+    if (r->on_device) {
+      if (nc != oc && tail > 0) {
+        int32_t *tmp = nullptr;
+        e = cudaMalloc((void **)&tmp, (size_t)tail * 4);
+        if (e == cudaSuccess) e = cudaMemcpy(tmp, r->sn_start + oc, (size_t)tail * 4, cudaMemcpyDeviceToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(r->sn_start + nc, tmp, (size_t)tail * 4, cudaMemcpyDeviceToDevice);
+        cudaFree(tmp);
+      }
+      if (e == cudaSuccess && nc)
+        e = cudaMemcpy(r->sn_start, d_out + 2, (size_t)nc * 4, cudaMemcpyDeviceToDevice);
+    } else {
+      std::memmove(r->sn_start + nc, r->sn_start + oc, (size_t)tail * 4);
+      std::memcpy(r->sn_start, h.data() + 2, (size_t)nc * 4);
+    }
+    cudaFree(d_out);
+    if (e != cudaSuccess) return cuda_fail(e, "supernode stitch copy");
+    r->nsuper += nc - oc;
+  }
+  if (out) {
+    int64_t up[2] = {0, 0};
+    int32_t lead = 0;
+    e = cudaMemcpy(up, r->U_rowptr + rows - 1, 16, cudaMemcpyDefault);
+    if (e == cudaSuccess && r->nsuper > 0)
+      e = cudaMemcpy(&lead, r->sn_start + r->nsuper - 1, 4, cudaMemcpyDefault);
+    if (e != cudaSuccess) return cuda_fail(e, "stitch tail");
+    out->row = re - 1;
+    out->nnzU = up[1] - up[0];
+    // every row joined the predecessor's block: its leader carries on
+    out->leader = r->nsuper > 0 ? lead : prev->leader;
+  }
+  return GSOFA_OK;
+}
+
 int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const int32_t *colidx,
                    const gsofa_opts *opts_in, gsofa_result **out) {
   if (!out) {
@@ -549,7 +614,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   }
   if (o.row_end < 0) o.row_end = n;
   if (o.chunk_size < 1 || o.row_begin < 0 || o.row_end > n || o.row_begin >= o.row_end ||
-      o.row_begin % o.chunk_size != 0 || o.max_concurrent < 0 || o.max_concurrent % 32 != 0 ||
+      o.max_concurrent < 0 || o.max_concurrent % 32 != 0 ||
       o.mem_budget_bytes < 0 || o.schedule < 0 || o.schedule > 1) {
     set_detail("bad opts: chunk=%d rows=[%lld,%lld) C=%d budget=%lld", o.chunk_size,
                (long long)o.row_begin, (long long)o.row_end, o.max_concurrent,
@@ -1083,6 +1148,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     res->nnz_A_offdiag = (int64_t)hs[5];
     res->fill_count = baseL + (baseU - rows) - res->nnz_A_offdiag;
     res->device = c->device;
+    reinterpret_cast<ResultImpl *>(res)->chunk_size = o.chunk_size;
     res->stats.frontier_items = (int64_t)hs[0];
     res->stats.edge_inspections = (int64_t)hs[1];
     res->stats.rounds = (int64_t)hs[2];
@@ -1108,7 +1174,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     // previous host result has been freed
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t need = al((rows + 1) * 8) * 2 + al(std::max<size_t>(nl, 1) * 4) +
-                        al(std::max<size_t>(nu, 1) * 4) + al(ns * 4);
+                        al(std::max<size_t>(nu, 1) * 4) + al((rows + 1) * 4);  // sn_start: room for a stitch
     HostBlock *blk = c->hpool;
     if (!blk || blk->in_use || blk->cap < need) {
       if (blk && !blk->in_use) {  // too small: drop it

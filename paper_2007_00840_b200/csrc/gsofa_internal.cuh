@@ -136,6 +136,10 @@ cudaError_t scan_exclusive_i32(const int32_t *in, int32_t *out, int64_t count, i
 cudaError_t scan_exclusive_i32_i64(const int32_t *in, int64_t *out, int64_t count, int64_t *total,
                                    void *tmp, size_t tmp_bytes, cudaStream_t st);
 size_t scan_tmp_bytes(int64_t count);  // enough for either scan
+cudaError_t launch_supernode_stitch(const int64_t *U_rowptr, const int64_t *L_rowptr,
+                                    const int32_t *L_colidx, int32_t rb, int32_t he,
+                                    int64_t prev_nnzU, int32_t prev_leader, const int32_t *sn_start,
+                                    int64_t nsuper, int32_t *out, cudaStream_t st);
 cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, int32_t row_begin,
                                      int32_t row_end, const int32_t *total, int32_t *sn_start,
                                      cudaStream_t st);

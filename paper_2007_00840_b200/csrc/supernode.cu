@@ -112,6 +112,37 @@ __global__ void sn_phase2_kernel(const int64_t *L_rowptr, const int32_t *L_colid
   }
 }
 
+// Supernode-boundary stitch (multi-range runs): the head rows [rb, he) of a
+// range that starts inside a chunk were scanned as if rb started a block;
+// re-run the greedy Def. def:T3 scan over them from the
+// predecessor's tail (its last row's nnz(U) and the leader of its block).
+// One thread: at most chunk_size - 1 rows.  out: [0] new head leaders,
+// [1] old head leaders (sn_start entries < he), [2..] the new leaders.
+__global__ void sn_stitch_kernel(const int64_t *U_rowptr, const int64_t *L_rowptr,
+                                 const int32_t *L_colidx, int32_t rb, int32_t he, int64_t prev_nnzU,
+                                 int32_t prev_leader, const int32_t *sn_start, int64_t nsuper,
+                                 int32_t *out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int32_t r = prev_leader;
+  int64_t pn = prev_nnzU;
+  int nc = 0;
+  for (int32_t s = rb; s < he; ++s) {
+    const int k = s - rb;
+    const int64_t nu = U_rowptr[k + 1] - U_rowptr[k];
+    // (i) nnz(U(s,:)) = nnz(U(s-1,:)) - 1 and (ii) L(s, r) != 0
+    const bool join = nu == pn - 1 && row_contains(L_colidx, L_rowptr[k], L_rowptr[k + 1], r);
+    if (!join) {
+      r = s;
+      out[2 + nc++] = s;
+    }
+    pn = nu;
+  }
+  int oc = 0;
+  while (oc < nsuper && sn_start[oc] < he) ++oc;
+  out[0] = nc;
+  out[1] = oc;
+}
+
 __global__ void sn_scatter_kernel(const int32_t *flags, const int32_t *pos, int32_t row_begin,
                                   int32_t row_end, const int32_t *total, int32_t *sn_start) {
   const int32_t s = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
@@ -246,6 +277,15 @@ cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, i
   const int32_t rows = row_end - row_begin;
   sn_scatter_kernel<<<(unsigned)((rows + 255) / 256 + 1), 256, 0, st>>>(flags, pos, row_begin,
                                                                         row_end, total, sn_start);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_supernode_stitch(const int64_t *U_rowptr, const int64_t *L_rowptr,
+                                    const int32_t *L_colidx, int32_t rb, int32_t he,
+                                    int64_t prev_nnzU, int32_t prev_leader, const int32_t *sn_start,
+                                    int64_t nsuper, int32_t *out, cudaStream_t st) {
+  sn_stitch_kernel<<<1, 32, 0, st>>>(U_rowptr, L_rowptr, L_colidx, rb, he, prev_nnzU, prev_leader,
+                                     sn_start, nsuper, out);
   return cudaGetLastError();
 }
 

@@ -2,16 +2,17 @@
 source rows split into contiguous work-balanced ranges.
 
 Rows are independent given the static G(A); only supernode detection
-couples consecutive rows.  Ranges start at multiples of
-chunk_size, and supernodes never cross a chunk boundary (chunkSize = maximum
-supernode size), so every rank's supernodes are final and there is no
-supernode-boundary exchange to make.  The one collective on the path is the
-final allgather of per-rank counts (nnz_L, nnz_U, fill, nsuper, nnz_A_offdiag),
-from which each rank derives the global CSR offsets of its slice -- a few
-dozen bytes per rank over NCCL (NVLink/NVSwitch on a B200 box).
-
-The partition comes from gsofa_partition_rows (host C++ in libgsofa.so):
-equal shares of an elimination-tree work estimate.
+couples consecutive rows.  Ranges are row-granular (equal shares
+of an elimination-tree work estimate, P:264, P:454-459 -- aligning them to
+chunk_size would cost balance: the heavy top-separator rows are few).  A range
+that starts inside a chunk has provisional head supernodes, so the ranks run
+the supernode-boundary exchange: a chain r -> r+1 of 24-byte tail records
+{last row, its nnz(U), leader of its block}; each rank re-runs Def. def:T3
+over its head rows with the incoming tail (gsofa_supernode_stitch, a CUDA
+kernel) and forwards its own tail.  Then one allgather of per-rank counts
+(nnz_L, nnz_U, fill, nsuper, nnz_A_offdiag) gives every rank the global CSR
+offsets of its slice.  Both are tiny messages over NCCL (NVLink/NVSwitch on a
+B200 box); nothing else crosses GPUs.
 """
 from __future__ import annotations
 
@@ -40,11 +41,11 @@ class RankSlice:
         return dict(zip(COUNT_FIELDS, (int(x) for x in t)))
 
 
-def partition(rowptr, colidx, world: int, chunk_size: int = 128, partition_fn=None):
-    """Contiguous row ranges, one per rank, starting at multiples of chunk_size."""
+def partition(rowptr, colidx, world: int, align: int = 1, partition_fn=None):
+    """Contiguous row ranges, one per rank (row-granular unless align > 1)."""
     if partition_fn is None:
         from . import partition_rows as partition_fn
-    return partition_fn(rowptr, colidx, world, chunk_size)
+    return partition_fn(rowptr, colidx, world, align)
 
 
 def global_offsets(counts: np.ndarray, rank: int):
@@ -66,24 +67,58 @@ def allgather_counts(local: np.ndarray, group=None, device=None) -> np.ndarray:
     return out.cpu().numpy().reshape(world, -1)
 
 
-def symbolic_distributed(rowptr, colidx, bounds, *, rank: int, compute_fn=None,
+NO_TAIL = (-1, -1, -1)
+
+
+def exchange_tail(tail, rank: int, world: int, recv: bool, group=None, device=None):
+    """One hop of the supernode-boundary chain: receive the predecessor's tail
+    (recv=True, from rank-1) or send ours to rank+1.  A tail is (row, nnzU,
+    leader); NO_TAIL stands for "none" (rank 0, or empty ranges before)."""
+    import torch
+    import torch.distributed as dist
+    if recv:
+        t = torch.empty(3, dtype=torch.int64, device=device)
+        dist.recv(t, src=rank - 1, group=group)
+        v = tuple(int(x) for x in t.cpu().tolist())
+        return None if v == NO_TAIL else v
+    t = torch.tensor(NO_TAIL if tail is None else tail, dtype=torch.int64, device=device)
+    dist.send(t, dst=rank + 1, group=group)
+    return None
+
+
+def _stitch_gpu(res, prev):
+    return res.stitch(prev).as_tuple()
+
+
+def symbolic_distributed(rowptr, colidx, bounds, *, rank: int, compute_fn=None, stitch_fn=None,
                          group=None, device=None, **kw) -> RankSlice:
-    """Run this rank's row range and exchange counts.
+    """Run this rank's row range, stitch supernodes with the neighbours and
+    exchange counts.
 
     compute_fn(rowptr, colidx, row_begin=..., row_end=..., **kw) -> object with
     nnz_L, nnz_U, fill_count, nsuper, nnz_A_offdiag (default: the CUDA
-    library's :func:`symbolic`).  Tests inject the CPU oracle here to check the
-    host logic with the gloo backend; the product path always uses the GPU.
+    library's :func:`symbolic`); stitch_fn(result, prev_tail) -> tail fixes the
+    head supernodes in place (default: gsofa_supernode_stitch).  Tests inject
+    the CPU oracle and a plain Def. def:T3 scan here to check the host logic
+    with the gloo backend; the product path always uses the GPU library.
     """
     import torch.distributed as dist
     world = dist.get_world_size(group)
     if compute_fn is None:
         from . import symbolic as compute_fn
+    if stitch_fn is None:
+        stitch_fn = _stitch_gpu
     rb, re = int(bounds[rank]), int(bounds[rank + 1])
     res = None
     local = np.zeros(len(COUNT_FIELDS), np.int64)
     if re > rb:
         res = compute_fn(rowptr, colidx, row_begin=rb, row_end=re, **kw)
+    # supernode-boundary exchange: chain rank-1 -> rank -> rank+1
+    prev = exchange_tail(None, rank, world, True, group, device) if rank > 0 else None
+    tail = stitch_fn(res, prev) if res is not None else prev
+    if rank + 1 < world:
+        exchange_tail(tail, rank, world, False, group, device)
+    if res is not None:
         local[:] = [res.nnz_L, res.nnz_U, res.fill_count, res.nsuper, res.nnz_A_offdiag, re - rb]
     counts = allgather_counts(local, group=group, device=device)
     assert counts.shape == (world, len(COUNT_FIELDS))

@@ -35,6 +35,7 @@ def test_exports_every_declared_symbol(g):
     for name in names:
         assert hasattr(lib, name), name
     assert sorted(g.EXPORTED_SYMBOLS) == names
+    assert "gsofa_supernode_stitch" in names
     out = subprocess.run(["nm", "-D", "--defined-only", g.LIB_PATH], capture_output=True, text=True).stdout
     for name in names:
         assert re.search(rf"\bT {name}$", out, re.M), name
@@ -46,7 +47,8 @@ def test_struct_layout_matches_header(g):
 #include <stdio.h>
 #include "gsofa.h"
 int main(void) {
-  printf("%zu %zu %zu\n", sizeof(gsofa_opts), sizeof(gsofa_stats), sizeof(gsofa_result));
+  printf("%zu %zu %zu %zu\n", sizeof(gsofa_opts), sizeof(gsofa_stats), sizeof(gsofa_result),
+         sizeof(gsofa_tail));
   printf("%zu %zu %zu\n", offsetof(gsofa_opts, stream), offsetof(gsofa_result, stats),
          offsetof(gsofa_result, fill_count));
   return 0;
@@ -60,7 +62,7 @@ int main(void) {
         a, b = subprocess.check_output([exe], text=True).split("\n")[:2]
     import ctypes
     assert [int(x) for x in a.split()] == [ctypes.sizeof(g.Opts), ctypes.sizeof(g.Stats),
-                                           ctypes.sizeof(g.CResult)]
+                                           ctypes.sizeof(g.CResult), ctypes.sizeof(g.Tail)]
     assert [int(x) for x in b.split()] == [g.Opts.stream.offset, g.CResult.stats.offset,
                                            g.CResult.fill_count.offset]
 

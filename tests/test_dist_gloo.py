@@ -29,10 +29,37 @@ def _oracle_compute(rowptr, colidx, row_begin, row_end, chunk_size=128):
     ns = types.SimpleNamespace(**{k: r[k] for k in ("nnz_L", "nnz_U", "fill_count", "nsuper",
                                                      "nnz_A_offdiag")})
     ns.arrays = {k: r[k] for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start")}
+    ns.row_begin, ns.row_end = row_begin, row_end
     return ns
 
 
-def _worker(rank, world, port, name, scale, chunk, q):
+def _oracle_stitch(res, prev, chunk=128):
+    """Plain Def. def:T3 scan of the head rows of a range whose
+    first block was computed as if row_begin started one: test-side stand-in
+    for gsofa_supernode_stitch on oracle results.  Returns the range's tail."""
+    a = res.arrays
+    rb, re = res.row_begin, res.row_end
+    Lp, Li, Up = a["L_rowptr"], a["L_colidx"], a["U_rowptr"]
+    sn = [int(x) for x in a["sn_start"]]
+    if prev is not None and rb % chunk:
+        he = min(re, (rb // chunk + 1) * chunk)
+        r, pn, new = prev[2], prev[1], []
+        for s in range(rb, he):
+            k = s - rb
+            nu = int(Up[k + 1] - Up[k])
+            if not (nu == pn - 1 and r in set(Li[Lp[k]:Lp[k + 1]].tolist())):
+                r = s
+                new.append(s)
+            pn = nu
+        old = sum(1 for x in sn[:-1] if x < he)
+        sn = new + sn[old:]
+        a["sn_start"] = np.array(sn, np.int32)
+        res.nsuper = len(sn) - 1
+    leader = sn[-2] if len(sn) > 1 else prev[2]
+    return (re - 1, int(Up[-1] - Up[-2]), leader)
+
+
+def _worker(rank, world, port, name, scale, chunk, q, fixed_bounds=None):
     import torch.distributed as dist
 
     import paper_2007_00840_b200 as g
@@ -42,8 +69,10 @@ def _worker(rank, world, port, name, scale, chunk, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         rp, ci = gen.config(name, scale)
-        bounds = gd.partition(rp, ci, world, chunk, partition_fn=g.partition_rows)
+        bounds = (np.array(fixed_bounds, np.int64) if fixed_bounds is not None
+                  else gd.partition(rp, ci, world, partition_fn=g.partition_rows))
         sl = gd.symbolic_distributed(rp, ci, bounds, rank=rank, compute_fn=_oracle_compute,
+                                     stitch_fn=lambda r, p: _oracle_stitch(r, p, chunk),
                                      chunk_size=chunk)
         q.put((rank, bounds.tolist(), sl.row_begin, sl.row_end, sl.counts.tolist(), sl.L_base,
                sl.U_base, sl.sn_base, sl.result.arrays if sl.result is not None else None))
@@ -51,13 +80,25 @@ def _worker(rank, world, port, name, scale, chunk, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,name,scale,chunk", [(2, "C5", 12, 128), (3, "C4", 40, 64),
-                                                    (2, "C1", None, 128)])
-def test_distributed_host_logic_gloo(world, name, scale, chunk):
+def _inside_supernodes(name, scale, chunk, world):
+    """Range starts strictly inside multi-row supernodes (not at chunk
+    multiples): every boundary must be stitched."""
+    rp, ci = gen.config(name, scale)
+    sn = oracle.symbolic(rp, ci, chunk_size=chunk)["sn_start"]
+    cand = [int(a) + 1 for a, b in zip(sn[:-1], sn[1:]) if b - a >= 3 and (a + 1) % chunk]
+    pick = [cand[(i + 1) * len(cand) // world] for i in range(world - 1)]
+    return [0] + sorted(pick) + [rp.size - 1]
+
+
+@pytest.mark.parametrize("world,name,scale,chunk,inside", [
+    (2, "C5", 12, 128, False), (3, "C4", 40, 64, False), (2, "C1", None, 128, False),
+    (3, "C3", 1500, 128, True), (2, "C2", 10, 16, True)])
+def test_distributed_host_logic_gloo(world, name, scale, chunk, inside):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, scale, chunk, q))
+    fb = _inside_supernodes(name, scale, chunk, world) if inside else None
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, scale, chunk, q, fb))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -72,7 +113,8 @@ def test_distributed_host_logic_gloo(world, name, scale, chunk):
     bounds = outs[0][1]
     assert all(o[1] == bounds for o in outs)            # identical partition on every rank
     assert bounds[0] == 0 and bounds[-1] == n
-    assert all(b % chunk == 0 for b in bounds[:-1])
+    if inside:
+        assert all(b % chunk for b in bounds[1:-1])  # every boundary needs the stitch
     counts = np.array(outs[0][4])
     assert all(np.array_equal(np.array(o[4]), counts) for o in outs)
     tot = counts.sum(axis=0)
@@ -84,8 +126,33 @@ def test_distributed_host_logic_gloo(world, name, scale, chunk):
         assert Lb == full["L_rowptr"][rb] and Ub == full["U_rowptr"][rb]
         if arr is not None:
             assert np.array_equal(arr["L_colidx"], full["L_colidx"][full["L_rowptr"][rb]:full["L_rowptr"][re]])
-            assert full["sn_start"][snb] == rb
+            lead = full["sn_start"][(full["sn_start"] >= rb) & (full["sn_start"] < re)]
+            assert np.array_equal(arr["sn_start"][:-1], lead)          # stitched supernodes
+            assert snb == int((full["sn_start"][:-1] < rb).sum())
     from paper_2007_00840_b200 import dist as gd
     asm = gd.assemble([o[8] for o in outs], n)
     for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start"):
         assert np.array_equal(asm[k], full[k]), k
+
+
+@pytest.mark.parametrize("name,scale,chunk", [("C1", None, 128), ("C3", 1500, 128), ("C2", 10, 16),
+                                              ("C4", 40, 64)])
+def test_stitch_chain_oracle(name, scale, chunk):
+    """Many ranges, cut everywhere (inside supernodes, at chunk multiples, one
+    row long): per-range oracle results stitched in order reproduce the
+    whole-matrix supernodes (the reading of Def. def:T3 the GPU stitch uses)."""
+    rp, ci = gen.config(name, scale)
+    n = rp.size - 1
+    full = oracle.symbolic(rp, ci, chunk_size=chunk)
+    rng = np.random.default_rng(7)
+    cuts = sorted(set(rng.integers(1, n, 12).tolist()) | {chunk, chunk + 1, chunk + 2, n // 2, n // 2 + 1})
+    bounds = [0] + [c for c in cuts if 0 < c < n] + [n]
+    prev, parts = None, []
+    for rb, re in zip(bounds[:-1], bounds[1:]):
+        res = _oracle_compute(rp, ci, rb, re, chunk)
+        res.row_begin, res.row_end = rb, re
+        prev = _oracle_stitch(res, prev, chunk)
+        parts.append(res.arrays)
+    from paper_2007_00840_b200 import dist as gd
+    asm = gd.assemble(parts, n)
+    assert np.array_equal(asm["sn_start"], full["sn_start"])

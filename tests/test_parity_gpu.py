@@ -130,6 +130,48 @@ def test_row_ranges_and_devices(ctx):
         assert_full_equal(part, want)
 
 
+def _stitched_ranges(rp, ci, ctx, bounds, chunk, **kw):
+    """Run every range through the C-ABI, stitch in order (the multi-GPU
+    supernode-boundary chain, single process), assemble."""
+    from paper_2007_00840_b200 import dist as gd
+    prev, parts, tails = None, [], []
+    for rb, re in zip(bounds[:-1], bounds[1:]):
+        r = g.symbolic(rp, ci, ctx=ctx, row_begin=rb, row_end=re, chunk_size=chunk, **kw)
+        t = r.stitch(prev)
+        prev = t.as_tuple()
+        tails.append(prev)
+        parts.append(dict(r.to_numpy()))
+        assert r.nsuper == parts[-1]["sn_start"].size - 1
+        r.free()
+    return gd.assemble(parts, rp.size - 1), tails
+
+
+@pytest.mark.parametrize("name,scale,chunk", [("C5", 14, 128), ("C3", 3000, 128), ("C2", 12, 16),
+                                              ("C4", 60, 64), ("C1", None, 128)])
+@pytest.mark.parametrize("on_device", [False, True])
+def test_supernode_stitch_row_granular(ctx, name, scale, chunk, on_device):
+    """Row-granular ranges (starts inside supernodes, one-row ranges, ranges
+    inside one chunk) stitched with gsofa_supernode_stitch reproduce the
+    whole-matrix supernodes of the oracle; tails report (last row, nnz(U),
+    leader of its block)."""
+    rp, ci = gen.config(name, scale)
+    n = rp.size - 1
+    full = oracle.symbolic(rp, ci, chunk_size=chunk)
+    sn = full["sn_start"]
+    inside = [int(a) + 1 for a, b in zip(sn[:-1], sn[1:]) if b - a >= 3 and (a + 1) % chunk]
+    rng = np.random.default_rng(3)
+    cuts = set(rng.integers(1, n, 6).tolist()) | set(inside[:: max(1, len(inside) // 6)][:6])
+    cuts |= {chunk + 1, chunk + 2, chunk + 3}
+    bounds = [0] + sorted(c for c in cuts if 0 < c < n) + [n]
+    asm, tails = _stitched_ranges(rp, ci, ctx, bounds, chunk, outputs_on_device=on_device)
+    for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start"):
+        assert np.array_equal(asm[k], full[k]), k
+    Up = full["U_rowptr"]
+    for (rb, re), t in zip(zip(bounds[:-1], bounds[1:]), tails):
+        assert t[0] == re - 1 and t[1] == Up[re] - Up[re - 1]
+        assert t[2] == sn[np.searchsorted(sn, re - 1, side="right") - 1]
+
+
 def test_input_diagonal_ignored(ctx):
     rp, ci = gen.random_graph(200, 0.03, seed=5)
     n = rp.size - 1
@@ -194,8 +236,13 @@ def test_errors():
             g.symbolic(rp, unsorted)
         assert e.value.code == -2
     with pytest.raises(g.GsofaError) as e:
-        g.symbolic(rp, ci, row_begin=5)
+        g.symbolic(rp, ci, row_begin=20, row_end=20)
     assert e.value.code == -1
+    r = g.symbolic(rp, ci, row_begin=5, row_end=20)  # any row_begin is accepted
+    with pytest.raises(g.GsofaError) as e:
+        r.stitch((3, 2, 1))                           # tail must end at row_begin - 1
+    assert e.value.code == -1
+    r.free()
     with pytest.raises(g.GsofaError) as e:
         g.symbolic(rp, ci, max_concurrent=33)
     assert e.value.code == -1
