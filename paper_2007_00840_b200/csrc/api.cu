@@ -522,9 +522,13 @@ void gsofa_result_free(gsofa_result *r) {
   ResultImpl *impl = reinterpret_cast<ResultImpl *>(r);
   void *ptrs[5] = {r->L_rowptr, r->L_colidx, r->U_rowptr, r->U_colidx, r->sn_start};
   if (r->on_device) {
+    // the arrays came from the device's stream-ordered pool (cudaMallocAsync):
+    // hand them back to it (no cudaFree: that would unmap the pages and the
+    // next call would pay for mapping them again)
     cudaSetDevice(r->device);
     for (void *p : ptrs)
-      if (p) cudaFree(p);
+      if (p) cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
   } else if (impl->block) {
     impl->block->in_use = false;
     host_block_release(impl->block);
@@ -638,14 +642,17 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   void *scan_tmp = nullptr;
   void *stream_scratch = nullptr;
   std::vector<cudaEvent_t> evs;
+  std::vector<int> ev_line;  // source line of each event (GSOFA_TIMELINE dev dump)
   int64_t launches = 0;
-  auto ev = [&]() {
+  auto ev_at = [&](int line) {
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, st);
     evs.push_back(e);
+    ev_line.push_back(line);
     return (int)evs.size() - 1;
   };
+#define ev() ev_at(__LINE__)
   const int64_t rb = o.row_begin, re = o.row_end, rows = re - rb;
   int64_t nnz = 0;
   bool in_dev;
@@ -719,6 +726,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     c->layout_sig = sig;
   }
   if ((rc = prepare_work(c, o.schedule, st)) != GSOFA_OK) goto fail;
+  ev();
   // validate (GSOFA_EBADCSR) and narrow row pointers to int32
   CK(cudaMemsetAsync(c->err, 0, sizeof(int), st));
   CK(cudaMemsetAsync(c->stats, 0, 8 * sizeof(unsigned long long), st));
@@ -733,6 +741,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     rc = GSOFA_EBADCSR;
     goto fail;
   }
+  ev();
   // ---------------------------------------------------- outputs
   {
     cudaError_t e1 = cudaMallocAsync((void **)&Lrp, (rows + 1) * sizeof(int64_t), st);
@@ -776,6 +785,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       hq_ready = hq + ngroups;
       CK(cudaMemsetAsync(hq_ready, 0, (size_t)ngroups * 4, st));
     }
+    ev();
     if (c->stage_cap == 0) {
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
@@ -1245,7 +1255,13 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     }
     cudaEventElapsedTime(&ms, evs[e_sn0], evs[e_sn1]);
     res->stats.ms_supernode = ms;
+    if (std::getenv("GSOFA_TIMELINE"))
+      for (size_t i = 1; i < evs.size(); ++i) {
+        cudaEventElapsedTime(&ms, evs[i - 1], evs[i]);
+        std::fprintf(stderr, "[timeline] api.cu:%d -> api.cu:%d  %.3f ms\n", ev_line[i - 1], ev_line[i], ms);
+      }
   }
+#undef ev
   if (sn_scratch) cudaFreeAsync(sn_scratch, st);
   if (scan_tmp) cudaFreeAsync(scan_tmp, st);
   if (stream_scratch) cudaFreeAsync(stream_scratch, st);

@@ -859,7 +859,10 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
 #undef PROF_MARK
 }
 
-__global__ void __launch_bounds__(kSoloWarps * 32, 2) solo_kernel(StreamParams p) {
+#ifndef GSOFA_SOLO_MINB
+#define GSOFA_SOLO_MINB 2
+#endif
+__global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(StreamParams p) {
   constexpr int kWarps = kSoloWarps;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   const int n = p.n, Vmax = p.Vmax;

@@ -1,0 +1,66 @@
+"""Strong-scaling emulation on ONE GPU: partition the rows for N ranks exactly
+as the multi-GPU layer does, run every rank's range alone on the GPU (each
+rank owns a whole B200 in the real run), and report per-range device times.
+The N-GPU step time is max over ranges (+ the two tiny collectives, ~0.1 ms);
+speedup = full single-GPU time / that max.
+
+usage: python scripts/scaling_emulation.py --config C5 --gpus 2 4 8 [--reps 2]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import gen  # noqa: E402
+import paper_2007_00840_b200 as g  # noqa: E402
+from paper_2007_00840_b200 import dist as gd  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C5")
+ap.add_argument("--gpus", type=int, nargs="+", default=[2, 4, 8])
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--calibrated", action="store_true", help="use the sampled calibration partition")
+ap.add_argument("--out", default=None)
+a = ap.parse_args()
+
+rp, ci = gen.config(a.config)
+n = rp.size - 1
+ctx = g.Context(0)
+
+
+def timed(rb, re):
+    best = None
+    for _ in range(a.reps):
+        r = g.symbolic(rp, ci, ctx=ctx, row_begin=rb, row_end=re, outputs_on_device=True)
+        ms = r.stats["ms_total"]
+        fill = r.fill_count
+        r.free()
+        best = ms if best is None else min(best, ms)
+    return best, fill
+
+
+full_ms, full_fill = timed(0, n)
+print(f"{a.config}: 1 GPU {full_ms:.1f} ms, fill {full_fill}", flush=True)
+report = {"config": a.config, "n": n, "one_gpu_ms": full_ms, "fill": full_fill, "runs": []}
+for N in a.gpus:
+    if a.calibrated:
+        bounds = gd.partition_calibrated(rp, ci, N, ctx=ctx)
+    else:
+        bounds = gd.partition(rp, ci, N)
+    per = []
+    fills = 0
+    for r in range(N):
+        ms, f = timed(int(bounds[r]), int(bounds[r + 1]))
+        per.append(ms)
+        fills += f
+    assert fills == full_fill
+    mx = max(per)
+    print(f"  N={N}: ranges {list(map(int, bounds))}\n        ms {[round(x, 1) for x in per]} -> max {mx:.1f} ms, "
+          f"speedup {full_ms / mx:.2f}x, efficiency {full_ms / mx / N:.2f}", flush=True)
+    report["runs"].append({"gpus": N, "bounds": [int(b) for b in bounds], "range_ms": per,
+                           "max_ms": mx, "speedup": full_ms / mx})
+if a.out:
+    json.dump(report, open(a.out, "w"), indent=1)
