@@ -209,8 +209,9 @@ bool make_plan(int schedule, int64_t n, int64_t rows, int64_t vb_max, int64_t cm
 bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int device, Plan &p) {
   if (gsofa::stream_smem_bytes(Vmax) > 200 * 1024) return false;
   const size_t ws = gsofa::stream_ws_words(Vmax), isw = gsofa::stream_is_words(n);
-  const size_t hws = gsofa::solo_ws_words(Vmax);
-  const size_t per_light = (ws + isw) * 4, per_heavy = (hws + isw) * 4;
+  const size_t hws = gsofa::solo_ws_words(Vmax, n);
+  const int64_t spc = gsofa::solo_warps_per_cta();
+  const size_t per_light = (ws + isw) * 4, per_heavy = hws * 4 * (size_t)spc;  // per solo CTA
   const size_t fixed = small_bytes(32) + 8192;
   if (budget <= (int64_t)(fixed + per_light)) return false;
   int sms = 0;
@@ -221,9 +222,12 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
   const int64_t res_heavy = gsofa::stream_max_blocks(device, Vmax, 1);
   if (res_light < 1) return false;
   // solo CTAs: one per SM is resident next to the lockstep CTAs from the
-  // start; a second wave becomes resident as lockstep CTAs finish and joins
-  // the heavy queue (the grid is deliberately larger than the first wave)
-  int64_t heavy = std::min<int64_t>(2 * (int64_t)sms, ngroups);
+  // start; more become resident as lockstep CTAs finish (the grid is
+  // deliberately larger than the first wave), up to the kernel's residency
+  // heavy sources are spread warp-major over at least one CTA per SM: a
+  // chain is paced by its SM's atomic issue rate, not by latency alone
+  int64_t heavy = std::min<int64_t>(std::max<int64_t>(res_heavy, (int64_t)sms),
+                                    std::max<int64_t>((int64_t)sms, ceil_div(rows, spc)));
   (void)res_heavy;
   if (const char *e = std::getenv("GSOFA_SOLO_CTAS")) heavy = std::min<int64_t>(heavy, atoll(e));
   heavy = std::max<int64_t>(0, std::min<int64_t>(heavy, (int64_t)(((size_t)budget - fixed) / 2 / per_heavy)));
@@ -245,8 +249,8 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
   p.ws_words = ws;
   p.hws_words = hws;
   p.slot_is_words = isw;
-  p.work_bytes = (size_t)light * ws * 4 + (size_t)heavy * hws * 4;
-  p.is_words = (size_t)(light + heavy) * isw;
+  p.work_bytes = (size_t)light * ws * 4 + (size_t)heavy * per_heavy;
+  p.is_words = (size_t)light * isw;  // solo slots keep their bitmap in hws
   p.cnt_words = 0;
   p.nsub = 0;
   p.total = p.work_bytes + p.is_words * 4 + small_bytes(32) + 4096 + 12 * 256;
@@ -852,6 +856,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.hq_head = c->qcount + 2;
     sp.hq_tail = c->qcount + 3;
     sp.done = c->qcount + 4;
+    sp.task_ctr = (unsigned long long *)(c->qcount + 6);  // qcount[6..7]
     sp.hws = c->work + (size_t)plan.light * plan.ws_words;
     sp.hws_words = plan.hws_words;
     sp.light_slots = (int32_t)plan.light;
@@ -864,6 +869,20 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       int64_t top = std::min<int64_t>(plan.heavy, sms);
       if (const char *e = std::getenv("GSOFA_SOLO_TOP")) top = std::min<int64_t>(plan.heavy, atoll(e));
       sp.solo_top = (int32_t)std::min<int64_t>(top, ngroups);
+      // the solo_top heaviest groups are queued for the solo kernel up front
+      if (sp.solo_top > 0) {
+        std::vector<int32_t> hv((size_t)sp.solo_top * 2);
+        for (int32_t i = 0; i < sp.solo_top; ++i) {
+          hv[i] = (int32_t)ngroups - 1 - i;
+          hv[sp.solo_top + i] = 1;
+        }
+        const uint32_t tail = (uint32_t)sp.solo_top;
+        CK(cudaMemcpyAsync(hq, hv.data(), (size_t)sp.solo_top * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(hq_ready, hv.data() + sp.solo_top, (size_t)sp.solo_top * 4,
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(sp.hq_tail, &tail, 4, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));  // hv is a host temporary
+      }
       double ms = 5.0;
       if (const char *e = std::getenv("GSOFA_ABORT_MS")) ms = atof(e);
       int khz = 0;
@@ -960,16 +979,19 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
             ++reported;
           }
       }
-      for (int64_t sl = 0; sl < plan.heavy && reported < 16; ++sl) {
-        const uint32_t *b = hw.data() + plan.light * plan.ws_words + sl * plan.hws_words;
-        const size_t rs0 = 2 * ((Vm + 3) & ~(size_t)3), th0 = rs0 + ((rsw + 3) & ~(size_t)3);
-        const size_t ts0 = th0 + 32 * tbw, q0 = ts0 + 32 * tsw;
-        for (size_t i = 0; i < q0 && reported < 16; ++i)
-          if (b[i]) {
-            std::fprintf(stderr, "[dirty] solo slot %lld word %zu (%s) = %08x\n", (long long)sl, i,
-                         i < rs0 ? "reached/pend" : (i < th0 ? "rsum" : (i < ts0 ? "thr" : "tsum")), b[i]);
-            ++reported;
-          }
+      {
+        const size_t Vw = ((Vm + 31) / 32 + 3) & ~(size_t)3, Vs = ((Vw + 31) / 32 + 3) & ~(size_t)3;
+        const size_t nw = (((size_t)n + 31) / 32 + 3) & ~(size_t)3, ns = ((nw + 31) / 32 + 3) & ~(size_t)3;
+        const size_t live = 3 * Vw + 2 * Vs + nw + ns;  // everything but the ring
+        const int64_t nslots = plan.heavy * gsofa::solo_warps_per_cta();
+        for (int64_t sl = 0; sl < nslots && reported < 16; ++sl) {
+          const uint32_t *b = hw.data() + plan.light * plan.ws_words + sl * plan.hws_words;
+          for (size_t i = 0; i < live && reported < 16; ++i)
+            if (b[i]) {
+              std::fprintf(stderr, "[dirty] solo slot %lld word %zu = %08x\n", (long long)sl, i, b[i]);
+              ++reported;
+            }
+        }
       }
       for (size_t i = 0; i < hi.size() && reported < 24; ++i)
         if (hi[i]) {

@@ -71,8 +71,9 @@ struct StreamParams {
   int32_t *hq;               // [ngroups] queued group ids
   unsigned int *hq_head, *hq_tail;
   int32_t *hq_ready;         // [ngroups] publication flags
-  unsigned int *done;        // groups completed (both kernels)
-  uint32_t *hws;             // [heavy slots][hws_words] solo workspaces
+  unsigned int *done;        // rows completed (both kernels)
+  unsigned long long *task_ctr;  // solo kernel: next dynamic source task
+  uint32_t *hws;             // [solo slots = solo CTAs x warps][hws_words] per-source workspaces
   size_t hws_words;
   int32_t light_slots;       // is[] slots [0, light_slots) lockstep, then solo
   const int32_t *group_list; // optional explicit group ids (retry pass)
@@ -95,7 +96,8 @@ size_t stream_is_words(int64_t n);
 int stream_max_blocks(int device, int64_t Vmax, int heavy);
 int stream_heavy_ratio();  // warps of a solo CTA / warps of a lockstep CTA
 int stream_warps_per_cta();  // lockstep slots (one group per warp) per CTA
-size_t solo_ws_words(int64_t Vmax);
+size_t solo_ws_words(int64_t Vmax, int64_t n);  // per solo slot (one warp, one source)
+int solo_warps_per_cta();
 int stream_light_per_sm_with_solo(int device, int64_t Vmax);
 size_t stream_smem_bytes(int64_t Vmax);  // dynamic smem: threshold-word summary
 cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st);

@@ -35,7 +35,7 @@ namespace gsofa {
 namespace {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr int kLightWarps = 4;   // lockstep CTA: 32 sources share frontier items
-constexpr int kSoloWarps = 32;   // solo CTA: one warp per source (heavy groups)
+constexpr int kSoloWarps = 16;   // solo CTA: independent warps, one source each
 
 // lanes k (sources s0g + k) with source > w, resp. source < w
 __device__ __forceinline__ uint32_t lanes_above(int w, int s0g) {
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
           t[7] = 0;  // lockstep kernel
         }
       }
-      if (tid == 0) atomicAdd(p.done, 1u);
+      if (tid == 0) atomicAdd(p.done, (unsigned)nsrc);  // rows completed
     }
     __syncthreads();
   }
@@ -533,25 +533,53 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
 }
 
 // ---------------------------------------------------------------- solo kernel
-// Heavy groups (rows of top separators, hub rows): their 32 sources share
-// almost no frontier items in threshold order, so lockstep only makes every
-// source wait for the union of all thresholds.  Here warp k runs source
-// s0g + k on its own: its own threshold bitmap + summary (global), its own
-// append-only closure queue (tail in a register), no CTA barriers during the
-// traversal.  The reached and in-structure words are still shared (bit k).
-constexpr int kSoloBatch = 1;
+// Heavy sources (rows of top separators, hub rows): in threshold order the 32
+// sources of such a group share few frontier items, and each is a long chain
+// of |L(s,:)| threshold steps.  Here every warp runs ONE source on its own
+// slot of per-source bitmaps (bit v of a word = vertex v), with no CTA
+// barriers and no coupling to the other sources of its group:
+//   * sources are tasks (queue entry e = t / 32, source k = t % 32); a warp's
+//     first task is fixed so that the heaviest sources land on different SMs
+//     (an SM's atomic issue rate, not latency alone, paces a chain when 32 of
+//     them share it), later tasks come from a global counter;
+//   * the queue holds groups: the top solo_top groups (pre-enqueued), groups
+//     the lockstep kernel abandons, and fresh groups claimed by idle warps.
+//
+// Slot layout (uint32 words; all zero between sources):
+//   reached[Vw] pend[Vw] thr[Vw]   bitmaps over [0, Vmax), Vw = Vmax/32
+//   rsum[Vw/32] tsum[Vw/32]        touched reached words / nonzero thr words
+//   is[nw] isum[nw/32]             in-structure bitmap over [0, n) + touched words
+//   ring[R]                        closure overflow (vertex ids)
+constexpr int kSoloQ = 64;  // shared-memory closure worklist entries per warp
 
-// closure ring capacity per source: a power of two, at most 64k entries
 __host__ __device__ inline int solo_ring(int64_t Vmax) {
   int r = 1024;
-  while (r < 65536 && r < Vmax) r <<= 1;
+  while (r < 16384 && r < Vmax) r <<= 1;
   return r;
 }
 
+__host__ __device__ inline size_t round4(size_t w) { return (w + 3) & ~(size_t)3; }
+
 struct SoloSlot {
-  uint32_t *reached, *pend, *rsum, *thr, *tsum, *queue, *is, *isum;
-  int qmask;  // ring capacity - 1 (power of two)
+  uint32_t *reached, *pend, *thr, *rsum, *tsum, *is, *isum, *queue;
+  int qmask;
 };
+
+__device__ __forceinline__ SoloSlot solo_slot(const StreamParams &p, size_t slot) {
+  const size_t Vw = round4((size_t)((p.Vmax + 31) >> 5)), Vs = round4((Vw + 31) >> 5);
+  const size_t nw = round4((size_t)((p.n + 31) >> 5)), ns = round4((nw + 31) >> 5);
+  SoloSlot sl;
+  sl.reached = p.hws + slot * p.hws_words;
+  sl.pend = sl.reached + Vw;
+  sl.thr = sl.pend + Vw;
+  sl.rsum = sl.thr + Vw;
+  sl.tsum = sl.rsum + Vs;
+  sl.is = sl.tsum + Vs;
+  sl.isum = sl.is + nw;
+  sl.queue = sl.isum + ns;
+  sl.qmask = solo_ring(p.Vmax) - 1;
+  return sl;
+}
 
 __device__ __forceinline__ int solo_scan_next(const uint32_t *thr, const uint32_t *tsum, int tbw,
                                               int T, int lane) {
@@ -581,24 +609,21 @@ __device__ __forceinline__ int solo_scan_next(const uint32_t *thr, const uint32_
 }
 
 // Per-warp shared memory of the solo kernel.
-//   win[32]   a window of 32 words (1024 vertices) of this source's threshold
-//             bitmap, starting at word wb: thresholds found while the window
-//             covers them are set here with shared-memory atomics, so finding
-//             the next threshold costs no global round trip; thresholds beyond
-//             the window go to the global bitmap + summary (REDs), published
-//             by one fence when the window moves on
+//   win[32]   a window of 32 words (1024 vertices) of the threshold bitmap,
+//             starting at word wb: thresholds found while the window covers
+//             them are set here with shared-memory atomics, so finding the
+//             next threshold costs no global round trip; thresholds beyond the
+//             window go to the global bitmap + summary (REDs), published by
+//             one fence when the window moves on
 //   q*[kSoloQ] closure worklist: (w, rowptr[w], rowptr[w+1]); the row
-//             pointers were loaded together with the atomic that reached w,
-//             so expanding w needs one dependent load (colidx) and one atomic
-//             round trip per level.  Overflow goes to the global ring (vertex
-//             only), then to the pend bitmap.
-constexpr int kSoloQ = 64;
+//             pointers were loaded together with the atomic that reached w.
+//             Overflow goes to the global ring (vertex only), then to pend.
 struct SoloWarpSmem {
   uint32_t win[32];
   int qw[kSoloQ], qb[kSoloQ], qe[kSoloQ];
 };
 
-// per-thread counters of the solo kernel, 32-bit, flushed after every group
+// per-thread counters of the solo kernel, 32-bit, flushed after every source
 struct SoloCounters {
   uint32_t items, pairs, levels, steps, sink;
 };
@@ -606,16 +631,20 @@ struct SoloCounters {
 struct SoloQueue {
   int sh, st;      // shared-memory worklist head / tail (warp-uniform)
   int gh, gt;      // global ring head / tail
-  bool spilled;    // items parked in pend (bit k)
+  bool spilled;    // items parked in pend
 };
 
-// one source, one warp: expand the items u (one per lane, -1 = none; beg/end
-// = its adjacency range) of the closure of T
+__device__ __forceinline__ uint32_t vbit(int v) { return 1u << (v & 31); }
+// summary bit of word (v >> 5): word (v >> 10), bit ((v >> 5) & 31)
+__device__ __forceinline__ void red_sum(uint32_t *sum, int v) {
+  atomicOr(sum + (v >> 10), 1u << ((v >> 5) & 31));
+}
+
+// expand the closure items u (one per lane, -1 = none; beg/end = adjacency)
+// of threshold T of source s
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
-                                            uint32_t *thr, uint32_t *tsum, uint32_t *q,
-                                            SoloWarpSmem &sw, int wb, SoloQueue &Q, int s,
-                                            uint32_t bit, int T, int u, int beg, int end, int lane,
-                                            SoloCounters &c) {
+                                            SoloWarpSmem &sw, int wb, SoloQueue &Q, int s, int T,
+                                            int u, int beg, int end, int lane, SoloCounters &c) {
   const int deg = u >= 0 ? end - beg : 0;
   c.items += u >= 0;
   c.pairs += (uint32_t)deg;
@@ -627,80 +656,71 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
   }
   const int total = __shfl_sync(kFull, incl, 31);
   const int excl = incl - deg;
-  for (int f0 = 0; f0 < total; f0 += 32 * kSoloBatch) {
-    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch];
-    uint32_t ro[kSoloBatch], io[kSoloBatch];
+  for (int f0 = 0; f0 < total; f0 += 32) {
+    const int f = f0 + lane;
+    int o = 0;
 #pragma unroll
-    for (int k = 0; k < kSoloBatch; ++k) {
-      const int f = f0 + 32 * k + lane;
-      int o = 0;
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const int cand = o + step;
-        const int e = __shfl_sync(kFull, excl, cand & 31);
-        if (cand < 32 && e <= f) o = cand;
-      }
-      const int ob = __shfl_sync(kFull, beg, o);
-      const int oe = __shfl_sync(kFull, excl, o);
-      w[k] = f < total ? __ldg(p.colidx + ob + (f - oe)) : s;
-      // w > s: entry of U; w < s: atomicMin(maxId(w), T) = first reach
-      ro[k] = w[k] < s ? atomicOr(sl.reached + w[k], bit) : bit;
-      io[k] = w[k] > s ? atomicOr(sl.is + w[k], bit) : kFull;
-      // w < T may join the closure: its row pointers travel with the atomic
-      rb[k] = re[k] = 0;
-      if (w[k] < T) {
-        rb[k] = __ldg(p.rowptr + w[k]);
-        re[k] = __ldg(p.rowptr + w[k] + 1);
-      }
+    for (int step = 16; step >= 1; step >>= 1) {
+      const int cand = o + step;
+      const int e = __shfl_sync(kFull, excl, cand & 31);
+      if (cand < 32 && e <= f) o = cand;
     }
-    bool push[kSoloBatch];
-#pragma unroll
-    for (int k = 0; k < kSoloBatch; ++k) {
-      push[k] = false;
-      if (io[k] == 0u) atomicOr(sl.isum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));  // RED
-      if (!(ro[k] & bit)) {
-        if (ro[k] == 0u) atomicOr(sl.rsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));  // RED
-        if (w[k] > T) {
-          // fill of L(s,:) (R4); w becomes a threshold of this source
-          atomicOr(sl.is + w[k], bit);                                                // RED
-          atomicOr(sl.isum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));                 // RED
-          const int d = (w[k] >> 5) - wb;
-          if (d < 32) {
-            atomicOr(&sw.win[d], 1u << (w[k] & 31));  // smem (d >= 0: w > T >= 32 wb)
-          } else {
-            atomicOr(thr + (w[k] >> 5), 1u << (w[k] & 31));                            // RED
-            atomicOr(tsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));                   // RED
-          }
+    const int ob = __shfl_sync(kFull, beg, o);
+    const int oe = __shfl_sync(kFull, excl, o);
+    const int w = f < total ? __ldg(p.colidx + ob + (f - oe)) : s;
+    const uint32_t bw = vbit(w);
+    // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds iff
+    // the source has not reached w yet (line 10 of fig:alg)
+    const uint32_t ro = w < s ? atomicOr(sl.reached + (w >> 5), bw) : bw;
+    const uint32_t io = w > s ? atomicOr(sl.is + (w >> 5), bw) : 1u;
+    // w < T may join the closure: its row pointers travel with the atomic
+    int rb = 0, re = 0;
+    if (w < T) {
+      rb = __ldg(p.rowptr + w);
+      re = __ldg(p.rowptr + w + 1);
+    }
+    if (io == 0u) red_sum(sl.isum, w);
+    bool push = false;
+    if (!(ro & bw)) {
+      if (ro == 0u) red_sum(sl.rsum, w);
+      if (w > T) {
+        // fill of L(s,:) (R4); w becomes a threshold of this source
+        atomicOr(sl.is + (w >> 5), bw);  // RED
+        red_sum(sl.isum, w);
+        const int d = (w >> 5) - wb;
+        if (d < 32) {
+          atomicOr(&sw.win[d], bw);  // smem (d >= 0: w > T >= 32 wb)
         } else {
-          push[k] = true;  // maxId(w) = T, not in the structure: continue with T
+          atomicOr(sl.thr + (w >> 5), bw);  // RED
+          red_sum(sl.tsum, w);
         }
+      } else {
+        push = true;  // maxId(w) = T, not in the structure: continue with T
       }
     }
-#pragma unroll
-    for (int k = 0; k < kSoloBatch; ++k) {
-      // shared worklist first, then the global ring, then park in pend
-      const uint32_t pb = __ballot_sync(kFull, push[k]);
-      if (!pb) continue;
+    // shared worklist, then the global ring, then park in pend
+    const uint32_t pb = __ballot_sync(kFull, push);
+    if (pb) {
       const int pos = Q.st + __popc(pb & lanemask_lt());
       const bool in_s = pos - Q.sh < kSoloQ;
-      if (push[k] && in_s) {
+      if (push && in_s) {
         const int i = pos & (kSoloQ - 1);
-        sw.qw[i] = w[k];
-        sw.qb[i] = rb[k];
-        sw.qe[i] = re[k];
+        sw.qw[i] = w;
+        sw.qb[i] = rb;
+        sw.qe[i] = re;
       }
-      const uint32_t sb = __ballot_sync(kFull, push[k] && in_s);
+      const uint32_t sb = __ballot_sync(kFull, push && in_s);
       Q.st += __popc(sb);
       const uint32_t gb = pb & ~sb;
       if (gb) {
         const int gpos = Q.gt + __popc(gb & lanemask_lt());
         const bool in_g = gpos - Q.gh <= sl.qmask;
-        if (push[k] && !in_s) {
-          if (in_g) q[gpos & sl.qmask] = (uint32_t)w[k];
-          else c.sink ^= atomicOr(sl.pend + w[k], bit);
+        if (push && !in_s) {
+          if (in_g) sl.queue[gpos & sl.qmask] = (uint32_t)w;
+          else atomicOr(sl.pend + (w >> 5), bw);  // RED
         }
-        Q.gt += __popc(__ballot_sync(kFull, push[k] && !in_s && in_g));
-        Q.spilled |= __ballot_sync(kFull, push[k] && !in_s && !in_g) != 0u;
+        Q.gt += __popc(__ballot_sync(kFull, push && !in_s && in_g));
+        Q.spilled |= __ballot_sync(kFull, push && !in_s && !in_g) != 0u;
       }
     }
   }
@@ -738,50 +758,29 @@ __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const ui
   return t;
 }
 
-__device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s, int k,
+// the max-id relaxation of source s in increasing threshold order
+__device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s,
                                             int lane, SoloCounters &c, SoloWarpSmem &sw) {
-  const uint32_t bit = 1u << k;
-  const int tbw_max = (p.Vmax + 31) >> 5;
-  const int tsw_max = (tbw_max + 31) >> 5;
-  uint32_t *thr = sl.thr + (size_t)k * tbw_max;
-  uint32_t *tsum = sl.tsum + (size_t)k * tsw_max;
-  uint32_t *q = sl.queue + (size_t)k * (sl.qmask + 1);
   const int tbw = (s + 31) >> 5;  // thresholds are < s
-  // seed
+  // seed: the out-neighbours of s are in the structure; the
+  // smaller ones are reached with maxId -1 and are thresholds
   const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
   for (int j = beg + lane; j < end; j += 32) {
     const int w = __ldg(p.colidx + j);
     if (w == s) continue;
-    atomicOr(sl.is + w, bit);                                  // RED
-    atomicOr(sl.isum + (w >> 10), 1u << ((w >> 5) & 31));      // RED
+    const uint32_t bw = vbit(w);
+    if (atomicOr(sl.is + (w >> 5), bw) == 0u) red_sum(sl.isum, w);
     if (w < s) {
-      if (atomicOr(sl.reached + w, bit) == 0u) atomicOr(sl.rsum + (w >> 10), 1u << ((w >> 5) & 31));
-      atomicOr(thr + (w >> 5), 1u << (w & 31));               // RED
-      atomicOr(tsum + (w >> 10), 1u << ((w >> 5) & 31));      // RED
+      if (atomicOr(sl.reached + (w >> 5), bw) == 0u) red_sum(sl.rsum, w);
+      atomicOr(sl.thr + (w >> 5), bw);  // RED
+      red_sum(sl.tsum, w);
     }
   }
   __syncwarp();
   int wb = -1;  // no window yet
   int T = -1;
-#ifdef GSOFA_PROF
-  // [0] next-threshold cycles [1] window misses [2] step-start cycles (rowptr of T)
-  // [3] expand cycles [4] worklist cycles [5] levels [6] steps [7] ring/pend levels
-  unsigned long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long t0 = clock64();
-#define PROF_MARK(i) do { const long long t1 = clock64(); pr[i] += t1 - t0; t0 = t1; } while (0)
-#else
-#define PROF_MARK(i) do {} while (0)
-#endif
   for (;;) {
-#ifdef GSOFA_PROF
-    const int wb_old = wb;
-#endif
-    T = solo_next_threshold(thr, tsum, tbw, T, wb, sw, lane);
-#ifdef GSOFA_PROF
-    pr[1] += wb != wb_old;
-    pr[6] += 1;
-#endif
-    PROF_MARK(0);
+    T = solo_next_threshold(sl.thr, sl.tsum, tbw, T, wb, sw, lane);
     if (T == INT_MAX) break;
     c.steps += 1;
     SoloQueue Q = {0, 0, 0, 0, false};
@@ -791,16 +790,10 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       ub = __ldg(p.rowptr + T);
       ue = __ldg(p.rowptr + T + 1);
     }
-    PROF_MARK(2);
     for (;;) {
       c.levels += 1;
-      solo_expand(p, sl, thr, tsum, q, sw, wb, Q, s, bit, T, u, ub, ue, lane, c);
+      solo_expand(p, sl, sw, wb, Q, s, T, u, ub, ue, lane, c);
       __syncwarp();
-#ifdef GSOFA_PROF
-      pr[5] += 1;
-      if (u >= 0) c.sink ^= (uint32_t)ub;  // wait for the expand's results
-#endif
-      PROF_MARK(3);
       if (Q.sh < Q.st) {
         const int cnt = min(32, Q.st - Q.sh);
         u = -1;
@@ -812,179 +805,223 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
         }
         Q.sh += cnt;
         __syncwarp();
-        PROF_MARK(4);
         continue;
       }
-#ifdef GSOFA_PROF
-      pr[7] += Q.gh < Q.gt || Q.spilled;
-#endif
       if (Q.gh >= Q.gt && Q.spilled) {
         // the ring overflowed during this closure: move parked items (pend
-        // bit k, all below T) back into the ring, as many as fit
+        // bits, all below T) back into the ring, as many as fit
         Q.spilled = false;
-        for (int b0 = 0; b0 < T; b0 += 32) {
-          const int v = b0 + lane;
-          const bool has = v < T && (__ldcg(sl.pend + v) & bit);
-          const uint32_t hb = __ballot_sync(kFull, has);
-          if (!hb) continue;
-          const int pos = Q.gt + __popc(hb & lanemask_lt());
-          const bool fits = pos - Q.gh <= sl.qmask;
-          if (has && fits) {
-            c.sink ^= atomicAnd(sl.pend + v, ~bit);
-            q[pos & sl.qmask] = (uint32_t)v;
-          }
-          Q.gt += __popc(__ballot_sync(kFull, has && fits));
-          if (__ballot_sync(kFull, has && !fits)) {
-            Q.spilled = true;  // still more parked: rescan after this batch drains
-            break;
+        __syncwarp();
+        fence_gpu();
+        for (int w0 = 0; w0 < ((T + 31) >> 5) && !Q.spilled; w0 += 32) {
+          const int wi = w0 + lane;
+          uint32_t x = wi < ((T + 31) >> 5) ? __ldcg(sl.pend + wi) : 0u;
+          for (;;) {
+            const bool has = x != 0u;
+            const uint32_t hb = __ballot_sync(kFull, has);
+            if (!hb) break;
+            const int pos = Q.gt + __popc(hb & lanemask_lt());
+            const bool fits = pos - Q.gh <= sl.qmask;
+            if (has && fits) {
+              const int b = __ffs(x) - 1;
+              x &= x - 1u;
+              atomicAnd(sl.pend + wi, ~(1u << b));  // RED
+              sl.queue[pos & sl.qmask] = (uint32_t)((wi << 5) + b);
+            }
+            Q.gt += __popc(__ballot_sync(kFull, has && fits));
+            if (__ballot_sync(kFull, has && !fits)) {
+              Q.spilled = true;  // still more parked: rescan after this batch drains
+              break;
+            }
           }
         }
         __syncwarp();
       }
       if (Q.gh >= Q.gt) break;
       const int cnt = min(32, Q.gt - Q.gh);
-      u = lane < cnt ? (int)q[(Q.gh + lane) & sl.qmask] : -1;
+      u = lane < cnt ? (int)sl.queue[(Q.gh + lane) & sl.qmask] : -1;
       Q.gh += cnt;
       if (u >= 0) {
         ub = __ldg(p.rowptr + u);
         ue = __ldg(p.rowptr + u + 1);
       }
-      PROF_MARK(4);
     }
   }
-#ifdef GSOFA_PROF
-  if (lane == 0 && p.prof)
-    for (int i = 0; i < 8; ++i) atomicAdd(p.prof + i, pr[i]);
-#endif
-#undef PROF_MARK
+}
+
+// Row s from the per-source structure bitmap: L(s,:) = bits below s, U(s,:) =
+// s then the bits above s, ascending; staged at one reservation; the bitmap
+// words read are zeroed.  Returns false if the staging area was full.
+__device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const SoloSlot &sl, int s,
+                                               int g, int lane) {
+  const int ns = (((p.n + 31) >> 5) + 31) >> 5;
+  // count pass: lane handles summary words i0 + lane (1024 vertices each)
+  uint32_t cl = 0, cu = 0;
+  for (int i0 = 0; i0 < ns; i0 += 32) {
+    const int i = i0 + lane;
+    uint32_t x = i < ns ? __ldcg(sl.isum + i) : 0u;
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1u;
+      const int wi = (i << 5) + b, v0 = wi << 5;
+      const uint32_t y = __ldcg(sl.is + wi);
+      const int d = s - v0;  // bits below d are < s, above d are > s
+      const uint32_t lm = d <= 0 ? 0u : (d >= 32 ? kFull : ((1u << d) - 1u));
+      const uint32_t um = d < 0 ? kFull : (d >= 31 ? 0u : (kFull << (d + 1)));
+      cl += __popc(y & lm);
+      cu += __popc(y & um);
+    }
+  }
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    cl += __shfl_xor_sync(kFull, cl, d);
+    cu += __shfl_xor_sync(kFull, cu, d);
+  }
+  const unsigned long long tot = (unsigned long long)cl + cu + 1;  // + the diagonal
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(p.stage_cursor, tot);
+  base = __shfl_sync(kFull, base, 0);
+  const bool ok = base + tot <= p.stage_cap;
+  const int r = s - p.row_begin;
+  if (lane == 0) {
+    p.row_off[r] = ok ? (long long)base : -1;
+    p.row_nL[r] = (int)cl;
+    p.row_nU[r] = (int)cu + 1;
+    if (ok) {
+      p.stage[base + cl] = s;  // U(s,:) starts with the diagonal
+    } else {
+      // the retry pass re-runs the whole group: ask for room for all of it
+      p.failed[atomicAdd(p.nfailed, 1)] = g;
+      atomicAdd(p.failed_need, tot * 32ull);
+    }
+  }
+  // write pass (zeroes what it reads): per summary word, lanes in ascending order
+  long long pl = (long long)base, pu = (long long)base + cl + 1;
+  for (int i0 = 0; i0 < ns; i0 += 32) {
+    const int i = i0 + lane;
+    const uint32_t x0 = i < ns ? __ldcg(sl.isum + i) : 0u;
+    if (!__ballot_sync(kFull, x0 != 0u)) continue;
+    if (x0) sl.isum[i] = 0u;
+    uint32_t nl = 0, nu = 0;
+    for (uint32_t x = x0; x;) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1u;
+      const int wi = (i << 5) + b, v0 = wi << 5;
+      const uint32_t y = __ldcg(sl.is + wi);
+      const int d = s - v0;
+      const uint32_t lm = d <= 0 ? 0u : (d >= 32 ? kFull : ((1u << d) - 1u));
+      const uint32_t um = d < 0 ? kFull : (d >= 31 ? 0u : (kFull << (d + 1)));
+      nl += __popc(y & lm);
+      nu += __popc(y & um);
+    }
+    uint32_t el = nl, eu = nu;  // inclusive prefix over lanes
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t a = __shfl_up_sync(kFull, el, d), bb = __shfl_up_sync(kFull, eu, d);
+      if (lane >= d) {
+        el += a;
+        eu += bb;
+      }
+    }
+    long long ol = pl + el - nl, ou = pu + eu - nu;
+    for (uint32_t x = x0; x;) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1u;
+      const int wi = (i << 5) + b, v0 = wi << 5;
+      uint32_t y = __ldcg(sl.is + wi);
+      sl.is[wi] = 0u;
+      if (!ok) continue;
+      while (y) {
+        const int v = v0 + __ffs(y) - 1;
+        y &= y - 1u;
+        if (v < s) p.stage[ol++] = v;
+        else p.stage[ou++] = v;
+      }
+    }
+    pl += __shfl_sync(kFull, el, 31);
+    pu += __shfl_sync(kFull, eu, 31);
+  }
+  return ok;
 }
 
 #ifndef GSOFA_SOLO_MINB
-#define GSOFA_SOLO_MINB 2
+#define GSOFA_SOLO_MINB (32 / kSoloWarps)  // 64 registers: measured faster than 32 with spills
 #endif
 __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(StreamParams p) {
-  constexpr int kWarps = kSoloWarps;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
-  const int n = p.n, Vmax = p.Vmax;
-  const int tbw_max = (Vmax + 31) >> 5;
-  const int tsw_max = (tbw_max + 31) >> 5;
-  const int rsw = (Vmax + 1023) >> 10;
-  SoloSlot sl;
-  uint32_t *base = p.hws + (size_t)blockIdx.x * p.hws_words;
-  sl.reached = base;
-  sl.pend = sl.reached + ((Vmax + 3) & ~3);
-  sl.rsum = sl.pend + ((Vmax + 3) & ~3);
-  sl.qmask = solo_ring(Vmax) - 1;
-  sl.thr = sl.rsum + ((rsw + 3) & ~3);
-  sl.tsum = sl.thr + (size_t)32 * tbw_max;
-  sl.queue = sl.tsum + (size_t)32 * tsw_max;
-  sl.is = p.is + ((size_t)p.light_slots + blockIdx.x) * p.is_words;
-  sl.isum = sl.is + n;
-
-  __shared__ int s_g;
-  __shared__ SoloWarpSmem s_sw[kWarps];
-  __shared__ uint32_t s_cnt[kWarps][2][32];
-  __shared__ long long s_rowoff[32];
-  __shared__ int s_nL[32];
-  __shared__ int s_ok;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rows = p.row_end - p.row_begin;
+  const size_t slot = (size_t)blockIdx.x * kSoloWarps + warp;
+  const SoloSlot sl = solo_slot(p, slot);
+  const int Vw = (p.Vmax + 31) >> 5, Vs = (Vw + 31) >> 5;
+  __shared__ SoloWarpSmem s_sw[kSoloWarps];
+  SoloWarpSmem &sw = s_sw[warp];
   SoloCounters c = {0u, 0u, 0u, 0u, 0u};
   uint32_t sink = 0u;
-
-  for (;;) {
-    if (tid == 0) {
-      // queued heavy groups first, then fresh groups (heaviest first); exit
-      // once every group is done
-      int gg = -1;
-      // the solo_top heaviest groups are reserved for this kernel
-      if (*(volatile unsigned *)p.solo_ctr < (unsigned)p.solo_top) {
-        const int j = (int)atomicAdd(p.solo_ctr, 1u);
-        if (j < p.solo_top) gg = p.ngroups - 1 - j;
-      }
-      for (; gg < 0;) {
-        const unsigned h = *(volatile unsigned *)p.hq_head;
-        const unsigned t = *(volatile unsigned *)p.hq_tail;
-        if (h < t) {
-          if (atomicCAS(p.hq_head, h, h + 1) == h) {
-            while (*(volatile int *)(p.hq_ready + h) == 0) __nanosleep(200);
-            gg = *(volatile int *)(p.hq + h);
-            break;
-          }
-          continue;
+  // first task: warp-major over the grid, so consecutive (heaviest) sources
+  // start on different SMs; then the global task counter
+  long long t = (long long)warp * gridDim.x + blockIdx.x;
+  const long long t_static = (long long)kSoloWarps * gridDim.x;
+  for (bool first = true;; first = false) {
+    if (!first) {
+      if (lane == 0) t = t_static + (long long)atomicAdd(p.task_ctr, 1ull);
+      t = __shfl_sync(kFull, t, 0);
+    }
+    const unsigned e = (unsigned)(t >> 5);
+    const int k = (int)(t & 31);
+    int g = -1;
+    if (lane == 0) {
+      for (;;) {
+        if (e < *(volatile unsigned *)p.hq_tail) {
+          while (*(volatile int *)(p.hq_ready + e) == 0) __nanosleep(200);
+          g = *(volatile int *)(p.hq + e);
+          break;
         }
+        // entry e does not exist yet: claim a fresh group (heaviest first)
+        // and queue it, unless every row is done
         const int nfresh = p.ngroups - p.solo_top;
         if (*(volatile unsigned *)p.group_ctr < (unsigned)nfresh) {
           const int j = (int)atomicAdd(p.group_ctr, 1u);
           if (j < nfresh) {
-            gg = nfresh - 1 - j;
-            break;
+            const unsigned idx = atomicAdd(p.hq_tail, 1u);
+            p.hq[idx] = nfresh - 1 - j;
+            __threadfence();
+            atomicExch(p.hq_ready + idx, 1);
+            continue;
           }
         }
-        if (*(volatile unsigned *)p.done >= (unsigned)p.ngroups) break;
+        if (*(volatile unsigned *)p.done >= (unsigned)rows) break;
         __nanosleep(1000);
       }
-      s_g = gg;
     }
-    __syncthreads();
-    const int g = s_g;
+    g = __shfl_sync(kFull, g, 0);
     if (g < 0) break;
-    const long long t_start = clock64();
-    const int s0g = p.row_begin + 32 * g;
-    const int nsrc = min(32, p.row_end - s0g);
-    if (warp < nsrc) solo_source(p, sl, s0g + warp, warp, lane, c, s_sw[warp]);
-    fence_gpu();
-    __syncthreads();
-    if (p.debug && warp == 0) {
-      for (int i = lane; i < Vmax; i += 32) {
-        const uint32_t v = __ldcg(sl.reached + i);
-        if (v && !((__ldcg(sl.rsum + (i >> 10)) >> ((i >> 5) & 31)) & 1)) {
-          const int slot_i = atomicAdd(p.debug, 1);
-          if (slot_i < 8) {
-            p.debug[1 + 4 * slot_i] = g;
-            p.debug[2 + 4 * slot_i] = i;
-            p.debug[3 + 4 * slot_i] = (int)v;
-            p.debug[4 + 4 * slot_i] = 2000 + (int)blockIdx.x;  // missing rsum bit
-          }
-          break;
-        }
+    const int s = p.row_begin + 32 * g + k;
+    if (s >= p.row_end) continue;  // tail of the last group
+    solo_source(p, sl, s, lane, c, sw);
+    fence_gpu();  // this warp's REDs are visible to its extraction
+    __syncwarp();
+    solo_stage_row(p, sl, s, g, lane);
+    // reset the touched words: reached | pend | thr, and the summaries
+    for (int i0 = 0; i0 < Vs; i0 += 32) {
+      const int i = i0 + lane;
+      uint32_t x = i < Vs ? __ldcg(sl.rsum + i) : 0u;
+      if (x) {
+        sl.rsum[i] = 0u;
+        sl.tsum[i] = 0u;
       }
-    }
-    __syncthreads();
-    const long long t_trav = clock64();
-    stage_rows<kWarps>(p, sl.is, sl.isum, s0g, nsrc, g, lane, warp, s_cnt, s_rowoff, s_nL, &s_ok,
-                       true);
-    const long long t_ext = clock64();
-    __syncthreads();  // extraction done in every warp before the reset below
-    // reset the touched lines: reached, and every source's thr word / tsum word
-    for (int i = warp; i < rsw; i += kWarps) {
-      uint32_t x = __ldcg(sl.rsum + i);
-      if (!x) continue;
-      if (lane == 0) sl.rsum[i] = 0u;
-      sl.tsum[(size_t)lane * tsw_max + i] = 0u;  // summary word of lines [32i, 32i+32)
       while (x) {
         const int b = __ffs(x) - 1;
         x &= x - 1u;
-        const int line = (i << 5) + b;
-        sl.reached[(line << 5) + lane] = 0u;
-        sl.thr[(size_t)lane * tbw_max + line] = 0u;
+        const int wi = (i << 5) + b;
+        sl.reached[wi] = 0u;
+        sl.pend[wi] = 0u;
+        sl.thr[wi] = 0u;
       }
     }
+    // the clears are plain stores; the next source's atomics act at L2
     __threadfence();
-    __syncthreads();
-    if (p.debug && warp == 0) {
-      for (int i = lane; i < Vmax; i += 32)
-        if (__ldcg(sl.reached + i)) {
-          const int slot_i = atomicAdd(p.debug, 1);
-          if (slot_i < 8) {
-            p.debug[1 + 4 * slot_i] = g;
-            p.debug[2 + 4 * slot_i] = i;
-            p.debug[3 + 4 * slot_i] = (int)__ldcg(sl.reached + i);
-            p.debug[4 + 4 * slot_i] = 3000 + (int)blockIdx.x;  // left after the reset
-          }
-          break;
-        }
-    }
+    __syncwarp();
     {
-      // flush this group's counters (warp sums; levels/steps are warp-uniform)
       uint32_t it = c.items, pr = c.pairs;
 #pragma unroll
       for (int d = 16; d >= 1; d >>= 1) {
@@ -997,29 +1034,14 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
         atomicAdd(p.stats + 4, (unsigned long long)pr);
         atomicAdd(p.stats + 2, (unsigned long long)c.levels);
         atomicAdd(p.stats + 3, (unsigned long long)c.steps);
-        if (p.group_trace) {
-          long long *tr = p.group_trace + 8 * (size_t)g;
-          atomicAdd((unsigned long long *)&tr[2], (unsigned long long)it);
-          atomicAdd((unsigned long long *)&tr[6], (unsigned long long)pr);
-          atomicMax((unsigned long long *)&tr[0], (unsigned long long)c.steps);
-          atomicMax((unsigned long long *)&tr[1], (unsigned long long)c.levels);
-          if (warp == 0) {
-            tr[3] = clock64() - t_start;
-            tr[4] = t_trav - t_start;
-            tr[5] = t_ext - t_trav;
-            tr[7] = 1;  // solo kernel
-          }
-        }
+        atomicAdd(p.done, 1u);
       }
       sink ^= c.sink;
       c = {0u, 0u, 0u, 0u, 0u};
     }
-    if (tid == 0) atomicAdd(p.done, 1u);
-    __syncthreads();
   }
   if (p.n < 0) p.stats[7] = sink;
 }
-
 
 // copies each staged row into the final CSR arrays (warp per row)
 __global__ void gather_kernel(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,
@@ -1094,13 +1116,14 @@ int stream_light_per_sm_with_solo(int device, int64_t Vmax) {
   return std::max(0, std::min(std::min(by_regs, by_warps), by_smem));
 }
 
-size_t solo_ws_words(int64_t Vmax) {
-  const size_t tbw = (size_t)((Vmax + 31) / 32), tsw = (tbw + 31) / 32;
-  const size_t rsw = (size_t)((Vmax + 1023) / 1024);
-  const size_t w = 2 * (((size_t)Vmax + 3) & ~(size_t)3) + ((rsw + 3) & ~(size_t)3) + 32 * tbw +
-                   32 * tsw + 32 * (size_t)solo_ring(Vmax);
+size_t solo_ws_words(int64_t Vmax, int64_t n) {
+  const size_t Vw = round4((size_t)((Vmax + 31) / 32)), Vs = round4((Vw + 31) / 32);
+  const size_t nw = round4((size_t)((n + 31) / 32)), ns = round4((nw + 31) / 32);
+  const size_t w = 3 * Vw + 2 * Vs + nw + ns + (size_t)solo_ring(Vmax);
   return (w + 7) / 8 * 8;
 }
+
+int solo_warps_per_cta() { return kSoloWarps; }
 
 cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st) {
   if (grid <= 0) return cudaSuccess;

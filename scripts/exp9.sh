@@ -1,0 +1,8 @@
+python -c "from paper_2007_00840_b200.build import build; build()"
+L=paper_2007_00840_b200
+timeout 900 python -m pytest tests/test_parity_gpu.py -x -q 2>&1 | tail -3
+for c in C2 C3 C4 C5; do
+  echo "== $c base"; timeout 120 python scripts/probe.py --config $c --reps 2 | tail -1
+  echo "== $c m2"; GSOFA_LIB=$L/libgsofa_m2.so timeout 120 python scripts/probe.py --config $c --reps 2 | tail -1
+done
+timeout 600 python scripts/scaling_emulation.py --config C2 --gpus 8

@@ -22,16 +22,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C5")
 ap.add_argument("--gpus", type=int, nargs="+", default=[2, 4, 8])
 ap.add_argument("--reps", type=int, default=2)
-ap.add_argument("--calibrated", action="store_true", help="use the sampled calibration partition")
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
 
 rp, ci = gen.config(a.config)
 n = rp.size - 1
-ctx = g.Context(0)
 
 
 def timed(rb, re):
+    # a fresh context per range, as each rank owns its GPU; best of reps
+    ctx = g.Context(0)
     best = None
     for _ in range(a.reps):
         r = g.symbolic(rp, ci, ctx=ctx, row_begin=rb, row_end=re, outputs_on_device=True)
@@ -39,6 +39,7 @@ def timed(rb, re):
         fill = r.fill_count
         r.free()
         best = ms if best is None else min(best, ms)
+    ctx.close()
     return best, fill
 
 
@@ -46,10 +47,7 @@ full_ms, full_fill = timed(0, n)
 print(f"{a.config}: 1 GPU {full_ms:.1f} ms, fill {full_fill}", flush=True)
 report = {"config": a.config, "n": n, "one_gpu_ms": full_ms, "fill": full_fill, "runs": []}
 for N in a.gpus:
-    if a.calibrated:
-        bounds = gd.partition_calibrated(rp, ci, N, ctx=ctx)
-    else:
-        bounds = gd.partition(rp, ci, N)
+    bounds = gd.partition(rp, ci, N)
     per = []
     fills = 0
     for r in range(N):
