@@ -324,22 +324,34 @@ def main():
     trav_ms = stats_acc.get("ms_traverse", 0.0)
     alg = algorithmic_bytes(stats_acc, args.schedule) if stats_acc else 0
     achieved = alg / (trav_ms / 1e3) / 1e9 if trav_ms > 0 else 0.0
-    traffic = None
+    traffic, traffic_src = None, None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         ent = tj.get(f"{args.config}/{args.schedule}")
         if ent:
-            traffic = {"dram_bytes_per_launch": ent["dram_bytes"], "kernel": ent["kernel"],
-                       "source": ent["source"]}
+            traffic = float(ent["dram_bytes"])  # per launch, from one ncu --set full capture
+            traffic_src = f'{ent["kernel"]}: {ent["source"]}'
     except Exception:
         pass
     roofline = {"kernel": ("solo_kernel+stream_kernel" if args.schedule == "threshold"
                            else "traverse_kernel"),
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": peak_src,
                 "algorithmic_bytes_per_step": alg / args.steps,
                 "kernel_ms_per_step": trav_ms / args.steps,
                 "kernel_share_of_step": (trav_ms / args.steps) / ms_per_step if ms_per_step else None}
+    # the unit operation of the traversal is a random 4-byte atomic (one per
+    # (item, neighbour) pair); its ceiling on this GPU was measured with
+    # scripts/atomics_bench.cu (profiles/atomic_peak.json)
+    try:
+        ap = json.load(open(os.path.join(ROOT, "profiles", "atomic_peak.json")))
+        a_peak = float(ap["atomicOr_returning_l2_gops"])
+        a_ach = stats_acc.get("item_edges", 0) / (trav_ms / 1e3) / 1e9 if trav_ms > 0 else 0.0
+        roofline["atomic"] = {"achieved": a_ach, "peak": a_peak, "unit": "G atomics/s",
+                              "frac": a_ach / a_peak, "peak_source": ap["source"]}
+    except Exception:
+        pass
     stats_step = {k: (v / args.steps) for k, v in stats_acc.items()}
 
     cpu = None
