@@ -769,10 +769,10 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     const int64_t ngroups = ceil_div(rows, 32);
     int64_t *row_off = nullptr;
     int32_t *row_nL = nullptr, *row_nU = nullptr, *failed = nullptr, *grp = nullptr;
-    int32_t *hq = nullptr, *hq_ready = nullptr;
+    int32_t *hq = nullptr, *hq_ready = nullptr, *gflag = nullptr;
     {
       cudaError_t e1 = cudaMallocAsync((void **)&stream_scratch,
-                                       (size_t)rows * 16 + (size_t)ngroups * 16 + 256, st);
+                                       (size_t)rows * 16 + (size_t)ngroups * 20 + 256, st);
       if (e1 != cudaSuccess) {
         cudaGetLastError();
         set_detail("row scratch allocation failed");
@@ -787,13 +787,16 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       grp = failed + ngroups;
       hq = grp + ngroups;
       hq_ready = hq + ngroups;
-      CK(cudaMemsetAsync(hq_ready, 0, (size_t)ngroups * 4, st));
+      gflag = hq_ready + ngroups;  // per group: already in the failed list
+      CK(cudaMemsetAsync(hq_ready, 0, (size_t)ngroups * 8, st));  // hq_ready + gflag
     }
     ev();
     if (c->stage_cap == 0) {
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
-      const size_t want = std::max<size_t>((size_t)1 << 24, (size_t)(fr * 0.3) / 4);
+      size_t want = std::max<size_t>((size_t)1 << 24, (size_t)(fr * 0.3) / 4);
+      // dev / tests: a small initial staging area exercises the overflow retry
+      if (const char *e = std::getenv("GSOFA_STAGE_CAP")) want = std::max<size_t>(1024, atoll(e));
       if ((rc = grow_device(&c->stage, &c->stage_cap, want, st)) != GSOFA_OK) goto fail;
     }
     unsigned int *group_ctr = c->qcount;
@@ -827,6 +830,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.row_nL = row_nL;
     sp.row_nU = row_nU;
     sp.failed = failed;
+    sp.failed_flag = gflag;
     sp.nfailed = nfailed;
     sp.failed_need = failed_need;
     sp.stats = c->stats;
@@ -859,6 +863,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.task_ctr = (unsigned long long *)(c->qcount + 6);  // qcount[6..7]
     sp.hws = c->work + (size_t)plan.light * plan.ws_words;
     sp.hws_words = plan.hws_words;
+    sp.solo_ring = gsofa::solo_ring(plan.Vmax);
     sp.light_slots = (int32_t)plan.light;
     sp.abort_cycles = 0;
     if (plan.heavy > 0) {
@@ -931,6 +936,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
                             st)) != GSOFA_OK)
         goto fail;
       CK(cudaMemcpyAsync(grp, failed, (size_t)nf * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemsetAsync(gflag, 0, (size_t)ngroups * 4, st));
       CK(cudaMemsetAsync(c->qcount, 0, 8, st));
       CK(cudaMemsetAsync(failed_need, 0, 8, st));
       sp.stage = c->stage;

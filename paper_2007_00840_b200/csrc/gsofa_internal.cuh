@@ -75,6 +75,7 @@ struct StreamParams {
   unsigned long long *task_ctr;  // solo kernel: next dynamic source task
   uint32_t *hws;             // [solo slots = solo CTAs x warps][hws_words] per-source workspaces
   size_t hws_words;
+  int32_t solo_ring;         // closure ring entries per solo slot (power of two)
   int32_t light_slots;       // is[] slots [0, light_slots) lockstep, then solo
   const int32_t *group_list; // optional explicit group ids (retry pass)
   int32_t list_len;
@@ -83,7 +84,8 @@ struct StreamParams {
   unsigned long long *stage_cursor;
   int64_t *row_off;          // [rows] staging offset (-1: not staged)
   int32_t *row_nL, *row_nU;  // [rows] counts (nU includes the diagonal)
-  int32_t *failed;           // groups whose rows did not fit the staging area
+  int32_t *failed;           // groups whose rows did not fit the staging area (each once)
+  int32_t *failed_flag;      // [ngroups] 1 once a group is in `failed`
   int32_t *nfailed;
   unsigned long long *failed_need;
   unsigned long long *stats; // items, edges, levels, thresholds, pairs
@@ -98,6 +100,7 @@ int stream_heavy_ratio();  // warps of a solo CTA / warps of a lockstep CTA
 int stream_warps_per_cta();  // lockstep slots (one group per warp) per CTA
 size_t solo_ws_words(int64_t Vmax, int64_t n);  // per solo slot (one warp, one source)
 int solo_warps_per_cta();
+int solo_ring(int64_t Vmax);
 int stream_light_per_sm_with_solo(int device, int64_t Vmax);
 size_t stream_smem_bytes(int64_t Vmax);  // dynamic smem: threshold-word summary
 cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st);

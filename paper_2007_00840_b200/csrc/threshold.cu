@@ -27,6 +27,7 @@
 // recorded in rsum/isum (first-touch tracking), never the whole slot.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "gsofa_internal.cuh"
 
@@ -282,7 +283,7 @@ __device__ __forceinline__ void stage_rows(const StreamParams &p, uint32_t *is, 
       if (lane == 0) {
         *s_ok = ok;
         if (!ok) {
-          p.failed[atomicAdd(p.nfailed, 1)] = g;
+          if (atomicExch(p.failed_flag + g, 1) == 0) p.failed[atomicAdd(p.nfailed, 1)] = g;
           atomicAdd(p.failed_need, (unsigned long long)tot);
         }
       }
@@ -551,12 +552,11 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
 //   is[nw] isum[nw/32]             in-structure bitmap over [0, n) + touched words
 //   ring[R]                        closure overflow (vertex ids)
 constexpr int kSoloQ = 64;  // shared-memory closure worklist entries per warp
+#ifndef GSOFA_SOLO_FILTER
+#define GSOFA_SOLO_FILTER 0
+#endif
 
-__host__ __device__ inline int solo_ring(int64_t Vmax) {
-  int r = 1024;
-  while (r < 16384 && r < Vmax) r <<= 1;
-  return r;
-}
+
 
 __host__ __device__ inline size_t round4(size_t w) { return (w + 3) & ~(size_t)3; }
 
@@ -577,7 +577,7 @@ __device__ __forceinline__ SoloSlot solo_slot(const StreamParams &p, size_t slot
   sl.is = sl.tsum + Vs;
   sl.isum = sl.is + nw;
   sl.queue = sl.isum + ns;
-  sl.qmask = solo_ring(p.Vmax) - 1;
+  sl.qmask = p.solo_ring - 1;
   return sl;
 }
 
@@ -671,8 +671,21 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
     const uint32_t bw = vbit(w);
     // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds iff
     // the source has not reached w yet (line 10 of fig:alg)
+#if GSOFA_SOLO_FILTER
+    // only this warp sets bits of its slot: a plain L2 load of the word is
+    // exact for everything set before this batch, so most inspections (w
+    // already reached / in the structure) need no atomic; the atomic stays
+    // the arbiter between lanes of this batch
+    uint32_t *wd = w < s ? sl.reached + (w >> 5) : (w > s ? sl.is + (w >> 5) : nullptr);
+    const uint32_t pre = wd ? __ldcg(wd) : bw;
+    const bool need = !(pre & bw);
+    const uint32_t ao = need ? atomicOr(wd, bw) : pre;
+    const uint32_t ro = w < s ? ao : bw;
+    const uint32_t io = w > s ? ao : 1u;
+#else
     const uint32_t ro = w < s ? atomicOr(sl.reached + (w >> 5), bw) : bw;
     const uint32_t io = w > s ? atomicOr(sl.is + (w >> 5), bw) : 1u;
+#endif
     // w < T may join the closure: its row pointers travel with the atomic
     int rb = 0, re = 0;
     if (w < T) {
@@ -891,7 +904,7 @@ __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const Solo
       p.stage[base + cl] = s;  // U(s,:) starts with the diagonal
     } else {
       // the retry pass re-runs the whole group: ask for room for all of it
-      p.failed[atomicAdd(p.nfailed, 1)] = g;
+      if (atomicExch(p.failed_flag + g, 1) == 0) p.failed[atomicAdd(p.nfailed, 1)] = g;
       atomicAdd(p.failed_need, tot * 32ull);
     }
   }
@@ -1114,6 +1127,18 @@ int stream_light_per_sm_with_solo(int device, int64_t Vmax) {
   const size_t light_smem = fl.sharedSizeBytes + stream_smem_bytes(Vmax) + 1024;
   const int by_smem = (int)((smem_sm - fs.sharedSizeBytes - 1024) / light_smem);
   return std::max(0, std::min(std::min(by_regs, by_warps), by_smem));
+}
+
+// closure ring entries per solo slot: a power of two; GSOFA_SOLO_RING (dev /
+// tests) forces a smaller one to exercise the pend-bitmap spill
+int solo_ring(int64_t Vmax) {
+  int r = 1024;
+  while (r < 16384 && r < Vmax) r <<= 1;
+  if (const char *e = std::getenv("GSOFA_SOLO_RING")) {
+    const int f = atoi(e);
+    if (f >= 32 && (f & (f - 1)) == 0) r = std::min(r, f);
+  }
+  return r;
 }
 
 size_t solo_ws_words(int64_t Vmax, int64_t n) {

@@ -284,3 +284,22 @@ def test_stream_paths_repeated(mode, monkeypatch):
         for rep in range(3):
             for (rp, ci), want in zip(cases, wants):
                 assert_full_equal(run(rp, ci, c), want, tag=f"{mode} rep {rep} n={rp.size - 1}")
+
+
+@pytest.mark.parametrize("knobs", [
+    {"GSOFA_STAGE_CAP": "4096"},                                  # staging overflow -> group retry
+    {"GSOFA_SOLO_RING": "32", "GSOFA_SOLO_TOP": "100000"},        # every group solo, ring spill to pend
+    {"GSOFA_STAGE_CAP": "20000", "GSOFA_SOLO_RING": "64", "GSOFA_ABORT_MS": "0.00001"},
+])
+def test_overflow_paths(knobs, monkeypatch):
+    """Rare paths of the streaming schedule, forced: a staging area far too
+    small (per-group and per-source reservations fail; the failed groups are
+    re-run on the lockstep kernel after the area grows) and a tiny solo
+    closure ring (items spill to the pend bitmap and are rescanned).  The
+    result must not change."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    cases = [gen.config("C5", 16), gen.config("C4", 70), gen.config("C3", 3000), gen.config("C2", 20)]
+    with g.Context(0) as c:
+        for rp, ci in cases:
+            assert_full_equal(run(rp, ci, c), oracle.symbolic(rp, ci), tag=f"{knobs} n={rp.size - 1}")
