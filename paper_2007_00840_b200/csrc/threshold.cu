@@ -552,9 +552,10 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
 //   is[nw] isum[nw/32]             in-structure bitmap over [0, n) + touched words
 //   ring[R]                        closure overflow (vertex ids)
 constexpr int kSoloQ = 64;  // shared-memory closure worklist entries per warp
-#ifndef GSOFA_SOLO_FILTER
-#define GSOFA_SOLO_FILTER 0
+#ifndef GSOFA_SOLO_BATCH
+#define GSOFA_SOLO_BATCH 2
 #endif
+constexpr int kSoloBatch = GSOFA_SOLO_BATCH;  // 32-pair batches a solo warp keeps in flight
 
 
 
@@ -656,84 +657,93 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
   }
   const int total = __shfl_sync(kFull, incl, 31);
   const int excl = incl - deg;
-  for (int f0 = 0; f0 < total; f0 += 32) {
-    const int f = f0 + lane;
-    int o = 0;
+  // kSoloBatch batches of 32 (item, neighbour) pairs are in flight at once:
+  // all their colidx loads, then all their atomics, then the pushes
+  for (int f0 = 0; f0 < total; f0 += 32 * kSoloBatch) {
+    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch];
+    uint32_t ro[kSoloBatch], io[kSoloBatch];
+    const int nb = min(kSoloBatch, (total - f0 + 31) >> 5);  // warp-uniform: skip empty batches
 #pragma unroll
-    for (int step = 16; step >= 1; step >>= 1) {
-      const int cand = o + step;
-      const int e = __shfl_sync(kFull, excl, cand & 31);
-      if (cand < 32 && e <= f) o = cand;
+    for (int k = 0; k < kSoloBatch; ++k) {
+      w[k] = s;
+      if (k >= nb) continue;
+      const int f = f0 + 32 * k + lane;
+      int o = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int cand = o + step;
+        const int e = __shfl_sync(kFull, excl, cand & 31);
+        if (cand < 32 && e <= f) o = cand;
+      }
+      const int ob = __shfl_sync(kFull, beg, o);
+      const int oe = __shfl_sync(kFull, excl, o);
+      w[k] = f < total ? __ldg(p.colidx + ob + (f - oe)) : s;
     }
-    const int ob = __shfl_sync(kFull, beg, o);
-    const int oe = __shfl_sync(kFull, excl, o);
-    const int w = f < total ? __ldg(p.colidx + ob + (f - oe)) : s;
-    const uint32_t bw = vbit(w);
-    // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds iff
-    // the source has not reached w yet (line 10 of fig:alg)
-#if GSOFA_SOLO_FILTER
-    // only this warp sets bits of its slot: a plain L2 load of the word is
-    // exact for everything set before this batch, so most inspections (w
-    // already reached / in the structure) need no atomic; the atomic stays
-    // the arbiter between lanes of this batch
-    uint32_t *wd = w < s ? sl.reached + (w >> 5) : (w > s ? sl.is + (w >> 5) : nullptr);
-    const uint32_t pre = wd ? __ldcg(wd) : bw;
-    const bool need = !(pre & bw);
-    const uint32_t ao = need ? atomicOr(wd, bw) : pre;
-    const uint32_t ro = w < s ? ao : bw;
-    const uint32_t io = w > s ? ao : 1u;
-#else
-    const uint32_t ro = w < s ? atomicOr(sl.reached + (w >> 5), bw) : bw;
-    const uint32_t io = w > s ? atomicOr(sl.is + (w >> 5), bw) : 1u;
-#endif
-    // w < T may join the closure: its row pointers travel with the atomic
-    int rb = 0, re = 0;
-    if (w < T) {
-      rb = __ldg(p.rowptr + w);
-      re = __ldg(p.rowptr + w + 1);
+#pragma unroll
+    for (int k = 0; k < kSoloBatch; ++k) {
+      ro[k] = io[k] = 1u;
+      rb[k] = re[k] = 0;
+      if (k >= nb) continue;
+      const uint32_t bw = vbit(w[k]);
+      // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds
+      // iff the source has not reached w yet (line 10 of fig:alg)
+      ro[k] = w[k] < s ? atomicOr(sl.reached + (w[k] >> 5), bw) : bw;
+      io[k] = w[k] > s ? atomicOr(sl.is + (w[k] >> 5), bw) : 1u;
+      // w < T may join the closure: its row pointers travel with the atomic
+      rb[k] = re[k] = 0;
+      if (w[k] < T) {
+        rb[k] = __ldg(p.rowptr + w[k]);
+        re[k] = __ldg(p.rowptr + w[k] + 1);
+      }
     }
-    if (io == 0u) red_sum(sl.isum, w);
-    bool push = false;
-    if (!(ro & bw)) {
-      if (ro == 0u) red_sum(sl.rsum, w);
-      if (w > T) {
-        // fill of L(s,:) (R4); w becomes a threshold of this source
-        atomicOr(sl.is + (w >> 5), bw);  // RED
-        red_sum(sl.isum, w);
-        const int d = (w >> 5) - wb;
-        if (d < 32) {
-          atomicOr(&sw.win[d], bw);  // smem (d >= 0: w > T >= 32 wb)
+#pragma unroll
+    for (int k = 0; k < kSoloBatch; ++k) {
+      if (k >= nb) continue;
+      const int wk = w[k];
+      const uint32_t bw = vbit(wk);
+      if (io[k] == 0u) red_sum(sl.isum, wk);
+      bool push = false;
+      if (!(ro[k] & bw)) {
+        if (ro[k] == 0u) red_sum(sl.rsum, wk);
+        if (wk > T) {
+          // fill of L(s,:) (R4); w becomes a threshold of this source
+          atomicOr(sl.is + (wk >> 5), bw);  // RED
+          red_sum(sl.isum, wk);
+          const int d = (wk >> 5) - wb;
+          if (d < 32) {
+            atomicOr(&sw.win[d], bw);  // smem (d >= 0: w > T >= 32 wb)
+          } else {
+            atomicOr(sl.thr + (wk >> 5), bw);  // RED
+            red_sum(sl.tsum, wk);
+          }
         } else {
-          atomicOr(sl.thr + (w >> 5), bw);  // RED
-          red_sum(sl.tsum, w);
+          push = true;  // maxId(w) = T, not in the structure: continue with T
         }
-      } else {
-        push = true;  // maxId(w) = T, not in the structure: continue with T
       }
-    }
-    // shared worklist, then the global ring, then park in pend
-    const uint32_t pb = __ballot_sync(kFull, push);
-    if (pb) {
-      const int pos = Q.st + __popc(pb & lanemask_lt());
-      const bool in_s = pos - Q.sh < kSoloQ;
-      if (push && in_s) {
-        const int i = pos & (kSoloQ - 1);
-        sw.qw[i] = w;
-        sw.qb[i] = rb;
-        sw.qe[i] = re;
-      }
-      const uint32_t sb = __ballot_sync(kFull, push && in_s);
-      Q.st += __popc(sb);
-      const uint32_t gb = pb & ~sb;
-      if (gb) {
-        const int gpos = Q.gt + __popc(gb & lanemask_lt());
-        const bool in_g = gpos - Q.gh <= sl.qmask;
-        if (push && !in_s) {
-          if (in_g) sl.queue[gpos & sl.qmask] = (uint32_t)w;
-          else atomicOr(sl.pend + (w >> 5), bw);  // RED
+      // shared worklist, then the global ring, then park in pend
+      const uint32_t pb = __ballot_sync(kFull, push);
+      if (pb) {
+        const int pos = Q.st + __popc(pb & lanemask_lt());
+        const bool in_s = pos - Q.sh < kSoloQ;
+        if (push && in_s) {
+          const int i = pos & (kSoloQ - 1);
+          sw.qw[i] = wk;
+          sw.qb[i] = rb[k];
+          sw.qe[i] = re[k];
         }
-        Q.gt += __popc(__ballot_sync(kFull, push && !in_s && in_g));
-        Q.spilled |= __ballot_sync(kFull, push && !in_s && !in_g) != 0u;
+        const uint32_t sb = __ballot_sync(kFull, push && in_s);
+        Q.st += __popc(sb);
+        const uint32_t gb = pb & ~sb;
+        if (gb) {
+          const int gpos = Q.gt + __popc(gb & lanemask_lt());
+          const bool in_g = gpos - Q.gh <= sl.qmask;
+          if (push && !in_s) {
+            if (in_g) sl.queue[gpos & sl.qmask] = (uint32_t)wk;
+            else atomicOr(sl.pend + (wk >> 5), bw);  // RED
+          }
+          Q.gt += __popc(__ballot_sync(kFull, push && !in_s && in_g));
+          Q.spilled |= __ballot_sync(kFull, push && !in_s && !in_g) != 0u;
+        }
       }
     }
   }
