@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -102,6 +103,7 @@ struct gsofa_context {
   int work_state = 0;        // WorkState
   uint64_t layout_sig = 0;   // streaming slot layout of the last call (Vmax, ws_words)
   int stream_blocks = 0;     // resident CTAs of the streaming kernel
+  int sms = 0, clock_khz = 0;  // device attributes, queried once (clock rate can be slow to query)
   int32_t *stage = nullptr;  // staging area for streamed rows (grow-only)
   size_t stage_cap = 0;
   uint32_t *work = nullptr, *is = nullptr;
@@ -460,6 +462,8 @@ int gsofa_context_create(int32_t device, int64_t mem_budget_bytes, gsofa_context
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   c->stream_blocks = gsofa::stream_max_blocks(device, 1 << 20, 0);
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&c->clock_khz, cudaDevAttrClockRate, device);
   c->max_blocks[0] = gsofa::traverse_max_blocks(device, 0);
   c->max_blocks[1] = gsofa::traverse_max_blocks(device, 1);
   if (c->max_blocks[0] <= 0 || c->max_blocks[1] <= 0 || c->stream_blocks <= 0) {
@@ -648,12 +652,15 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   std::vector<cudaEvent_t> evs;
   std::vector<int> ev_line;  // source line of each event (GSOFA_TIMELINE dev dump)
   int64_t launches = 0;
+  std::vector<double> ev_host;  // host clock at each event record (GSOFA_TIMELINE)
   auto ev_at = [&](int line) {
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, st);
     evs.push_back(e);
     ev_line.push_back(line);
+    ev_host.push_back(std::chrono::duration<double, std::milli>(
+                          std::chrono::steady_clock::now().time_since_epoch()).count());
     return (int)evs.size() - 1;
   };
 #define ev() ev_at(__LINE__)
@@ -869,11 +876,10 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     if (plan.heavy > 0) {
       // the heaviest groups (top separator / hub rows) start on
       // the solo kernel: one per first-wave solo CTA (one per SM)
-      int sms = 0;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-      int64_t top = std::min<int64_t>(plan.heavy, sms);
+      int64_t top = std::min<int64_t>(plan.heavy, c->sms);
       if (const char *e = std::getenv("GSOFA_SOLO_TOP")) top = std::min<int64_t>(plan.heavy, atoll(e));
       sp.solo_top = (int32_t)std::min<int64_t>(top, ngroups);
+      ev();
       // the solo_top heaviest groups are queued for the solo kernel up front
       if (sp.solo_top > 0) {
         std::vector<int32_t> hv((size_t)sp.solo_top * 2);
@@ -890,8 +896,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       }
       double ms = 5.0;
       if (const char *e = std::getenv("GSOFA_ABORT_MS")) ms = atof(e);
-      int khz = 0;
-      cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, c->device);
+      const int khz = c->clock_khz;
       sp.abort_cycles = (long long)(ms * (double)khz);
     }
     int64_t grid = plan.light;
@@ -1286,7 +1291,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     if (std::getenv("GSOFA_TIMELINE"))
       for (size_t i = 1; i < evs.size(); ++i) {
         cudaEventElapsedTime(&ms, evs[i - 1], evs[i]);
-        std::fprintf(stderr, "[timeline] api.cu:%d -> api.cu:%d  %.3f ms\n", ev_line[i - 1], ev_line[i], ms);
+        std::fprintf(stderr, "[timeline] api.cu:%d -> api.cu:%d  gpu %.3f ms  host %.3f ms\n", ev_line[i - 1],
+                     ev_line[i], ms, ev_host[i] - ev_host[i - 1]);
       }
   }
 #undef ev
