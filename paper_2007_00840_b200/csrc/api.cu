@@ -843,12 +843,6 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.stats = c->stats;
     sp.group_trace = nullptr;
     sp.debug = nullptr;
-    sp.prof = nullptr;
-    const char *prof_path = std::getenv("GSOFA_PROF");  // dev: cycle accounting (-DGSOFA_PROF builds)
-    if (prof_path && cudaMallocAsync((void **)&sp.prof, 16 * 8, st) == cudaSuccess)
-      cudaMemsetAsync(sp.prof, 0, 16 * 8, st);
-    else
-      cudaGetLastError();
     if (std::getenv("GSOFA_CHECK_CLEAN")) {
       cudaMallocAsync((void **)&sp.debug, 256, st);
       cudaMemsetAsync(sp.debug, 0, 256, st);
@@ -952,16 +946,6 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       sp.abort_cycles = 0;  // retries run on the lockstep kernel alone
       sp.solo_top = 0;
     }
-    if (sp.prof) {
-      unsigned long long h[16];
-      cudaMemcpyAsync(h, sp.prof, sizeof h, cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      if (FILE *f = std::fopen(prof_path, "ab")) {
-        std::fwrite(h, 8, 16, f);
-        std::fclose(f);
-      }
-      cudaFreeAsync(sp.prof, st);
-    }
     if (sp.group_trace) {
       std::vector<long long> h((size_t)ngroups * 8);
       cudaMemcpyAsync(h.data(), sp.group_trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
@@ -979,7 +963,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       std::vector<uint32_t> hw(c->work_bytes / 4), hi(c->is_words);
       cudaMemcpy(hw.data(), c->work, c->work_bytes, cudaMemcpyDeviceToHost);
       cudaMemcpy(hi.data(), c->is, c->is_words * 4, cudaMemcpyDeviceToHost);
-      const size_t Vm = plan.Vmax, tbw = (Vm + 31) / 32, tsw = (tbw + 31) / 32, rsw = (Vm + 1023) / 1024;
+      const size_t Vm = plan.Vmax, tbw = (Vm + 31) / 32, rsw = (Vm + 1023) / 1024;
       int reported = 0;
       for (int64_t sl = 0; sl < plan.light && reported < 8; ++sl) {
         const uint32_t *b = hw.data() + sl * plan.ws_words;

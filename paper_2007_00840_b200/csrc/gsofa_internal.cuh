@@ -91,7 +91,6 @@ struct StreamParams {
   unsigned long long *stats; // items, edges, levels, thresholds, pairs
   long long *group_trace;    // optional [ngroups][8]: steps, levels, items, cycles, ...
   int *debug;                // optional dev checks
-  unsigned long long *prof;  // optional [16] solo-kernel cycle accounting (GSOFA_PROF builds)
 };
 size_t stream_ws_words(int64_t Vmax);
 size_t stream_is_words(int64_t n);

@@ -338,7 +338,6 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
   const int n = p.n, Vmax = p.Vmax;
   const int tbw_max = (Vmax + 31) >> 5;
   const int rsw = (Vmax + 1023) >> 10;
-  const int isw = (n + 1023) >> 10;
   Slot sl;
   const size_t slot = blockIdx.x;
   sl.state = p.ws + slot * p.ws_words;
