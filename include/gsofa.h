@@ -205,6 +205,24 @@ int gsofa_supernode_stitch(gsofa_result *r, const gsofa_tail *prev, gsofa_tail *
 int gsofa_result_copy(const gsofa_result *r, int64_t *L_rowptr, int32_t *L_colidx,
                       int64_t *U_rowptr, int32_t *U_colidx, int32_t *sn_start);
 
+/*
+ * gsofa_result_l_csc -- L of a result in compressed sparse COLUMN form
+ * (SuperLU-style column storage; north_star "L and U patterns as CSR/CSC").
+ *   r          a gsofa_symbolic result over rows [row_begin, row_end)
+ *   on_device  1: the arrays are device memory (cudaMallocAsync), 0: host (malloc)
+ *   col_ptr    receives int64[n+1]: column j's entries are row_idx[col_ptr[j] ..
+ *              col_ptr[j+1]); columns span [0, n) (L(i,j) != 0 needs j < i)
+ *   row_idx    receives int32[nnz_L]: the rows i in [row_begin, row_end) with
+ *              L(i,j) != 0, ascending within each column
+ * The caller owns both arrays: release them with gsofa_buffer_free(p, on_device).
+ * Runs on the result's device: a stable radix sort of the (column, row) pairs
+ * by column, then a binary search per column.  Errors: GSOFA_EINVAL,
+ * GSOFA_ENOMEM, GSOFA_ECUDA (no arrays are returned).
+ */
+int gsofa_result_l_csc(const gsofa_result *r, int32_t on_device, int64_t **col_ptr,
+                       int32_t **row_idx);
+void gsofa_buffer_free(void *p, int32_t on_device);
+
 /* Frees every array of r (host or device) and r itself.  NULL is a no-op. */
 void gsofa_result_free(gsofa_result *r);
 

@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = [
     "gsofa_default_opts", "gsofa_context_create", "gsofa_context_destroy",
     "gsofa_symbolic", "gsofa_result_copy", "gsofa_result_free",
     "gsofa_partition_rows", "gsofa_strerror", "gsofa_last_error_detail",
-    "gsofa_version", "gsofa_supernode_stitch",
+    "gsofa_version", "gsofa_supernode_stitch", "gsofa_result_l_csc", "gsofa_buffer_free",
 ]
 
 _I64, _I32 = ctypes.c_int64, ctypes.c_int32
@@ -99,6 +99,9 @@ def load():
     lib.gsofa_partition_rows.argtypes = [_I64, ctypes.c_void_p, ctypes.c_void_p, _I32, _I32,
                                          ctypes.c_void_p]
     lib.gsofa_supernode_stitch.argtypes = [_P(CResult), ctypes.c_void_p, ctypes.c_void_p]
+    lib.gsofa_result_l_csc.argtypes = [_P(CResult), _I32, _P(_P(_I64)), _P(_P(_I32))]
+    lib.gsofa_buffer_free.argtypes = [ctypes.c_void_p, _I32]
+    lib.gsofa_buffer_free.restype = None
     lib.gsofa_strerror.restype = ctypes.c_char_p
     lib.gsofa_strerror.argtypes = [ctypes.c_int]
     lib.gsofa_last_error_detail.restype = ctypes.c_char_p
@@ -227,6 +230,23 @@ class Result:
         self.nsuper = self._p.contents.nsuper
         self._arrays = None
         return out
+
+    def l_csc(self):
+        """gsofa_result_l_csc: L in compressed sparse column form, as numpy
+        arrays col_ptr int64[n+1] (columns [0, n)) and row_idx int32[nnz_L]
+        (rows ascending within each column)."""
+        lib = load()
+        cp, ri = _P(_I64)(), _P(_I32)()
+        _check(lib.gsofa_result_l_csc(self._p, 0, ctypes.byref(cp), ctypes.byref(ri)),
+               "gsofa_result_l_csc")
+        try:
+            col_ptr = np.ctypeslib.as_array(cp, shape=(self.n + 1,)).copy()
+            row_idx = (np.ctypeslib.as_array(ri, shape=(self.nnz_L,)).copy() if self.nnz_L
+                       else np.empty(0, np.int32))
+        finally:
+            lib.gsofa_buffer_free(ctypes.cast(cp, ctypes.c_void_p), 0)
+            lib.gsofa_buffer_free(ctypes.cast(ri, ctypes.c_void_p), 0)
+        return dict(col_ptr=col_ptr, row_idx=row_idx)
 
     def __getitem__(self, k):
         return self.to_numpy()[k]

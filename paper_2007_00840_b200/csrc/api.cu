@@ -493,6 +493,93 @@ void gsofa_context_destroy(gsofa_context *c) {
   delete c;
 }
 
+int gsofa_result_l_csc(const gsofa_result *r, int32_t on_device, int64_t **col_ptr,
+                       int32_t **row_idx) {
+  if (!r || !col_ptr || !row_idx) {
+    set_detail("NULL argument to gsofa_result_l_csc");
+    return GSOFA_EINVAL;
+  }
+  *col_ptr = nullptr;
+  *row_idx = nullptr;
+  cudaError_t e = cudaSetDevice(r->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  const int64_t n = r->n, rows = r->row_end - r->row_begin, nnz = r->nnz_L;
+  int64_t *d_rp = nullptr, *d_cp = nullptr;
+  int32_t *d_ci = nullptr, *d_ri = nullptr;
+  bool own_in = false;
+  int rc = GSOFA_OK;
+  cudaStream_t st = nullptr;
+  auto dev_alloc = [&](void **p, size_t b) { return cudaMallocAsync(p, std::max<size_t>(b, 4), st); };
+  if (r->on_device) {
+    d_rp = r->L_rowptr;
+    d_ci = r->L_colidx;
+  } else {
+    own_in = true;
+    if ((e = dev_alloc((void **)&d_rp, (size_t)(rows + 1) * 8)) != cudaSuccess ||
+        (e = dev_alloc((void **)&d_ci, (size_t)nnz * 4)) != cudaSuccess)
+      goto cuda_err;
+    if ((e = cudaMemcpyAsync(d_rp, r->L_rowptr, (size_t)(rows + 1) * 8, cudaMemcpyHostToDevice, st)) !=
+            cudaSuccess ||
+        (nnz && (e = cudaMemcpyAsync(d_ci, r->L_colidx, (size_t)nnz * 4, cudaMemcpyHostToDevice, st)) !=
+                    cudaSuccess))
+      goto cuda_err;
+  }
+  if ((e = dev_alloc((void **)&d_cp, (size_t)(n + 1) * 8)) != cudaSuccess ||
+      (e = dev_alloc((void **)&d_ri, (size_t)nnz * 4)) != cudaSuccess)
+    goto cuda_err;
+  if ((e = gsofa::l_rows_to_csc(d_rp, d_ci, rows, r->row_begin, n, nnz, d_cp, d_ri, st)) != cudaSuccess)
+    goto cuda_err;
+  if (on_device) {
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) goto cuda_err;
+    *col_ptr = d_cp;
+    *row_idx = d_ri;
+    d_cp = nullptr;
+    d_ri = nullptr;
+  } else {
+    int64_t *h_cp = (int64_t *)std::malloc((size_t)(n + 1) * 8);
+    int32_t *h_ri = (int32_t *)std::malloc(std::max<size_t>((size_t)nnz * 4, 4));
+    if (!h_cp || !h_ri) {
+      std::free(h_cp);
+      std::free(h_ri);
+      set_detail("host allocation for L in CSC failed");
+      rc = GSOFA_ENOMEM;
+      goto done;
+    }
+    e = cudaMemcpyAsync(h_cp, d_cp, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(h_ri, d_ri, (size_t)nnz * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      std::free(h_cp);
+      std::free(h_ri);
+      goto cuda_err;
+    }
+    *col_ptr = h_cp;
+    *row_idx = h_ri;
+  }
+  goto done;
+cuda_err:
+  rc = cuda_fail(e, "gsofa_result_l_csc");
+done:
+  if (own_in) {
+    if (d_rp) cudaFreeAsync(d_rp, st);
+    if (d_ci) cudaFreeAsync(d_ci, st);
+  }
+  if (d_cp) cudaFreeAsync(d_cp, st);
+  if (d_ri) cudaFreeAsync(d_ri, st);
+  cudaStreamSynchronize(st);
+  return rc;
+}
+
+void gsofa_buffer_free(void *p, int32_t on_device) {
+  if (!p) return;
+  if (on_device) {
+    cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
+  } else {
+    std::free(p);
+  }
+}
+
 int gsofa_result_copy(const gsofa_result *r, int64_t *L_rowptr, int32_t *L_colidx,
                       int64_t *U_rowptr, int32_t *U_colidx, int32_t *sn_start) {
   if (!r) {

@@ -108,6 +108,12 @@ cudaError_t launch_gather(const int32_t *stage, const int64_t *row_off, const in
                           const int64_t *L_rowptr, const int64_t *U_rowptr, int rows,
                           int32_t *L_out, int32_t *U_out, cudaStream_t st);
 
+// csc.cu: L (CSR over rows [row_begin, row_begin + rows)) -> CSC over columns
+// [0, n): col_ptr[n+1], row_idx[nnz] (rows ascending per column); device arrays
+cudaError_t l_rows_to_csc(const int64_t *L_rowptr, const int32_t *L_colidx, int64_t rows,
+                          int64_t row_begin, int64_t n, int64_t nnz, int64_t *col_ptr,
+                          int32_t *row_idx, cudaStream_t st);
+
 // extract.cu
 struct ExtractParams {
   const uint32_t *is_ro;

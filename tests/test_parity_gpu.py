@@ -303,3 +303,32 @@ def test_overflow_paths(knobs, monkeypatch):
     with g.Context(0) as c:
         for rp, ci in cases:
             assert_full_equal(run(rp, ci, c), oracle.symbolic(rp, ci), tag=f"{knobs} n={rp.size - 1}")
+
+
+def _csc_of_rows(Lp, Li, row_begin, n):
+    """Reference CSC of an L slice (rows [row_begin, row_begin + rows)): plain
+    numpy, rows ascending within each column."""
+    rows = np.repeat(np.arange(row_begin, row_begin + Lp.size - 1, dtype=np.int64), np.diff(Lp))
+    order = np.lexsort((rows, Li))                     # by column, then row
+    cols = Li[order]
+    col_ptr = np.searchsorted(cols, np.arange(n + 1), side="left").astype(np.int64)
+    return col_ptr, rows[order].astype(np.int32)
+
+
+@pytest.mark.parametrize("name,scale,rb,re", [("C5", 14, 0, None), ("C3", 2000, 700, 1900),
+                                              ("C4", 60, 1000, None), ("C1", None, 0, None)])
+@pytest.mark.parametrize("on_device", [False, True])
+def test_l_csc(ctx, name, scale, rb, re, on_device):
+    """gsofa_result_l_csc: L by columns equals the transpose of the oracle's
+    L rows (column pointers over [0, n), rows ascending per column)."""
+    rp, ci = gen.config(name, scale)
+    n = rp.size - 1
+    re = n if re is None else re
+    want = oracle.symbolic(rp, ci, row_begin=rb, row_end=re)
+    r = g.symbolic(rp, ci, ctx=ctx, row_begin=rb, row_end=re, outputs_on_device=on_device)
+    got = r.l_csc()
+    r.free()
+    cp, ri = _csc_of_rows(want["L_rowptr"], want["L_colidx"], rb, n)
+    assert got["col_ptr"].dtype == np.int64 and got["row_idx"].dtype == np.int32
+    assert np.array_equal(got["col_ptr"], cp)
+    assert np.array_equal(got["row_idx"], ri)
