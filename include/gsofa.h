@@ -223,6 +223,21 @@ int gsofa_result_l_csc(const gsofa_result *r, int32_t on_device, int64_t **col_p
                        int32_t **row_idx);
 void gsofa_buffer_free(void *p, int32_t on_device);
 
+/*
+ * gsofa_permute -- symmetric permutation B = P A P^T of a pattern, for applying
+ * a fill-reducing ordering computed elsewhere (ordering itself is out of
+ * scope): new vertex i is old vertex perm[i], so
+ * B(i, j) != 0 iff A(perm[i], perm[j]) != 0.
+ *   n, rowptr int64[n+1], colidx int32[nnz]   input CSR (columns ascending)
+ *   perm      int32[n], a permutation of [0, n) (else GSOFA_EINVAL)
+ *   out_rowptr int64[n+1], out_colidx int32[nnz]   caller-allocated output,
+ *             columns ascending in every row
+ * All five pointers host, or all device.  Runs on the current CUDA device
+ * (one radix sort of (row, column) keys).  Synchronous.
+ */
+int gsofa_permute(int64_t n, const int64_t *rowptr, const int32_t *colidx, const int32_t *perm,
+                  int64_t *out_rowptr, int32_t *out_colidx);
+
 /* Frees every array of r (host or device) and r itself.  NULL is a no-op. */
 void gsofa_result_free(gsofa_result *r);
 

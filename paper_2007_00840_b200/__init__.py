@@ -19,7 +19,7 @@ import numpy as np
 
 from .build import LIB_PATH, build  # noqa: F401
 
-__all__ = ["Context", "Result", "Tail", "symbolic", "partition_rows", "load", "GsofaError",
+__all__ = ["Context", "Result", "Tail", "symbolic", "permute", "partition_rows", "load", "GsofaError",
            "EXPORTED_SYMBOLS", "build", "LIB_PATH"]
 
 EXPORTED_SYMBOLS = [
@@ -27,6 +27,7 @@ EXPORTED_SYMBOLS = [
     "gsofa_symbolic", "gsofa_result_copy", "gsofa_result_free",
     "gsofa_partition_rows", "gsofa_strerror", "gsofa_last_error_detail",
     "gsofa_version", "gsofa_supernode_stitch", "gsofa_result_l_csc", "gsofa_buffer_free",
+    "gsofa_permute",
 ]
 
 _I64, _I32 = ctypes.c_int64, ctypes.c_int32
@@ -102,6 +103,7 @@ def load():
     lib.gsofa_result_l_csc.argtypes = [_P(CResult), _I32, _P(_P(_I64)), _P(_P(_I32))]
     lib.gsofa_buffer_free.argtypes = [ctypes.c_void_p, _I32]
     lib.gsofa_buffer_free.restype = None
+    lib.gsofa_permute.argtypes = [_I64] + [ctypes.c_void_p] * 5
     lib.gsofa_strerror.restype = ctypes.c_char_p
     lib.gsofa_strerror.argtypes = [ctypes.c_int]
     lib.gsofa_last_error_detail.restype = ctypes.c_char_p
@@ -310,3 +312,21 @@ def partition_rows(rowptr, colidx, nparts: int, align: int = 1) -> np.ndarray:
                                     int(nparts), int(align), b.ctypes.data),
            "gsofa_partition_rows")
     return b
+
+
+def permute(rowptr, colidx, perm):
+    """gsofa_permute: B = P A P^T (new vertex i = old vertex perm[i]) on the
+    GPU; numpy in, numpy out (columns ascending per row)."""
+    lib = load()
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    perm = np.ascontiguousarray(perm, dtype=np.int32)
+    n = rowptr.size - 1
+    if perm.size != n:
+        raise ValueError(f"perm has {perm.size} entries, expected n = {n}")
+    out_rp = np.empty(n + 1, np.int64)
+    out_ci = np.empty(max(colidx.size, 1), np.int32)
+    ci = colidx if colidx.size else np.zeros(1, np.int32)
+    _check(lib.gsofa_permute(n, rowptr.ctypes.data, ci.ctypes.data, perm.ctypes.data,
+                             out_rp.ctypes.data, out_ci.ctypes.data), "gsofa_permute")
+    return out_rp, out_ci[:colidx.size]

@@ -570,6 +570,92 @@ done:
   return rc;
 }
 
+int gsofa_permute(int64_t n, const int64_t *rowptr, const int32_t *colidx, const int32_t *perm,
+                  int64_t *out_rowptr, int32_t *out_colidx) {
+  if (n <= 0 || n >= (int64_t(1) << 31) || !rowptr || !colidx || !perm || !out_rowptr || !out_colidx) {
+    set_detail("bad arguments to gsofa_permute");
+    return GSOFA_EINVAL;
+  }
+  cudaStream_t st = nullptr;
+  const bool dev = is_device_ptr(rowptr);
+  if (dev != is_device_ptr(colidx) || dev != is_device_ptr(perm) || dev != is_device_ptr(out_rowptr) ||
+      dev != is_device_ptr(out_colidx)) {
+    set_detail("gsofa_permute: pointers must all be host or all be device");
+    return GSOFA_EINVAL;
+  }
+  int64_t nnz = 0;
+  cudaError_t e = cudaSuccess;
+  if (dev) {
+    if ((e = cudaMemcpy(&nnz, rowptr + n, 8, cudaMemcpyDeviceToHost)) != cudaSuccess)
+      return cuda_fail(e, "gsofa_permute");
+  } else {
+    nnz = rowptr[n];
+  }
+  if (nnz < 0 || nnz >= (int64_t(1) << 31)) {
+    set_detail("gsofa_permute: nnz=%lld out of range", (long long)nnz);
+    return GSOFA_EBADCSR;
+  }
+  int64_t *d_rp = nullptr, *d_nrp = nullptr, *tot = nullptr;
+  int32_t *d_ci = nullptr, *d_perm = nullptr, *d_nci = nullptr, *d_iperm = nullptr, *d_deg = nullptr;
+  int *d_bad = nullptr;
+  void *tmp = nullptr;
+  int rc = GSOFA_OK, bad = 0;
+  const size_t tmpb = gsofa::scan_tmp_bytes(n);
+  auto A = [&](void **p, size_t b) { return cudaMallocAsync(p, std::max<size_t>(b, 8), st); };
+  if ((e = A((void **)&d_iperm, (size_t)n * 4)) != cudaSuccess || (e = A((void **)&d_deg, (size_t)n * 4)) != cudaSuccess ||
+      (e = A((void **)&d_bad, 64)) != cudaSuccess || (e = A(&tmp, tmpb)) != cudaSuccess)
+    goto cuda_err;
+  if (dev) {
+    d_rp = const_cast<int64_t *>(rowptr);
+    d_ci = const_cast<int32_t *>(colidx);
+    d_perm = const_cast<int32_t *>(perm);
+    d_nrp = out_rowptr;
+    d_nci = out_colidx;
+  } else {
+    if ((e = A((void **)&d_rp, (size_t)(n + 1) * 8)) != cudaSuccess || (e = A((void **)&d_ci, (size_t)nnz * 4)) != cudaSuccess ||
+        (e = A((void **)&d_perm, (size_t)n * 4)) != cudaSuccess || (e = A((void **)&d_nrp, (size_t)(n + 1) * 8)) != cudaSuccess ||
+        (e = A((void **)&d_nci, (size_t)nnz * 4)) != cudaSuccess)
+      goto cuda_err;
+    if ((e = cudaMemcpyAsync(d_rp, rowptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (nnz && (e = cudaMemcpyAsync(d_ci, colidx, (size_t)nnz * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) ||
+        (e = cudaMemcpyAsync(d_perm, perm, (size_t)n * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      goto cuda_err;
+  }
+  tot = (int64_t *)((char *)d_bad + 8);
+  if ((e = cudaMemsetAsync(d_bad, 0, 64, st)) != cudaSuccess) goto cuda_err;
+  if ((e = gsofa::launch_iperm(d_perm, n, d_iperm, d_bad, st)) != cudaSuccess) goto cuda_err;
+  if ((e = cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost)) != cudaSuccess) goto cuda_err;
+  if (bad) {
+    set_detail("gsofa_permute: perm is not a permutation of [0, n)%s%s", (bad & 1) ? " (entry out of range)" : "",
+               (bad & 2) ? " (duplicate entry)" : "");
+    rc = GSOFA_EINVAL;
+    goto done;
+  }
+  if ((e = gsofa::launch_perm_degrees(d_rp, d_perm, n, d_deg, st)) != cudaSuccess ||
+      (e = gsofa::scan_exclusive_i32_i64(d_deg, d_nrp, n, d_nrp + n, tmp, tmpb, st)) != cudaSuccess ||
+      (e = gsofa::permute_pattern(d_rp, d_ci, d_perm, d_iperm, n, nnz, d_nrp, d_nci, st)) != cudaSuccess)
+    goto cuda_err;
+  if (!dev) {
+    if ((e = cudaMemcpyAsync(out_rowptr, d_nrp, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (nnz && (e = cudaMemcpyAsync(out_colidx, d_nci, (size_t)nnz * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess))
+      goto cuda_err;
+  }
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) goto cuda_err;
+  goto done;
+cuda_err:
+  rc = cuda_fail(e, "gsofa_permute");
+done:
+  (void)tot;
+  if (!dev) {
+    for (void *p : {(void *)d_rp, (void *)d_ci, (void *)d_perm, (void *)d_nrp, (void *)d_nci})
+      if (p) cudaFreeAsync(p, st);
+  }
+  for (void *p : {(void *)d_iperm, (void *)d_deg, (void *)d_bad, tmp})
+    if (p) cudaFreeAsync(p, st);
+  cudaStreamSynchronize(st);
+  return rc;
+}
+
 void gsofa_buffer_free(void *p, int32_t on_device) {
   if (!p) return;
   if (on_device) {

@@ -114,6 +114,14 @@ cudaError_t l_rows_to_csc(const int64_t *L_rowptr, const int32_t *L_colidx, int6
                           int64_t row_begin, int64_t n, int64_t nnz, int64_t *col_ptr,
                           int32_t *row_idx, cudaStream_t st);
 
+// csc.cu: symmetric permutation B = P A P^T of a pattern (device arrays)
+cudaError_t launch_iperm(const int32_t *perm, int64_t n, int32_t *iperm, int *bad, cudaStream_t st);
+cudaError_t launch_perm_degrees(const int64_t *rowptr, const int32_t *perm, int64_t n, int32_t *deg,
+                                cudaStream_t st);
+cudaError_t permute_pattern(const int64_t *rowptr, const int32_t *colidx, const int32_t *perm,
+                            const int32_t *iperm, int64_t n, int64_t nnz, const int64_t *new_rowptr,
+                            int32_t *new_colidx, cudaStream_t st);
+
 // extract.cu
 struct ExtractParams {
   const uint32_t *is_ro;

@@ -332,3 +332,35 @@ def test_l_csc(ctx, name, scale, rb, re, on_device):
     assert got["col_ptr"].dtype == np.int64 and got["row_idx"].dtype == np.int32
     assert np.array_equal(got["col_ptr"], cp)
     assert np.array_equal(got["row_idx"], ri)
+
+
+def _permute_ref(rp, ci, perm):
+    """B = P A P^T by plain numpy: B(i, j) != 0 iff A(perm[i], perm[j]) != 0."""
+    n = rp.size - 1
+    iperm = np.empty(n, np.int64)
+    iperm[perm] = np.arange(n)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    r2, c2 = iperm[rows], iperm[ci]
+    key = np.sort(r2 * n + c2)
+    return (np.concatenate([[0], np.cumsum(np.bincount(key // n, minlength=n))]).astype(np.int64),
+            (key % n).astype(np.int32))
+
+
+@pytest.mark.parametrize("name,scale", [("C4", 60), ("C3", 1500), ("C1", None)])
+def test_permute(ctx, name, scale):
+    """gsofa_permute equals the numpy permutation, and factorizing the
+    permuted pattern matches the oracle on it (an ordering applied on the
+    GPU, then the symbolic factorization)."""
+    rp, ci = gen.config(name, scale)
+    n = rp.size - 1
+    perm = np.random.default_rng(11).permutation(n).astype(np.int32)
+    brp, bci = g.permute(rp, ci, perm)
+    wrp, wci = _permute_ref(rp, ci, perm)
+    assert np.array_equal(brp, wrp) and np.array_equal(bci, wci)
+    assert np.array_equal(g.permute(rp, ci, np.arange(n, dtype=np.int32))[1], ci)  # identity
+    assert_full_equal(run(brp, bci, ctx), oracle.symbolic(brp, bci))
+    bad = perm.copy()
+    bad[0] = bad[1]
+    with pytest.raises(g.GsofaError) as e:
+        g.permute(rp, ci, bad)
+    assert e.value.code == -1
