@@ -87,6 +87,17 @@ struct ResultImpl {
 };
 
 // ------------------------------------------------------------------ context
+struct Plan {
+  int64_t Cmax, Gmax;
+  int gbits;
+  size_t work_bytes, is_words, cnt_words;
+  int64_t nsub;
+  size_t total;
+  // streaming (threshold) schedule
+  int64_t slots = 0, heavy = 0, light = 0, Vmax = 0;
+  size_t ws_words = 0, slot_is_words = 0, hws_words = 0;
+};
+
 struct gsofa_context {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -104,6 +115,10 @@ struct gsofa_context {
   uint64_t layout_sig = 0;   // streaming slot layout of the last call (Vmax, ws_words)
   int stream_blocks = 0;     // resident CTAs of the streaming kernel
   int sms = 0, clock_khz = 0;  // device attributes, queried once (clock rate can be slow to query)
+  // last plan and its key: repeated calls on the same problem skip the
+  // free-memory query and the occupancy queries, and keep the arena layout
+  Plan plan_cache;
+  int64_t plan_key[6] = {-1, -1, -1, -1, -1, -1};
   int32_t *stage = nullptr;  // staging area for streamed rows (grow-only)
   size_t stage_cap = 0;
   uint32_t *work = nullptr, *is = nullptr;
@@ -132,16 +147,7 @@ void release_arena(gsofa_context *c) {
   c->key_n = -1;
 }
 
-struct Plan {
-  int64_t Cmax, Gmax;
-  int gbits;
-  size_t work_bytes, is_words, cnt_words;
-  int64_t nsub;
-  size_t total;
-  // streaming (threshold) schedule
-  int64_t slots = 0, heavy = 0, light = 0, Vmax = 0;
-  size_t ws_words = 0, slot_is_words = 0, hws_words = 0;
-};
+
 
 size_t small_bytes(int64_t Cmax) {
   return (size_t)Cmax * 2 * sizeof(int64_t) + 64 + 64 + 64 + 256;
@@ -886,13 +892,25 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   {
     const int64_t cmax_req =
         o.max_concurrent ? o.max_concurrent : (o.schedule == GSOFA_SCHEDULE_FIFO ? 16384 : 65536);
-    int64_t budget = o.mem_budget_bytes ? o.mem_budget_bytes : c->budget;
-    if (!budget) budget = auto_budget(c->device) + (int64_t)c->arena_bytes;
-    const int64_t vb_max = std::min<int64_t>(n, re + 32);
-    const bool ok = o.schedule == GSOFA_SCHEDULE_FIFO
-                        ? make_plan(o.schedule, n, rows, vb_max, cmax_req, budget, plan)
-                        : make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device,
-                                           plan);
+    const int64_t budget_req = o.mem_budget_bytes ? o.mem_budget_bytes : c->budget;
+    const int64_t key[6] = {o.schedule, n, rb, re, budget_req, cmax_req};
+    bool ok = true;
+    if (std::equal(key, key + 6, c->plan_key)) {
+      plan = c->plan_cache;
+    } else {
+      int64_t budget = budget_req;
+      if (!budget) budget = auto_budget(c->device) + (int64_t)c->arena_bytes;
+      const int64_t vb_max = std::min<int64_t>(n, re + 32);
+      ok = o.schedule == GSOFA_SCHEDULE_FIFO
+               ? make_plan(o.schedule, n, rows, vb_max, cmax_req, budget, plan)
+               : make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan);
+      if (ok && !std::getenv("GSOFA_LIGHT_CTAS") && !std::getenv("GSOFA_SOLO_CTAS") &&
+          !std::getenv("GSOFA_SOLO_RING")) {
+        c->plan_cache = plan;
+        std::copy(key, key + 6, c->plan_key);
+      }
+    }
+    const int64_t budget = budget_req;  // (for the message below; 0 = automatic)
     if (!ok) {
       set_detail("budget %lld B cannot hold one 32-source group for n=%lld", (long long)budget,
                  (long long)n);
