@@ -648,13 +648,19 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
   const int deg = u >= 0 ? end - beg : 0;
   c.items += u >= 0;
   c.pairs += (uint32_t)deg;
+  // fast path (every threshold's level 0, most closure levels of a chain):
+  // one item in lane 0 with at most 32 neighbours -- lane j takes neighbour
+  // j, no prefix scan or owner search on the chain's critical path
+  const bool single = __ballot_sync(kFull, u >= 0) == 1u && __shfl_sync(kFull, deg, 0) <= 32;
   int incl = deg;
+  if (!single) {
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int y = __shfl_up_sync(kFull, incl, d);
-    if (lane >= d) incl += y;
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += y;
+    }
   }
-  const int total = __shfl_sync(kFull, incl, 31);
+  const int total = single ? __shfl_sync(kFull, deg, 0) : __shfl_sync(kFull, incl, 31);
   const int excl = incl - deg;
   // kSoloBatch batches of 32 (item, neighbour) pairs are in flight at once:
   // all their colidx loads, then all their atomics, then the pushes
@@ -667,6 +673,11 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       w[k] = s;
       if (k >= nb) continue;
       const int f = f0 + 32 * k + lane;
+      if (single) {
+        const int b0 = __shfl_sync(kFull, beg, 0);
+        w[k] = f < total ? __ldg(p.colidx + b0 + f) : s;
+        continue;
+      }
       int o = 0;
 #pragma unroll
       for (int step = 16; step >= 1; step >>= 1) {
