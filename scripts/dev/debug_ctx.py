@@ -1,6 +1,6 @@
 """Dev: repeated calls on one context vs the oracle."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import gen, oracle
 import paper_2007_00840_b200 as g

@@ -1,6 +1,6 @@
 """Dev: which rows differ from the oracle under lockstep-only / solo-forced / default."""
 import os, sys, subprocess
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import gen, oracle
 mode = sys.argv[1] if len(sys.argv) > 1 else "default"
