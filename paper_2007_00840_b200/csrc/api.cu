@@ -378,6 +378,18 @@ int grow_device(T **buf, size_t *cap, size_t need, cudaStream_t st) {
   return GSOFA_OK;
 }
 
+// gsofa_partition_rows cost exponent: cost(s) = work(s)^alpha.  With many
+// ranks, the ranks holding the top separator are bound by their longest
+// chains rather than their total work, so heavy rows are weighted slightly
+// below their work.  With few ranks the top rank is throughput-bound and
+// alpha = 1 balances best.  Measured with scripts/scaling_emulation.py: C5 at
+// 8 ranks max rank 685 -> 633 ms (alpha 0.94), but at 2 ranks 1.82x -> 1.61x.
+double part_alpha(int nparts) {
+  if (nparts <= 4) return 1.0;
+  if (nparts >= 8) return 0.94;
+  return 1.0 - 0.015 * (nparts - 4);
+}
+
 int64_t auto_budget(int device) {
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
@@ -1566,8 +1578,11 @@ int gsofa_partition_rows(int64_t n, const int64_t *rowptr, const int32_t *colidx
   for (int64_t v = 0; v < n; ++v) w[v] = 1.0 + (double)(rowptr[v + 1] - rowptr[v]);
   for (int64_t v = 0; v < n; ++v)
     if (parent[v] >= 0) w[parent[v]] += w[v];
+  // cost(s) = work(s)^alpha; GSOFA_PART_ALPHA overrides (dev calibration)
+  double alpha = part_alpha(nparts);
+  if (const char *e = std::getenv("GSOFA_PART_ALPHA")) alpha = atof(e);
   std::vector<double> pre(n + 1, 0.0);
-  for (int64_t v = 0; v < n; ++v) pre[v + 1] = pre[v] + w[v];
+  for (int64_t v = 0; v < n; ++v) pre[v + 1] = pre[v] + (alpha == 1.0 ? w[v] : std::pow(w[v], alpha));
   bounds[0] = 0;
   for (int32_t p = 1; p < nparts; ++p) {
     const double target = pre[n] * p / nparts;

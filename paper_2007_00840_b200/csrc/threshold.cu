@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
 //   ring[R]                        closure overflow (vertex ids)
 constexpr int kSoloQ = 64;  // shared-memory closure worklist entries per warp
 #ifndef GSOFA_SOLO_BATCH
-#define GSOFA_SOLO_BATCH 2
+#define GSOFA_SOLO_BATCH 1
 #endif
 constexpr int kSoloBatch = GSOFA_SOLO_BATCH;  // 32-pair batches a solo warp keeps in flight
 
@@ -560,25 +560,37 @@ constexpr int kSoloBatch = GSOFA_SOLO_BATCH;  // 32-pair batches a solo warp kee
 
 __host__ __device__ inline size_t round4(size_t w) { return (w + 3) & ~(size_t)3; }
 
+// A solo slot is one base pointer; the array offsets are recomputed from
+// the launch parameters where they are used (fewer live registers: the
+// kernel runs at the register budget of 32 warps per SM).
 struct SoloSlot {
-  uint32_t *reached, *pend, *thr, *rsum, *tsum, *is, *isum, *queue;
-  int qmask;
+  uint32_t *base;
 };
 
+__device__ __forceinline__ size_t solo_vw(const StreamParams &p) {
+  return round4((size_t)((p.Vmax + 31) >> 5));
+}
+__device__ __forceinline__ size_t solo_vs(const StreamParams &p) {
+  return round4((solo_vw(p) + 31) >> 5);
+}
+__device__ __forceinline__ size_t solo_nw(const StreamParams &p) {
+  return round4((size_t)((p.n + 31) >> 5));
+}
+__device__ __forceinline__ size_t solo_ns(const StreamParams &p) {
+  return round4((solo_nw(p) + 31) >> 5);
+}
+#define SL_REACHED (sl.base)
+#define SL_PEND (sl.base + solo_vw(p))
+#define SL_THR (sl.base + 2 * solo_vw(p))
+#define SL_RSUM (sl.base + 3 * solo_vw(p))
+#define SL_TSUM (sl.base + 3 * solo_vw(p) + solo_vs(p))
+#define SL_IS (sl.base + 3 * solo_vw(p) + 2 * solo_vs(p))
+#define SL_ISUM (SL_IS + solo_nw(p))
+#define SL_QUEUE (SL_ISUM + solo_ns(p))
+#define SL_QMASK (p.solo_ring - 1)
+
 __device__ __forceinline__ SoloSlot solo_slot(const StreamParams &p, size_t slot) {
-  const size_t Vw = round4((size_t)((p.Vmax + 31) >> 5)), Vs = round4((Vw + 31) >> 5);
-  const size_t nw = round4((size_t)((p.n + 31) >> 5)), ns = round4((nw + 31) >> 5);
-  SoloSlot sl;
-  sl.reached = p.hws + slot * p.hws_words;
-  sl.pend = sl.reached + Vw;
-  sl.thr = sl.pend + Vw;
-  sl.rsum = sl.thr + Vw;
-  sl.tsum = sl.rsum + Vs;
-  sl.is = sl.tsum + Vs;
-  sl.isum = sl.is + nw;
-  sl.queue = sl.isum + ns;
-  sl.qmask = p.solo_ring - 1;
-  return sl;
+  return SoloSlot{p.hws + slot * p.hws_words};
 }
 
 __device__ __forceinline__ int solo_scan_next(const uint32_t *thr, const uint32_t *tsum, int tbw,
@@ -621,11 +633,7 @@ __device__ __forceinline__ int solo_scan_next(const uint32_t *thr, const uint32_
 struct SoloWarpSmem {
   uint32_t win[32];
   int qw[kSoloQ], qb[kSoloQ], qe[kSoloQ];
-};
-
-// per-thread counters of the solo kernel, 32-bit, flushed after every source
-struct SoloCounters {
-  uint32_t items, pairs, levels, steps, sink;
+  uint32_t items, pairs, levels, steps;  // this source's counters (lane 0 updates)
 };
 
 struct SoloQueue {
@@ -644,10 +652,8 @@ __device__ __forceinline__ void red_sum(uint32_t *sum, int v) {
 // of threshold T of source s
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
                                             SoloWarpSmem &sw, int wb, SoloQueue &Q, int s, int T,
-                                            int u, int beg, int end, int lane, SoloCounters &c) {
+                                            int u, int beg, int end, int lane) {
   const int deg = u >= 0 ? end - beg : 0;
-  c.items += u >= 0;
-  c.pairs += (uint32_t)deg;
   // fast path (every threshold's level 0, most closure levels of a chain):
   // one item in lane 0 with at most 32 neighbours -- lane j takes neighbour
   // j, no prefix scan or owner search on the chain's critical path
@@ -662,6 +668,14 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
   }
   const int total = single ? __shfl_sync(kFull, deg, 0) : __shfl_sync(kFull, incl, 31);
   const int excl = incl - deg;
+  {
+    const uint32_t nitems = __popc(__ballot_sync(kFull, u >= 0));
+    if (lane == 0) {
+      sw.items += nitems;
+      sw.pairs += (uint32_t)total;
+      sw.levels += 1;
+    }
+  }
   // kSoloBatch batches of 32 (item, neighbour) pairs are in flight at once:
   // all their colidx loads, then all their atomics, then the pushes
   for (int f0 = 0; f0 < total; f0 += 32 * kSoloBatch) {
@@ -697,8 +711,8 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       const uint32_t bw = vbit(w[k]);
       // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds
       // iff the source has not reached w yet (line 10 of fig:alg)
-      ro[k] = w[k] < s ? atomicOr(sl.reached + (w[k] >> 5), bw) : bw;
-      io[k] = w[k] > s ? atomicOr(sl.is + (w[k] >> 5), bw) : 1u;
+      ro[k] = w[k] < s ? atomicOr(SL_REACHED + (w[k] >> 5), bw) : bw;
+      io[k] = w[k] > s ? atomicOr(SL_IS + (w[k] >> 5), bw) : 1u;
       // w < T may join the closure: its row pointers travel with the atomic
       rb[k] = re[k] = 0;
       if (w[k] < T) {
@@ -711,20 +725,20 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       if (k >= nb) continue;
       const int wk = w[k];
       const uint32_t bw = vbit(wk);
-      if (io[k] == 0u) red_sum(sl.isum, wk);
+      if (io[k] == 0u) red_sum(SL_ISUM, wk);
       bool push = false;
       if (!(ro[k] & bw)) {
-        if (ro[k] == 0u) red_sum(sl.rsum, wk);
+        if (ro[k] == 0u) red_sum(SL_RSUM, wk);
         if (wk > T) {
           // fill of L(s,:) (R4); w becomes a threshold of this source
-          atomicOr(sl.is + (wk >> 5), bw);  // RED
-          red_sum(sl.isum, wk);
+          atomicOr(SL_IS + (wk >> 5), bw);  // RED
+          red_sum(SL_ISUM, wk);
           const int d = (wk >> 5) - wb;
           if (d < 32) {
             atomicOr(&sw.win[d], bw);  // smem (d >= 0: w > T >= 32 wb)
           } else {
-            atomicOr(sl.thr + (wk >> 5), bw);  // RED
-            red_sum(sl.tsum, wk);
+            atomicOr(SL_THR + (wk >> 5), bw);  // RED
+            red_sum(SL_TSUM, wk);
           }
         } else {
           push = true;  // maxId(w) = T, not in the structure: continue with T
@@ -746,10 +760,10 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
         const uint32_t gb = pb & ~sb;
         if (gb) {
           const int gpos = Q.gt + __popc(gb & lanemask_lt());
-          const bool in_g = gpos - Q.gh <= sl.qmask;
+          const bool in_g = gpos - Q.gh <= SL_QMASK;
           if (push && !in_s) {
-            if (in_g) sl.queue[gpos & sl.qmask] = (uint32_t)wk;
-            else atomicOr(sl.pend + (wk >> 5), bw);  // RED
+            if (in_g) SL_QUEUE[gpos & SL_QMASK] = (uint32_t)wk;
+            else atomicOr(SL_PEND + (wk >> 5), bw);  // RED
           }
           Q.gt += __popc(__ballot_sync(kFull, push && !in_s && in_g));
           Q.spilled |= __ballot_sync(kFull, push && !in_s && !in_g) != 0u;
@@ -793,7 +807,7 @@ __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const ui
 
 // the max-id relaxation of source s in increasing threshold order
 __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s,
-                                            int lane, SoloCounters &c, SoloWarpSmem &sw) {
+                                            int lane, SoloWarpSmem &sw) {
   const int tbw = (s + 31) >> 5;  // thresholds are < s
   // seed: the out-neighbours of s are in the structure; the
   // smaller ones are reached with maxId -1 and are thresholds
@@ -802,20 +816,20 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
     const int w = __ldg(p.colidx + j);
     if (w == s) continue;
     const uint32_t bw = vbit(w);
-    if (atomicOr(sl.is + (w >> 5), bw) == 0u) red_sum(sl.isum, w);
+    if (atomicOr(SL_IS + (w >> 5), bw) == 0u) red_sum(SL_ISUM, w);
     if (w < s) {
-      if (atomicOr(sl.reached + (w >> 5), bw) == 0u) red_sum(sl.rsum, w);
-      atomicOr(sl.thr + (w >> 5), bw);  // RED
-      red_sum(sl.tsum, w);
+      if (atomicOr(SL_REACHED + (w >> 5), bw) == 0u) red_sum(SL_RSUM, w);
+      atomicOr(SL_THR + (w >> 5), bw);  // RED
+      red_sum(SL_TSUM, w);
     }
   }
   __syncwarp();
   int wb = -1;  // no window yet
   int T = -1;
   for (;;) {
-    T = solo_next_threshold(sl.thr, sl.tsum, tbw, T, wb, sw, lane);
+    T = solo_next_threshold(SL_THR, SL_TSUM, tbw, T, wb, sw, lane);
     if (T == INT_MAX) break;
-    c.steps += 1;
+    if (lane == 0) sw.steps += 1;
     SoloQueue Q = {0, 0, 0, 0, false};
     int u = -1, ub = 0, ue = 0;
     if (lane == 0) {
@@ -824,8 +838,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       ue = __ldg(p.rowptr + T + 1);
     }
     for (;;) {
-      c.levels += 1;
-      solo_expand(p, sl, sw, wb, Q, s, T, u, ub, ue, lane, c);
+      solo_expand(p, sl, sw, wb, Q, s, T, u, ub, ue, lane);
       __syncwarp();
       if (Q.sh < Q.st) {
         const int cnt = min(32, Q.st - Q.sh);
@@ -848,18 +861,18 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
         fence_gpu();
         for (int w0 = 0; w0 < ((T + 31) >> 5) && !Q.spilled; w0 += 32) {
           const int wi = w0 + lane;
-          uint32_t x = wi < ((T + 31) >> 5) ? __ldcg(sl.pend + wi) : 0u;
+          uint32_t x = wi < ((T + 31) >> 5) ? __ldcg(SL_PEND + wi) : 0u;
           for (;;) {
             const bool has = x != 0u;
             const uint32_t hb = __ballot_sync(kFull, has);
             if (!hb) break;
             const int pos = Q.gt + __popc(hb & lanemask_lt());
-            const bool fits = pos - Q.gh <= sl.qmask;
+            const bool fits = pos - Q.gh <= SL_QMASK;
             if (has && fits) {
               const int b = __ffs(x) - 1;
               x &= x - 1u;
-              atomicAnd(sl.pend + wi, ~(1u << b));  // RED
-              sl.queue[pos & sl.qmask] = (uint32_t)((wi << 5) + b);
+              atomicAnd(SL_PEND + wi, ~(1u << b));  // RED (result unused)
+              SL_QUEUE[pos & SL_QMASK] = (uint32_t)((wi << 5) + b);
             }
             Q.gt += __popc(__ballot_sync(kFull, has && fits));
             if (__ballot_sync(kFull, has && !fits)) {
@@ -872,7 +885,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       }
       if (Q.gh >= Q.gt) break;
       const int cnt = min(32, Q.gt - Q.gh);
-      u = lane < cnt ? (int)sl.queue[(Q.gh + lane) & sl.qmask] : -1;
+      u = lane < cnt ? (int)SL_QUEUE[(Q.gh + lane) & SL_QMASK] : -1;
       Q.gh += cnt;
       if (u >= 0) {
         ub = __ldg(p.rowptr + u);
@@ -892,12 +905,12 @@ __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const Solo
   uint32_t cl = 0, cu = 0;
   for (int i0 = 0; i0 < ns; i0 += 32) {
     const int i = i0 + lane;
-    uint32_t x = i < ns ? __ldcg(sl.isum + i) : 0u;
+    uint32_t x = i < ns ? __ldcg(SL_ISUM + i) : 0u;
     while (x) {
       const int b = __ffs(x) - 1;
       x &= x - 1u;
       const int wi = (i << 5) + b, v0 = wi << 5;
-      const uint32_t y = __ldcg(sl.is + wi);
+      const uint32_t y = __ldcg(SL_IS + wi);
       const int d = s - v0;  // bits below d are < s, above d are > s
       const uint32_t lm = d <= 0 ? 0u : (d >= 32 ? kFull : ((1u << d) - 1u));
       const uint32_t um = d < 0 ? kFull : (d >= 31 ? 0u : (kFull << (d + 1)));
@@ -932,15 +945,15 @@ __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const Solo
   long long pl = (long long)base, pu = (long long)base + cl + 1;
   for (int i0 = 0; i0 < ns; i0 += 32) {
     const int i = i0 + lane;
-    const uint32_t x0 = i < ns ? __ldcg(sl.isum + i) : 0u;
+    const uint32_t x0 = i < ns ? __ldcg(SL_ISUM + i) : 0u;
     if (!__ballot_sync(kFull, x0 != 0u)) continue;
-    if (x0) sl.isum[i] = 0u;
+    if (x0) SL_ISUM[i] = 0u;
     uint32_t nl = 0, nu = 0;
     for (uint32_t x = x0; x;) {
       const int b = __ffs(x) - 1;
       x &= x - 1u;
       const int wi = (i << 5) + b, v0 = wi << 5;
-      const uint32_t y = __ldcg(sl.is + wi);
+      const uint32_t y = __ldcg(SL_IS + wi);
       const int d = s - v0;
       const uint32_t lm = d <= 0 ? 0u : (d >= 32 ? kFull : ((1u << d) - 1u));
       const uint32_t um = d < 0 ? kFull : (d >= 31 ? 0u : (kFull << (d + 1)));
@@ -961,8 +974,8 @@ __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const Solo
       const int b = __ffs(x) - 1;
       x &= x - 1u;
       const int wi = (i << 5) + b, v0 = wi << 5;
-      uint32_t y = __ldcg(sl.is + wi);
-      sl.is[wi] = 0u;
+      uint32_t y = __ldcg(SL_IS + wi);
+      SL_IS[wi] = 0u;
       if (!ok) continue;
       while (y) {
         const int v = v0 + __ffs(y) - 1;
@@ -978,7 +991,9 @@ __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const Solo
 }
 
 #ifndef GSOFA_SOLO_MINB
-#define GSOFA_SOLO_MINB (32 / kSoloWarps)  // 64 registers: measured faster than 32 with spills
+// 48 warps per SM (40 registers, one 32-pair batch in flight): measured best
+// against 32 warps / 64 registers and 64 warps / 32 registers
+#define GSOFA_SOLO_MINB (48 / kSoloWarps)
 #endif
 __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(StreamParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -988,8 +1003,8 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
   const int Vw = (p.Vmax + 31) >> 5, Vs = (Vw + 31) >> 5;
   __shared__ SoloWarpSmem s_sw[kSoloWarps];
   SoloWarpSmem &sw = s_sw[warp];
-  SoloCounters c = {0u, 0u, 0u, 0u, 0u};
-  uint32_t sink = 0u;
+  if (lane == 0) sw.items = sw.pairs = sw.levels = sw.steps = 0u;
+  __syncwarp();
   // first task: warp-major over the grid, so consecutive (heaviest) sources
   // start on different SMs; then the global task counter
   long long t = (long long)warp * gridDim.x + blockIdx.x;
@@ -1030,50 +1045,41 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
     if (g < 0) break;
     const int s = p.row_begin + 32 * g + k;
     if (s >= p.row_end) continue;  // tail of the last group
-    solo_source(p, sl, s, lane, c, sw);
+    solo_source(p, sl, s, lane, sw);
     fence_gpu();  // this warp's REDs are visible to its extraction
     __syncwarp();
     solo_stage_row(p, sl, s, g, lane);
     // reset the touched words: reached | pend | thr, and the summaries
     for (int i0 = 0; i0 < Vs; i0 += 32) {
       const int i = i0 + lane;
-      uint32_t x = i < Vs ? __ldcg(sl.rsum + i) : 0u;
+      uint32_t x = i < Vs ? __ldcg(SL_RSUM + i) : 0u;
       if (x) {
-        sl.rsum[i] = 0u;
-        sl.tsum[i] = 0u;
+        SL_RSUM[i] = 0u;
+        SL_TSUM[i] = 0u;
       }
       while (x) {
         const int b = __ffs(x) - 1;
         x &= x - 1u;
         const int wi = (i << 5) + b;
-        sl.reached[wi] = 0u;
-        sl.pend[wi] = 0u;
-        sl.thr[wi] = 0u;
+        SL_REACHED[wi] = 0u;
+        SL_PEND[wi] = 0u;
+        SL_THR[wi] = 0u;
       }
     }
     // the clears are plain stores; the next source's atomics act at L2
     __threadfence();
     __syncwarp();
-    {
-      uint32_t it = c.items, pr = c.pairs;
-#pragma unroll
-      for (int d = 16; d >= 1; d >>= 1) {
-        it += __shfl_xor_sync(kFull, it, d);
-        pr += __shfl_xor_sync(kFull, pr, d);
-      }
-      if (lane == 0) {
-        atomicAdd(p.stats + 0, (unsigned long long)it);
-        atomicAdd(p.stats + 1, (unsigned long long)pr);  // solo: one source per item
-        atomicAdd(p.stats + 4, (unsigned long long)pr);
-        atomicAdd(p.stats + 2, (unsigned long long)c.levels);
-        atomicAdd(p.stats + 3, (unsigned long long)c.steps);
-        atomicAdd(p.done, 1u);
-      }
-      sink ^= c.sink;
-      c = {0u, 0u, 0u, 0u, 0u};
+    if (lane == 0) {
+      atomicAdd(p.stats + 0, (unsigned long long)sw.items);
+      atomicAdd(p.stats + 1, (unsigned long long)sw.pairs);  // solo: one source per item
+      atomicAdd(p.stats + 4, (unsigned long long)sw.pairs);
+      atomicAdd(p.stats + 2, (unsigned long long)sw.levels);
+      atomicAdd(p.stats + 3, (unsigned long long)sw.steps);
+      atomicAdd(p.done, 1u);
+      sw.items = sw.pairs = sw.levels = sw.steps = 0u;
     }
+    __syncwarp();
   }
-  if (p.n < 0) p.stats[7] = sink;
 }
 
 // copies each staged row into the final CSR arrays (warp per row)
