@@ -712,7 +712,12 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds
       // iff the source has not reached w yet (line 10 of fig:alg)
       ro[k] = w[k] < s ? atomicOr(SL_REACHED + (w[k] >> 5), bw) : bw;
-      io[k] = w[k] > s ? atomicOr(SL_IS + (w[k] >> 5), bw) : 1u;
+      io[k] = 1u;
+      if (w[k] > s) {
+        // U entry: nothing waits for it -- two REDs (the summary bit is idempotent)
+        atomicOr(SL_IS + (w[k] >> 5), bw);
+        red_sum(SL_ISUM, w[k]);
+      }
       // w < T may join the closure: its row pointers travel with the atomic
       rb[k] = re[k] = 0;
       if (w[k] < T) {
