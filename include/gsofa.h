@@ -91,6 +91,13 @@ typedef struct gsofa_opts {
   int32_t outputs_on_device;
   /* cudaStream_t to run on (NULL = the context's own stream). */
   void *stream;
+  /* 1 = checked mode: after the factorization a GPU
+   * audit verifies every output row (L strictly lower and ascending, U
+   * starting with the diagonal and ascending), pattern(A) within L+U, and
+   * Definition def:T3 for every supernode row; a violation returns
+   * GSOFA_EINTERNAL with the failed checks in gsofa_last_error_detail().
+   * Costs one extra pass over the output; default 0. */
+  int32_t checked;
 } gsofa_opts;
 
 /* ------------------------------------------------------------ statistics -- */

@@ -38,7 +38,7 @@ class Opts(ctypes.Structure):
     _fields_ = [("chunk_size", _I32), ("max_concurrent", _I32), ("mem_budget_bytes", _I64),
                 ("fill_first", _I32), ("schedule", _I32), ("row_begin", _I64),
                 ("row_end", _I64), ("device", _I32), ("outputs_on_device", _I32),
-                ("stream", ctypes.c_void_p)]
+                ("stream", ctypes.c_void_p), ("checked", _I32)]
 
 
 class Stats(ctypes.Structure):
@@ -268,7 +268,8 @@ class Result:
 def symbolic(rowptr, colidx, *, ctx: Context | None = None, chunk_size: int = 128,
              max_concurrent: int = 0, mem_budget_bytes: int = 0, fill_first: bool = False,
              row_begin: int = 0, row_end: int = -1, device: int = 0,
-             outputs_on_device: bool = False, stream=None, schedule: str = "threshold") -> Result:
+             outputs_on_device: bool = False, stream=None, schedule: str = "threshold",
+             checked: bool = False) -> Result:
     """gsofa_symbolic: L/U patterns, supernodes and fill count of the pattern
     (rowptr int64[n+1], colidx int32[nnz]) for rows [row_begin, row_end).
     Inputs: numpy (host) or torch tensors (host or CUDA).  ``stream``: a
@@ -287,6 +288,7 @@ def symbolic(rowptr, colidx, *, ctx: Context | None = None, chunk_size: int = 12
     o.row_begin, o.row_end, o.device = int(row_begin), int(row_end), int(device)
     o.outputs_on_device = int(bool(outputs_on_device))
     o.schedule = SCHEDULES[schedule]
+    o.checked = int(bool(checked))
     if stream is not None:
         o.stream = ctypes.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
     if ci == 0:  # empty colidx: pass a valid dummy pointer

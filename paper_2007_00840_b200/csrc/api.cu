@@ -433,6 +433,7 @@ int gsofa_default_opts(gsofa_opts *o) {
   o->device = 0;
   o->outputs_on_device = 1;
   o->stream = nullptr;
+  o->checked = 0;
   return GSOFA_OK;
 }
 
@@ -1358,6 +1359,32 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     ++launches;
   }
   e_sn1 = ev();
+  if (o.checked) {
+    // ---------------------------------------------------- checked mode
+    CK(cudaMemsetAsync(c->err, 0, sizeof(int), st));
+    if (const char *inj = std::getenv("GSOFA_AUDIT_INJECT")) {
+      // tests only: corrupt one output entry to show the audit catches it
+      const int32_t v = (int32_t)n - 1;
+      if (inj[0] == 'L' && baseL > 0) CK(cudaMemcpyAsync(Lci, &v, 4, cudaMemcpyHostToDevice, st));
+      if (inj[0] == 'U' && baseU > 0) CK(cudaMemsetAsync(Uci, 0xFF, 4, st));
+      if (inj[0] == 'A' && baseL > 1) CK(cudaMemcpyAsync(Lci + 1, Lci, 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    CK(gsofa::launch_audit(c->rowptr32, d_colidx, Lrp, Lci, Urp, Uci, sn, (int32_t *)c->totals + 4,
+                           (int32_t)rb, (int32_t)rows, (int32_t)n, o.chunk_size, c->err, st));
+    ++launches;
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, c->err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (bad) {
+      set_detail("checked mode: output invariants violated (bits %d:%s%s%s%s%s)", bad,
+                 (bad & 1) ? " L-row order" : "", (bad & 2) ? " U-row order" : "",
+                 (bad & 4) ? " A not within L+U" : "", (bad & 8) ? " supernode Def. T3" : "",
+                 (bad & 16) ? " supernode maximality" : "");
+      rc = GSOFA_EINTERNAL;
+      goto fail;
+    }
+  }
   // ---------------------------------------------------- result
   res = (gsofa_result *)std::calloc(1, sizeof(ResultImpl));
   if (!res) {

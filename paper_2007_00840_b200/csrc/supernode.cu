@@ -143,6 +143,67 @@ __global__ void sn_stitch_kernel(const int64_t *U_rowptr, const int64_t *L_rowpt
   out[1] = oc;
 }
 
+// Checked mode (gsofa_opts.checked): audit of the finished
+// structure, one warp per row s = row_begin + r.  Bits of *err:
+//   1  an L row is not strictly increasing or not strictly below s
+//   2  a U row does not start with s or is not strictly increasing above s
+//   4  an entry of A is missing from L+U (pattern(A) must be a subset)
+//   8  an interior supernode row violates Def. def:T3 against its leader
+//  16  a leader (not a chunk start, not row_begin) could have joined the
+//      previous block (the greedy scan would not have split there)
+__global__ void audit_kernel(const int32_t *A_rowptr, const int32_t *A_colidx, const int64_t *L_rowptr,
+                             const int32_t *L_colidx, const int64_t *U_rowptr, const int32_t *U_colidx,
+                             const int32_t *sn_start, const int32_t *nsuper_p, int32_t row_begin,
+                             int32_t rows, int32_t n, int32_t chunk, int *err) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int32_t s = row_begin + r;
+  const int64_t la = L_rowptr[r], lb = L_rowptr[r + 1], ua = U_rowptr[r], ub = U_rowptr[r + 1];
+  int bad = 0;
+  for (int64_t e = la + lane; e < lb; e += 32) {
+    const int32_t c = L_colidx[e];
+    if (c < 0 || c >= s || (e > la && L_colidx[e - 1] >= c)) bad |= 1;
+  }
+  if (ub <= ua || U_colidx[ua] != s) bad |= 2;
+  for (int64_t e = ua + 1 + lane; e < ub; e += 32) {
+    const int32_t c = U_colidx[e];
+    if (c <= s || c >= n || U_colidx[e - 1] >= c) bad |= 2;
+  }
+  for (int32_t e = A_rowptr[s] + lane; e < A_rowptr[s + 1]; e += 32) {
+    const int32_t c = A_colidx[e];
+    if (c == s) continue;
+    const bool found = c < s ? row_contains(L_colidx, la, lb, c) : row_contains(U_colidx, ua + 1, ub, c);
+    if (!found) bad |= 4;
+  }
+  if (lane == 0) {
+    // leader of s: the last sn_start entry <= s
+    const int32_t ns = *nsuper_p;
+    int32_t lo = 0, hi = ns;
+    while (hi - lo > 1) {
+      const int32_t m = (lo + hi) >> 1;
+      if (sn_start[m] <= s) lo = m;
+      else hi = m;
+    }
+    const int32_t lead = sn_start[lo];
+    if (s != lead) {
+      const int64_t nu = ub - ua, np = ua - U_rowptr[r - 1];
+      if (s % chunk == 0 || nu != np - 1 || !row_contains(L_colidx, la, lb, lead)) bad |= 8;
+    } else if (s != row_begin && s % chunk != 0) {
+      int32_t lo2 = 0, hi2 = ns;  // leader of s - 1
+      while (hi2 - lo2 > 1) {
+        const int32_t m = (lo2 + hi2) >> 1;
+        if (sn_start[m] <= s - 1) lo2 = m;
+        else hi2 = m;
+      }
+      const int64_t nu = ub - ua, np = ua - U_rowptr[r - 1];
+      if (nu == np - 1 && row_contains(L_colidx, la, lb, sn_start[lo2])) bad |= 16;
+    }
+  }
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (lane == 0 && bad) atomicOr(err, bad);
+}
+
 __global__ void sn_scatter_kernel(const int32_t *flags, const int32_t *pos, int32_t row_begin,
                                   int32_t row_end, const int32_t *total, int32_t *sn_start) {
   const int32_t s = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
@@ -286,6 +347,17 @@ cudaError_t launch_supernode_stitch(const int64_t *U_rowptr, const int64_t *L_ro
                                     int64_t nsuper, int32_t *out, cudaStream_t st) {
   sn_stitch_kernel<<<1, 32, 0, st>>>(U_rowptr, L_rowptr, L_colidx, rb, he, prev_nnzU, prev_leader,
                                      sn_start, nsuper, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_audit(const int32_t *A_rowptr, const int32_t *A_colidx, const int64_t *L_rowptr,
+                         const int32_t *L_colidx, const int64_t *U_rowptr, const int32_t *U_colidx,
+                         const int32_t *sn_start, const int32_t *nsuper, int32_t row_begin, int32_t rows,
+                         int32_t n, int32_t chunk, int *err, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  audit_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(A_rowptr, A_colidx, L_rowptr, L_colidx,
+                                                           U_rowptr, U_colidx, sn_start, nsuper,
+                                                           row_begin, rows, n, chunk, err);
   return cudaGetLastError();
 }
 

@@ -364,3 +364,29 @@ def test_permute(ctx, name, scale):
     with pytest.raises(g.GsofaError) as e:
         g.permute(rp, ci, bad)
     assert e.value.code == -1
+
+
+@pytest.mark.parametrize("schedule", ["threshold", "fifo"])
+def test_checked_mode(ctx, schedule):
+    """checked=True audits every output row, pattern(A) within L+U and Def.
+    def:T3; correct outputs pass and are unchanged."""
+    for name, scale in [("C5", 14), ("C4", 60), ("C3", 2000), ("C1", None)]:
+        rp, ci = gen.config(name, scale)
+        assert_full_equal(run(rp, ci, ctx, checked=True, schedule=schedule), oracle.symbolic(rp, ci))
+
+
+@pytest.mark.parametrize("inject,check", [("L", "L-row order"), ("U", "U-row order"),
+                                          ("A", "L-row order")])
+def test_checked_mode_catches_corruption(ctx, inject, check, monkeypatch):
+    """Fault injection (tests only): a corrupted output entry makes the
+    checked call fail with GSOFA_EINTERNAL and names the broken check."""
+    monkeypatch.setenv("GSOFA_AUDIT_INJECT", inject)
+    rp, ci = gen.config("C5", 12)
+    with pytest.raises(g.GsofaError) as e:
+        g.symbolic(rp, ci, ctx=ctx, checked=True)
+    assert e.value.code == -6
+    assert check in str(e.value)
+    monkeypatch.delenv("GSOFA_AUDIT_INJECT")
+    r = g.symbolic(rp, ci, ctx=ctx, checked=True)   # the context is still usable
+    assert r.fill_count == oracle.symbolic(rp, ci)["fill_count"]
+    r.free()
