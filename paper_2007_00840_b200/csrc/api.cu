@@ -1367,7 +1367,6 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       const int32_t v = (int32_t)n - 1;
       if (inj[0] == 'L' && baseL > 0) CK(cudaMemcpyAsync(Lci, &v, 4, cudaMemcpyHostToDevice, st));
       if (inj[0] == 'U' && baseU > 0) CK(cudaMemsetAsync(Uci, 0xFF, 4, st));
-      if (inj[0] == 'A' && baseL > 1) CK(cudaMemcpyAsync(Lci + 1, Lci, 4, cudaMemcpyDeviceToDevice, st));
       CK(cudaStreamSynchronize(st));
     }
     CK(gsofa::launch_audit(c->rowptr32, d_colidx, Lrp, Lci, Urp, Uci, sn, (int32_t *)c->totals + 4,
