@@ -614,7 +614,7 @@ int gsofa_permute(int64_t n, const int64_t *rowptr, const int32_t *colidx, const
     set_detail("gsofa_permute: nnz=%lld out of range", (long long)nnz);
     return GSOFA_EBADCSR;
   }
-  int64_t *d_rp = nullptr, *d_nrp = nullptr, *tot = nullptr;
+  int64_t *d_rp = nullptr, *d_nrp = nullptr;
   int32_t *d_ci = nullptr, *d_perm = nullptr, *d_nci = nullptr, *d_iperm = nullptr, *d_deg = nullptr;
   int *d_bad = nullptr;
   void *tmp = nullptr;
@@ -640,7 +640,6 @@ int gsofa_permute(int64_t n, const int64_t *rowptr, const int32_t *colidx, const
         (e = cudaMemcpyAsync(d_perm, perm, (size_t)n * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
       goto cuda_err;
   }
-  tot = (int64_t *)((char *)d_bad + 8);
   if ((e = cudaMemsetAsync(d_bad, 0, 64, st)) != cudaSuccess) goto cuda_err;
   if ((e = gsofa::launch_iperm(d_perm, n, d_iperm, d_bad, st)) != cudaSuccess) goto cuda_err;
   if ((e = cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost)) != cudaSuccess) goto cuda_err;
@@ -664,7 +663,6 @@ int gsofa_permute(int64_t n, const int64_t *rowptr, const int32_t *colidx, const
 cuda_err:
   rc = cuda_fail(e, "gsofa_permute");
 done:
-  (void)tot;
   if (!dev) {
     for (void *p : {(void *)d_rp, (void *)d_ci, (void *)d_perm, (void *)d_nrp, (void *)d_nci})
       if (p) cudaFreeAsync(p, st);
