@@ -14,6 +14,7 @@ ap.add_argument("--scale", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--C", type=int, default=0)
 ap.add_argument("--fill-first", action="store_true")
+ap.add_argument("--schedule", default="threshold", choices=["threshold", "fifo"])
 ap.add_argument("--rows", type=str, default=None, help="row range b:e")
 a = ap.parse_args()
 t = time.time()
@@ -24,7 +25,7 @@ for i in range(a.reps):
     t = time.time()
     rb, re_ = (int(x) for x in a.rows.split(":")) if a.rows else (0, -1)
     r = g.symbolic(rp, ci, ctx=ctx, max_concurrent=a.C, fill_first=a.fill_first, outputs_on_device=True,
-                   row_begin=rb, row_end=re_)
+                   row_begin=rb, row_end=re_, schedule=a.schedule)
     dt = time.time() - t
     s = r.stats
     print(f"rep {i}: wall {dt*1e3:.1f} ms  dev {s['ms_total']:.1f} ms  trav {s['ms_traverse']:.1f} "
