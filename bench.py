@@ -182,7 +182,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2", choices=sorted(CONFIG_DESC))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--schedule", default="threshold", choices=["threshold", "fifo"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "threshold", "fifo"])
     ap.add_argument("--max-concurrent", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -261,6 +261,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize(dev)
     step_ms, stats_acc, launches = [], {}, 0
+    sched_used = args.schedule
     fills_step = 0
     with ClockSampler(dev_index) as clk:
         for _ in range(args.steps):
@@ -273,6 +274,7 @@ def main():
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
             if r is not None:
+                sched_used = r.schedule  # the library's choice under "auto"
                 for k, v in r.stats.items():
                     stats_acc[k] = stats_acc.get(k, 0) + v
                 launches += int(r.stats["kernel_launches"])
@@ -322,18 +324,18 @@ def main():
     # ---- roofline of the dominant kernel (traversal), measured live
     peak, peak_src = load_peaks()
     trav_ms = stats_acc.get("ms_traverse", 0.0)
-    alg = algorithmic_bytes(stats_acc, args.schedule) if stats_acc else 0
+    alg = algorithmic_bytes(stats_acc, sched_used) if stats_acc else 0
     achieved = alg / (trav_ms / 1e3) / 1e9 if trav_ms > 0 else 0.0
     traffic, traffic_src = None, None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        ent = tj.get(f"{args.config}/{args.schedule}")
+        ent = tj.get(f"{args.config}/{sched_used}")
         if ent:
             traffic = float(ent["dram_bytes"])  # per launch, from one ncu --set full capture
             traffic_src = f'{ent["kernel"]}: {ent["source"]}'
     except Exception:
         pass
-    roofline = {"kernel": ("solo_kernel+stream_kernel" if args.schedule == "threshold"
+    roofline = {"kernel": ("solo_kernel+stream_kernel" if sched_used == "threshold"
                            else "traverse_kernel"),
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
@@ -366,7 +368,7 @@ def main():
                "dtype": "int32", "data": "synthetic (gen.config, seeded; no datasets)",
                "config": {"workload": CONFIG_DESC[args.config], "n": n, "nnz_offdiag": int(ci.size),
                           "row_ranges": [int(b) for b in bounds],
-                          "fill_ins": fills_step, "schedule": args.schedule,
+                          "fill_ins": fills_step, "schedule": sched_used,
                           "parallelism": f"rows split over {world} GPU(s)" if world > 1 else "1 GPU",
                           "l2": "flushed between timed steps (256 MiB write, untimed)"},
                "e2e": {"value": fills_step / (e2e_step / 1e3), "unit": UNIT,

@@ -50,6 +50,7 @@ extern "C" {
 
 #define GSOFA_SCHEDULE_THRESHOLD 0
 #define GSOFA_SCHEDULE_FIFO      1
+#define GSOFA_SCHEDULE_AUTO      2
 
 /* -------------------------------------------------------------- options -- */
 typedef struct gsofa_opts {
@@ -70,13 +71,18 @@ typedef struct gsofa_opts {
   int32_t fill_first;
   /* Processing order of the max-id relaxation (result-invariant; DESIGN.md
    * "Schedules"):
-   *   GSOFA_SCHEDULE_THRESHOLD (0, default): frontier items in increasing
-   *     newMaxId, one CTA per 32-source group ("Dijkstra order"); no
-   *     revisits, no grid-wide barriers.
+   *   GSOFA_SCHEDULE_THRESHOLD (0): frontier items in increasing newMaxId
+   *     ("Dijkstra order"): no revisits, no grid-wide barriers;
+   *     lockstep 32-source groups plus per-source solo warps.
    *   GSOFA_SCHEDULE_FIFO (1): the paper's order -- all frontiers of an
    *     iteration in parallel with revisits, one
    *     persistent grid-wide kernel per batch with epoch-encoded maxId
-   *     labels. */
+   *     labels.
+   *   GSOFA_SCHEDULE_AUTO (2, default): FIFO when the pattern is banded and
+   *     dense (bandwidth <= n/8 and nnz >= 8n: few rounds, almost no
+   *     revisits -- measured 1.3-2.9x faster there), threshold otherwise
+   *     (ND orders, hubs: 15x the inspections in FIFO).  The bandwidth is
+   *     one GPU pass over A.  gsofa_result.schedule reports the choice. */
   int32_t schedule;
   /* source rows [row_begin, row_end); row_end = -1 means n.  Any row_begin:
    * if it is not a multiple of chunk_size, the supernodes of the head rows
@@ -140,6 +146,8 @@ typedef struct gsofa_result {
   int32_t on_device;      /* 1 if the arrays above are device pointers */
   int32_t device;
   gsofa_stats stats;
+  int32_t schedule;       /* the schedule that ran (THRESHOLD or FIFO) */
+  int32_t reserved;
 } gsofa_result;
 
 typedef struct gsofa_context gsofa_context;

@@ -57,7 +57,7 @@ class CResult(ctypes.Structure):
                 ("nsuper", _I64), ("sn_start", _P(_I32)),
                 ("nnz_L", _I64), ("nnz_U", _I64), ("nnz_A_offdiag", _I64),
                 ("fill_count", _I64), ("on_device", _I32), ("device", _I32),
-                ("stats", Stats)]
+                ("stats", Stats), ("schedule", _I32), ("reserved", _I32)]
 
 
 class Tail(ctypes.Structure):
@@ -75,7 +75,8 @@ class GsofaError(RuntimeError):
 
 
 _lib = None
-SCHEDULES = {"threshold": 0, "fifo": 1}
+SCHEDULES = {"threshold": 0, "fifo": 1, "auto": 2}
+SCHEDULE_NAMES = {0: "threshold", 1: "fifo"}
 
 
 def load():
@@ -178,6 +179,7 @@ class Result:
         self.nnz_L, self.nnz_U, self.nsuper = r.nnz_L, r.nnz_U, r.nsuper
         self.nnz_A_offdiag, self.fill_count = r.nnz_A_offdiag, r.fill_count
         self.on_device = bool(r.on_device)
+        self.schedule = SCHEDULE_NAMES.get(r.schedule, str(r.schedule))
         s = r.stats
         self.stats = {f: getattr(s, f) for f, _ in Stats._fields_}
         self._arrays = None
@@ -268,13 +270,14 @@ class Result:
 def symbolic(rowptr, colidx, *, ctx: Context | None = None, chunk_size: int = 128,
              max_concurrent: int = 0, mem_budget_bytes: int = 0, fill_first: bool = False,
              row_begin: int = 0, row_end: int = -1, device: int = 0,
-             outputs_on_device: bool = False, stream=None, schedule: str = "threshold",
+             outputs_on_device: bool = False, stream=None, schedule: str = "auto",
              checked: bool = False) -> Result:
     """gsofa_symbolic: L/U patterns, supernodes and fill count of the pattern
     (rowptr int64[n+1], colidx int32[nnz]) for rows [row_begin, row_end).
     Inputs: numpy (host) or torch tensors (host or CUDA).  ``stream``: a
     torch.cuda.Stream or raw cudaStream_t integer.  ``schedule``:
-    "threshold" (default) or "fifo" (the paper's all-frontiers order)."""
+    "auto" (default: FIFO for banded dense patterns, else threshold),
+    "threshold" or "fifo" (the paper's all-frontiers order)."""
     lib = load()
     rp, _, krp = _ptr(rowptr)
     ci, _, kci = _ptr(colidx)

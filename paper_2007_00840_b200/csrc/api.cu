@@ -115,6 +115,7 @@ struct gsofa_context {
   uint64_t layout_sig = 0;   // streaming slot layout of the last call (Vmax, ws_words)
   int stream_blocks = 0;     // resident CTAs of the streaming kernel
   int sms = 0, clock_khz = 0;  // device attributes, queried once (clock rate can be slow to query)
+  unsigned int *bw_dev = nullptr;  // bandwidth scratch (GSOFA_SCHEDULE_AUTO)
   // last plan and its key: repeated calls on the same problem skip the
   // free-memory query and the occupancy queries, and keep the arena layout
   Plan plan_cache;
@@ -428,6 +429,7 @@ int gsofa_default_opts(gsofa_opts *o) {
   o->max_concurrent = 0;
   o->mem_budget_bytes = 0;
   o->fill_first = 0;
+  o->schedule = GSOFA_SCHEDULE_AUTO;
   o->row_begin = 0;
   o->row_end = -1;
   o->device = 0;
@@ -504,6 +506,7 @@ void gsofa_context_destroy(gsofa_context *c) {
   if (c->in_rowptr) cudaFree(c->in_rowptr);
   if (c->in_colidx) cudaFree(c->in_colidx);
   if (c->rowptr32) cudaFree(c->rowptr32);
+  if (c->bw_dev) cudaFree(c->bw_dev);
   if (c->stage) cudaFree(c->stage);
   if (c->h_small) cudaFreeHost(c->h_small);
   host_block_release(c->hpool);
@@ -817,7 +820,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   if (o.row_end < 0) o.row_end = n;
   if (o.chunk_size < 1 || o.row_begin < 0 || o.row_end > n || o.row_begin >= o.row_end ||
       o.max_concurrent < 0 || o.max_concurrent % 32 != 0 ||
-      o.mem_budget_bytes < 0 || o.schedule < 0 || o.schedule > 1) {
+      o.mem_budget_bytes < 0 || o.schedule < 0 || o.schedule > 2) {
     set_detail("bad opts: chunk=%d rows=[%lld,%lld) C=%d budget=%lld", o.chunk_size,
                (long long)o.row_begin, (long long)o.row_end, o.max_concurrent,
                (long long)o.mem_budget_bytes);
@@ -898,6 +901,16 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     d_colidx = c->in_colidx;
   }
   e_up = ev();
+  if (o.schedule == GSOFA_SCHEDULE_AUTO) {
+    // banded and dense -> the paper's FIFO order (few rounds, no revisits);
+    // otherwise threshold order (DESIGN.md §8 "Schedule")
+    unsigned int bw = 0;
+    if (!c->bw_dev) CK(cudaMalloc((void **)&c->bw_dev, 64));
+    CK(gsofa::launch_bandwidth(d_rowptr64, d_colidx, n, c->bw_dev, st));
+    CK(cudaMemcpyAsync(&bw, c->bw_dev, sizeof bw, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    o.schedule = ((int64_t)bw * 8 <= n && nnz >= 8 * n) ? GSOFA_SCHEDULE_FIFO : GSOFA_SCHEDULE_THRESHOLD;
+  }
   if ((rc = grow_device(&c->rowptr32, &c->rowptr32_cap, (size_t)n + 1, st)) != GSOFA_OK) goto fail;
   // ---------------------------------------------------- plan + arena
   {
@@ -1402,6 +1415,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     res->nnz_A_offdiag = (int64_t)hs[5];
     res->fill_count = baseL + (baseU - rows) - res->nnz_A_offdiag;
     res->device = c->device;
+    res->schedule = o.schedule;
     reinterpret_cast<ResultImpl *>(res)->chunk_size = o.chunk_size;
     res->stats.frontier_items = (int64_t)hs[0];
     res->stats.edge_inspections = (int64_t)hs[1];

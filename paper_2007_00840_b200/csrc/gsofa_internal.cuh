@@ -158,6 +158,8 @@ cudaError_t launch_supernode_stitch(const int64_t *U_rowptr, const int64_t *L_ro
                                     const int32_t *L_colidx, int32_t rb, int32_t he,
                                     int64_t prev_nnzU, int32_t prev_leader, const int32_t *sn_start,
                                     int64_t nsuper, int32_t *out, cudaStream_t st);
+cudaError_t launch_bandwidth(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
+                             unsigned int *out, cudaStream_t st);
 cudaError_t launch_audit(const int32_t *A_rowptr, const int32_t *A_colidx, const int64_t *L_rowptr,
                          const int32_t *L_colidx, const int64_t *U_rowptr, const int32_t *U_colidx,
                          const int32_t *sn_start, const int32_t *nsuper, int32_t row_begin, int32_t rows,

@@ -11,6 +11,8 @@
 //   it ("continue this process until no supernode grows").  Runs
 //   between Phase-I leaders are independent, which is the parallelism the
 //   paper's first phase exposes.
+#include <climits>
+
 #include "gsofa_internal.cuh"
 
 namespace gsofa {
@@ -204,6 +206,24 @@ __global__ void audit_kernel(const int32_t *A_rowptr, const int32_t *A_colidx, c
   if (lane == 0 && bad) atomicOr(err, bad);
 }
 
+// bandwidth of A: max |i - j| over its entries (GSOFA_SCHEDULE_AUTO)
+__global__ void bandwidth_kernel(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
+                                 unsigned int *out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t a = rowptr64[i], b = rowptr64[i + 1];
+  unsigned int m = 0;
+  if (b > a) {  // columns ascend: the extremes are the first and last entries
+    const int64_t d0 = i - (int64_t)colidx[a], d1 = (int64_t)colidx[b - 1] - i;
+    int64_t d = d0 > d1 ? d0 : d1;
+    if (d < 0) d = 0;
+    if (d > INT32_MAX) d = INT32_MAX;
+    m = (unsigned int)d;
+  }
+  m = __reduce_max_sync(0xFFFFFFFFu, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 __global__ void sn_scatter_kernel(const int32_t *flags, const int32_t *pos, int32_t row_begin,
                                   int32_t row_end, const int32_t *total, int32_t *sn_start) {
   const int32_t s = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
@@ -358,6 +378,14 @@ cudaError_t launch_audit(const int32_t *A_rowptr, const int32_t *A_colidx, const
   audit_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(A_rowptr, A_colidx, L_rowptr, L_colidx,
                                                            U_rowptr, U_colidx, sn_start, nsuper,
                                                            row_begin, rows, n, chunk, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bandwidth(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
+                             unsigned int *out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned int), st);
+  if (e != cudaSuccess) return e;
+  bandwidth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rowptr64, colidx, n, out);
   return cudaGetLastError();
 }
 

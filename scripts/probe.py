@@ -14,7 +14,7 @@ ap.add_argument("--scale", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--C", type=int, default=0)
 ap.add_argument("--fill-first", action="store_true")
-ap.add_argument("--schedule", default="threshold", choices=["threshold", "fifo"])
+ap.add_argument("--schedule", default="auto", choices=["auto", "threshold", "fifo"])
 ap.add_argument("--rows", type=str, default=None, help="row range b:e")
 a = ap.parse_args()
 t = time.time()
@@ -28,7 +28,7 @@ for i in range(a.reps):
                    row_begin=rb, row_end=re_, schedule=a.schedule)
     dt = time.time() - t
     s = r.stats
-    print(f"rep {i}: wall {dt*1e3:.1f} ms  dev {s['ms_total']:.1f} ms  trav {s['ms_traverse']:.1f} "
+    print(f"rep {i} [{r.schedule}]: wall {dt*1e3:.1f} ms  dev {s['ms_total']:.1f} ms  trav {s['ms_traverse']:.1f} "
           f"ext {s['ms_extract']:.1f} sn {s['ms_supernode']:.2f} | fill {r.fill_count} nnzL {r.nnz_L} "
           f"nnzU {r.nnz_U} nsuper {r.nsuper} | edges {s['edge_inspections']:.3e} items {s['frontier_items']:.3e} "
           f"rounds {s['rounds']} batches {s['batches']} C {s['max_batch']} launches {s['kernel_launches']}",

@@ -389,3 +389,20 @@ def test_checked_mode_catches_corruption(ctx, inject, check, monkeypatch):
     r = g.symbolic(rp, ci, ctx=ctx, checked=True)   # the context is still usable
     assert r.fill_count == oracle.symbolic(rp, ci)["fill_count"]
     r.free()
+
+
+@pytest.mark.parametrize("name,scale,want", [("C3", 3000, "threshold"), ("C3", 10000, "fifo"),
+                                             ("C3", 20000, "fifo"),
+                                             ("C2", 20, "threshold"), ("C4", 60, "threshold"),
+                                             ("C1", None, "threshold")])
+def test_auto_schedule(ctx, name, scale, want):
+    """schedule="auto" (the default) picks FIFO for banded dense patterns and
+    threshold order otherwise; the result is the oracle's either way."""
+    rp, ci = gen.config(name, scale)
+    r = g.symbolic(rp, ci, ctx=ctx)
+    assert r.schedule == want
+    got = dict(r.to_numpy())
+    got.update(nnz_L=r.nnz_L, nnz_U=r.nnz_U, nsuper=r.nsuper, fill_count=r.fill_count,
+               nnz_A_offdiag=r.nnz_A_offdiag)
+    r.free()
+    assert_full_equal(got, oracle.symbolic(rp, ci))
