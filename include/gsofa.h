@@ -60,8 +60,7 @@ typedef struct gsofa_opts {
   int32_t chunk_size;
   /* #C, the number of concurrent sources per batch.  Multiple of
    * 32 (one 32-source slot group per warp lane set).  0 = automatic (the
-   * largest batch the memory budget allows, capped at 65536 for the threshold
-   * schedule and 16384 for FIFO). */
+   * largest batch the memory budget allows, capped at 65536). */
   int32_t max_concurrent;
   /* memory budget in bytes for the traversal arena.  0 = automatic
    * (about half of the free device memory). */
