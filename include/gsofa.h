@@ -79,7 +79,8 @@ typedef struct gsofa_opts {
    *     labels.
    *   GSOFA_SCHEDULE_AUTO (2, default): FIFO when the pattern is banded and
    *     dense (bandwidth <= n/8 and nnz >= 8n: few rounds, almost no
-   *     revisits -- measured 1.3-2.9x faster there), threshold otherwise
+   *     revisits -- measured 1.3-2.9x faster there) and one batch of labels
+   *     (min(rows, 65536) x n x 4 B) fits half the free memory; threshold otherwise
    *     (ND orders, hubs: 15x the inspections in FIFO).  The bandwidth is
    *     one GPU pass over A.  gsofa_result.schedule reports the choice. */
   int32_t schedule;

@@ -909,7 +909,16 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     CK(gsofa::launch_bandwidth(d_rowptr64, d_colidx, n, c->bw_dev, st));
     CK(cudaMemcpyAsync(&bw, c->bw_dev, sizeof bw, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    o.schedule = ((int64_t)bw * 8 <= n && nnz >= 8 * n) ? GSOFA_SCHEDULE_FIFO : GSOFA_SCHEDULE_THRESHOLD;
+    bool fifo = (int64_t)bw * 8 <= n && nnz >= 8 * n;
+    if (fifo) {
+      // and only if one batch of maxId labels (sources x vertices x 4 B)
+      // fits half of the free memory: FIFO in many small batches loses its edge
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      const double labels = (double)std::min<int64_t>(rows, 65536) * (double)n * 4.0;
+      fifo = labels <= 0.5 * (double)fr;
+    }
+    o.schedule = fifo ? GSOFA_SCHEDULE_FIFO : GSOFA_SCHEDULE_THRESHOLD;
   }
   if ((rc = grow_device(&c->rowptr32, &c->rowptr32_cap, (size_t)n + 1, st)) != GSOFA_OK) goto fail;
   // ---------------------------------------------------- plan + arena
