@@ -406,3 +406,16 @@ def test_auto_schedule(ctx, name, scale, want):
                nnz_A_offdiag=r.nnz_A_offdiag)
     r.free()
     assert_full_equal(got, oracle.symbolic(rp, ci))
+
+
+@pytest.mark.parametrize("name,scale,chunk", [("C3", 10000, 128), ("C5", 12, 64)])
+def test_supernode_stitch_fifo(ctx, name, scale, chunk):
+    """The paper's FIFO order over row-granular ranges (what AUTO runs for
+    banded patterns on several GPUs), stitched, equals the oracle."""
+    rp, ci = gen.config(name, scale)
+    n = rp.size - 1
+    full = oracle.symbolic(rp, ci, chunk_size=chunk)
+    cuts = sorted({n // 7, n // 3 + 1, n // 2 + 5, (2 * n) // 3 + 3, n - 40})
+    asm, _ = _stitched_ranges(rp, ci, ctx, [0] + cuts + [n], chunk, schedule="fifo")
+    for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start"):
+        assert np.array_equal(asm[k], full[k]), k
