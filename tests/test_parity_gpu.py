@@ -419,3 +419,24 @@ def test_supernode_stitch_fifo(ctx, name, scale, chunk):
     asm, _ = _stitched_ranges(rp, ci, ctx, [0] + cuts + [n], chunk, schedule="fifo")
     for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start"):
         assert np.array_equal(asm[k], full[k]), k
+
+
+def test_randomized_sweep(ctx):
+    """200 random patterns (size, density, a random ordering), each with a
+    random row range, schedule and chunk size, in checked mode: bit-exact
+    against the oracle's slice."""
+    rng = np.random.default_rng(2024)
+    for it in range(200):
+        n = int(rng.integers(1, 2500))
+        dens = float(rng.choice([0.0005, 0.002, 0.01, 0.05]))
+        rp, ci = gen.random_graph(n, dens, seed=int(rng.integers(1 << 30)))
+        if n > 1 and rng.random() < 0.5:
+            rp, ci = g.permute(rp, ci, rng.permutation(n).astype(np.int32))
+        rb = int(rng.integers(0, n))
+        re = int(rng.integers(rb + 1, n + 1))
+        sched = str(rng.choice(["threshold", "fifo", "auto"]))
+        chunk = int(rng.choice([1, 7, 64, 128]))
+        got = run(rp, ci, ctx, row_begin=rb, row_end=re, schedule=sched, chunk_size=chunk,
+                  checked=True)
+        want = oracle.symbolic(rp, ci, chunk_size=chunk, row_begin=rb, row_end=re)
+        assert_full_equal(got, want, tag=f"it {it} n={n} rows=[{rb},{re}) {sched} chunk {chunk}")
