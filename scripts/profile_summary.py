@@ -65,9 +65,11 @@ out += [f"{k:62s} {v[0]:8d} {v[1] / 1e6:10.2f} {v[1] / tot * 100:6.1f}%"
 open(os.path.join(dst, f"launches_{cfg}_{tag}_summary.txt"), "w").write("\n".join(out) + "\n")
 shutil.copy(os.path.join(src, f"launches_{tag}_{cfg}.csv"), os.path.join(dst, f"launches_{cfg}_{tag}.csv"))
 shutil.copy(os.path.join(src, f"bench_{tag}_{cfg}.json"), os.path.join(dst, f"bench_{cfg}_{tag}.json"))
-json.dump({f"{cfg}/threshold": {"kernel": "solo_kernel", "dram_bytes": traffic["solo_kernel"],
-                                "stream_kernel_dram_bytes": traffic["stream_kernel"],
-                                "source": f"profiles/r1/{full}"}},
-          open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
+tpath = os.path.join(ROOT, "profiles", "traffic.json")
+tj = json.load(open(tpath)) if os.path.exists(tpath) else {}
+tj[f"{cfg}/threshold"] = {"kernel": "solo_kernel", "dram_bytes": traffic["solo_kernel"],
+                          "stream_kernel_dram_bytes": traffic["stream_kernel"],
+                          "source": f"profiles/r1/{full}"}
+json.dump(tj, open(tpath, "w"), indent=1)
 print("\n".join(out[:6]))
 print(traffic)
