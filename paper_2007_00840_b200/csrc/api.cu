@@ -866,6 +866,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   std::vector<std::pair<int, int>> e_trav, e_ext;
   int64_t baseL = 0, baseU = 0, nbatches = 0, maxC = 0;
   Plan plan;
+  bool auto_fifo = false;
 
   CK(cudaSetDevice(c->device));
   e_start = ev();
@@ -901,32 +902,44 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     d_colidx = c->in_colidx;
   }
   e_up = ev();
+  // ---------------------------------------------------- A1: validation
+  // CSR checks (GSOFA_EBADCSR) and int32 row pointers, before anything else
+  // reads the input; the same pass measures the bandwidth for AUTO
+  if ((rc = grow_device(&c->rowptr32, &c->rowptr32_cap, (size_t)n + 1, st)) != GSOFA_OK) goto fail;
+  if (!c->bw_dev) CK(cudaMalloc((void **)&c->bw_dev, 64));
+  CK(cudaMemsetAsync(c->bw_dev, 0, 8, st));  // [0] bandwidth, [1] error flags
+  CK(gsofa::launch_validate(d_rowptr64, d_colidx, n, nnz, c->rowptr32, (int *)(c->bw_dev + 1),
+                            o.schedule == GSOFA_SCHEDULE_AUTO ? c->bw_dev : nullptr, st));
+  ++launches;
+  CK(cudaMemcpyAsync(c->h_small, c->bw_dev, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (const int f = ((int *)c->h_small)[1]) {
+    set_detail("CSR check failed:%s%s%s", (f & 1) ? " bad rowptr" : "",
+               (f & 2) ? " column out of range" : "", (f & 4) ? " columns not strictly increasing" : "");
+    rc = GSOFA_EBADCSR;
+    goto fail;
+  }
   if (o.schedule == GSOFA_SCHEDULE_AUTO) {
     // banded and dense -> the paper's FIFO order (few rounds, no revisits);
-    // otherwise threshold order (DESIGN.md §8 "Schedule")
-    unsigned int bw = 0;
-    if (!c->bw_dev) CK(cudaMalloc((void **)&c->bw_dev, 64));
-    CK(gsofa::launch_bandwidth(d_rowptr64, d_colidx, n, c->bw_dev, st));
-    CK(cudaMemcpyAsync(&bw, c->bw_dev, sizeof bw, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    bool fifo = (int64_t)bw * 8 <= n && nnz >= 8 * n;
-    if (fifo) {
-      // and only if one batch of maxId labels (sources x vertices x 4 B)
-      // fits half of the free memory: FIFO in many small batches loses its edge
-      size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
+    // otherwise threshold order (DESIGN.md §8 "Schedule").  FIFO also needs
+    // one batch of maxId labels (sources x vertices x 4 B) to fit the budget
+    // the plan will use: FIFO in many small batches loses its edge.
+    const unsigned int bw = ((unsigned int *)c->h_small)[0];
+    auto_fifo = (int64_t)bw * 8 <= n && nnz >= 8 * n;
+    if (auto_fifo) {
+      int64_t budget = o.mem_budget_bytes ? o.mem_budget_bytes : c->budget;
+      if (!budget) budget = auto_budget(c->device) + (int64_t)c->arena_bytes;
       const double labels = (double)std::min<int64_t>(rows, 65536) * (double)n * 4.0;
-      fifo = labels <= 0.5 * (double)fr;
+      auto_fifo = labels <= (double)budget;
     }
-    o.schedule = fifo ? GSOFA_SCHEDULE_FIFO : GSOFA_SCHEDULE_THRESHOLD;
+    o.schedule = auto_fifo ? GSOFA_SCHEDULE_FIFO : GSOFA_SCHEDULE_THRESHOLD;
   }
-  if ((rc = grow_device(&c->rowptr32, &c->rowptr32_cap, (size_t)n + 1, st)) != GSOFA_OK) goto fail;
   // ---------------------------------------------------- plan + arena
   {
     const int64_t cmax_req =
         o.max_concurrent ? o.max_concurrent : 65536;  // FIFO: one batch when it fits (C3 -6% vs 16k)
     const int64_t budget_req = o.mem_budget_bytes ? o.mem_budget_bytes : c->budget;
-    const int64_t key[6] = {o.schedule, n, rb, re, budget_req, cmax_req};
+    int64_t key[6] = {o.schedule, n, rb, re, budget_req, cmax_req};
     bool ok = true;
     if (std::equal(key, key + 6, c->plan_key)) {
       plan = c->plan_cache;
@@ -937,6 +950,13 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       ok = o.schedule == GSOFA_SCHEDULE_FIFO
                ? make_plan(o.schedule, n, rows, vb_max, cmax_req, budget, plan)
                : make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan);
+      if (!ok && auto_fifo) {
+        // AUTO picked FIFO but its smallest batch does not fit: threshold
+        // order needs far less memory per source (no maxId labels)
+        o.schedule = GSOFA_SCHEDULE_THRESHOLD;
+        key[0] = o.schedule;
+        ok = make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan);
+      }
       if (ok && !std::getenv("GSOFA_LIGHT_CTAS") && !std::getenv("GSOFA_SOLO_CTAS") &&
           !std::getenv("GSOFA_SOLO_RING")) {
         c->plan_cache = plan;
@@ -962,21 +982,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   }
   if ((rc = prepare_work(c, o.schedule, st)) != GSOFA_OK) goto fail;
   ev();
-  // validate (GSOFA_EBADCSR) and narrow row pointers to int32
-  CK(cudaMemsetAsync(c->err, 0, sizeof(int), st));
   CK(cudaMemsetAsync(c->stats, 0, 8 * sizeof(unsigned long long), st));
-  CK(gsofa::launch_validate(d_rowptr64, d_colidx, n, nnz, c->rowptr32, c->err, st));
-  ++launches;
-  CK(cudaMemcpyAsync(c->h_small, c->err, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (*(int *)c->h_small) {
-    const int f = *(int *)c->h_small;
-    set_detail("CSR check failed:%s%s%s", (f & 1) ? " bad rowptr" : "",
-               (f & 2) ? " column out of range" : "", (f & 4) ? " columns not strictly increasing" : "");
-    rc = GSOFA_EBADCSR;
-    goto fail;
-  }
-  ev();
   // ---------------------------------------------------- outputs
   {
     cudaError_t e1 = cudaMallocAsync((void **)&Lrp, (rows + 1) * sizeof(int64_t), st);
@@ -1024,7 +1030,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     ev();
     if (c->stage_cap == 0) {
       size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
+      CK(cudaMemGetInfo(&fr, &tot));
       size_t want = std::max<size_t>((size_t)1 << 24, (size_t)(fr * 0.3) / 4);
       // dev / tests: a small initial staging area exercises the overflow retry
       if (const char *e = std::getenv("GSOFA_STAGE_CAP")) want = std::max<size_t>(1024, atoll(e));
@@ -1582,6 +1588,17 @@ int gsofa_partition_rows(int64_t n, const int64_t *rowptr, const int32_t *colidx
     return GSOFA_EINVAL;
   }
   const int64_t nnz = rowptr[n];
+  // the loops below index colidx through rowptr: check it first (the same
+  // row-pointer rules as the GPU validation)
+  if (rowptr[0] != 0 || nnz < 0 || nnz >= (int64_t(1) << 31)) {
+    set_detail("bad rowptr (rowptr[0] != 0 or nnz out of range)");
+    return GSOFA_EBADCSR;
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (rowptr[i + 1] < rowptr[i] || rowptr[i + 1] > nnz) {
+      set_detail("bad rowptr at row %lld", (long long)i);
+      return GSOFA_EBADCSR;
+    }
   // transpose pattern (for the symmetrised A + A^T)
   std::vector<int64_t> tp(n + 1, 0);
   std::vector<int32_t> ti(std::max<int64_t>(nnz, 1));

@@ -142,7 +142,8 @@ int extract_sub_columns();  // columns per extraction warp unit
 
 // supernode.cu + utilities
 cudaError_t launch_validate(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
-                            int64_t nnz, int32_t *rowptr32, int *err_flag, cudaStream_t st);
+                            int64_t nnz, int32_t *rowptr32, int *err_flag, unsigned int *bw,
+                            cudaStream_t st);
 cudaError_t launch_count_offdiag(const int32_t *rowptr, const int32_t *colidx, int32_t r0,
                                  int32_t r1, unsigned long long *out, cudaStream_t st);
 cudaError_t launch_supernode_flags(const int64_t *L_rowptr, const int32_t *L_colidx,
@@ -158,8 +159,6 @@ cudaError_t launch_supernode_stitch(const int64_t *U_rowptr, const int64_t *L_ro
                                     const int32_t *L_colidx, int32_t rb, int32_t he,
                                     int64_t prev_nnzU, int32_t prev_leader, const int32_t *sn_start,
                                     int64_t nsuper, int32_t *out, cudaStream_t st);
-cudaError_t launch_bandwidth(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
-                             unsigned int *out, cudaStream_t st);
 cudaError_t launch_audit(const int32_t *A_rowptr, const int32_t *A_colidx, const int64_t *L_rowptr,
                          const int32_t *L_colidx, const int64_t *U_rowptr, const int32_t *U_colidx,
                          const int32_t *sn_start, const int32_t *nsuper, int32_t row_begin, int32_t rows,

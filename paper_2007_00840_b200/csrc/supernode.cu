@@ -20,28 +20,45 @@ namespace gsofa {
 namespace {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
+// CSR checks + int64 -> int32 row pointers; with bw != NULL also the
+// bandwidth max |i - j| of A (GSOFA_SCHEDULE_AUTO), taken only from rows that
+// passed the row-pointer check, so a malformed rowptr never leads to a read
+// outside colidx
 __global__ void validate_kernel(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
-                                int64_t nnz, int32_t *rowptr32, int *err) {
+                                int64_t nnz, int32_t *rowptr32, int *err, unsigned int *bw) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > n) return;
-  const int64_t a = rowptr64[i];
-  rowptr32[i] = (int32_t)a;
-  if (i == 0 && a != 0) atomicOr(err, 1);
-  if (i == n) {
-    if (a != nnz) atomicOr(err, 1);
-    return;
+  unsigned int m = 0;
+  if (i <= n) {
+    const int64_t a = rowptr64[i];
+    rowptr32[i] = (int32_t)a;
+    if (i == 0 && a != 0) atomicOr(err, 1);
+    if (i == n) {
+      if (a != nnz) atomicOr(err, 1);
+    } else {
+      const int64_t b = rowptr64[i + 1];
+      if (b < a || a < 0 || b > nnz) {
+        atomicOr(err, 1);
+      } else {
+        int32_t prev = -1;
+        for (int64_t e = a; e < b; ++e) {
+          const int32_t c = colidx[e];
+          if (c < 0 || c >= n) atomicOr(err, 2);
+          if (c <= prev) atomicOr(err, 4);
+          prev = c;
+        }
+        if (b > a) {  // columns ascend: the extremes are the first and last entries
+          const int64_t d0 = i - (int64_t)colidx[a], d1 = (int64_t)colidx[b - 1] - i;
+          int64_t d = d0 > d1 ? d0 : d1;
+          if (d < 0) d = 0;
+          if (d > INT32_MAX) d = INT32_MAX;
+          m = (unsigned int)d;
+        }
+      }
+    }
   }
-  const int64_t b = rowptr64[i + 1];
-  if (b < a || a < 0 || b > nnz) {
-    atomicOr(err, 1);
-    return;
-  }
-  int32_t prev = -1;
-  for (int64_t e = a; e < b; ++e) {
-    const int32_t c = colidx[e];
-    if (c < 0 || c >= n) atomicOr(err, 2);
-    if (c <= prev) atomicOr(err, 4);
-    prev = c;
+  if (bw) {
+    m = __reduce_max_sync(0xFFFFFFFFu, m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(bw, m);
   }
 }
 
@@ -206,24 +223,6 @@ __global__ void audit_kernel(const int32_t *A_rowptr, const int32_t *A_colidx, c
   if (lane == 0 && bad) atomicOr(err, bad);
 }
 
-// bandwidth of A: max |i - j| over its entries (GSOFA_SCHEDULE_AUTO)
-__global__ void bandwidth_kernel(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
-                                 unsigned int *out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t a = rowptr64[i], b = rowptr64[i + 1];
-  unsigned int m = 0;
-  if (b > a) {  // columns ascend: the extremes are the first and last entries
-    const int64_t d0 = i - (int64_t)colidx[a], d1 = (int64_t)colidx[b - 1] - i;
-    int64_t d = d0 > d1 ? d0 : d1;
-    if (d < 0) d = 0;
-    if (d > INT32_MAX) d = INT32_MAX;
-    m = (unsigned int)d;
-  }
-  m = __reduce_max_sync(0xFFFFFFFFu, m);
-  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
-}
-
 __global__ void sn_scatter_kernel(const int32_t *flags, const int32_t *pos, int32_t row_begin,
                                   int32_t row_end, const int32_t *total, int32_t *sn_start) {
   const int32_t s = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
@@ -326,9 +325,10 @@ cudaError_t scan_exclusive_i32_i64(const int32_t *in, int64_t *out, int64_t coun
 }
 
 cudaError_t launch_validate(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
-                            int64_t nnz, int32_t *rowptr32, int *err_flag, cudaStream_t st) {
+                            int64_t nnz, int32_t *rowptr32, int *err_flag, unsigned int *bw,
+                            cudaStream_t st) {
   validate_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(rowptr64, colidx, n, nnz,
-                                                                   rowptr32, err_flag);
+                                                                   rowptr32, err_flag, bw);
   return cudaGetLastError();
 }
 
@@ -378,14 +378,6 @@ cudaError_t launch_audit(const int32_t *A_rowptr, const int32_t *A_colidx, const
   audit_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(A_rowptr, A_colidx, L_rowptr, L_colidx,
                                                            U_rowptr, U_colidx, sn_start, nsuper,
                                                            row_begin, rows, n, chunk, err);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_bandwidth(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
-                             unsigned int *out, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned int), st);
-  if (e != cudaSuccess) return e;
-  bandwidth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rowptr64, colidx, n, out);
   return cudaGetLastError();
 }
 

@@ -106,3 +106,18 @@ def test_partition_rows_balanced_and_aligned(g):
 def test_partition_rows_deterministic(g):
     rp, ci = gen.config("C4", 50)
     assert np.array_equal(g.partition_rows(rp, ci, 4), g.partition_rows(rp, ci, 4))
+
+
+def test_partition_rows_rejects_bad_rowptr(g):
+    """Malformed row pointers are rejected before any colidx access
+    (GSOFA_EBADCSR), not read out of bounds."""
+    import gen
+    rp, ci = gen.random_graph(64, 0.1, seed=3)
+    for bad in (lambda r: r.__setitem__(5, r[-1] + 1000),   # rowptr[i] > nnz
+                lambda r: r.__setitem__(7, r[6] - 1 if r[6] > 0 else -1),  # decreasing
+                lambda r: r.__setitem__(0, 1)):             # rowptr[0] != 0
+        b = rp.copy()
+        bad(b)
+        with pytest.raises(g.GsofaError) as e:
+            g.partition_rows(b, ci, 4)
+        assert e.value.code == -2
