@@ -1,11 +1,14 @@
 #!/usr/bin/env python
 """Benchmark of the gSoFa symbolic-factorization hot path on B200.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
 
 A step = one full symbolic factorization (seed -> traversal -> extraction ->
 supernodes, plus for N > 1 the NCCL count allgather) of the synthetic
-BASELINE config (default C2 = configs[1], 3D 7-point 64^3, ND order).
+BASELINE config (default C5 = configs[4], 3D 7-point 128^3, ND order: the
+largest matrix, on which north_star's 1/2/4/8-GPU strong scaling is quoted).
+``--gpus N`` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one GPU each, NCCL).
 value = fill-ins found per second over the whole job (max over ranks of the
 device time); e2e = the same through the public API with host (pinned)
 buffers, uploads and result downloads inside the timed region.
@@ -136,16 +139,56 @@ def cpu_oracle_sample(rp, ci, target_s: float, seed: int = 0):
     return fills / dt, desc, threads, dt
 
 
-def algorithmic_bytes(stats, schedule):
-    """Algorithmic bytes of the traversal kernel:
-    threshold: 12 B per (item, neighbour) pair (4 B colidx + 8 B RMW of the
-    32-source state word of the neighbour) + 24 B per item (8 B pend exchange,
-    8 B rowptr, 8 B list write+read);  FIFO: additionally 8 B per
-    (source, edge) label RMW."""
-    b = 12 * stats["item_edges"] + 24 * stats["frontier_items"]
-    if schedule == "fifo":
-        b += 8 * stats["edge_inspections"]
-    return b
+def algorithmic_bytes(stats, n, rows, fills):
+    """Algorithmic bytes of the traversal per SURVEY.md §8(d):
+      4 B label read per (source, edge) inspection      (edge_inspections)
+      4 B label write per improvement                   (first_visits: each
+          (source, vertex) label is lowered once in threshold order; a lower
+          bound for the FIFO order)
+      4 B colidx per (item, neighbour) pair             (item_edges: one read
+          shared by the sources of a lockstep item, A_g)
+      12 B per (source, frontier entry)                 (source_expansions:
+          4 B label(u) + ~8 B queue)
+      4 B output per fill-in
+      2 * n/8 B per source                              (row extraction + clear)
+    Returns (bytes, breakdown dict)."""
+    parts = {
+        "label_reads": 4 * stats["edge_inspections"],
+        "label_writes": 4 * stats.get("first_visits", 0),
+        "colidx": 4 * stats["item_edges"],
+        "frontier": 12 * stats.get("source_expansions", 0),
+        "fill_output": 4 * fills,
+        "extraction": 2 * (n / 8) * rows,
+    }
+    return sum(parts.values()), parts
+
+
+def ncu_kernels(config, schedule):
+    """Per-kernel DRAM traffic from the committed ncu --set full captures
+    (profiles/traffic.json): dram bytes per launch and ncu's own duration."""
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except Exception:
+        return None, None
+    ent = tj.get(f"{config}/{schedule}")
+    if not ent:
+        return None, None
+    return ent.get("kernels", {}), ent.get("source")
+
+
+def self_launch(args):
+    """--gpus N without a torchrun environment: re-run this script under
+    torch.distributed.run with N ranks (one per GPU, NCCL), rendezvous on
+    127.0.0.1; rank 0's JSON line is this process's stdout."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd)
 
 
 def run_reference(args, rank, world):
@@ -180,7 +223,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIG_DESC))
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIG_DESC))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--schedule", default="auto", choices=["auto", "threshold", "fifo"])
     ap.add_argument("--max-concurrent", type=int, default=0)
@@ -190,11 +233,18 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
+    if args.impl == "reference":
+        # the oracle arm runs on host cores, rank 0 only (other ranks exit 0)
+        rank = int(os.environ.get("RANK", "0"))
+        return run_reference(args, rank, int(os.environ.get("WORLD_SIZE", str(args.gpus))))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        return run_reference(args, rank, world)
+    if world != args.gpus:
+        log(f"[bench] WORLD_SIZE={world} but --gpus {args.gpus}")
+        return 2
 
     import torch
     import torch.distributed as dist
@@ -263,6 +313,7 @@ def main():
     step_ms, stats_acc, launches = [], {}, 0
     sched_used = args.schedule
     fills_step = 0
+    local_fills = 0
     with ClockSampler(dev_index) as clk:
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (256 MiB > 126 MB L2), untimed
@@ -274,6 +325,7 @@ def main():
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
             if r is not None:
+                local_fills += r.fill_count  # this rank's rows (roofline of its kernels)
                 sched_used = r.schedule  # the library's choice under "auto"
                 for k, v in r.stats.items():
                     stats_acc[k] = stats_acc.get(k, 0) + v
@@ -283,12 +335,14 @@ def main():
     if world > 1:
         dist.barrier()
     tot_ms = sum(step_ms)
+    per_rank_ms = [tot_ms / args.steps]
     if world > 1:
         t = torch.tensor([tot_ms, float(launches)], dtype=torch.float64, device=coll_dev or "cpu")
-        tmax = t.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
-        tot_ms, launches_all = float(tmax[0]), int(t[1])
+        allt = torch.empty(2 * world, dtype=torch.float64, device=t.device)
+        dist.all_gather_into_tensor(allt, t)
+        allt = allt.cpu().view(world, 2)
+        per_rank_ms = [float(x) / args.steps for x in allt[:, 0]]
+        tot_ms, launches_all = float(allt[:, 0].max()), int(allt[:, 1].sum())
     else:
         launches_all = launches
     ms_per_step = tot_ms / args.steps
@@ -321,28 +375,41 @@ def main():
         dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
         e2e_step, h2d, d2h = float(m[0]), int(t[1]), int(t[2])
 
-    # ---- roofline of the dominant kernel (traversal), measured live
+    # ---- roofline of the dominant kernel (traversal), measured live: the
+    # traversal kernels' device time (CUDA events on the launch stream inside
+    # the call) and SURVEY §8(d)'s algorithmic bytes of the work they did
     peak, peak_src = load_peaks()
     trav_ms = stats_acc.get("ms_traverse", 0.0)
-    alg = algorithmic_bytes(stats_acc, sched_used) if stats_acc else 0
+    alg, alg_parts = (algorithmic_bytes(stats_acc, n, (re - rb) * args.steps, local_fills)
+                      if stats_acc else (0, {}))
     achieved = alg / (trav_ms / 1e3) / 1e9 if trav_ms > 0 else 0.0
-    traffic, traffic_src = None, None
-    try:
-        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        ent = tj.get(f"{args.config}/{sched_used}")
-        if ent:
-            traffic = float(ent["dram_bytes"])  # per launch, from one ncu --set full capture
-            traffic_src = f'{ent["kernel"]}: {ent["source"]}'
-    except Exception:
-        pass
-    roofline = {"kernel": ("solo_kernel+stream_kernel" if sched_used == "threshold"
-                           else "traverse_kernel"),
-                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                "peak_source": peak_src,
+    kern = "solo_kernel+stream_kernel" if sched_used == "threshold" else "traverse_kernel"
+    roofline = {"kernel": kern, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "bytes_model": "SURVEY.md §8(d): 4 B/edge inspection + 4 B/first visit + "
+                               "4 B/(item,neighbour) colidx + 12 B/(source, frontier entry) + "
+                               "4 B/fill + n/4 B/source",
                 "algorithmic_bytes_per_step": alg / args.steps,
+                "algorithmic_bytes_parts_per_step": {k: v / args.steps for k, v in alg_parts.items()},
                 "kernel_ms_per_step": trav_ms / args.steps,
                 "kernel_share_of_step": (trav_ms / args.steps) / ms_per_step if ms_per_step else None}
+    # what ncu says the same kernels do to DRAM (one --set full capture per
+    # kernel, committed under profiles/): bytes per launch, its GB/s, and
+    # the fraction of the measured copy bandwidth
+    kinfo, ksrc = ncu_kernels(args.config, sched_used)
+    if kinfo:
+        nk = {}
+        tot_b = 0.0
+        for k, v in kinfo.items():
+            b = float(v["dram_bytes"])
+            tot_b += b
+            gbs = b / float(v["duration_s"]) / 1e9
+            nk[k] = {"dram_bytes": b, "ncu_ms": float(v["duration_s"]) * 1e3, "dram_gbs": gbs,
+                     "dram_frac": gbs / peak}
+        roofline["traffic"] = tot_b  # dram read + write of the traversal kernels, per launch
+        roofline["ncu"] = {"kernels": nk, "source": ksrc}
+        roofline["limiter"] = ("latency of dependent L2 atomics (ncu: long-scoreboard stalls "
+                               "dominate, DRAM well below peak; see roofline.ncu)")
     # the unit operation of the traversal is a random 4-byte atomic (one per
     # (item, neighbour) pair); its ceiling on this GPU was measured with
     # scripts/atomics_bench.cu (profiles/atomic_peak.json)
@@ -354,6 +421,8 @@ def main():
                               "frac": a_ach / a_peak, "peak_source": ap["source"]}
     except Exception:
         pass
+    if stats_acc.get("first_visits"):
+        roofline["revisit_factor"] = stats_acc["source_expansions"] / stats_acc["first_visits"]
     stats_step = {k: (v / args.steps) for k, v in stats_acc.items()}
 
     cpu = None
@@ -368,6 +437,7 @@ def main():
                "dtype": "int32", "data": "synthetic (gen.config, seeded; no datasets)",
                "config": {"workload": CONFIG_DESC[args.config], "n": n, "nnz_offdiag": int(ci.size),
                           "row_ranges": [int(b) for b in bounds],
+                          "per_rank_ms": per_rank_ms,
                           "fill_ins": fills_step, "schedule": sched_used,
                           "parallelism": f"rows split over {world} GPU(s)" if world > 1 else "1 GPU",
                           "l2": "flushed between timed steps (256 MiB write, untimed)"},

@@ -80,9 +80,11 @@ typedef struct gsofa_opts {
    *   GSOFA_SCHEDULE_AUTO (2, default): FIFO when the pattern is banded and
    *     dense (bandwidth <= n/8 and nnz >= 8n: few rounds, almost no
    *     revisits -- measured 1.3-2.9x faster there) and one batch of labels
-   *     (min(rows, 65536) x n x 4 B) fits half the free memory; threshold otherwise
-   *     (ND orders, hubs: 15x the inspections in FIFO).  The bandwidth is
-   *     one GPU pass over A.  gsofa_result.schedule reports the choice. */
+   *     (min(rows, 65536) x n x 4 B) fits the memory budget of the call;
+   *     threshold otherwise (ND orders, hubs: 15x the inspections in FIFO),
+   *     and also when the FIFO plan turns out infeasible.  The bandwidth is
+   *     measured by the CSR validation pass.  gsofa_result.schedule reports
+   *     the choice. */
   int32_t schedule;
   /* source rows [row_begin, row_end); row_end = -1 means n.  Any row_begin:
    * if it is not a multiple of chunk_size, the supernodes of the head rows
@@ -124,6 +126,15 @@ typedef struct gsofa_stats {
   double ms_extract;         /* row extraction (count + scan + write) */
   double ms_supernode;       /* supernode detection */
   double ms_transfer;        /* host<->device copies inside the call */
+  /* R11: first-visit vs total work.  first_visits = (source, vertex)
+   * pairs, vertex < source, whose maxId left "unvisited" (each such vertex is
+   * expanded at least once); source_expansions = (source, vertex) frontier
+   * expansions including revisits.  revisit factor = source_expansions /
+   * first_visits: exactly 1 in threshold order (every reached vertex is
+   * expanded once), > 1 in the paper's FIFO order.  Groups the lockstep
+   * kernel abandons to the solo kernel count once (their redo). */
+  int64_t first_visits;
+  int64_t source_expansions;
 } gsofa_stats;
 
 /* --------------------------------------------------------------- result -- */

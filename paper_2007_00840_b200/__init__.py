@@ -47,7 +47,8 @@ class Stats(ctypes.Structure):
                 ("thresholds", _I64), ("batches", _I64), ("max_batch", _I64), ("kernel_launches", _I64),
                 ("ms_total", ctypes.c_double), ("ms_traverse", ctypes.c_double),
                 ("ms_extract", ctypes.c_double), ("ms_supernode", ctypes.c_double),
-                ("ms_transfer", ctypes.c_double)]
+                ("ms_transfer", ctypes.c_double), ("first_visits", _I64),
+                ("source_expansions", _I64)]
 
 
 class CResult(ctypes.Structure):

@@ -317,7 +317,7 @@ int ensure_arena(gsofa_context *c, int64_t n, const Plan &p, cudaStream_t st) {
     c->rowU = (int64_t *)carve(p.Cmax * 8);
     c->totals = (int64_t *)carve(64);
     c->qcount = (uint32_t *)carve(64);
-    c->stats = (unsigned long long *)carve(64);
+    c->stats = (unsigned long long *)carve(128);
     c->err = (int *)carve(64);
   }
   c->key_n = n;
@@ -982,7 +982,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   }
   if ((rc = prepare_work(c, o.schedule, st)) != GSOFA_OK) goto fail;
   ev();
-  CK(cudaMemsetAsync(c->stats, 0, 8 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(c->stats, 0, 16 * sizeof(unsigned long long), st));
   // ---------------------------------------------------- outputs
   {
     cudaError_t e1 = cudaMallocAsync((void **)&Lrp, (rows + 1) * sizeof(int64_t), st);
@@ -1416,8 +1416,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     rc = GSOFA_ENOMEM;
     goto fail;
   }
-  CK(cudaMemcpyAsync(c->h_small, c->stats, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(c->h_small + 8, (int32_t *)c->totals + 4, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->h_small, c->stats, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->h_small + 16, (int32_t *)c->totals + 4, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   {
     const unsigned long long *hs = (const unsigned long long *)c->h_small;
@@ -1426,7 +1426,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     res->row_end = re;
     res->nnz_L = baseL;
     res->nnz_U = baseU;
-    res->nsuper = *(int32_t *)(c->h_small + 8);
+    res->nsuper = *(int32_t *)(c->h_small + 16);
     res->nnz_A_offdiag = (int64_t)hs[5];
     res->fill_count = baseL + (baseU - rows) - res->nnz_A_offdiag;
     res->device = c->device;
@@ -1437,6 +1437,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     res->stats.rounds = (int64_t)hs[2];
     res->stats.thresholds = (int64_t)hs[3];
     res->stats.item_edges = (int64_t)hs[4];
+    res->stats.first_visits = (int64_t)hs[8];
+    res->stats.source_expansions = (int64_t)hs[9];
     res->stats.batches = nbatches;
     res->stats.max_batch = maxC;
     res->stats.kernel_launches = launches;

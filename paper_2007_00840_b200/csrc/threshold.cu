@@ -106,6 +106,7 @@ __device__ __forceinline__ int scan_next(const uint32_t *thr, const uint32_t *ts
 
 struct Counters {
   unsigned long long items, edges, pairs, levels, steps;
+  unsigned long long fv, sx;  // first visits (source, w < source); (source, item) expansions
   uint32_t sink;
 };
 
@@ -137,6 +138,7 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
     if (!mask) deg = 0;
   }
   c.items += mask != 0u;
+  c.sx += (unsigned long long)__popc(mask);
   c.pairs += (unsigned long long)deg;
   c.edges += (unsigned long long)__popc(mask) * (unsigned long long)deg;
   // load-balanced expansion of the (item, neighbour) pairs over the lanes
@@ -181,6 +183,7 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
       if (io[k] == 0u) atomicOr(sl.isum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));  // RED
       if (ro[k] == 0u) atomicOr(sl.rsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));  // RED
       const uint32_t nw = lm[k] & ~ro[k];
+      c.fv += (unsigned long long)__popc(nw);  // sources that reach w < source for the first time
       push[k] = false;
       po[k] = kFull;
       if (nw) {
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
   __shared__ long long s_rowoff[32];
   __shared__ int s_nL[32];
   __shared__ int s_ok, s_abort;
-  Counters c = {0, 0, 0, 0, 0, 0u};
+  Counters c = {0, 0, 0, 0, 0, 0, 0, 0u};
 
   for (;;) {
     if (tid == 0) {
@@ -378,6 +381,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
     if (g < 0) break;
     const long long t_start = clock64();
     const unsigned long long st0 = c.steps, lv0 = c.levels, it0 = c.items, pr0 = c.pairs;
+    const unsigned long long fv0 = c.fv, sx0 = c.sx;
     long long t_trav = 0, t_ext = 0;
     const int s0g = p.row_begin + 32 * g;
     const int nsrc = min(32, p.row_end - s0g);
@@ -398,6 +402,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
         atomicOr(sl.is + w, bit);                                     // RED
         atomicOr(sl.isum + (w >> 10), 1u << ((w >> 5) & 31));       // RED
         if (w < s) {
+          c.fv += 1;                                                  // first visit of (s, w)
           atomicOr(sl.state + 2 * w, bit);                            // RED
           atomicOr(sl.rsum + (w >> 10), 1u << ((w >> 5) & 31));       // RED
           atomicOr(sl.state + 2 * w + 1, bit);                        // RED
@@ -488,6 +493,10 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
     // words are performed at L2, so make the stores globally visible first
     __threadfence();
     if (aborted) {
+      // the visit counters describe completed traversals only: the solo
+      // kernel redoes this group from its seed
+      c.fv = fv0;
+      c.sx = sx0;
       // hand the group to the solo kernel (it restarts from the seed)
       __syncthreads();
       if (tid == 0) {
@@ -519,11 +528,15 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
     c.items += __shfl_xor_sync(kFull, c.items, d);
     c.edges += __shfl_xor_sync(kFull, c.edges, d);
     c.pairs += __shfl_xor_sync(kFull, c.pairs, d);
+    c.fv += __shfl_xor_sync(kFull, c.fv, d);
+    c.sx += __shfl_xor_sync(kFull, c.sx, d);
   }
   if (lane == 0) {
     atomicAdd(p.stats + 0, c.items);
     atomicAdd(p.stats + 1, c.edges);
     atomicAdd(p.stats + 4, c.pairs);
+    atomicAdd(p.stats + 8, c.fv);
+    atomicAdd(p.stats + 9, c.sx);
   }
   if (tid == 0) {
     atomicAdd(p.stats + 2, c.levels);
@@ -634,6 +647,7 @@ struct SoloWarpSmem {
   uint32_t win[32];
   int qw[kSoloQ], qb[kSoloQ], qe[kSoloQ];
   uint32_t items, pairs, levels, steps;  // this source's counters (lane 0 updates)
+  uint32_t fv;                           // first visits (vertices < s reached)
 };
 
 struct SoloQueue {
@@ -730,6 +744,11 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       if (k >= nb) continue;
       const int wk = w[k];
       const uint32_t bw = vbit(wk);
+      {
+        // first visits: the reached bit of w < s was clear (w >= s: ro = bw)
+        const uint32_t nv = __popc(__ballot_sync(kFull, !(ro[k] & bw)));
+        if (lane == 0) sw.fv += nv;
+      }
       if (io[k] == 0u) red_sum(SL_ISUM, wk);
       bool push = false;
       if (!(ro[k] & bw)) {
@@ -817,8 +836,11 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
   // seed: the out-neighbours of s are in the structure; the
   // smaller ones are reached with maxId -1 and are thresholds
   const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
-  for (int j = beg + lane; j < end; j += 32) {
-    const int w = __ldg(p.colidx + j);
+  for (int j0 = beg; j0 < end; j0 += 32) {
+    const int j = j0 + lane;
+    const int w = j < end ? __ldg(p.colidx + j) : s;
+    const uint32_t nv = __popc(__ballot_sync(kFull, w < s));  // first visits of the seeds
+    if (lane == 0) sw.fv += nv;
     if (w == s) continue;
     const uint32_t bw = vbit(w);
     if (atomicOr(SL_IS + (w >> 5), bw) == 0u) red_sum(SL_ISUM, w);
@@ -1008,7 +1030,7 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
   const int Vw = (p.Vmax + 31) >> 5, Vs = (Vw + 31) >> 5;
   __shared__ SoloWarpSmem s_sw[kSoloWarps];
   SoloWarpSmem &sw = s_sw[warp];
-  if (lane == 0) sw.items = sw.pairs = sw.levels = sw.steps = 0u;
+  if (lane == 0) sw.items = sw.pairs = sw.levels = sw.steps = sw.fv = 0u;
   __syncwarp();
   // first task: warp-major over the grid, so consecutive (heaviest) sources
   // start on different SMs; then the global task counter
@@ -1080,8 +1102,10 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
       atomicAdd(p.stats + 4, (unsigned long long)sw.pairs);
       atomicAdd(p.stats + 2, (unsigned long long)sw.levels);
       atomicAdd(p.stats + 3, (unsigned long long)sw.steps);
+      atomicAdd(p.stats + 8, (unsigned long long)sw.fv);
+      atomicAdd(p.stats + 9, (unsigned long long)sw.items);  // solo: items are per source
       atomicAdd(p.done, 1u);
-      sw.items = sw.pairs = sw.levels = sw.steps = 0u;
+      sw.items = sw.pairs = sw.levels = sw.steps = sw.fv = 0u;
     }
     __syncwarp();
   }

@@ -46,9 +46,11 @@ __global__ void __launch_bounds__(256) seed_kernel(BatchParams p) {
   uint32_t *isg = p.is + (size_t)g * p.n;
   uint32_t *labg = p.lab + (size_t)g * p.Vb * 32 + k;
   uint32_t *fmg = p.fm0 + (size_t)g * p.Vb;
+  unsigned long long fv = 0;  // first visits of (s, w < s): the seeds
   for (int j = beg + lane; j < end; j += 32) {
     const int w = p.colidx[j];
     if (w == s) continue;
+    fv += w < s;
     atomicOr(isg + w, bit);
     if (w < s) {
       labg[(size_t)w * 32] = p.base;  // enc(-1)
@@ -58,6 +60,8 @@ __global__ void __launch_bounds__(256) seed_kernel(BatchParams p) {
       }
     }
   }
+  fv = __reduce_add_sync(kFull, (unsigned)fv);
+  if (lane == 0 && fv) atomicAdd(p.stats + 8, fv);
 }
 
 // coalesced 32-source label atomics a warp keeps in flight per item
@@ -72,7 +76,9 @@ __device__ __forceinline__ void expand_item(const BatchParams &p, uint32_t u, ui
                                             uint32_t *ncount, uint32_t *buf, int &nb,
                                             int lane, unsigned long long &st_items,
                                             unsigned long long &st_edges,
-                                            unsigned long long &st_pairs) {
+                                            unsigned long long &st_pairs,
+                                            unsigned long long &st_fv,
+                                            unsigned long long &st_sx) {
   const size_t row = (size_t)g * p.Vb + u;
   uint32_t mask = 0;
   if (lane == 0) {
@@ -89,6 +95,7 @@ __device__ __forceinline__ void expand_item(const BatchParams &p, uint32_t u, ui
   const int beg = __ldg(p.rowptr + u), end = __ldg(p.rowptr + u + 1);
   if (lane == 0) {
     st_items += 1;
+    st_sx += (unsigned long long)__popc(mask);
     st_edges += (unsigned long long)__popc(mask) * (unsigned long long)(end - beg);
     st_pairs += (unsigned long long)(end - beg);
   }
@@ -120,6 +127,10 @@ __device__ __forceinline__ void expand_item(const BatchParams &p, uint32_t u, ui
       }
 #pragma unroll
       for (int i = 0; i < kFifoInflight; ++i) {
+        // first visit of (s, w): the old label is not of this batch's epoch
+        // (values of the epoch are base .. base + n + 1)
+        const uint32_t nv = __popc(__ballot_sync(kFull, lo[i] && old[i] > p.base + (uint32_t)p.n + 1u));
+        if (lane == 0) st_fv += nv;
         const bool enq = lo[i] && encc < old[i] && old[i] > p.base + (uint32_t)w[i] + 1u;
         const bool fill = enq && c < w[i];
         const uint32_t ib = __ballot_sync(kFull, up[i] || fill);
@@ -162,7 +173,7 @@ __global__ void __launch_bounds__(kTraverseThreads, 2) traverse_kernel(BatchPara
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
   const uint32_t gmask = (1u << p.gbits) - 1u;
   uint32_t *buf = sbuf[wib];
-  unsigned long long st_items = 0, st_edges = 0, st_pairs = 0;
+  unsigned long long st_items = 0, st_edges = 0, st_pairs = 0, st_fv = 0, st_sx = 0;
   int round = 0;
   for (;; ++round) {
     const uint32_t *q = (round & 1) ? p.q1 : p.q0;
@@ -181,7 +192,7 @@ __global__ void __launch_bounds__(kTraverseThreads, 2) traverse_kernel(BatchPara
       for (uint32_t t = 0; t < cnt; ++t) {
         const uint32_t item = __shfl_sync(kFull, my, t);
         expand_item<kFillFirst>(p, item >> p.gbits, item & gmask, fmc, fmn, nq, ncount, buf,
-                                nb, lane, st_items, st_edges, st_pairs);
+                                nb, lane, st_items, st_edges, st_pairs, st_fv, st_sx);
       }
     }
     if (nb > 0) {
@@ -197,6 +208,8 @@ __global__ void __launch_bounds__(kTraverseThreads, 2) traverse_kernel(BatchPara
     atomicAdd(p.stats + 0, st_items);
     atomicAdd(p.stats + 1, st_edges);
     atomicAdd(p.stats + 4, st_pairs);
+    atomicAdd(p.stats + 8, st_fv);
+    atomicAdd(p.stats + 9, st_sx);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.stats + 2, (unsigned long long)(round + 1));
 }

@@ -470,3 +470,25 @@ def test_randomized_sweep(ctx):
                   checked=True)
         want = oracle.symbolic(rp, ci, chunk_size=chunk, row_begin=rb, row_end=re)
         assert_full_equal(got, want, tag=f"it {it} n={n} rows=[{rb},{re}) {sched} chunk {chunk}")
+
+
+@pytest.mark.parametrize("name,scale", [("C5", 16), ("C4", 60), ("C2", 20), ("C3", 3000)])
+def test_visit_stats(ctx, name, scale, monkeypatch):
+    """R11 first-visit vs total work.  The reached set of a source is
+    order-independent, so first_visits is the same in both schedules; in
+    threshold order every reached vertex is expanded exactly once
+    (source_expansions == first_visits) and the edge inspections equal the
+    oracle's DFS visit count (which also counts each source's own row); the
+    paper's FIFO order revisits (>=)."""
+    monkeypatch.setenv("GSOFA_ABORT_MS", "100000")  # no abandoned lockstep attempts
+    rp, ci = gen.config(name, scale)
+    n = rp.size - 1
+    visits = oracle.rows(rp, ci)["visits"]
+    t = run(rp, ci, ctx, schedule="threshold")["stats"]
+    f = run(rp, ci, ctx, schedule="fifo")["stats"]
+    assert t["first_visits"] > 0
+    assert t["source_expansions"] == t["first_visits"]
+    assert t["edge_inspections"] == visits - int(rp[n])
+    assert f["first_visits"] == t["first_visits"]
+    assert f["source_expansions"] >= f["first_visits"]
+    assert f["edge_inspections"] >= t["edge_inspections"]
