@@ -51,6 +51,7 @@ extern "C" {
 #define GSOFA_SCHEDULE_THRESHOLD 0
 #define GSOFA_SCHEDULE_FIFO      1
 #define GSOFA_SCHEDULE_AUTO      2
+#define GSOFA_SCHEDULE_HEIGHT    3
 
 /* -------------------------------------------------------------- options -- */
 typedef struct gsofa_opts {
@@ -77,6 +78,13 @@ typedef struct gsofa_opts {
    *     iteration in parallel with revisits, one
    *     persistent grid-wide kernel per batch with epoch-encoded maxId
    *     labels.
+   *   GSOFA_SCHEDULE_HEIGHT (3): the threshold order by elimination-tree
+   *     height instead of vertex id: thresholds of one height have disjoint
+   *     closures (they lie in disjoint subtrees of the etree of A + A^T,
+   *     P:264), so a step expands all thresholds of one height at once;
+   *     no revisits, |L(s,:)| steps per source become at most the tree
+   *     height.  The plan computes the etree on the host (Liu's algorithm,
+   *     O(nnz alpha)).
    *   GSOFA_SCHEDULE_AUTO (2, default): FIFO when the pattern is banded and
    *     dense (bandwidth <= n/8 and nnz >= 8n: few rounds, almost no
    *     revisits -- measured 1.3-2.9x faster there) and one batch of labels

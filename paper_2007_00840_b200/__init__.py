@@ -76,8 +76,8 @@ class GsofaError(RuntimeError):
 
 
 _lib = None
-SCHEDULES = {"threshold": 0, "fifo": 1, "auto": 2}
-SCHEDULE_NAMES = {0: "threshold", 1: "fifo"}
+SCHEDULES = {"threshold": 0, "fifo": 1, "auto": 2, "height": 3}
+SCHEDULE_NAMES = {0: "threshold", 1: "fifo", 3: "height"}
 
 
 def load():

@@ -119,7 +119,7 @@ struct gsofa_context {
   // last plan and its key: repeated calls on the same problem skip the
   // free-memory query and the occupancy queries, and keep the arena layout
   Plan plan_cache;
-  int64_t plan_key[6] = {-1, -1, -1, -1, -1, -1};
+  int64_t plan_key[7] = {-1, -1, -1, -1, -1, -1, -1};
   int32_t *stage = nullptr;  // staging area for streamed rows (grow-only)
   size_t stage_cap = 0;
   uint32_t *work = nullptr, *is = nullptr;
@@ -136,6 +136,9 @@ struct gsofa_context {
   int32_t *in_colidx = nullptr, *rowptr32 = nullptr;
   size_t in_rowptr_cap = 0, in_colidx_cap = 0, rowptr32_cap = 0;
   int64_t *h_small = nullptr;  // pinned host scratch
+  // height order (order.cu): per-vertex records, position -> vertex, word heights
+  int32_t *ord_rec = nullptr, *ord_vert = nullptr, *ord_wkey = nullptr;
+  size_t ord_rec_cap = 0, ord_vert_cap = 0, ord_wkey_cap = 0;
   HostBlock *hpool = nullptr;  // pinned storage reused by host-side results
 };
 
@@ -162,7 +165,7 @@ size_t small_bytes(int64_t Cmax) {
 size_t work_need(int schedule, int64_t C, int64_t Vb) {
   const int64_t G = C / 32;
   if (schedule == GSOFA_SCHEDULE_FIFO) return (size_t)C * Vb * 4 + (size_t)G * Vb * 16;
-  return (size_t)G * gsofa::stream_ws_words(Vb) * 4;
+  return (size_t)G * gsofa::stream_ws_words(Vb, 0) * 4;
 }
 
 // FIFO keeps its label region apart from masks/queues so that every label
@@ -215,10 +218,12 @@ bool make_plan(int schedule, int64_t n, int64_t rows, int64_t vb_max, int64_t cm
 // (bubble removal).  Slot counts follow the residency of both kernels
 // sharing the SMs and the memory budget ("reduce the number of concurrent
 // sources").
-bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int device, Plan &p) {
-  if (gsofa::stream_smem_bytes(Vmax) > 200 * 1024) return false;
-  const size_t ws = gsofa::stream_ws_words(Vmax), isw = gsofa::stream_is_words(n);
-  const size_t hws = gsofa::solo_ws_words(Vmax, n);
+// npos > 0: height order (threshold bitmaps over npos positions, order.cu)
+bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int device, Plan &p,
+                      int64_t npos) {
+  if (gsofa::stream_smem_bytes(Vmax, npos) > 200 * 1024) return false;
+  const size_t ws = gsofa::stream_ws_words(Vmax, npos), isw = gsofa::stream_is_words(n);
+  const size_t hws = gsofa::solo_ws_words(Vmax, n, npos);
   const int64_t spc = gsofa::solo_warps_per_cta();
   const size_t per_light = (ws + isw) * 4, per_heavy = hws * 4 * (size_t)spc;  // per solo CTA
   const size_t fixed = small_bytes(32) + 8192;
@@ -227,8 +232,8 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const int64_t ngroups = ceil_div(rows, 32);
   const int64_t wpc = gsofa::stream_warps_per_cta();  // lockstep slots (warps) per CTA
-  const int64_t res_light = gsofa::stream_max_blocks(device, Vmax, 0) * wpc;
-  const int64_t res_heavy = gsofa::stream_max_blocks(device, Vmax, 1);
+  const int64_t res_light = gsofa::stream_max_blocks(device, Vmax, 0, npos) * wpc;
+  const int64_t res_heavy = gsofa::stream_max_blocks(device, Vmax, 1, npos);
   if (res_light < 1) return false;
   // solo CTAs: one per SM is resident next to the lockstep CTAs from the
   // start; more become resident as lockstep CTAs finish (the grid is
@@ -240,7 +245,7 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
   (void)res_heavy;
   if (const char *e = std::getenv("GSOFA_SOLO_CTAS")) heavy = std::min<int64_t>(heavy, atoll(e));
   heavy = std::max<int64_t>(0, std::min<int64_t>(heavy, (int64_t)(((size_t)budget - fixed) / 2 / per_heavy)));
-  int64_t light = heavy > 0 ? (int64_t)sms * gsofa::stream_light_per_sm_with_solo(device, Vmax) * wpc
+  int64_t light = heavy > 0 ? (int64_t)sms * gsofa::stream_light_per_sm_with_solo(device, Vmax, npos) * wpc
                             : res_light;
   if (res_heavy < 1) heavy = 0;
   light = std::min<int64_t>(light, res_light);
@@ -482,7 +487,7 @@ int gsofa_context_create(int32_t device, int64_t mem_budget_bytes, gsofa_context
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  c->stream_blocks = gsofa::stream_max_blocks(device, 1 << 20, 0);
+  c->stream_blocks = gsofa::stream_max_blocks(device, 1 << 20, 0, 0);
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&c->clock_khz, cudaDevAttrClockRate, device);
   c->max_blocks[0] = gsofa::traverse_max_blocks(device, 0);
@@ -508,6 +513,9 @@ void gsofa_context_destroy(gsofa_context *c) {
   if (c->rowptr32) cudaFree(c->rowptr32);
   if (c->bw_dev) cudaFree(c->bw_dev);
   if (c->stage) cudaFree(c->stage);
+  if (c->ord_rec) cudaFree(c->ord_rec);
+  if (c->ord_vert) cudaFree(c->ord_vert);
+  if (c->ord_wkey) cudaFree(c->ord_wkey);
   if (c->h_small) cudaFreeHost(c->h_small);
   host_block_release(c->hpool);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -820,7 +828,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   if (o.row_end < 0) o.row_end = n;
   if (o.chunk_size < 1 || o.row_begin < 0 || o.row_end > n || o.row_begin >= o.row_end ||
       o.max_concurrent < 0 || o.max_concurrent % 32 != 0 ||
-      o.mem_budget_bytes < 0 || o.schedule < 0 || o.schedule > 2) {
+      o.mem_budget_bytes < 0 || o.schedule < 0 || o.schedule > GSOFA_SCHEDULE_HEIGHT) {
     set_detail("bad opts: chunk=%d rows=[%lld,%lld) C=%d budget=%lld", o.chunk_size,
                (long long)o.row_begin, (long long)o.row_end, o.max_concurrent,
                (long long)o.mem_budget_bytes);
@@ -867,6 +875,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   int64_t baseL = 0, baseU = 0, nbatches = 0, maxC = 0;
   Plan plan;
   bool auto_fifo = false;
+  int64_t ord_npos = 0;  // > 0: height order
 
   CK(cudaSetDevice(c->device));
   e_start = ev();
@@ -934,14 +943,42 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     }
     o.schedule = auto_fifo ? GSOFA_SCHEDULE_FIFO : GSOFA_SCHEDULE_THRESHOLD;
   }
+  // ---------------------------------------------------- A2: height order
+  if (o.schedule == GSOFA_SCHEDULE_HEIGHT) {
+    // elimination tree of A + A^T and the (height, id) positions (order.cu);
+    // host computation of the plan, O(nnz alpha)
+    std::vector<int64_t> hrp;
+    std::vector<int32_t> hci;
+    const int64_t *rp_h = rowptr;
+    const int32_t *ci_h = colidx;
+    if (in_dev) {
+      hrp.resize((size_t)n + 1);
+      hci.resize((size_t)std::max<int64_t>(nnz, 1));
+      CK(cudaMemcpyAsync(hrp.data(), rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      if (nnz) CK(cudaMemcpyAsync(hci.data(), colidx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      rp_h = hrp.data();
+      ci_h = hci.data();
+    }
+    std::vector<int32_t> rec, vert, wkey;
+    int32_t hmax = 0;
+    ord_npos = gsofa::height_order(n, rp_h, ci_h, rec, vert, wkey, &hmax);
+    if ((rc = grow_device(&c->ord_rec, &c->ord_rec_cap, rec.size(), st)) != GSOFA_OK) goto fail;
+    if ((rc = grow_device(&c->ord_vert, &c->ord_vert_cap, vert.size(), st)) != GSOFA_OK) goto fail;
+    if ((rc = grow_device(&c->ord_wkey, &c->ord_wkey_cap, wkey.size(), st)) != GSOFA_OK) goto fail;
+    CK(cudaMemcpyAsync(c->ord_rec, rec.data(), rec.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->ord_vert, vert.data(), vert.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->ord_wkey, wkey.data(), wkey.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // the host vectors go out of scope
+  }
   // ---------------------------------------------------- plan + arena
   {
     const int64_t cmax_req =
         o.max_concurrent ? o.max_concurrent : 65536;  // FIFO: one batch when it fits (C3 -6% vs 16k)
     const int64_t budget_req = o.mem_budget_bytes ? o.mem_budget_bytes : c->budget;
-    int64_t key[6] = {o.schedule, n, rb, re, budget_req, cmax_req};
+    int64_t key[7] = {o.schedule, n, rb, re, budget_req, cmax_req, ord_npos};
     bool ok = true;
-    if (std::equal(key, key + 6, c->plan_key)) {
+    if (std::equal(key, key + 7, c->plan_key)) {
       plan = c->plan_cache;
     } else {
       int64_t budget = budget_req;
@@ -949,18 +986,19 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       const int64_t vb_max = std::min<int64_t>(n, re + 32);
       ok = o.schedule == GSOFA_SCHEDULE_FIFO
                ? make_plan(o.schedule, n, rows, vb_max, cmax_req, budget, plan)
-               : make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan);
+               : make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan,
+                                  ord_npos);
       if (!ok && auto_fifo) {
         // AUTO picked FIFO but its smallest batch does not fit: threshold
         // order needs far less memory per source (no maxId labels)
         o.schedule = GSOFA_SCHEDULE_THRESHOLD;
         key[0] = o.schedule;
-        ok = make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan);
+        ok = make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan, 0);
       }
       if (ok && !std::getenv("GSOFA_LIGHT_CTAS") && !std::getenv("GSOFA_SOLO_CTAS") &&
           !std::getenv("GSOFA_SOLO_RING")) {
         c->plan_cache = plan;
-        std::copy(key, key + 6, c->plan_key);
+        std::copy(key, key + 7, c->plan_key);
       }
     }
     const int64_t budget = budget_req;  // (for the message below; 0 = automatic)
@@ -976,7 +1014,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     // the slot layout (Vmax, ws_words) moved: list garbage could now sit
     // under state words, so start from an all-zero work region
     const uint64_t sig = ((uint64_t)plan.Vmax << 32) ^ (uint64_t)plan.ws_words ^
-                         ((uint64_t)plan.light << 48) ^ ((uint64_t)plan.heavy << 40);
+                         ((uint64_t)plan.light << 48) ^ ((uint64_t)plan.heavy << 40) ^
+                         ((uint64_t)plan.hws_words << 8) ^ ((uint64_t)ord_npos << 20);
     if (c->layout_sig != sig && c->work_state == kWorkZero && c->layout_sig != 0) c->work_state = kWorkDirty;
     c->layout_sig = sig;
   }
@@ -1097,6 +1136,12 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.solo_ring = gsofa::solo_ring(plan.Vmax);
     sp.light_slots = (int32_t)plan.light;
     sp.abort_cycles = 0;
+    gsofa::solo_layout(plan.Vmax, n, ord_npos, &sp);
+    sp.hmode = ord_npos > 0;
+    sp.npos = (int32_t)ord_npos;
+    sp.rec = reinterpret_cast<const int4 *>(c->ord_rec);
+    sp.vert = c->ord_vert;
+    sp.wkey = c->ord_wkey;
     if (plan.heavy > 0) {
       // the heaviest groups (top separator / hub rows) start on
       // the solo kernel: one per first-wave solo CTA (one per SM)
@@ -1205,9 +1250,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
           }
       }
       {
-        const size_t Vw = ((Vm + 31) / 32 + 3) & ~(size_t)3, Vs = ((Vw + 31) / 32 + 3) & ~(size_t)3;
-        const size_t nw = (((size_t)n + 31) / 32 + 3) & ~(size_t)3, ns = ((nw + 31) / 32 + 3) & ~(size_t)3;
-        const size_t live = 3 * Vw + 2 * Vs + nw + ns;  // everything but the ring
+        const size_t live = sp.so_queue;  // everything but the ring
         const int64_t nslots = plan.heavy * gsofa::solo_warps_per_cta();
         for (int64_t sl = 0; sl < nslots && reported < 16; ++sl) {
           const uint32_t *b = hw.data() + plan.light * plan.ws_words + sl * plan.hws_words;

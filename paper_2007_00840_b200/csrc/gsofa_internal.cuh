@@ -21,6 +21,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <vector>
 
 namespace gsofa {
 
@@ -91,17 +92,34 @@ struct StreamParams {
   unsigned long long *stats; // items, edges, levels, thresholds, pairs
   long long *group_trace;    // optional [ngroups][8]: steps, levels, items, cycles, ...
   int *debug;                // optional dev checks
+  // processing order of the thresholds (order.cu): hmode = 0: increasing
+  // vertex id (one threshold per step, bitmaps indexed by vertex); hmode = 1:
+  // increasing etree height (all thresholds of one bitmap word -- one height --
+  // per step; threshold bitmaps indexed by position, npos bits)
+  int32_t hmode;
+  int32_t npos;
+  const int4 *rec;           // [n] {rowptr[v], rowptr[v+1], height(v), pos(v)} (hmode 1)
+  const int32_t *vert;       // [npos] position -> vertex, -1 = padding (hmode 1)
+  const int32_t *wkey;       // [npos / 32] height of a bitmap word (hmode 1)
+  // solo slot layout: word offsets of its arrays (solo_layout)
+  uint32_t so_pend, so_thr, so_rsum, so_tsum, so_is, so_isum, so_queue;
 };
-size_t stream_ws_words(int64_t Vmax);
+size_t stream_ws_words(int64_t Vmax, int64_t npos);
 size_t stream_is_words(int64_t n);
-int stream_max_blocks(int device, int64_t Vmax, int heavy);
+int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos);
 int stream_heavy_ratio();  // warps of a solo CTA / warps of a lockstep CTA
 int stream_warps_per_cta();  // lockstep slots (one group per warp) per CTA
-size_t solo_ws_words(int64_t Vmax, int64_t n);  // per solo slot (one warp, one source)
+size_t solo_ws_words(int64_t Vmax, int64_t n, int64_t npos);  // per solo slot (one warp, one source)
+size_t solo_layout(int64_t Vmax, int64_t n, int64_t npos, StreamParams *p);  // + offsets
 int solo_warps_per_cta();
 int solo_ring(int64_t Vmax);
-int stream_light_per_sm_with_solo(int device, int64_t Vmax);
-size_t stream_smem_bytes(int64_t Vmax);  // dynamic smem: threshold-word summary
+int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos);
+size_t stream_smem_bytes(int64_t Vmax, int64_t npos);  // dynamic smem: threshold-word summary
+// order.cu (host): elimination tree of A + A^T and the height order
+void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *parent);
+int64_t height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                     std::vector<int32_t> &rec, std::vector<int32_t> &vert,
+                     std::vector<int32_t> &wkey, int32_t *max_height);
 cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st);
 cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st);
 cudaError_t launch_gather(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,

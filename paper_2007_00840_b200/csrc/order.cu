@@ -1,0 +1,120 @@
+// order.cu -- the processing order of the threshold schedule (plan step A2).
+//
+// The relaxation is confluent: any order that expands a threshold only after
+// every threshold whose closure can reach into its own has the same result
+// (R16, R18).  Increasing vertex id (fill2) is one such
+// order; it makes a source a chain of |L(s,:)| threshold steps.  The
+// elimination tree of the symmetrised pattern A + A^T gives a much
+// shorter one:
+//   * the closure of threshold T (vertices < T reached from T through
+//     unreached vertices < T) lies in the subtree of T: it is connected to T
+//     in G(A+A^T) restricted to {0..T}, and that connected component is the
+//     subtree of T;
+//   * a vertex w > T adjacent to that subtree is an ancestor of T, so every
+//     fill a closure finds is an ancestor of its threshold;
+//   * hence thresholds that are not ancestor-related have disjoint closures,
+//     and processing them by increasing etree HEIGHT (one round per height,
+//     all thresholds of a round together) is exact, with no revisits: a
+//     vertex newly reached in the round of height h is a fill iff its height
+//     exceeds h, otherwise it joins the closure (it is a descendant).
+// Rounds per source drop from |L(s,:)| to at most the tree height (C4's
+// hub rows: 577k -> 4.2k; C5's top separator rows: ~1.5x).
+//
+// The threshold bitmaps of the kernels are indexed by POSITION: vertices
+// sorted by (height, id), each height's segment starting at a multiple of
+// 32, so a bitmap word never mixes two heights.  The plan builds, per
+// vertex, rec[v] = {rowptr[v], rowptr[v+1], height(v), pos(v)}, and per
+// position vert[pos] (-1 in padding) and per bitmap word its height.
+//
+// Host code ("int32 parent[n] ... from the etree of
+// A+A^T, O(nnz alpha)"): Liu's algorithm with path compression.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "gsofa_internal.cuh"
+
+namespace gsofa {
+
+// Elimination tree of A + A^T (parent[v] = -1 for roots) from the CSR of A.
+// Row u's lower entries of A and of A^T (column u of A) are the edges
+// (x, u), x < u, of the symmetrised graph; each links the root of x's
+// current tree under u (Liu's algorithm; `anc` compresses paths).
+void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *parent) {
+  const int64_t nnz = rowptr[n];
+  // lower entries of column u of A, i.e. rows x < u with A(x, u) != 0
+  std::vector<int64_t> cp(n + 1, 0);
+  for (int64_t e = 0; e < nnz; ++e) cp[colidx[e] + 1] += 1;
+  for (int64_t i = 0; i < n; ++i) cp[i + 1] += cp[i];
+  std::vector<int32_t> cr((size_t)std::max<int64_t>(nnz, 1));
+  {
+    std::vector<int64_t> at(cp.begin(), cp.end() - 1);
+    for (int64_t x = 0; x < n; ++x)
+      for (int64_t e = rowptr[x]; e < rowptr[x + 1]; ++e) cr[at[colidx[e]]++] = (int32_t)x;
+  }
+  std::vector<int32_t> anc((size_t)n);
+  for (int64_t u = 0; u < n; ++u) {
+    parent[u] = -1;
+    anc[u] = -1;
+    for (int pass = 0; pass < 2; ++pass) {
+      const int64_t *P = pass ? cp.data() : rowptr;
+      const int32_t *I = pass ? cr.data() : colidx;
+      for (int64_t e = P[u]; e < P[u + 1]; ++e) {
+        int32_t k = I[e];
+        if (k >= u) {
+          if (pass) break;  // column entries ascend: the rest is >= u
+          continue;
+        }
+        while (k != -1 && k != (int32_t)u) {
+          const int32_t nx = anc[k];
+          anc[k] = (int32_t)u;
+          if (nx == -1) parent[k] = (int32_t)u;
+          k = nx;
+        }
+      }
+    }
+  }
+}
+
+// Height order of the vertices (see the header comment).  Outputs:
+//   rec[4n]   {rowptr[v], rowptr[v+1], height(v), pos(v)}   (int4 per vertex)
+//   vert      position -> vertex (-1 in padding), npos entries
+//   wkey      bitmap word -> height of its positions, npos / 32 entries
+// Returns npos (a multiple of 32).
+int64_t height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                     std::vector<int32_t> &rec, std::vector<int32_t> &vert,
+                     std::vector<int32_t> &wkey, int32_t *max_height) {
+  std::vector<int32_t> parent((size_t)n), h((size_t)n, 0);
+  etree_sym(n, rowptr, colidx, parent.data());
+  int32_t H = 0;
+  for (int64_t v = 0; v < n; ++v) {  // parents are larger: one ascending pass
+    if (parent[v] >= 0) h[parent[v]] = std::max(h[parent[v]], h[v] + 1);
+    H = std::max(H, h[v]);
+  }
+  std::vector<int64_t> start((size_t)H + 2, 0);
+  for (int64_t v = 0; v < n; ++v) start[h[v] + 1] += 1;
+  int64_t acc = 0;
+  for (int32_t k = 0; k <= H; ++k) {
+    const int64_t c = start[k + 1];
+    start[k] = acc;
+    acc += (c + 31) / 32 * 32;  // each height's segment starts a bitmap word
+  }
+  const int64_t npos = std::max<int64_t>(acc, 32);
+  vert.assign((size_t)npos, -1);
+  wkey.assign((size_t)(npos / 32), 0);
+  rec.resize((size_t)n * 4);
+  for (int64_t v = 0; v < n; ++v) {
+    const int64_t p = start[h[v]]++;
+    vert[p] = (int32_t)v;
+    wkey[p >> 5] = h[v];
+    rec[4 * v + 0] = (int32_t)rowptr[v];
+    rec[4 * v + 1] = (int32_t)rowptr[v + 1];
+    rec[4 * v + 2] = h[v];
+    rec[4 * v + 3] = (int32_t)p;
+  }
+  *max_height = H;
+  return npos;
+}
+
+}  // namespace gsofa

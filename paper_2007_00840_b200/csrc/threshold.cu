@@ -124,6 +124,10 @@ constexpr int kBatch = 4;  // 32-pair batches whose atomics a warp keeps in flig
 // pend mask (enqueue test); both are issued for kBatch*32 pairs before any
 // result is used.  Every other update is a RED, published by fence_gpu()
 // before the next barrier.
+// Height order (kH): T is the step's etree height; a newly reached w < source
+// is a fill iff height(w) > T (else a closure member), and fills are set at
+// their bitmap position (order.cu).
+template <bool kH>
 __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, int s0g, int T,
                                        int u, uint32_t *nq, int *nqn, int *minfill, int lane,
                                        Counters &c) {
@@ -153,6 +157,7 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
   const int excl = incl - deg;
   for (int f0 = 0; f0 < total; f0 += 32 * kBatch) {
     int w[kBatch];
+    int2 hp[kBatch];  // (height, position) of w (height order), (w, w) in id order
     uint32_t lm[kBatch], ro[kBatch], io[kBatch];
 #pragma unroll
     for (int k = 0; k < kBatch; ++k) {
@@ -175,6 +180,8 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
       // old value.  Both are issued now and consumed below.
       ro[k] = lm[k] ? atomicOr(sl.state + 2 * w[k], lm[k]) : kFull;
       io[k] = um ? atomicOr(sl.is + w[k], um) : kFull;
+      hp[k] = make_int2(w[k], w[k]);
+      if (kH && lm[k]) hp[k] = __ldg(reinterpret_cast<const int2 *>(p.rec + w[k]) + 1);
     }
     bool push[kBatch];
     uint32_t po[kBatch];
@@ -187,15 +194,16 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
       push[k] = false;
       po[k] = kFull;
       if (nw) {
-        if (w[k] > T) {
+        if (hp[k].x > T) {
           // newMaxId T < w: (src, w) is a fill of L (R4); w proposes newMaxId
-          // = w later, as a threshold
+          // = w later, as a threshold (at bitmap position hp.y)
+          const int q = hp[k].y;
           atomicOr(sl.is + w[k], nw);                                           // RED
           atomicOr(sl.isum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));          // RED
           atomicOr(sl.state + 2 * w[k] + 1, nw);                                // RED
-          atomicOr(sl.thr + (w[k] >> 5), 1u << (w[k] & 31));                    // RED
-          atomicOr(sl.tsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));          // smem
-          atomicMin(minfill, w[k]);                                             // smem
+          atomicOr(sl.thr + (q >> 5), 1u << (q & 31));                          // RED
+          atomicOr(sl.tsum + (q >> 10), 1u << ((q >> 5) & 31));                // smem
+          atomicMin(minfill, q);                                                // smem
         } else {
           // w < T: maxId(w) = T, not in the structure: continue with T
           po[k] = atomicOr(sl.state + 2 * w[k] + 1, nw);
@@ -334,12 +342,13 @@ __device__ __forceinline__ void stage_rows(const StreamParams &p, uint32_t *is, 
 // Lockstep kernel: the 32 sources of a group share frontier items (one bit
 // each); a group that runs longer than p.abort_cycles is abandoned -- its
 // slot is cleaned -- and handed to the solo kernel through the heavy queue.
+template <bool kH>
 __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParams p) {
   constexpr int kWarps = kLightWarps;
   constexpr int kThreads = kWarps * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   const int n = p.n, Vmax = p.Vmax;
-  const int tbw_max = (Vmax + 31) >> 5;
+  const int tbw_max = kH ? (p.npos + 31) >> 5 : (Vmax + 31) >> 5;  // threshold bitmap words
   const int rsw = (Vmax + 1023) >> 10;
   Slot sl;
   const size_t slot = blockIdx.x;
@@ -386,7 +395,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
     const int s0g = p.row_begin + 32 * g;
     const int nsrc = min(32, p.row_end - s0g);
     const int Vb = min(n, s0g + nsrc);  // maxId only below the largest source
-    const int tbw = (Vb + 31) >> 5;
+    const int tbw = kH ? tbw_max : (Vb + 31) >> 5;
     for (int i = tid; i < ((tbw + 31) >> 5); i += kThreads) s_tsum[i] = 0u;
     __syncthreads();
 
@@ -403,11 +412,12 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
         atomicOr(sl.isum + (w >> 10), 1u << ((w >> 5) & 31));       // RED
         if (w < s) {
           c.fv += 1;                                                  // first visit of (s, w)
+          const int q = kH ? __ldg(&p.rec[w].w) : w;                  // bitmap position
           atomicOr(sl.state + 2 * w, bit);                            // RED
           atomicOr(sl.rsum + (w >> 10), 1u << ((w >> 5) & 31));       // RED
           atomicOr(sl.state + 2 * w + 1, bit);                        // RED
-          atomicOr(sl.thr + (w >> 5), 1u << (w & 31));                // RED
-          atomicOr(sl.tsum + (w >> 10), 1u << ((w >> 5) & 31));       // smem
+          atomicOr(sl.thr + (q >> 5), 1u << (q & 31));                // RED
+          atomicOr(sl.tsum + (q >> 10), 1u << ((q >> 5) & 31));       // smem
         }
       }
     }
@@ -432,12 +442,23 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
         s_scan[(step + 2) % 3] = INT_MAX;
         s_minfill[(step + 2) % 3] = INT_MAX;
       }
-      // level 0: warp 0 expands T itself; warp 1 finds the next threshold
-      // above T in parallel (new fills of this step go to s_minfill[nx3])
+      const int hT = kH ? __ldg(p.wkey + (T >> 5)) : T;  // the step's height (height order)
+      // level 0: warp 0 expands the step's thresholds -- T itself (id
+      // order), or every threshold of the bitmap word holding position T, all
+      // of one height (height order); warp 1 finds the next threshold after
+      // them in parallel (new fills of this step go to s_minfill[nx3])
       if (warp == 0) {
-        expand(p, sl, s0g, T, lane == 0 ? T : -1, sl.list1, &s_qn[1], &s_minfill[nx3], lane, c);
+        if (kH) {
+          const int word = T >> 5;
+          const uint32_t x = __ldcg(sl.thr + word) & (kFull << (T & 31));
+          const int u = ((x >> lane) & 1u) ? __ldg(p.vert + (word << 5) + lane) : -1;
+          expand<kH>(p, sl, s0g, hT, u, sl.list1, &s_qn[1], &s_minfill[nx3], lane, c);
+        } else {
+          expand<kH>(p, sl, s0g, T, lane == 0 ? T : -1, sl.list1, &s_qn[1], &s_minfill[nx3], lane,
+                     c);
+        }
       } else if (warp == 1) {
-        const int nt = scan_next(sl.thr, sl.tsum, tbw, T, lane);
+        const int nt = scan_next(sl.thr, sl.tsum, tbw, kH ? (T | 31) : T, lane);
         if (lane == 0) s_scan[nx3] = nt;
       }
       __syncthreads();
@@ -459,7 +480,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
         c.levels += 1;
         for (int b0 = warp * 32; b0 < qn; b0 += kThreads) {
           const int u = (b0 + lane < qn) ? (int)cq[b0 + lane] : -1;
-          expand(p, sl, s0g, T, u, nq, &s_qn[nxt], &s_minfill[nx3], lane, c);
+          expand<kH>(p, sl, s0g, hT, u, nq, &s_qn[nxt], &s_minfill[nx3], lane, c);
         }
         __syncthreads();
       }
@@ -485,7 +506,19 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
           x &= x - 1u;
           const int line = (i << 5) + b;
           reinterpret_cast<uint2 *>(sl.state)[(line << 5) + lane] = make_uint2(0u, 0u);
-          if (lane == 0) sl.thr[line] = 0u;
+          if (!kH && lane == 0) sl.thr[line] = 0u;
+        }
+      }
+      if (kH) {
+        // height order: the threshold words are the ones the smem summary lists
+        const int tsw = (tbw + 31) >> 5;
+        for (int i = tid; i < tsw; i += kThreads) {
+          uint32_t x = s_tsum[i];
+          while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1u;
+            sl.thr[(i << 5) + b] = 0u;
+          }
         }
       }
     }
@@ -580,26 +613,16 @@ struct SoloSlot {
   uint32_t *base;
 };
 
-__device__ __forceinline__ size_t solo_vw(const StreamParams &p) {
-  return round4((size_t)((p.Vmax + 31) >> 5));
-}
-__device__ __forceinline__ size_t solo_vs(const StreamParams &p) {
-  return round4((solo_vw(p) + 31) >> 5);
-}
-__device__ __forceinline__ size_t solo_nw(const StreamParams &p) {
-  return round4((size_t)((p.n + 31) >> 5));
-}
-__device__ __forceinline__ size_t solo_ns(const StreamParams &p) {
-  return round4((solo_nw(p) + 31) >> 5);
-}
+// slot offsets (in words) are computed on the host (solo_layout) and read
+// from the kernel parameters: no per-use arithmetic, no registers
 #define SL_REACHED (sl.base)
-#define SL_PEND (sl.base + solo_vw(p))
-#define SL_THR (sl.base + 2 * solo_vw(p))
-#define SL_RSUM (sl.base + 3 * solo_vw(p))
-#define SL_TSUM (sl.base + 3 * solo_vw(p) + solo_vs(p))
-#define SL_IS (sl.base + 3 * solo_vw(p) + 2 * solo_vs(p))
-#define SL_ISUM (SL_IS + solo_nw(p))
-#define SL_QUEUE (SL_ISUM + solo_ns(p))
+#define SL_PEND (sl.base + p.so_pend)
+#define SL_THR (sl.base + p.so_thr)
+#define SL_RSUM (sl.base + p.so_rsum)
+#define SL_TSUM (sl.base + p.so_tsum)
+#define SL_IS (sl.base + p.so_is)
+#define SL_ISUM (sl.base + p.so_isum)
+#define SL_QUEUE (sl.base + p.so_queue)
 #define SL_QMASK (p.solo_ring - 1)
 
 __device__ __forceinline__ SoloSlot solo_slot(const StreamParams &p, size_t slot) {
@@ -663,7 +686,12 @@ __device__ __forceinline__ void red_sum(uint32_t *sum, int v) {
 }
 
 // expand the closure items u (one per lane, -1 = none; beg/end = adjacency)
-// of threshold T of source s
+// of the current step of source s.  Id order (kH = false): the step is one
+// threshold T = h; a newly reached w < s is a fill iff w > T.  Height order
+// (kH = true): the step is a set of thresholds of etree height h; a newly
+// reached w < s is a fill iff height(w) > h, else it joins the closure
+// (order.cu).  Fills are recorded at their bitmap position.
+template <bool kH>
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
                                             SoloWarpSmem &sw, int wb, SoloQueue &Q, int s, int T,
                                             int u, int beg, int end, int lane) {
@@ -693,7 +721,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
   // kSoloBatch batches of 32 (item, neighbour) pairs are in flight at once:
   // all their colidx loads, then all their atomics, then the pushes
   for (int f0 = 0; f0 < total; f0 += 32 * kSoloBatch) {
-    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch];
+    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch], wh[kSoloBatch], wp[kSoloBatch];
     uint32_t ro[kSoloBatch], io[kSoloBatch];
     const int nb = min(kSoloBatch, (total - f0 + 31) >> 5);  // warp-uniform: skip empty batches
 #pragma unroll
@@ -733,8 +761,18 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
         red_sum(SL_ISUM, w[k]);
       }
       // w < T may join the closure: its row pointers travel with the atomic
+      // (height order: its record -- row pointers, height, position)
       rb[k] = re[k] = 0;
-      if (w[k] < T) {
+      wh[k] = wp[k] = w[k];
+      if (kH) {
+        if (w[k] < s) {
+          const int4 r = __ldg(p.rec + w[k]);
+          rb[k] = r.x;
+          re[k] = r.y;
+          wh[k] = r.z;
+          wp[k] = r.w;
+        }
+      } else if (w[k] < T) {
         rb[k] = __ldg(p.rowptr + w[k]);
         re[k] = __ldg(p.rowptr + w[k] + 1);
       }
@@ -753,16 +791,17 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       bool push = false;
       if (!(ro[k] & bw)) {
         if (ro[k] == 0u) red_sum(SL_RSUM, wk);
-        if (wk > T) {
-          // fill of L(s,:) (R4); w becomes a threshold of this source
+        if (wh[k] > T) {
+          // fill of L(s,:) (R4); w becomes a threshold of this source, at
+          // bitmap position wp (its id in id order)
           atomicOr(SL_IS + (wk >> 5), bw);  // RED
           red_sum(SL_ISUM, wk);
-          const int d = (wk >> 5) - wb;
+          const int d = (wp[k] >> 5) - wb;
           if (d < 32) {
-            atomicOr(&sw.win[d], bw);  // smem (d >= 0: w > T >= 32 wb)
+            atomicOr(&sw.win[d], vbit(wp[k]));  // smem (d >= 0: position after the step's)
           } else {
-            atomicOr(SL_THR + (wk >> 5), bw);  // RED
-            red_sum(SL_TSUM, wk);
+            atomicOr(SL_THR + (wp[k] >> 5), vbit(wp[k]));  // RED
+            red_sum(SL_TSUM, wp[k]);
           }
         } else {
           push = true;  // maxId(w) = T, not in the structure: continue with T
@@ -829,10 +868,13 @@ __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const ui
   return t;
 }
 
-// the max-id relaxation of source s in increasing threshold order
+// the max-id relaxation of source s in increasing threshold order (kH:
+// increasing etree height, one bitmap word of same-height thresholds per step)
+template <bool kH>
 __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s,
                                             int lane, SoloWarpSmem &sw) {
-  const int tbw = (s + 31) >> 5;  // thresholds are < s
+  // thresholds are < s (id order) / anywhere in [0, npos) (height order)
+  const int tbw = kH ? (p.npos + 31) >> 5 : (s + 31) >> 5;
   // seed: the out-neighbours of s are in the structure; the
   // smaller ones are reached with maxId -1 and are thresholds
   const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
@@ -846,26 +888,52 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
     if (atomicOr(SL_IS + (w >> 5), bw) == 0u) red_sum(SL_ISUM, w);
     if (w < s) {
       if (atomicOr(SL_REACHED + (w >> 5), bw) == 0u) red_sum(SL_RSUM, w);
-      atomicOr(SL_THR + (w >> 5), bw);  // RED
-      red_sum(SL_TSUM, w);
+      const int pw = kH ? __ldg(&p.rec[w].w) : w;  // bitmap position
+      atomicOr(SL_THR + (pw >> 5), vbit(pw));  // RED
+      red_sum(SL_TSUM, pw);
     }
   }
   __syncwarp();
   int wb = -1;  // no window yet
-  int T = -1;
+  int P = -1;   // position of the last threshold taken
   for (;;) {
-    T = solo_next_threshold(SL_THR, SL_TSUM, tbw, T, wb, sw, lane);
-    if (T == INT_MAX) break;
+    P = solo_next_threshold(SL_THR, SL_TSUM, tbw, P, wb, sw, lane);
+    if (P == INT_MAX) break;
     if (lane == 0) sw.steps += 1;
     SoloQueue Q = {0, 0, 0, 0, false};
-    int u = -1, ub = 0, ue = 0;
-    if (lane == 0) {
-      u = T;
-      ub = __ldg(p.rowptr + T);
-      ue = __ldg(p.rowptr + T + 1);
+    int u = -1, ub = 0, ue = 0, T;
+    if (kH) {
+      // the step: every threshold of the window word holding P at or after P
+      // (a word holds one height: segments are word-aligned), one per lane
+      const int word = P >> 5;
+      const uint32_t x = sw.win[word - wb] & (kFull << (P & 31));
+      T = __ldg(p.wkey + word);  // the round's height
+      if ((x >> lane) & 1u) {
+        u = __ldg(p.vert + (word << 5) + lane);
+        const int4 r = __ldg(p.rec + u);
+        ub = r.x;
+        ue = r.y;
+      }
+      // compact the items to the low lanes (the single-item fast path)
+      const uint32_t b = __ballot_sync(kFull, u >= 0);
+      const int src = __fns(b, 0, lane + 1);
+      const int cu = __shfl_sync(kFull, u, src & 31), cb = __shfl_sync(kFull, ub, src & 31),
+                ce = __shfl_sync(kFull, ue, src & 31);
+      const bool ok = lane < __popc(b);
+      u = ok ? cu : -1;
+      ub = ok ? cb : 0;
+      ue = ok ? ce : 0;
+      P = (word << 5) + 31;  // the next step starts after this word
+    } else {
+      T = P;
+      if (lane == 0) {
+        u = T;
+        ub = __ldg(p.rowptr + T);
+        ue = __ldg(p.rowptr + T + 1);
+      }
     }
     for (;;) {
-      solo_expand(p, sl, sw, wb, Q, s, T, u, ub, ue, lane);
+      solo_expand<kH>(p, sl, sw, wb, Q, s, T, u, ub, ue, lane);
       __syncwarp();
       if (Q.sh < Q.st) {
         const int cnt = min(32, Q.st - Q.sh);
@@ -886,9 +954,10 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
         Q.spilled = false;
         __syncwarp();
         fence_gpu();
-        for (int w0 = 0; w0 < ((T + 31) >> 5) && !Q.spilled; w0 += 32) {
+        const int pwords = kH ? (s + 31) >> 5 : (T + 31) >> 5;  // closure vertices are below
+        for (int w0 = 0; w0 < pwords && !Q.spilled; w0 += 32) {
           const int wi = w0 + lane;
-          uint32_t x = wi < ((T + 31) >> 5) ? __ldcg(SL_PEND + wi) : 0u;
+          uint32_t x = wi < pwords ? __ldcg(SL_PEND + wi) : 0u;
           for (;;) {
             const bool has = x != 0u;
             const uint32_t hb = __ballot_sync(kFull, has);
@@ -1022,6 +1091,7 @@ __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const Solo
 // against 32 warps / 64 registers and 64 warps / 32 registers
 #define GSOFA_SOLO_MINB (48 / kSoloWarps)
 #endif
+template <bool kH>
 __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(StreamParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rows = p.row_end - p.row_begin;
@@ -1072,17 +1142,18 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
     if (g < 0) break;
     const int s = p.row_begin + 32 * g + k;
     if (s >= p.row_end) continue;  // tail of the last group
-    solo_source(p, sl, s, lane, sw);
+    solo_source<kH>(p, sl, s, lane, sw);
     fence_gpu();  // this warp's REDs are visible to its extraction
     __syncwarp();
     solo_stage_row(p, sl, s, g, lane);
-    // reset the touched words: reached | pend | thr, and the summaries
+    // reset the touched words: reached | pend (| thr in id order, where a
+    // threshold bit sits in the word of its reached bit), and the summaries
     for (int i0 = 0; i0 < Vs; i0 += 32) {
       const int i = i0 + lane;
       uint32_t x = i < Vs ? __ldcg(SL_RSUM + i) : 0u;
       if (x) {
         SL_RSUM[i] = 0u;
-        SL_TSUM[i] = 0u;
+        if (!kH) SL_TSUM[i] = 0u;
       }
       while (x) {
         const int b = __ffs(x) - 1;
@@ -1090,7 +1161,22 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
         const int wi = (i << 5) + b;
         SL_REACHED[wi] = 0u;
         SL_PEND[wi] = 0u;
-        SL_THR[wi] = 0u;
+        if (!kH) SL_THR[wi] = 0u;
+      }
+    }
+    if (kH) {
+      // height order: threshold bits live at positions; the summary lists
+      // every global word written (window bits never reach global memory)
+      const int Ts = (int)(p.so_is - p.so_tsum);
+      for (int i0 = 0; i0 < Ts; i0 += 32) {
+        const int i = i0 + lane;
+        uint32_t x = i < Ts ? __ldcg(SL_TSUM + i) : 0u;
+        if (x) SL_TSUM[i] = 0u;
+        while (x) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1u;
+          SL_THR[(i << 5) + b] = 0u;
+        }
       }
     }
     // the clears are plain stores; the next source's atomics act at L2
@@ -1127,8 +1213,10 @@ __global__ void gather_kernel(const int32_t *stage, const int64_t *row_off, cons
 }
 }  // namespace
 
-size_t stream_ws_words(int64_t Vmax) {
-  const size_t w = 2 * (size_t)Vmax + (size_t)((Vmax + 31) / 32) + (size_t)((Vmax + 1023) / 1024) +
+// npos > 0: height order (threshold bitmap over npos positions)
+size_t stream_ws_words(int64_t Vmax, int64_t npos) {
+  const int64_t tb = npos > 0 ? npos : Vmax;
+  const size_t w = 2 * (size_t)Vmax + (size_t)((tb + 31) / 32) + (size_t)((Vmax + 1023) / 1024) +
                    2 * (size_t)Vmax;
   return (w + 7) / 8 * 8;
 }
@@ -1138,23 +1226,33 @@ size_t stream_is_words(int64_t n) {
   return (w + 7) / 8 * 8;
 }
 
-size_t stream_smem_bytes(int64_t Vmax) {
-  return (size_t)((((Vmax + 31) / 32) + 31) / 32) * 4;
+size_t stream_smem_bytes(int64_t Vmax, int64_t npos) {
+  const int64_t tb = npos > 0 ? npos : Vmax;
+  return (size_t)((((tb + 31) / 32) + 31) / 32) * 4;
 }
 
-int stream_max_blocks(int device, int64_t Vmax, int heavy) {
+// kernel instances of the two threshold orders (kH = height order)
+const void *stream_fn(bool h) {
+  return h ? (const void *)stream_kernel<true> : (const void *)stream_kernel<false>;
+}
+const void *solo_fn(bool h) {
+  return h ? (const void *)solo_kernel<true> : (const void *)solo_kernel<false>;
+}
+
+int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos) {
   int sms = 0, per = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
   cudaError_t e;
+  const bool h = npos > 0;
   if (heavy) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solo_kernel, kSoloWarps * 32, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solo_fn(h), kSoloWarps * 32, 0);
   } else {
-    const size_t smem = stream_smem_bytes(Vmax);
+    const size_t smem = stream_smem_bytes(Vmax, npos);
     if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaFuncSetAttribute(stream_fn(h), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
       return 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_kernel, kLightWarps * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_fn(h), kLightWarps * 32, smem);
   }
   if (e != cudaSuccess) return 0;
   return sms * per;
@@ -1165,10 +1263,11 @@ int stream_heavy_ratio() { return kSoloWarps / kLightWarps; }
 int stream_warps_per_cta() { return 1; }  // slots are CTAs
 
 // lockstep CTAs that still fit on an SM next to one solo CTA
-int stream_light_per_sm_with_solo(int device, int64_t Vmax) {
+int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos) {
   cudaFuncAttributes fs, fl;
-  if (cudaFuncGetAttributes(&fs, solo_kernel) != cudaSuccess ||
-      cudaFuncGetAttributes(&fl, stream_kernel) != cudaSuccess)
+  const bool h = npos > 0;
+  if (cudaFuncGetAttributes(&fs, solo_fn(h)) != cudaSuccess ||
+      cudaFuncGetAttributes(&fl, stream_fn(h)) != cudaSuccess)
     return 0;
   int regs = 0, warps = 0, smem_sm = 0;
   cudaDeviceGetAttribute(&regs, cudaDevAttrMaxRegistersPerMultiprocessor, device);
@@ -1179,7 +1278,7 @@ int stream_light_per_sm_with_solo(int device, int64_t Vmax) {
   const int light_regs = ((fl.numRegs * 32 + 255) / 256 * 256) * kLightWarps;
   const int by_regs = (regs - solo_regs) / light_regs;
   const int by_warps = (warps - kSoloWarps) / kLightWarps;
-  const size_t light_smem = fl.sharedSizeBytes + stream_smem_bytes(Vmax) + 1024;
+  const size_t light_smem = fl.sharedSizeBytes + stream_smem_bytes(Vmax, npos) + 1024;
   const int by_smem = (int)((smem_sm - fs.sharedSizeBytes - 1024) / light_smem);
   return std::max(0, std::min(std::min(by_regs, by_warps), by_smem));
 }
@@ -1196,30 +1295,48 @@ int solo_ring(int64_t Vmax) {
   return r;
 }
 
-size_t solo_ws_words(int64_t Vmax, int64_t n) {
+// solo slot layout (words): reached, pend [Vw] (bitmaps over [0, Vmax));
+// thr [Tw] (over vertices, or positions in height order); rsum [Vs], tsum
+// [Ts] (summaries: one bit per word); is [nw], isum [ns] (structure over
+// [0, n)); the closure ring.  npos > 0: height order.  Returns the total.
+size_t solo_layout(int64_t Vmax, int64_t n, int64_t npos, StreamParams *p) {
   const size_t Vw = round4((size_t)((Vmax + 31) / 32)), Vs = round4((Vw + 31) / 32);
+  const size_t Tw = npos > 0 ? round4((size_t)((npos + 31) / 32)) : Vw, Ts = round4((Tw + 31) / 32);
   const size_t nw = round4((size_t)((n + 31) / 32)), ns = round4((nw + 31) / 32);
-  const size_t w = 3 * Vw + 2 * Vs + nw + ns + (size_t)solo_ring(Vmax);
+  if (p) {
+    p->so_pend = (uint32_t)Vw;
+    p->so_thr = (uint32_t)(2 * Vw);
+    p->so_rsum = (uint32_t)(2 * Vw + Tw);
+    p->so_tsum = p->so_rsum + (uint32_t)Vs;
+    p->so_is = p->so_tsum + (uint32_t)Ts;
+    p->so_isum = p->so_is + (uint32_t)nw;
+    p->so_queue = p->so_isum + (uint32_t)ns;
+  }
+  const size_t w = 2 * Vw + Tw + Vs + Ts + nw + ns + (size_t)solo_ring(Vmax);
   return (w + 7) / 8 * 8;
 }
+
+size_t solo_ws_words(int64_t Vmax, int64_t n, int64_t npos) { return solo_layout(Vmax, n, npos, nullptr); }
 
 int solo_warps_per_cta() { return kSoloWarps; }
 
 cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st) {
   if (grid <= 0) return cudaSuccess;
-  const size_t smem = stream_smem_bytes(p.Vmax);
+  const size_t smem = stream_smem_bytes(p.Vmax, p.hmode ? p.npos : 0);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(stream_fn(p.hmode), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  stream_kernel<<<grid, kLightWarps * 32, smem, st>>>(p);
+  if (p.hmode) stream_kernel<true><<<grid, kLightWarps * 32, smem, st>>>(p);
+  else stream_kernel<false><<<grid, kLightWarps * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st) {
   if (grid <= 0) return cudaSuccess;
-  solo_kernel<<<grid, kSoloWarps * 32, 0, st>>>(p);
+  if (p.hmode) solo_kernel<true><<<grid, kSoloWarps * 32, 0, st>>>(p);
+  else solo_kernel<false><<<grid, kSoloWarps * 32, 0, st>>>(p);
   return cudaGetLastError();
 }
 

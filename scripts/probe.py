@@ -14,7 +14,7 @@ ap.add_argument("--scale", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--C", type=int, default=0)
 ap.add_argument("--fill-first", action="store_true")
-ap.add_argument("--schedule", default="auto", choices=["auto", "threshold", "fifo"])
+ap.add_argument("--schedule", default="auto", choices=["auto", "threshold", "fifo", "height"])
 ap.add_argument("--rows", type=str, default=None, help="row range b:e")
 a = ap.parse_args()
 t = time.time()

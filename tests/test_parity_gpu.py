@@ -55,7 +55,7 @@ def test_paper_example(ctx, schedule):
     assert_full_equal(run(rp, ci, ctx, schedule=schedule), oracle.symbolic(rp, ci))
 
 
-@pytest.mark.parametrize("schedule", ["threshold", "fifo"])
+@pytest.mark.parametrize("schedule", ["threshold", "fifo", "height"])
 @pytest.mark.parametrize("seed", range(40))
 def test_random_graphs(ctx, seed, schedule):
     rng = np.random.default_rng(seed)
@@ -73,7 +73,8 @@ def test_config_shapes_full(ctx, name, scale):
     rp, ci = gen.config(name, scale)
     want = oracle.symbolic(rp, ci)
     for kw in (dict(), dict(max_concurrent=32), dict(schedule="fifo"),
-               dict(schedule="fifo", fill_first=True, max_concurrent=96)):
+               dict(schedule="fifo", fill_first=True, max_concurrent=96),
+               dict(schedule="height"), dict(schedule="height", max_concurrent=32)):
         assert_full_equal(run(rp, ci, ctx, **kw), want, tag=f"{name}-{scale} {kw}")
 
 
@@ -242,12 +243,14 @@ def test_errors():
 def test_full_config_exact(ctx, name):
     """Full BASELINE configs C2 (n=262,144) and C4 (n=1,585,478): every array
     (L/U row pointers and columns, sn_start) and every count byte-compared
-    with the oracle's whole-matrix result (the 16-core oracle takes ~5-7 s)."""
+    with the oracle's whole-matrix result (the 16-core oracle takes ~5-7 s),
+    for the default schedule and for each threshold order."""
     rp, ci = gen.config(name)
-    got = run(rp, ci, ctx)
     want = oracle.symbolic(rp, ci)
-    assert_full_equal(got, want, tag=name)
-    assert got["nnz_A_offdiag"] == ci.size
+    for sched in ("auto", "threshold", "height"):
+        got = run(rp, ci, ctx, schedule=sched)
+        assert_full_equal(got, want, tag=f"{name} {sched}")
+        assert got["nnz_A_offdiag"] == ci.size
 
 
 def _blocks_by_entries(rowptr_sum, max_entries):
@@ -302,8 +305,9 @@ def test_full_C5_exact(ctx):
 # kernel: lockstep-only, every group handed to the solo kernel, and repeated
 # calls on one context (the workspace must be left clean by every group)
 
+@pytest.mark.parametrize("schedule", ["threshold", "height"])
 @pytest.mark.parametrize("mode", ["default", "lockstep_only", "all_solo"])
-def test_stream_paths_repeated(mode, monkeypatch):
+def test_stream_paths_repeated(mode, schedule, monkeypatch):
     if mode == "lockstep_only":
         monkeypatch.setenv("GSOFA_SOLO_CTAS", "0")
     if mode == "all_solo":
@@ -313,7 +317,8 @@ def test_stream_paths_repeated(mode, monkeypatch):
     with g.Context(0) as c:
         for rep in range(3):
             for (rp, ci), want in zip(cases, wants):
-                assert_full_equal(run(rp, ci, c), want, tag=f"{mode} rep {rep} n={rp.size - 1}")
+                assert_full_equal(run(rp, ci, c, schedule=schedule), want,
+                                  tag=f"{mode} {schedule} rep {rep} n={rp.size - 1}")
 
 
 @pytest.mark.parametrize("knobs", [
@@ -332,7 +337,10 @@ def test_overflow_paths(knobs, monkeypatch):
     cases = [gen.config("C5", 16), gen.config("C4", 70), gen.config("C3", 3000), gen.config("C2", 20)]
     with g.Context(0) as c:
         for rp, ci in cases:
-            assert_full_equal(run(rp, ci, c), oracle.symbolic(rp, ci), tag=f"{knobs} n={rp.size - 1}")
+            want = oracle.symbolic(rp, ci)
+            for sched in ("threshold", "height"):
+                assert_full_equal(run(rp, ci, c, schedule=sched), want,
+                                  tag=f"{knobs} {sched} n={rp.size - 1}")
 
 
 def _csc_of_rows(Lp, Li, row_begin, n):
@@ -464,7 +472,7 @@ def test_randomized_sweep(ctx):
             rp, ci = g.permute(rp, ci, rng.permutation(n).astype(np.int32))
         rb = int(rng.integers(0, n))
         re = int(rng.integers(rb + 1, n + 1))
-        sched = str(rng.choice(["threshold", "fifo", "auto"]))
+        sched = str(rng.choice(["threshold", "fifo", "auto", "height"]))
         chunk = int(rng.choice([1, 7, 64, 128]))
         got = run(rp, ci, ctx, row_begin=rb, row_end=re, schedule=sched, chunk_size=chunk,
                   checked=True)
@@ -492,3 +500,7 @@ def test_visit_stats(ctx, name, scale, monkeypatch):
     assert f["first_visits"] == t["first_visits"]
     assert f["source_expansions"] >= f["first_visits"]
     assert f["edge_inspections"] >= t["edge_inspections"]
+    h = run(rp, ci, ctx, schedule="height")["stats"]   # etree-height order: no revisits either
+    assert h["first_visits"] == t["first_visits"]
+    assert h["source_expansions"] == h["first_visits"]
+    assert h["edge_inspections"] == t["edge_inspections"]

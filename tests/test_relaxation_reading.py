@@ -115,3 +115,112 @@ def test_relaxation_reaches_oracle(seed):
                 got = relax_source(rp, ci, src, fill_first=ff, jacobi=jac,
                                    rng=np.random.default_rng(seed * 131 + src))
                 assert got == want, (src, ff, jac)
+
+
+# ---------------------------------------------------------------- R18
+# Height order (GSOFA_SCHEDULE_HEIGHT, csrc/order.cu): thresholds are
+# processed by increasing height in the elimination tree of A + A^T,
+# all thresholds of one height in the same round; a vertex newly reached in
+# the round of height h is a fill iff its height exceeds h, else it joins the
+# round's closure.  Test-side model in plain Python (its own etree from the
+# definition parent(v) = min{u > v : u adjacent to the component of v in
+# G(A+A^T) restricted to {0..v}}), checked against the oracle.
+
+def etree_by_definition(rp, ci):
+    n = rp.size - 1
+    adj = [set() for _ in range(n)]
+    for i in range(n):
+        for j in ci[rp[i]:rp[i + 1]].tolist():
+            if j != i:
+                adj[i].add(j)
+                adj[j].add(i)
+    parent = [-1] * n
+    for v in range(n):
+        comp, stack = {v}, [v]          # component of v in G[{0..v}]
+        while stack:
+            x = stack.pop()
+            for y in adj[x]:
+                if y <= v and y not in comp:
+                    comp.add(y)
+                    stack.append(y)
+        higher = [u for x in comp for u in adj[x] if u > v]
+        parent[v] = min(higher) if higher else -1
+    height = [0] * n
+    for v in range(n):
+        if parent[v] >= 0:
+            height[parent[v]] = max(height[parent[v]], height[v] + 1)
+    return parent, height
+
+
+def height_order_source(rp, ci, src, height, rounds=None):
+    n = rp.size - 1
+    reached = {src}
+    instruct = set()
+    bucket = {}
+    for w in ci[rp[src]:rp[src + 1]].tolist():
+        if w == src:
+            continue
+        instruct.add(w)
+        if w < src:
+            reached.add(w)
+            bucket.setdefault(height[w], set()).add(w)
+    nround = 0
+    while bucket:
+        h = min(bucket)
+        frontier = sorted(bucket.pop(h))
+        nround += 1
+        while frontier:
+            nxt = []
+            for u in frontier:
+                for w in ci[rp[u]:rp[u + 1]].tolist():
+                    if w == src:
+                        continue
+                    if w > src:
+                        instruct.add(w)
+                        continue
+                    if w in reached:
+                        continue
+                    reached.add(w)
+                    assert height[w] != h        # neither ancestor nor descendant: impossible
+                    if height[w] > h:            # an ancestor of its threshold: fill
+                        assert height[w] > h
+                        instruct.add(w)
+                        bucket.setdefault(height[w], set()).add(w)
+                    else:                        # a descendant: the round's closure
+                        nxt.append(w)
+            frontier = nxt
+    if rounds is not None:
+        rounds.append(nround)
+    return sorted(instruct)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_height_order_reaches_oracle(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(8, 80))
+    rp, ci = gen.random_graph(n, float(rng.uniform(0.02, 0.25)), seed=9100 + seed)
+    _, height = etree_by_definition(rp, ci)
+    r = oracle.rows(rp, ci)
+    for src in range(n):
+        want = sorted(set(r["L_colidx"][r["L_rowptr"][src]:r["L_rowptr"][src + 1]].tolist())
+                      | set(r["U_colidx"][r["U_rowptr"][src] + 1:r["U_rowptr"][src + 1]].tolist()))
+        assert height_order_source(rp, ci, src, height) == want, src
+
+
+@pytest.mark.parametrize("name,scale", [("C4", 20), ("C5", 7), ("C2", 8)])
+def test_height_order_rounds_on_grid(name, scale):
+    """On nested-dissection grids the top rows need fewer rounds in height
+    order than their threshold counts |L(s,:)| (the chain of id order), with
+    the same structure."""
+    rp, ci = gen.config(name, scale)
+    n = rp.size - 1
+    _, height = etree_by_definition(rp, ci)
+    r = oracle.rows(rp, ci, np.array([n - 1], np.int64))
+    rounds = []
+    got = height_order_source(rp, ci, n - 1, height, rounds)
+    want = sorted(set(r["L_colidx"].tolist()) | set(r["U_colidx"][1:].tolist()))
+    assert got == want
+    nL = int(r["L_rowptr"][1])
+    assert rounds[0] <= nL                 # every round takes at least one threshold
+    if name == "C4":
+        assert rounds[0] < nL / 2          # 2D ND: a bushy tree
