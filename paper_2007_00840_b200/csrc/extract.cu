@@ -21,25 +21,7 @@ constexpr int kSub = 2048;            // columns per warp unit
 constexpr int kTilesPerSub = kSub / 32;
 constexpr int kWarpsPerBlock = 4;
 
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-  // Row `lane` of a 32x32 bit matrix in, column `lane` out (bit j of the
-  // result = bit `lane` of row j): swap off-diagonal blocks at widths 16..1.
-  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    const int j = 16 >> i;
-    const uint32_t m = masks[i];
-    const uint32_t y = __shfl_xor_sync(kFull, x, j);
-    x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
-  }
-  return x;
-}
 
-__device__ __forceinline__ void split_masks(int d, uint32_t &lm, uint32_t &um) {
-  // columns v0 + i with i < d are in L, i > d in U (d = s - v0)
-  lm = d <= 0 ? 0u : (d >= 32 ? kFull : ((1u << d) - 1u));
-  um = d < 0 ? kFull : (d >= 31 ? 0u : (kFull << (d + 1)));
-}
 
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) extract_count_kernel(ExtractParams e) {
   const int lane = threadIdx.x & 31;

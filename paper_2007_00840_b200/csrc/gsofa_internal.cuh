@@ -186,6 +186,27 @@ cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, i
                                      cudaStream_t st);
 
 // ------------------------------------------------------------- helpers
+// Row `lane` of a 32x32 bit matrix in, column `lane` out (bit j of the result
+// = bit `lane` of row j): swap off-diagonal blocks at widths 16..1
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int j = 16 >> i;
+    const uint32_t m = masks[i];
+    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
+
+// bits of a 32-column word below / above column d (d = source - first column):
+// lm = columns < d (entries of L), um = columns > d (entries of U)
+__device__ __forceinline__ void split_masks(int d, uint32_t &lm, uint32_t &um) {
+  lm = d <= 0 ? 0u : (d >= 32 ? 0xFFFFFFFFu : ((1u << d) - 1u));
+  um = d < 0 ? 0xFFFFFFFFu : (d >= 31 ? 0u : (0xFFFFFFFFu << (d + 1)));
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

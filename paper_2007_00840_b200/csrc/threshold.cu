@@ -52,22 +52,7 @@ __device__ __forceinline__ uint32_t lanes_below(int w, int s0g) {
   return kFull >> (32 - d);
 }
 
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    const int j = 16 >> i;
-    const uint32_t m = masks[i];
-    const uint32_t y = __shfl_xor_sync(kFull, x, j);
-    x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
-  }
-  return x;
-}
 
-__device__ __forceinline__ void split_masks(int d, uint32_t &lm, uint32_t &um) {
-  lm = d <= 0 ? 0u : (d >= 32 ? kFull : ((1u << d) - 1u));
-  um = d < 0 ? kFull : (d >= 31 ? 0u : (kFull << (d + 1)));
-}
 
 struct Slot {
   uint32_t *state, *thr, *rsum, *list0, *list1, *is, *isum;
