@@ -136,9 +136,12 @@ struct gsofa_context {
   int32_t *in_colidx = nullptr, *rowptr32 = nullptr;
   size_t in_rowptr_cap = 0, in_colidx_cap = 0, rowptr32_cap = 0;
   int64_t *h_small = nullptr;  // pinned host scratch
-  // height order (order.cu): per-vertex records, position -> vertex, word heights
-  int32_t *ord_rec = nullptr, *ord_vert = nullptr, *ord_wkey = nullptr;
-  size_t ord_rec_cap = 0, ord_vert_cap = 0, ord_wkey_cap = 0;
+  // height order (order.cu): one grow-only buffer for the positions, their
+  // inverse, word heights, segment bounds and the relabelled graph
+  int32_t *ord_buf = nullptr;
+  size_t ord_cap = 0;
+  int32_t *ord_pos = nullptr, *ord_vert = nullptr, *ord_wkey = nullptr, *ord_seg = nullptr;
+  int32_t *ord_rowptrP = nullptr, *ord_colidxP = nullptr;
   HostBlock *hpool = nullptr;  // pinned storage reused by host-side results
 };
 
@@ -221,8 +224,9 @@ bool make_plan(int schedule, int64_t n, int64_t rows, int64_t vb_max, int64_t cm
 // npos > 0: height order (threshold bitmaps over npos positions, order.cu)
 bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int device, Plan &p,
                       int64_t npos) {
-  if (gsofa::stream_smem_bytes(Vmax, npos) > 200 * 1024) return false;
-  const size_t ws = gsofa::stream_ws_words(Vmax, npos), isw = gsofa::stream_is_words(n);
+  // the lockstep kernel runs id order (its slots do not depend on npos)
+  if (gsofa::stream_smem_bytes(Vmax, 0) > 200 * 1024) return false;
+  const size_t ws = gsofa::stream_ws_words(Vmax, 0), isw = gsofa::stream_is_words(n);
   const size_t hws = gsofa::solo_ws_words(Vmax, n, npos);
   const int64_t spc = gsofa::solo_warps_per_cta();
   const size_t per_light = (ws + isw) * 4, per_heavy = hws * 4 * (size_t)spc;  // per solo CTA
@@ -513,9 +517,7 @@ void gsofa_context_destroy(gsofa_context *c) {
   if (c->rowptr32) cudaFree(c->rowptr32);
   if (c->bw_dev) cudaFree(c->bw_dev);
   if (c->stage) cudaFree(c->stage);
-  if (c->ord_rec) cudaFree(c->ord_rec);
-  if (c->ord_vert) cudaFree(c->ord_vert);
-  if (c->ord_wkey) cudaFree(c->ord_wkey);
+  if (c->ord_buf) cudaFree(c->ord_buf);
   if (c->h_small) cudaFreeHost(c->h_small);
   host_block_release(c->hpool);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -946,7 +948,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   // ---------------------------------------------------- A2: height order
   if (o.schedule == GSOFA_SCHEDULE_HEIGHT) {
     // elimination tree of A + A^T and the (height, id) positions (order.cu);
-    // host computation of the plan, O(nnz alpha)
+    // host computation of the plan, O(nnz alpha); then
+    // the graph relabelled to positions on the GPU
     std::vector<int64_t> hrp;
     std::vector<int32_t> hci;
     const int64_t *rp_h = rowptr;
@@ -960,15 +963,32 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       rp_h = hrp.data();
       ci_h = hci.data();
     }
-    std::vector<int32_t> rec, vert, wkey;
-    int32_t hmax = 0;
-    ord_npos = gsofa::height_order(n, rp_h, ci_h, rec, vert, wkey, &hmax);
-    if ((rc = grow_device(&c->ord_rec, &c->ord_rec_cap, rec.size(), st)) != GSOFA_OK) goto fail;
-    if ((rc = grow_device(&c->ord_vert, &c->ord_vert_cap, vert.size(), st)) != GSOFA_OK) goto fail;
-    if ((rc = grow_device(&c->ord_wkey, &c->ord_wkey_cap, wkey.size(), st)) != GSOFA_OK) goto fail;
-    CK(cudaMemcpyAsync(c->ord_rec, rec.data(), rec.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->ord_vert, vert.data(), vert.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->ord_wkey, wkey.data(), wkey.size() * 4, cudaMemcpyHostToDevice, st));
+    std::vector<int32_t> hpos, hvert, hwkey, hseg;
+    ord_npos = gsofa::height_order(n, rp_h, ci_h, hpos, hvert, hwkey, hseg);
+    const size_t tmpb = gsofa::relabel_tmp_bytes(ord_npos);
+    const size_t need = (size_t)n + 2 * (size_t)ord_npos + hwkey.size() + hseg.size() + 1 +
+                        (size_t)std::max<int64_t>(nnz, 1) + tmpb / 4 + 256;
+    if ((rc = grow_device(&c->ord_buf, &c->ord_cap, need, st)) != GSOFA_OK) goto fail;
+    int32_t *q = c->ord_buf;
+    auto take = [&](size_t words) {
+      int32_t *r = q;
+      q += (words + 63) / 64 * 64;
+      return r;
+    };
+    c->ord_pos = take(n);
+    c->ord_vert = take(ord_npos);
+    c->ord_wkey = take(hwkey.size());
+    c->ord_seg = take(hseg.size());
+    c->ord_rowptrP = take(ord_npos + 1);
+    c->ord_colidxP = take(std::max<int64_t>(nnz, 1));
+    void *tmp = take(tmpb / 4 + 1);
+    CK(cudaMemcpyAsync(c->ord_pos, hpos.data(), hpos.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->ord_vert, hvert.data(), hvert.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->ord_wkey, hwkey.data(), hwkey.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->ord_seg, hseg.data(), hseg.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(gsofa::launch_relabel(c->rowptr32, d_colidx, c->ord_pos, n, ord_npos, c->ord_rowptrP,
+                             c->ord_colidxP, tmp, tmpb + 4, st));
+    launches += 4;
     CK(cudaStreamSynchronize(st));  // the host vectors go out of scope
   }
   // ---------------------------------------------------- plan + arena
@@ -1139,9 +1159,12 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     gsofa::solo_layout(plan.Vmax, n, ord_npos, &sp);
     sp.hmode = ord_npos > 0;
     sp.npos = (int32_t)ord_npos;
-    sp.rec = reinterpret_cast<const int4 *>(c->ord_rec);
+    sp.rowptrP = c->ord_rowptrP;
+    sp.colidxP = c->ord_colidxP;
+    sp.pos = c->ord_pos;
     sp.vert = c->ord_vert;
     sp.wkey = c->ord_wkey;
+    sp.seg = c->ord_seg;
     if (plan.heavy > 0) {
       // the heaviest groups (top separator / hub rows) start on
       // the solo kernel: one per first-wave solo CTA (one per SM)

@@ -109,10 +109,6 @@ constexpr int kBatch = 4;  // 32-pair batches whose atomics a warp keeps in flig
 // pend mask (enqueue test); both are issued for kBatch*32 pairs before any
 // result is used.  Every other update is a RED, published by fence_gpu()
 // before the next barrier.
-// Height order (kH): T is the step's etree height; a newly reached w < source
-// is a fill iff height(w) > T (else a closure member), and fills are set at
-// their bitmap position (order.cu).
-template <bool kH>
 __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, int s0g, int T,
                                        int u, uint32_t *nq, int *nqn, int *minfill, int lane,
                                        Counters &c) {
@@ -142,7 +138,6 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
   const int excl = incl - deg;
   for (int f0 = 0; f0 < total; f0 += 32 * kBatch) {
     int w[kBatch];
-    int2 hp[kBatch];  // (height, position) of w (height order), (w, w) in id order
     uint32_t lm[kBatch], ro[kBatch], io[kBatch];
 #pragma unroll
     for (int k = 0; k < kBatch; ++k) {
@@ -165,8 +160,6 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
       // old value.  Both are issued now and consumed below.
       ro[k] = lm[k] ? atomicOr(sl.state + 2 * w[k], lm[k]) : kFull;
       io[k] = um ? atomicOr(sl.is + w[k], um) : kFull;
-      hp[k] = make_int2(w[k], w[k]);
-      if (kH && lm[k]) hp[k] = __ldg(reinterpret_cast<const int2 *>(p.rec + w[k]) + 1);
     }
     bool push[kBatch];
     uint32_t po[kBatch];
@@ -179,16 +172,15 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
       push[k] = false;
       po[k] = kFull;
       if (nw) {
-        if (hp[k].x > T) {
+        if (w[k] > T) {
           // newMaxId T < w: (src, w) is a fill of L (R4); w proposes newMaxId
-          // = w later, as a threshold (at bitmap position hp.y)
-          const int q = hp[k].y;
+          // = w later, as a threshold
           atomicOr(sl.is + w[k], nw);                                           // RED
           atomicOr(sl.isum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));          // RED
           atomicOr(sl.state + 2 * w[k] + 1, nw);                                // RED
-          atomicOr(sl.thr + (q >> 5), 1u << (q & 31));                          // RED
-          atomicOr(sl.tsum + (q >> 10), 1u << ((q >> 5) & 31));                // smem
-          atomicMin(minfill, q);                                                // smem
+          atomicOr(sl.thr + (w[k] >> 5), 1u << (w[k] & 31));                    // RED
+          atomicOr(sl.tsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));          // smem
+          atomicMin(minfill, w[k]);                                             // smem
         } else {
           // w < T: maxId(w) = T, not in the structure: continue with T
           po[k] = atomicOr(sl.state + 2 * w[k] + 1, nw);
@@ -327,13 +319,12 @@ __device__ __forceinline__ void stage_rows(const StreamParams &p, uint32_t *is, 
 // Lockstep kernel: the 32 sources of a group share frontier items (one bit
 // each); a group that runs longer than p.abort_cycles is abandoned -- its
 // slot is cleaned -- and handed to the solo kernel through the heavy queue.
-template <bool kH>
 __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParams p) {
   constexpr int kWarps = kLightWarps;
   constexpr int kThreads = kWarps * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   const int n = p.n, Vmax = p.Vmax;
-  const int tbw_max = kH ? (p.npos + 31) >> 5 : (Vmax + 31) >> 5;  // threshold bitmap words
+  const int tbw_max = (Vmax + 31) >> 5;
   const int rsw = (Vmax + 1023) >> 10;
   Slot sl;
   const size_t slot = blockIdx.x;
@@ -380,7 +371,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
     const int s0g = p.row_begin + 32 * g;
     const int nsrc = min(32, p.row_end - s0g);
     const int Vb = min(n, s0g + nsrc);  // maxId only below the largest source
-    const int tbw = kH ? tbw_max : (Vb + 31) >> 5;
+    const int tbw = (Vb + 31) >> 5;
     for (int i = tid; i < ((tbw + 31) >> 5); i += kThreads) s_tsum[i] = 0u;
     __syncthreads();
 
@@ -397,12 +388,11 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
         atomicOr(sl.isum + (w >> 10), 1u << ((w >> 5) & 31));       // RED
         if (w < s) {
           c.fv += 1;                                                  // first visit of (s, w)
-          const int q = kH ? __ldg(&p.rec[w].w) : w;                  // bitmap position
           atomicOr(sl.state + 2 * w, bit);                            // RED
           atomicOr(sl.rsum + (w >> 10), 1u << ((w >> 5) & 31));       // RED
           atomicOr(sl.state + 2 * w + 1, bit);                        // RED
-          atomicOr(sl.thr + (q >> 5), 1u << (q & 31));                // RED
-          atomicOr(sl.tsum + (q >> 10), 1u << ((q >> 5) & 31));       // smem
+          atomicOr(sl.thr + (w >> 5), 1u << (w & 31));                // RED
+          atomicOr(sl.tsum + (w >> 10), 1u << ((w >> 5) & 31));       // smem
         }
       }
     }
@@ -427,23 +417,12 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
         s_scan[(step + 2) % 3] = INT_MAX;
         s_minfill[(step + 2) % 3] = INT_MAX;
       }
-      const int hT = kH ? __ldg(p.wkey + (T >> 5)) : T;  // the step's height (height order)
-      // level 0: warp 0 expands the step's thresholds -- T itself (id
-      // order), or every threshold of the bitmap word holding position T, all
-      // of one height (height order); warp 1 finds the next threshold after
-      // them in parallel (new fills of this step go to s_minfill[nx3])
+      // level 0: warp 0 expands T itself; warp 1 finds the next threshold
+      // above T in parallel (new fills of this step go to s_minfill[nx3])
       if (warp == 0) {
-        if (kH) {
-          const int word = T >> 5;
-          const uint32_t x = __ldcg(sl.thr + word) & (kFull << (T & 31));
-          const int u = ((x >> lane) & 1u) ? __ldg(p.vert + (word << 5) + lane) : -1;
-          expand<kH>(p, sl, s0g, hT, u, sl.list1, &s_qn[1], &s_minfill[nx3], lane, c);
-        } else {
-          expand<kH>(p, sl, s0g, T, lane == 0 ? T : -1, sl.list1, &s_qn[1], &s_minfill[nx3], lane,
-                     c);
-        }
+        expand(p, sl, s0g, T, lane == 0 ? T : -1, sl.list1, &s_qn[1], &s_minfill[nx3], lane, c);
       } else if (warp == 1) {
-        const int nt = scan_next(sl.thr, sl.tsum, tbw, kH ? (T | 31) : T, lane);
+        const int nt = scan_next(sl.thr, sl.tsum, tbw, T, lane);
         if (lane == 0) s_scan[nx3] = nt;
       }
       __syncthreads();
@@ -465,7 +444,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
         c.levels += 1;
         for (int b0 = warp * 32; b0 < qn; b0 += kThreads) {
           const int u = (b0 + lane < qn) ? (int)cq[b0 + lane] : -1;
-          expand<kH>(p, sl, s0g, hT, u, nq, &s_qn[nxt], &s_minfill[nx3], lane, c);
+          expand(p, sl, s0g, T, u, nq, &s_qn[nxt], &s_minfill[nx3], lane, c);
         }
         __syncthreads();
       }
@@ -491,19 +470,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
           x &= x - 1u;
           const int line = (i << 5) + b;
           reinterpret_cast<uint2 *>(sl.state)[(line << 5) + lane] = make_uint2(0u, 0u);
-          if (!kH && lane == 0) sl.thr[line] = 0u;
-        }
-      }
-      if (kH) {
-        // height order: the threshold words are the ones the smem summary lists
-        const int tsw = (tbw + 31) >> 5;
-        for (int i = tid; i < tsw; i += kThreads) {
-          uint32_t x = s_tsum[i];
-          while (x) {
-            const int b = __ffs(x) - 1;
-            x &= x - 1u;
-            sl.thr[(i << 5) + b] = 0u;
-          }
+          if (lane == 0) sl.thr[line] = 0u;
         }
       }
     }
@@ -670,16 +637,61 @@ __device__ __forceinline__ void red_sum(uint32_t *sum, int v) {
   atomicOr(sum + (v >> 10), 1u << ((v >> 5) & 31));
 }
 
+// The tests of one step, in the coordinates of the traversal: vertex ids (id
+// order) or positions of the relabelled graph (height order, order.cu).
+//   w == self               the source itself (the implicit diagonal)
+//   w >= ulim               an entry of U
+//   w <  blim               below the source: atomicMin(maxId(w), .)
+//   w <  clim               may join the closure (its adjacency is prefetched)
+//   newly reached, w >= flim  a fill of L (R4) and a later threshold
+// id order:     self = s, ulim = s + 1, blim = s, clim = T, flim = T + 1
+// height order: self = pos(s), ulim = seg[h(s)+1], blim = seg[h(s)],
+//               clim = seg[h], flim = seg[h+1] for the step's height h
+struct SoloStep {
+  int self, ulim, blim, clim, flim;
+};
+
+// one closure item per lane into the worklist: shared memory, then the
+// global ring, then parked in pend (push = this lane has an item)
+__device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot &sl,
+                                          SoloWarpSmem &sw, SoloQueue &Q, bool push, int wk,
+                                          int rb, int re, int lane) {
+  const uint32_t pb = __ballot_sync(kFull, push);
+  if (!pb) return;
+  const int pos = Q.st + __popc(pb & lanemask_lt());
+  const bool in_s = pos - Q.sh < kSoloQ;
+  if (push && in_s) {
+    const int i = pos & (kSoloQ - 1);
+    sw.qw[i] = wk;
+    sw.qb[i] = rb;
+    sw.qe[i] = re;
+  }
+  const uint32_t sb = __ballot_sync(kFull, push && in_s);
+  Q.st += __popc(sb);
+  const uint32_t gb = pb & ~sb;
+  if (gb) {
+    const int gpos = Q.gt + __popc(gb & lanemask_lt());
+    const bool in_g = gpos - Q.gh <= SL_QMASK;
+    if (push && !in_s) {
+      if (in_g) SL_QUEUE[gpos & SL_QMASK] = (uint32_t)wk;
+      else atomicOr(SL_PEND + (wk >> 5), vbit(wk));  // RED
+    }
+    Q.gt += __popc(__ballot_sync(kFull, push && !in_s && in_g));
+    Q.spilled |= __ballot_sync(kFull, push && !in_s && !in_g) != 0u;
+  }
+}
+
 // expand the closure items u (one per lane, -1 = none; beg/end = adjacency)
-// of the current step of source s.  Id order (kH = false): the step is one
-// threshold T = h; a newly reached w < s is a fill iff w > T.  Height order
-// (kH = true): the step is a set of thresholds of etree height h; a newly
-// reached w < s is a fill iff height(w) > h, else it joins the closure
-// (order.cu).  Fills are recorded at their bitmap position.
+// of the current step (SoloStep) of one source.  kH: the graph is the
+// position-relabelled one and structure bits are set at vert[w] (the
+// structure bitmap stays in vertex ids so rows come out sorted).
 template <bool kH>
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
-                                            SoloWarpSmem &sw, int wb, SoloQueue &Q, int s, int T,
-                                            int u, int beg, int end, int lane) {
+                                            SoloWarpSmem &sw, int wb, SoloQueue &Q,
+                                            const SoloStep &t, int u, int beg, int end,
+                                            int lane) {
+  const int32_t *__restrict__ colidx = kH ? p.colidxP : p.colidx;
+  const int32_t *__restrict__ rowptr = kH ? p.rowptrP : p.rowptr;
   const int deg = u >= 0 ? end - beg : 0;
   // fast path (every threshold's level 0, most closure levels of a chain):
   // one item in lane 0 with at most 32 neighbours -- lane j takes neighbour
@@ -706,17 +718,17 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
   // kSoloBatch batches of 32 (item, neighbour) pairs are in flight at once:
   // all their colidx loads, then all their atomics, then the pushes
   for (int f0 = 0; f0 < total; f0 += 32 * kSoloBatch) {
-    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch], wh[kSoloBatch], wp[kSoloBatch];
-    uint32_t ro[kSoloBatch], io[kSoloBatch];
+    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch], iw[kSoloBatch];
+    uint32_t ro[kSoloBatch];
     const int nb = min(kSoloBatch, (total - f0 + 31) >> 5);  // warp-uniform: skip empty batches
 #pragma unroll
     for (int k = 0; k < kSoloBatch; ++k) {
-      w[k] = s;
+      w[k] = t.self;
       if (k >= nb) continue;
       const int f = f0 + 32 * k + lane;
       if (single) {
         const int b0 = __shfl_sync(kFull, beg, 0);
-        w[k] = f < total ? __ldg(p.colidx + b0 + f) : s;
+        w[k] = f < total ? __ldg(colidx + b0 + f) : t.self;
         continue;
       }
       int o = 0;
@@ -728,39 +740,25 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       }
       const int ob = __shfl_sync(kFull, beg, o);
       const int oe = __shfl_sync(kFull, excl, o);
-      w[k] = f < total ? __ldg(p.colidx + ob + (f - oe)) : s;
+      w[k] = f < total ? __ldg(colidx + ob + (f - oe)) : t.self;
     }
 #pragma unroll
     for (int k = 0; k < kSoloBatch; ++k) {
-      ro[k] = io[k] = 1u;
+      ro[k] = 1u;
       rb[k] = re[k] = 0;
+      iw[k] = w[k];
       if (k >= nb) continue;
       const uint32_t bw = vbit(w[k]);
-      // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds
-      // iff the source has not reached w yet (line 10 of fig:alg)
-      ro[k] = w[k] < s ? atomicOr(SL_REACHED + (w[k] >> 5), bw) : bw;
-      io[k] = 1u;
-      if (w[k] > s) {
-        // U entry: nothing waits for it -- two REDs (the summary bit is idempotent)
-        atomicOr(SL_IS + (w[k] >> 5), bw);
-        red_sum(SL_ISUM, w[k]);
+      // below the source: atomicMin(maxId(w), T) succeeds iff the source has
+      // not reached w yet (line 10 of fig:alg)
+      ro[k] = w[k] < t.blim ? atomicOr(SL_REACHED + (w[k] >> 5), bw) : bw;
+      // w < clim may join the closure: its row pointers travel with the atomic
+      if (w[k] < t.clim) {
+        rb[k] = __ldg(rowptr + w[k]);
+        re[k] = __ldg(rowptr + w[k] + 1);
       }
-      // w < T may join the closure: its row pointers travel with the atomic
-      // (height order: its record -- row pointers, height, position)
-      rb[k] = re[k] = 0;
-      wh[k] = wp[k] = w[k];
-      if (kH) {
-        if (w[k] < s) {
-          const int4 r = __ldg(p.rec + w[k]);
-          rb[k] = r.x;
-          re[k] = r.y;
-          wh[k] = r.z;
-          wp[k] = r.w;
-        }
-      } else if (w[k] < T) {
-        rb[k] = __ldg(p.rowptr + w[k]);
-        re[k] = __ldg(p.rowptr + w[k] + 1);
-      }
+      // U entries and fill candidates: their vertex id, for the structure bit
+      if (kH && w[k] >= t.flim && w[k] != t.self) iw[k] = __ldg(p.vert + w[k]);
     }
 #pragma unroll
     for (int k = 0; k < kSoloBatch; ++k) {
@@ -768,55 +766,34 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       const int wk = w[k];
       const uint32_t bw = vbit(wk);
       {
-        // first visits: the reached bit of w < s was clear (w >= s: ro = bw)
+        // first visits: the reached bit of w below s was clear (else ro = bw)
         const uint32_t nv = __popc(__ballot_sync(kFull, !(ro[k] & bw)));
         if (lane == 0) sw.fv += nv;
       }
-      if (io[k] == 0u) red_sum(SL_ISUM, wk);
+      if (wk >= t.ulim) {
+        // U entry: nothing waits for it -- two REDs (the summary bit is idempotent)
+        atomicOr(SL_IS + (iw[k] >> 5), vbit(iw[k]));
+        red_sum(SL_ISUM, iw[k]);
+      }
       bool push = false;
       if (!(ro[k] & bw)) {
         if (ro[k] == 0u) red_sum(SL_RSUM, wk);
-        if (wh[k] > T) {
-          // fill of L(s,:) (R4); w becomes a threshold of this source, at
-          // bitmap position wp (its id in id order)
-          atomicOr(SL_IS + (wk >> 5), bw);  // RED
-          red_sum(SL_ISUM, wk);
-          const int d = (wp[k] >> 5) - wb;
+        if (wk >= t.flim) {
+          // fill of L(s,:) (R4); w becomes a threshold of this source
+          atomicOr(SL_IS + (iw[k] >> 5), vbit(iw[k]));  // RED
+          red_sum(SL_ISUM, iw[k]);
+          const int d = (wk >> 5) - wb;
           if (d < 32) {
-            atomicOr(&sw.win[d], vbit(wp[k]));  // smem (d >= 0: position after the step's)
+            atomicOr(&sw.win[d], bw);  // smem (d >= 0: after the step's thresholds)
           } else {
-            atomicOr(SL_THR + (wp[k] >> 5), vbit(wp[k]));  // RED
-            red_sum(SL_TSUM, wp[k]);
+            atomicOr(SL_THR + (wk >> 5), bw);  // RED
+            red_sum(SL_TSUM, wk);
           }
         } else {
           push = true;  // maxId(w) = T, not in the structure: continue with T
         }
       }
-      // shared worklist, then the global ring, then park in pend
-      const uint32_t pb = __ballot_sync(kFull, push);
-      if (pb) {
-        const int pos = Q.st + __popc(pb & lanemask_lt());
-        const bool in_s = pos - Q.sh < kSoloQ;
-        if (push && in_s) {
-          const int i = pos & (kSoloQ - 1);
-          sw.qw[i] = wk;
-          sw.qb[i] = rb[k];
-          sw.qe[i] = re[k];
-        }
-        const uint32_t sb = __ballot_sync(kFull, push && in_s);
-        Q.st += __popc(sb);
-        const uint32_t gb = pb & ~sb;
-        if (gb) {
-          const int gpos = Q.gt + __popc(gb & lanemask_lt());
-          const bool in_g = gpos - Q.gh <= SL_QMASK;
-          if (push && !in_s) {
-            if (in_g) SL_QUEUE[gpos & SL_QMASK] = (uint32_t)wk;
-            else atomicOr(SL_PEND + (wk >> 5), bw);  // RED
-          }
-          Q.gt += __popc(__ballot_sync(kFull, push && !in_s && in_g));
-          Q.spilled |= __ballot_sync(kFull, push && !in_s && !in_g) != 0u;
-        }
-      }
+      solo_push(p, sl, sw, Q, push, wk, rb[k], re[k], lane);
     }
   }
 }
@@ -853,72 +830,98 @@ __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const ui
   return t;
 }
 
-// the max-id relaxation of source s in increasing threshold order (kH:
-// increasing etree height, one bitmap word of same-height thresholds per step)
+// the max-id relaxation of source s in increasing threshold order -- by
+// vertex id, or (kH) by etree height in position space: a step then takes
+// every threshold of one height within the 32-word window (order.cu)
 template <bool kH>
 __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s,
                                             int lane, SoloWarpSmem &sw) {
-  // thresholds are < s (id order) / anywhere in [0, npos) (height order)
-  const int tbw = kH ? (p.npos + 31) >> 5 : (s + 31) >> 5;
+  const int32_t *__restrict__ rowptr = kH ? p.rowptrP : p.rowptr;
+  const int32_t *__restrict__ colidx = kH ? p.colidxP : p.colidx;
+  SoloStep t;
+  if (kH) {
+    const int ps = __ldg(p.pos + s), hs = __ldg(p.wkey + (ps >> 5));
+    t.self = ps;
+    t.blim = __ldg(p.seg + hs);      // subtree(s): heights below s's
+    t.ulim = __ldg(p.seg + hs + 1);  // ancestors of s: entries of U
+  } else {
+    t.self = s;
+    t.blim = s;
+    t.ulim = s + 1;
+  }
+  const int tbw = (t.blim + 31) >> 5;  // thresholds lie below the source
   // seed: the out-neighbours of s are in the structure; the
   // smaller ones are reached with maxId -1 and are thresholds
-  const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
+  const int beg = __ldg(rowptr + t.self), end = __ldg(rowptr + t.self + 1);
   for (int j0 = beg; j0 < end; j0 += 32) {
     const int j = j0 + lane;
-    const int w = j < end ? __ldg(p.colidx + j) : s;
-    const uint32_t nv = __popc(__ballot_sync(kFull, w < s));  // first visits of the seeds
+    const int w = j < end ? __ldg(colidx + j) : t.self;
+    const uint32_t nv = __popc(__ballot_sync(kFull, w < t.blim));  // first visits of the seeds
     if (lane == 0) sw.fv += nv;
-    if (w == s) continue;
-    const uint32_t bw = vbit(w);
-    if (atomicOr(SL_IS + (w >> 5), bw) == 0u) red_sum(SL_ISUM, w);
-    if (w < s) {
+    if (w == t.self) continue;
+    const int iw = kH ? __ldg(p.vert + w) : w;  // vertex id (structure bitmap)
+    if (atomicOr(SL_IS + (iw >> 5), vbit(iw)) == 0u) red_sum(SL_ISUM, iw);
+    if (w < t.blim) {
+      const uint32_t bw = vbit(w);
       if (atomicOr(SL_REACHED + (w >> 5), bw) == 0u) red_sum(SL_RSUM, w);
-      const int pw = kH ? __ldg(&p.rec[w].w) : w;  // bitmap position
-      atomicOr(SL_THR + (pw >> 5), vbit(pw));  // RED
-      red_sum(SL_TSUM, pw);
+      atomicOr(SL_THR + (w >> 5), bw);  // RED
+      red_sum(SL_TSUM, w);
     }
   }
   __syncwarp();
   int wb = -1;  // no window yet
-  int P = -1;   // position of the last threshold taken
+  int P = -1;   // the last threshold (position) taken
   for (;;) {
     P = solo_next_threshold(SL_THR, SL_TSUM, tbw, P, wb, sw, lane);
     if (P == INT_MAX) break;
     if (lane == 0) sw.steps += 1;
     SoloQueue Q = {0, 0, 0, 0, false};
-    int u = -1, ub = 0, ue = 0, T;
+    int u = -1, ub = 0, ue = 0;
     if (kH) {
-      // the step: every threshold of the window word holding P at or after P
-      // (a word holds one height: segments are word-aligned), one per lane
-      const int word = P >> 5;
-      const uint32_t x = sw.win[word - wb] & (kFull << (P & 31));
-      T = __ldg(p.wkey + word);  // the round's height
-      if ((x >> lane) & 1u) {
-        u = __ldg(p.vert + (word << 5) + lane);
-        const int4 r = __ldg(p.rec + u);
-        ub = r.x;
-        ue = r.y;
+      // the step: every threshold of height h = height(P) in the window at
+      // or after P -- the window words of h's segment (segments are
+      // word-aligned); the first word's items go to the lanes, the others
+      // to the worklist
+      const int word = P >> 5, h = __ldg(p.wkey + word);
+      t.clim = __ldg(p.seg + h);
+      t.flim = __ldg(p.seg + h + 1);
+      const int wend = min(wb + 32, t.flim >> 5);  // one past the last word of the step
+      for (int wi = word; wi < wend; ++wi) {
+        uint32_t x = sw.win[wi - wb];
+        if (wi == word) x &= kFull << (P & 31);
+        const bool has = (x >> lane) & 1u;
+        const int v = (wi << 5) + lane;
+        int vb = 0, ve = 0;
+        if (has) {
+          vb = __ldg(rowptr + v);
+          ve = __ldg(rowptr + v + 1);
+        }
+        if (wi == word) {
+          // compact to the low lanes (the single-item fast path)
+          const uint32_t b = __ballot_sync(kFull, has);
+          const int src = __fns(b, 0, lane + 1) & 31;
+          const int cu = __shfl_sync(kFull, v, src), cb = __shfl_sync(kFull, vb, src),
+                    ce = __shfl_sync(kFull, ve, src);
+          const bool ok = lane < __popc(b);
+          u = ok ? cu : -1;
+          ub = ok ? cb : 0;
+          ue = ok ? ce : 0;
+        } else {
+          solo_push(p, sl, sw, Q, has, v, vb, ve, lane);
+        }
       }
-      // compact the items to the low lanes (the single-item fast path)
-      const uint32_t b = __ballot_sync(kFull, u >= 0);
-      const int src = __fns(b, 0, lane + 1);
-      const int cu = __shfl_sync(kFull, u, src & 31), cb = __shfl_sync(kFull, ub, src & 31),
-                ce = __shfl_sync(kFull, ue, src & 31);
-      const bool ok = lane < __popc(b);
-      u = ok ? cu : -1;
-      ub = ok ? cb : 0;
-      ue = ok ? ce : 0;
-      P = (word << 5) + 31;  // the next step starts after this word
+      P = (wend << 5) - 1;  // the next step starts after these words
     } else {
-      T = P;
+      t.clim = P;
+      t.flim = P + 1;
       if (lane == 0) {
-        u = T;
-        ub = __ldg(p.rowptr + T);
-        ue = __ldg(p.rowptr + T + 1);
+        u = P;
+        ub = __ldg(rowptr + P);
+        ue = __ldg(rowptr + P + 1);
       }
     }
     for (;;) {
-      solo_expand<kH>(p, sl, sw, wb, Q, s, T, u, ub, ue, lane);
+      solo_expand<kH>(p, sl, sw, wb, Q, t, u, ub, ue, lane);
       __syncwarp();
       if (Q.sh < Q.st) {
         const int cnt = min(32, Q.st - Q.sh);
@@ -935,11 +938,11 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       }
       if (Q.gh >= Q.gt && Q.spilled) {
         // the ring overflowed during this closure: move parked items (pend
-        // bits, all below T) back into the ring, as many as fit
+        // bits, all below clim) back into the ring, as many as fit
         Q.spilled = false;
         __syncwarp();
         fence_gpu();
-        const int pwords = kH ? (s + 31) >> 5 : (T + 31) >> 5;  // closure vertices are below
+        const int pwords = (t.clim + 31) >> 5;
         for (int w0 = 0; w0 < pwords && !Q.spilled; w0 += 32) {
           const int wi = w0 + lane;
           uint32_t x = wi < pwords ? __ldcg(SL_PEND + wi) : 0u;
@@ -969,8 +972,8 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       u = lane < cnt ? (int)SL_QUEUE[(Q.gh + lane) & SL_QMASK] : -1;
       Q.gh += cnt;
       if (u >= 0) {
-        ub = __ldg(p.rowptr + u);
-        ue = __ldg(p.rowptr + u + 1);
+        ub = __ldg(rowptr + u);
+        ue = __ldg(rowptr + u + 1);
       }
     }
   }
@@ -1082,7 +1085,7 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
   const int rows = p.row_end - p.row_begin;
   const size_t slot = (size_t)blockIdx.x * kSoloWarps + warp;
   const SoloSlot sl = solo_slot(p, slot);
-  const int Vw = (p.Vmax + 31) >> 5, Vs = (Vw + 31) >> 5;
+  const int Vs = (int)(p.so_tsum - p.so_rsum);  // reached-word summary words
   __shared__ SoloWarpSmem s_sw[kSoloWarps];
   SoloWarpSmem &sw = s_sw[warp];
   if (lane == 0) sw.items = sw.pairs = sw.levels = sw.steps = sw.fv = 0u;
@@ -1131,14 +1134,14 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
     fence_gpu();  // this warp's REDs are visible to its extraction
     __syncwarp();
     solo_stage_row(p, sl, s, g, lane);
-    // reset the touched words: reached | pend (| thr in id order, where a
-    // threshold bit sits in the word of its reached bit), and the summaries
+    // reset the touched words: reached | pend | thr (a threshold bit sits in
+    // the word of its reached bit), and the summaries
     for (int i0 = 0; i0 < Vs; i0 += 32) {
       const int i = i0 + lane;
       uint32_t x = i < Vs ? __ldcg(SL_RSUM + i) : 0u;
       if (x) {
         SL_RSUM[i] = 0u;
-        if (!kH) SL_TSUM[i] = 0u;
+        SL_TSUM[i] = 0u;
       }
       while (x) {
         const int b = __ffs(x) - 1;
@@ -1146,22 +1149,7 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
         const int wi = (i << 5) + b;
         SL_REACHED[wi] = 0u;
         SL_PEND[wi] = 0u;
-        if (!kH) SL_THR[wi] = 0u;
-      }
-    }
-    if (kH) {
-      // height order: threshold bits live at positions; the summary lists
-      // every global word written (window bits never reach global memory)
-      const int Ts = (int)(p.so_is - p.so_tsum);
-      for (int i0 = 0; i0 < Ts; i0 += 32) {
-        const int i = i0 + lane;
-        uint32_t x = i < Ts ? __ldcg(SL_TSUM + i) : 0u;
-        if (x) SL_TSUM[i] = 0u;
-        while (x) {
-          const int b = __ffs(x) - 1;
-          x &= x - 1u;
-          SL_THR[(i << 5) + b] = 0u;
-        }
+        SL_THR[wi] = 0u;
       }
     }
     // the clears are plain stores; the next source's atomics act at L2
@@ -1217,9 +1205,7 @@ size_t stream_smem_bytes(int64_t Vmax, int64_t npos) {
 }
 
 // kernel instances of the two threshold orders (kH = height order)
-const void *stream_fn(bool h) {
-  return h ? (const void *)stream_kernel<true> : (const void *)stream_kernel<false>;
-}
+const void *stream_fn(bool) { return (const void *)stream_kernel; }  // id order only
 const void *solo_fn(bool h) {
   return h ? (const void *)solo_kernel<true> : (const void *)solo_kernel<false>;
 }
@@ -1232,7 +1218,7 @@ int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos) {
   if (heavy) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solo_fn(h), kSoloWarps * 32, 0);
   } else {
-    const size_t smem = stream_smem_bytes(Vmax, npos);
+    const size_t smem = stream_smem_bytes(Vmax, 0);  // the lockstep kernel runs id order
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(stream_fn(h), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
@@ -1263,7 +1249,7 @@ int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos) {
   const int light_regs = ((fl.numRegs * 32 + 255) / 256 * 256) * kLightWarps;
   const int by_regs = (regs - solo_regs) / light_regs;
   const int by_warps = (warps - kSoloWarps) / kLightWarps;
-  const size_t light_smem = fl.sharedSizeBytes + stream_smem_bytes(Vmax, npos) + 1024;
+  const size_t light_smem = fl.sharedSizeBytes + stream_smem_bytes(Vmax, 0) + 1024;
   const int by_smem = (int)((smem_sm - fs.sharedSizeBytes - 1024) / light_smem);
   return std::max(0, std::min(std::min(by_regs, by_warps), by_smem));
 }
@@ -1285,8 +1271,10 @@ int solo_ring(int64_t Vmax) {
 // [Ts] (summaries: one bit per word); is [nw], isum [ns] (structure over
 // [0, n)); the closure ring.  npos > 0: height order.  Returns the total.
 size_t solo_layout(int64_t Vmax, int64_t n, int64_t npos, StreamParams *p) {
-  const size_t Vw = round4((size_t)((Vmax + 31) / 32)), Vs = round4((Vw + 31) / 32);
-  const size_t Tw = npos > 0 ? round4((size_t)((npos + 31) / 32)) : Vw, Ts = round4((Tw + 31) / 32);
+  // reached / pend / thr over vertex ids [0, Vmax), or positions [0, npos)
+  const int64_t V = npos > 0 ? npos : Vmax;
+  const size_t Vw = round4((size_t)((V + 31) / 32)), Vs = round4((Vw + 31) / 32);
+  const size_t Tw = Vw, Ts = Vs;
   const size_t nw = round4((size_t)((n + 31) / 32)), ns = round4((nw + 31) / 32);
   if (p) {
     p->so_pend = (uint32_t)Vw;
@@ -1307,14 +1295,13 @@ int solo_warps_per_cta() { return kSoloWarps; }
 
 cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st) {
   if (grid <= 0) return cudaSuccess;
-  const size_t smem = stream_smem_bytes(p.Vmax, p.hmode ? p.npos : 0);
+  const size_t smem = stream_smem_bytes(p.Vmax, 0);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(stream_fn(p.hmode), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  if (p.hmode) stream_kernel<true><<<grid, kLightWarps * 32, smem, st>>>(p);
-  else stream_kernel<false><<<grid, kLightWarps * 32, smem, st>>>(p);
+  stream_kernel<<<grid, kLightWarps * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
 
