@@ -136,12 +136,10 @@ struct gsofa_context {
   int32_t *in_colidx = nullptr, *rowptr32 = nullptr;
   size_t in_rowptr_cap = 0, in_colidx_cap = 0, rowptr32_cap = 0;
   int64_t *h_small = nullptr;  // pinned host scratch
-  // height order (order.cu): one grow-only buffer for the positions, their
-  // inverse, word heights, segment bounds and the relabelled graph
+  // height order (order.cu): heights | positions | inverse | per-position
+  // {height, segment end}, one grow-only buffer
   int32_t *ord_buf = nullptr;
   size_t ord_cap = 0;
-  int32_t *ord_pos = nullptr, *ord_vert = nullptr, *ord_wkey = nullptr, *ord_seg = nullptr;
-  int32_t *ord_rowptrP = nullptr, *ord_colidxP = nullptr;
   HostBlock *hpool = nullptr;  // pinned storage reused by host-side results
 };
 
@@ -947,9 +945,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   }
   // ---------------------------------------------------- A2: height order
   if (o.schedule == GSOFA_SCHEDULE_HEIGHT) {
-    // elimination tree of A + A^T and the (height, id) positions (order.cu);
-    // host computation of the plan, O(nnz alpha); then
-    // the graph relabelled to positions on the GPU
+    // elimination tree of A + A^T, heights and (height, id) positions
+    // (order.cu): host computation of the plan, O(nnz alpha)
     std::vector<int64_t> hrp;
     std::vector<int32_t> hci;
     const int64_t *rp_h = rowptr;
@@ -963,33 +960,13 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       rp_h = hrp.data();
       ci_h = hci.data();
     }
-    std::vector<int32_t> hpos, hvert, hwkey, hseg;
-    ord_npos = gsofa::height_order(n, rp_h, ci_h, hpos, hvert, hwkey, hseg);
-    const size_t tmpb = gsofa::relabel_tmp_bytes(ord_npos);
-    const size_t need = (size_t)n + 2 * (size_t)ord_npos + hwkey.size() + hseg.size() + 1 +
-                        (size_t)std::max<int64_t>(nnz, 1) + tmpb / 4 + 256;
-    if ((rc = grow_device(&c->ord_buf, &c->ord_cap, need, st)) != GSOFA_OK) goto fail;
-    int32_t *q = c->ord_buf;
-    auto take = [&](size_t words) {
-      int32_t *r = q;
-      q += (words + 63) / 64 * 64;
-      return r;
-    };
-    c->ord_pos = take(n);
-    c->ord_vert = take(ord_npos);
-    c->ord_wkey = take(hwkey.size());
-    c->ord_seg = take(hseg.size());
-    c->ord_rowptrP = take(ord_npos + 1);
-    c->ord_colidxP = take(std::max<int64_t>(nnz, 1));
-    void *tmp = take(tmpb / 4 + 1);
-    CK(cudaMemcpyAsync(c->ord_pos, hpos.data(), hpos.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->ord_vert, hvert.data(), hvert.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->ord_wkey, hwkey.data(), hwkey.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->ord_seg, hseg.data(), hseg.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(gsofa::launch_relabel(c->rowptr32, d_colidx, c->ord_pos, n, ord_npos, c->ord_rowptrP,
-                             c->ord_colidxP, tmp, tmpb + 4, st));
-    launches += 4;
-    CK(cudaStreamSynchronize(st));  // the host vectors go out of scope
+    std::vector<int32_t> hord((size_t)n * 5);  // hgt | pos | vert | pseg (2 per position)
+    gsofa::height_order(n, rp_h, ci_h, hord.data(), hord.data() + n, hord.data() + 2 * n,
+                        hord.data() + 3 * n);
+    if ((rc = grow_device(&c->ord_buf, &c->ord_cap, hord.size(), st)) != GSOFA_OK) goto fail;
+    CK(cudaMemcpyAsync(c->ord_buf, hord.data(), hord.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // the host vector goes out of scope
+    ord_npos = n;
   }
   // ---------------------------------------------------- plan + arena
   {
@@ -1159,12 +1136,10 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     gsofa::solo_layout(plan.Vmax, n, ord_npos, &sp);
     sp.hmode = ord_npos > 0;
     sp.npos = (int32_t)ord_npos;
-    sp.rowptrP = c->ord_rowptrP;
-    sp.colidxP = c->ord_colidxP;
-    sp.pos = c->ord_pos;
-    sp.vert = c->ord_vert;
-    sp.wkey = c->ord_wkey;
-    sp.seg = c->ord_seg;
+    sp.hgt = c->ord_buf;
+    sp.pos = c->ord_buf + n;
+    sp.vert = c->ord_buf + 2 * n;
+    sp.pseg = reinterpret_cast<const int2 *>(c->ord_buf + 3 * n);
     if (plan.heavy > 0) {
       // the heaviest groups (top separator / hub rows) start on
       // the solo kernel: one per first-wave solo CTA (one per SM)

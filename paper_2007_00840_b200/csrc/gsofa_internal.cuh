@@ -93,17 +93,15 @@ struct StreamParams {
   long long *group_trace;    // optional [ngroups][8]: steps, levels, items, cycles, ...
   int *debug;                // optional dev checks
   // processing order of the solo kernel's thresholds (order.cu): hmode = 0:
-  // increasing vertex id (one threshold per step); hmode = 1: increasing
-  // etree height, traversed in position space (the relabelled graph below;
-  // reached / pend / threshold bitmaps over npos positions)
+  // increasing vertex id (one threshold per step); hmode = 1: increasing etree
+  // height (all same-height thresholds of the window per step); threshold
+  // bitmaps then indexed by position (vertices sorted by (height, id), npos = n)
   int32_t hmode;
   int32_t npos;
-  const int32_t *rowptrP;    // [npos+1] relabelled graph: row pos(v) = {pos(w)}
-  const int32_t *colidxP;    // [nnz]
+  const int32_t *hgt;        // [n] etree height of a vertex
   const int32_t *pos;        // [n] vertex -> position
-  const int32_t *vert;       // [npos] position -> vertex, -1 = padding
-  const int32_t *wkey;       // [npos / 32] height of a bitmap word
-  const int32_t *seg;        // [H+2] height h occupies positions [seg[h], seg[h+1])
+  const int32_t *vert;       // [n] position -> vertex
+  const int2 *pseg;          // [n] per position: {height, end of its height's segment}
   // solo slot layout: word offsets of its arrays (solo_layout)
   uint32_t so_pend, so_thr, so_rsum, so_tsum, so_is, so_isum, so_queue;
 };
@@ -120,15 +118,10 @@ int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos);
 size_t stream_smem_bytes(int64_t Vmax, int64_t npos);  // dynamic smem: threshold-word summary
 // order.cu (host): elimination tree of A + A^T and the height order
 void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *parent);
-int64_t height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx,
-                     std::vector<int32_t> &pos, std::vector<int32_t> &vert,
-                     std::vector<int32_t> &wkey, std::vector<int32_t> &seg);
-// relabel the CSR to positions: row pos(v) of (rowptrP, colidxP) holds
-// {pos(w) : w in row v}; rows of padding positions are empty
-cudaError_t launch_relabel(const int32_t *rowptr, const int32_t *colidx, const int32_t *pos,
-                           int64_t n, int64_t npos, int32_t *rowptrP, int32_t *colidxP,
-                           void *tmp, size_t tmp_bytes, cudaStream_t st);
-size_t relabel_tmp_bytes(int64_t npos);
+// heights, positions (sorted by (height, id)), inverse, and per position
+// {height, segment end} (int2 as two int32) of the etree of A + A^T
+void height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *hgt,
+                  int32_t *pos, int32_t *vert, int32_t *pseg);
 cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st);
 cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st);
 cudaError_t launch_gather(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,

@@ -20,18 +20,14 @@
 // Rounds per source drop from |L(s,:)| to at most the tree height (C4's
 // hub rows: 577k -> 4.2k; C5's top separator rows: ~1.5x).
 //
-// The solo kernel runs this order in POSITION space: vertices sorted by
-// (height, id), each height's segment starting at a multiple of 32 (a bitmap
-// word never mixes two heights), and the graph relabelled to positions.  All
-// tests of the traversal become position comparisons against segment
-// bounds, with no per-edge lookups (threshold.cu, solo_expand<true>):
-//   * a neighbour of a vertex of subtree(s) is in subtree(s) (height below
-//     s's: position < seg[h(s)]), s itself, or an ancestor of s (an entry of
-//     U, position >= seg[h(s)+1]) -- so "w < s" is "pos(w) < seg[h(s)]";
-//   * in the round of height h a newly reached vertex is a fill iff
-//     pos(w) >= seg[h+1], a closure member iff pos(w) < seg[h].
-// Rows are still written in vertex ids (the structure bitmap stays in id
-// space; vert[] maps a position back when a bit is set).
+// The solo kernel keeps the graph and its reached / structure bitmaps in
+// vertex ids (the nested-dissection order's locality) and only its threshold
+// bitmap in POSITIONS: vertices sorted by (height, id), so a forward scan
+// meets thresholds by increasing height.  A step takes every threshold of one
+// height in its window; with tmin / tmax their smallest / largest id, a newly
+// reached w is a fill if w > tmax (a descendant of a threshold is smaller than
+// it), a closure member if w < tmin (an ancestor is larger), and otherwise by
+// height(w) > h -- one lookup for those in-between edges only.
 //
 // Host code ("int32 parent[n] ... from the etree of
 // A+A^T, O(nnz alpha)"): Liu's algorithm with path compression.
@@ -84,87 +80,31 @@ void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t 
   }
 }
 
-// Height order of the vertices (see the header comment).  Outputs:
-//   pos[n]        vertex -> position (sorted by (height, id))
-//   vert[npos]    position -> vertex (-1 in padding)
-//   wkey[npos/32] bitmap word -> height of its positions
-//   seg[H+2]      height h occupies positions [seg[h], seg[h+1]) (padding at the end)
-// Returns npos (a multiple of 32).
-int64_t height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx,
-                     std::vector<int32_t> &pos, std::vector<int32_t> &vert,
-                     std::vector<int32_t> &wkey, std::vector<int32_t> &seg) {
-  std::vector<int32_t> parent((size_t)n), h((size_t)n, 0);
+// Height order of the vertices (see the header comment), into caller
+// arrays of n entries: hgt (etree height), pos (vertex -> position, sorted by
+// (height, id)), vert (position -> vertex), pseg (per position, two int32:
+// its height and the end of that height's segment of positions).
+void height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *hgt,
+                  int32_t *pos, int32_t *vert, int32_t *pseg) {
+  std::vector<int32_t> parent((size_t)n);
   etree_sym(n, rowptr, colidx, parent.data());
   int32_t H = 0;
+  for (int64_t v = 0; v < n; ++v) hgt[v] = 0;
   for (int64_t v = 0; v < n; ++v) {  // parents are larger: one ascending pass
-    if (parent[v] >= 0) h[parent[v]] = std::max(h[parent[v]], h[v] + 1);
-    H = std::max(H, h[v]);
+    if (parent[v] >= 0) hgt[parent[v]] = std::max(hgt[parent[v]], hgt[v] + 1);
+    H = std::max(H, hgt[v]);
   }
-  std::vector<int64_t> cnt((size_t)H + 1, 0);
-  for (int64_t v = 0; v < n; ++v) cnt[h[v]] += 1;
-  seg.assign((size_t)H + 2, 0);
-  int64_t acc = 0;
-  for (int32_t k = 0; k <= H; ++k) {
-    seg[k] = (int32_t)acc;
-    acc += (cnt[k] + 31) / 32 * 32;  // each height's segment starts a bitmap word
-  }
-  seg[H + 1] = (int32_t)acc;
-  const int64_t npos = std::max<int64_t>(acc, 32);
-  vert.assign((size_t)npos, -1);
-  wkey.assign((size_t)(npos / 32), 0);
-  pos.resize((size_t)n);
+  std::vector<int64_t> seg((size_t)H + 2, 0);
+  for (int64_t v = 0; v < n; ++v) seg[hgt[v] + 1] += 1;
+  for (int32_t k = 0; k <= H; ++k) seg[k + 1] += seg[k];
   std::vector<int64_t> at(seg.begin(), seg.end() - 1);
   for (int64_t v = 0; v < n; ++v) {
-    const int64_t p = at[h[v]]++;
-    vert[p] = (int32_t)v;
-    wkey[p >> 5] = h[v];
-    pos[v] = (int32_t)p;
+    const int64_t q = at[hgt[v]]++;
+    pos[v] = (int32_t)q;
+    vert[q] = (int32_t)v;
+    pseg[2 * q] = hgt[v];
+    pseg[2 * q + 1] = (int32_t)seg[hgt[v] + 1];
   }
-  return npos;
-}
-
-namespace {
-__global__ void relabel_degree_kernel(const int32_t *rowptr, const int32_t *pos, int64_t n,
-                                      int32_t *degP) {
-  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v < n) degP[pos[v]] = rowptr[v + 1] - rowptr[v];
-}
-
-// warp per row: row pos(v) of the relabelled graph = positions of v's neighbours
-__global__ void relabel_scatter_kernel(const int32_t *rowptr, const int32_t *colidx,
-                                       const int32_t *pos, int64_t n, const int32_t *rowptrP,
-                                       int32_t *colidxP) {
-  const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (v >= n) return;
-  const int a = rowptr[v], b = rowptr[v + 1];
-  const int o = rowptrP[pos[v]];
-  for (int e = a + lane; e < b; e += 32) colidxP[o + (e - a)] = __ldg(pos + colidx[e]);
-}
-}  // namespace
-
-cudaError_t launch_relabel(const int32_t *rowptr, const int32_t *colidx, const int32_t *pos,
-                           int64_t n, int64_t npos, int32_t *rowptrP, int32_t *colidxP,
-                           void *tmp, size_t tmp_bytes, cudaStream_t st) {
-  // degrees by position (padding rows empty) -> row pointers -> columns
-  cudaError_t e = cudaMemsetAsync(rowptrP, 0, (size_t)(npos + 1) * sizeof(int32_t), st);
-  if (e != cudaSuccess) return e;
-  int32_t *deg = (int32_t *)tmp;
-  const size_t deg_bytes = ((size_t)npos * 4 + 255) / 256 * 256;
-  if (tmp_bytes < deg_bytes + scan_tmp_bytes(npos)) return cudaErrorInvalidValue;
-  e = cudaMemsetAsync(deg, 0, (size_t)npos * 4, st);
-  if (e != cudaSuccess) return e;
-  relabel_degree_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rowptr, pos, n, deg);
-  e = scan_exclusive_i32(deg, rowptrP, npos, rowptrP + npos, (char *)tmp + deg_bytes,
-                         tmp_bytes - deg_bytes, st);
-  if (e != cudaSuccess) return e;
-  relabel_scatter_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(rowptr, colidx, pos, n,
-                                                                        rowptrP, colidxP);
-  return cudaGetLastError();
-}
-
-size_t relabel_tmp_bytes(int64_t npos) {
-  return ((size_t)npos * 4 + 255) / 256 * 256 + scan_tmp_bytes(npos);
 }
 
 }  // namespace gsofa

@@ -637,18 +637,15 @@ __device__ __forceinline__ void red_sum(uint32_t *sum, int v) {
   atomicOr(sum + (v >> 10), 1u << ((v >> 5) & 31));
 }
 
-// The tests of one step, in the coordinates of the traversal: vertex ids (id
-// order) or positions of the relabelled graph (height order, order.cu).
-//   w == self               the source itself (the implicit diagonal)
-//   w >= ulim               an entry of U
-//   w <  blim               below the source: atomicMin(maxId(w), .)
-//   w <  clim               may join the closure (its adjacency is prefetched)
-//   newly reached, w >= flim  a fill of L (R4) and a later threshold
-// id order:     self = s, ulim = s + 1, blim = s, clim = T, flim = T + 1
-// height order: self = pos(s), ulim = seg[h(s)+1], blim = seg[h(s)],
-//               clim = seg[h], flim = seg[h+1] for the step's height h
+// The thresholds of one step of source s, and how a newly reached w < s is
+// classified.  Id order: one threshold T (tmin = tmax = T, h unused): a fill
+// iff w > T, else a closure member.  Height order (order.cu): every
+// threshold of one etree height h (ids tmin..tmax); a fill is an ancestor of
+// one of them (so w > tmin) and a closure member a descendant (so w < tmax):
+//   w > tmax -> fill,  w < tmin -> closure,  else fill iff height(w) > h
+// (height(w) is loaded only for those in-between pairs).
 struct SoloStep {
-  int self, ulim, blim, clim, flim;
+  int tmin, tmax, h;
 };
 
 // one closure item per lane into the worklist: shared memory, then the
@@ -682,16 +679,14 @@ __device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot 
 }
 
 // expand the closure items u (one per lane, -1 = none; beg/end = adjacency)
-// of the current step (SoloStep) of one source.  kH: the graph is the
-// position-relabelled one and structure bits are set at vert[w] (the
-// structure bitmap stays in vertex ids so rows come out sorted).
+// of the current step t of source s.  Thresholds are kept at their bitmap
+// position: the vertex id (id order) or pos(w) (height order, loaded for
+// each new fill).
 template <bool kH>
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
-                                            SoloWarpSmem &sw, int wb, SoloQueue &Q,
+                                            SoloWarpSmem &sw, int wb, SoloQueue &Q, int s,
                                             const SoloStep &t, int u, int beg, int end,
                                             int lane) {
-  const int32_t *__restrict__ colidx = kH ? p.colidxP : p.colidx;
-  const int32_t *__restrict__ rowptr = kH ? p.rowptrP : p.rowptr;
   const int deg = u >= 0 ? end - beg : 0;
   // fast path (every threshold's level 0, most closure levels of a chain):
   // one item in lane 0 with at most 32 neighbours -- lane j takes neighbour
@@ -718,17 +713,17 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
   // kSoloBatch batches of 32 (item, neighbour) pairs are in flight at once:
   // all their colidx loads, then all their atomics, then the pushes
   for (int f0 = 0; f0 < total; f0 += 32 * kSoloBatch) {
-    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch], iw[kSoloBatch];
+    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch], hw[kSoloBatch];
     uint32_t ro[kSoloBatch];
     const int nb = min(kSoloBatch, (total - f0 + 31) >> 5);  // warp-uniform: skip empty batches
 #pragma unroll
     for (int k = 0; k < kSoloBatch; ++k) {
-      w[k] = t.self;
+      w[k] = s;
       if (k >= nb) continue;
       const int f = f0 + 32 * k + lane;
       if (single) {
         const int b0 = __shfl_sync(kFull, beg, 0);
-        w[k] = f < total ? __ldg(colidx + b0 + f) : t.self;
+        w[k] = f < total ? __ldg(p.colidx + b0 + f) : s;
         continue;
       }
       int o = 0;
@@ -740,25 +735,30 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       }
       const int ob = __shfl_sync(kFull, beg, o);
       const int oe = __shfl_sync(kFull, excl, o);
-      w[k] = f < total ? __ldg(colidx + ob + (f - oe)) : t.self;
+      w[k] = f < total ? __ldg(p.colidx + ob + (f - oe)) : s;
     }
 #pragma unroll
     for (int k = 0; k < kSoloBatch; ++k) {
       ro[k] = 1u;
       rb[k] = re[k] = 0;
-      iw[k] = w[k];
+      hw[k] = 0;
       if (k >= nb) continue;
       const uint32_t bw = vbit(w[k]);
-      // below the source: atomicMin(maxId(w), T) succeeds iff the source has
-      // not reached w yet (line 10 of fig:alg)
-      ro[k] = w[k] < t.blim ? atomicOr(SL_REACHED + (w[k] >> 5), bw) : bw;
-      // w < clim may join the closure: its row pointers travel with the atomic
-      if (w[k] < t.clim) {
-        rb[k] = __ldg(rowptr + w[k]);
-        re[k] = __ldg(rowptr + w[k] + 1);
+      // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds
+      // iff the source has not reached w yet (line 10 of fig:alg)
+      ro[k] = w[k] < s ? atomicOr(SL_REACHED + (w[k] >> 5), bw) : bw;
+      if (w[k] > s) {
+        // U entry: nothing waits for it -- two REDs (the summary bit is idempotent)
+        atomicOr(SL_IS + (w[k] >> 5), bw);
+        red_sum(SL_ISUM, w[k]);
       }
-      // U entries and fill candidates: their vertex id, for the structure bit
-      if (kH && w[k] >= t.flim && w[k] != t.self) iw[k] = __ldg(p.vert + w[k]);
+      // w < tmax may join the closure: its row pointers travel with the atomic
+      if (w[k] < t.tmax) {
+        rb[k] = __ldg(p.rowptr + w[k]);
+        re[k] = __ldg(p.rowptr + w[k] + 1);
+      }
+      // between the step's thresholds: its height decides (height order)
+      if (kH && w[k] > t.tmin && w[k] < t.tmax) hw[k] = __ldg(p.hgt + w[k]);
     }
 #pragma unroll
     for (int k = 0; k < kSoloBatch; ++k) {
@@ -766,28 +766,24 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       const int wk = w[k];
       const uint32_t bw = vbit(wk);
       {
-        // first visits: the reached bit of w below s was clear (else ro = bw)
+        // first visits: the reached bit of w < s was clear (w >= s: ro = bw)
         const uint32_t nv = __popc(__ballot_sync(kFull, !(ro[k] & bw)));
         if (lane == 0) sw.fv += nv;
-      }
-      if (wk >= t.ulim) {
-        // U entry: nothing waits for it -- two REDs (the summary bit is idempotent)
-        atomicOr(SL_IS + (iw[k] >> 5), vbit(iw[k]));
-        red_sum(SL_ISUM, iw[k]);
       }
       bool push = false;
       if (!(ro[k] & bw)) {
         if (ro[k] == 0u) red_sum(SL_RSUM, wk);
-        if (wk >= t.flim) {
+        if (wk > t.tmax || (kH && wk > t.tmin && hw[k] > t.h)) {
           // fill of L(s,:) (R4); w becomes a threshold of this source
-          atomicOr(SL_IS + (iw[k] >> 5), vbit(iw[k]));  // RED
-          red_sum(SL_ISUM, iw[k]);
-          const int d = (wk >> 5) - wb;
+          atomicOr(SL_IS + (wk >> 5), bw);  // RED
+          red_sum(SL_ISUM, wk);
+          const int q = kH ? __ldg(p.pos + wk) : wk;  // its bitmap position
+          const int d = (q >> 5) - wb;
           if (d < 32) {
-            atomicOr(&sw.win[d], bw);  // smem (d >= 0: after the step's thresholds)
+            atomicOr(&sw.win[d], vbit(q));  // smem (d >= 0: after the step's thresholds)
           } else {
-            atomicOr(SL_THR + (wk >> 5), bw);  // RED
-            red_sum(SL_TSUM, wk);
+            atomicOr(SL_THR + (q >> 5), vbit(q));  // RED
+            red_sum(SL_TSUM, q);
           }
         } else {
           push = true;  // maxId(w) = T, not in the structure: continue with T
@@ -831,41 +827,31 @@ __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const ui
 }
 
 // the max-id relaxation of source s in increasing threshold order -- by
-// vertex id, or (kH) by etree height in position space: a step then takes
-// every threshold of one height within the 32-word window (order.cu)
+// vertex id, or (kH) by etree height: the threshold bitmap is then indexed by
+// position (vertices sorted by (height, id)) and a step takes every threshold
+// of one height within the 32-word window (order.cu); the graph, reached and
+// structure bitmaps stay in vertex ids (the ND order's locality)
 template <bool kH>
 __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s,
                                             int lane, SoloWarpSmem &sw) {
-  const int32_t *__restrict__ rowptr = kH ? p.rowptrP : p.rowptr;
-  const int32_t *__restrict__ colidx = kH ? p.colidxP : p.colidx;
-  SoloStep t;
-  if (kH) {
-    const int ps = __ldg(p.pos + s), hs = __ldg(p.wkey + (ps >> 5));
-    t.self = ps;
-    t.blim = __ldg(p.seg + hs);      // subtree(s): heights below s's
-    t.ulim = __ldg(p.seg + hs + 1);  // ancestors of s: entries of U
-  } else {
-    t.self = s;
-    t.blim = s;
-    t.ulim = s + 1;
-  }
-  const int tbw = (t.blim + 31) >> 5;  // thresholds lie below the source
+  // threshold positions: below s (id order), anywhere in [0, n) (height order)
+  const int tbw = kH ? (p.n + 31) >> 5 : (s + 31) >> 5;
   // seed: the out-neighbours of s are in the structure; the
   // smaller ones are reached with maxId -1 and are thresholds
-  const int beg = __ldg(rowptr + t.self), end = __ldg(rowptr + t.self + 1);
+  const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
   for (int j0 = beg; j0 < end; j0 += 32) {
     const int j = j0 + lane;
-    const int w = j < end ? __ldg(colidx + j) : t.self;
-    const uint32_t nv = __popc(__ballot_sync(kFull, w < t.blim));  // first visits of the seeds
+    const int w = j < end ? __ldg(p.colidx + j) : s;
+    const uint32_t nv = __popc(__ballot_sync(kFull, w < s));  // first visits of the seeds
     if (lane == 0) sw.fv += nv;
-    if (w == t.self) continue;
-    const int iw = kH ? __ldg(p.vert + w) : w;  // vertex id (structure bitmap)
-    if (atomicOr(SL_IS + (iw >> 5), vbit(iw)) == 0u) red_sum(SL_ISUM, iw);
-    if (w < t.blim) {
-      const uint32_t bw = vbit(w);
+    if (w == s) continue;
+    const uint32_t bw = vbit(w);
+    if (atomicOr(SL_IS + (w >> 5), bw) == 0u) red_sum(SL_ISUM, w);
+    if (w < s) {
       if (atomicOr(SL_REACHED + (w >> 5), bw) == 0u) red_sum(SL_RSUM, w);
-      atomicOr(SL_THR + (w >> 5), bw);  // RED
-      red_sum(SL_TSUM, w);
+      const int q = kH ? __ldg(p.pos + w) : w;  // bitmap position
+      atomicOr(SL_THR + (q >> 5), vbit(q));     // RED
+      red_sum(SL_TSUM, q);
     }
   }
   __syncwarp();
@@ -877,26 +863,29 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
     if (lane == 0) sw.steps += 1;
     SoloQueue Q = {0, 0, 0, 0, false};
     int u = -1, ub = 0, ue = 0;
+    SoloStep t;
     if (kH) {
-      // the step: every threshold of height h = height(P) in the window at
-      // or after P -- the window words of h's segment (segments are
-      // word-aligned); the first word's items go to the lanes, the others
-      // to the worklist
-      const int word = P >> 5, h = __ldg(p.wkey + word);
-      t.clim = __ldg(p.seg + h);
-      t.flim = __ldg(p.seg + h + 1);
-      const int wend = min(wb + 32, t.flim >> 5);  // one past the last word of the step
-      for (int wi = word; wi < wend; ++wi) {
+      // the step: every threshold of h = height(P) in the window at or after
+      // P, i.e. positions [P, min(seg_end(h), window end)); the first word's
+      // items go to the lanes, the others to the worklist
+      const int2 hs = __ldg(p.pseg + P);  // {height, end of its segment}
+      t.h = hs.x;
+      const int lim = min(hs.y, (wb + 32) << 5);
+      int tmin = INT_MAX, tmax = -1;
+      for (int wi = P >> 5; (wi << 5) < lim; ++wi) {
         uint32_t x = sw.win[wi - wb];
-        if (wi == word) x &= kFull << (P & 31);
+        if (wi == (P >> 5)) x &= kFull << (P & 31);
+        if (lim - (wi << 5) < 32) x &= (1u << (lim - (wi << 5))) - 1u;
         const bool has = (x >> lane) & 1u;
-        const int v = (wi << 5) + lane;
-        int vb = 0, ve = 0;
+        int v = -1, vb = 0, ve = 0;
         if (has) {
-          vb = __ldg(rowptr + v);
-          ve = __ldg(rowptr + v + 1);
+          v = __ldg(p.vert + (wi << 5) + lane);
+          vb = __ldg(p.rowptr + v);
+          ve = __ldg(p.rowptr + v + 1);
+          tmin = min(tmin, v);
+          tmax = max(tmax, v);
         }
-        if (wi == word) {
+        if (wi == (P >> 5)) {
           // compact to the low lanes (the single-item fast path)
           const uint32_t b = __ballot_sync(kFull, has);
           const int src = __fns(b, 0, lane + 1) & 31;
@@ -910,18 +899,20 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
           solo_push(p, sl, sw, Q, has, v, vb, ve, lane);
         }
       }
-      P = (wend << 5) - 1;  // the next step starts after these words
+      t.tmin = __reduce_min_sync(kFull, tmin);
+      t.tmax = __reduce_max_sync(kFull, tmax);
+      P = lim - 1;  // the next step starts after these positions
     } else {
-      t.clim = P;
-      t.flim = P + 1;
+      t.tmin = t.tmax = P;
+      t.h = 0;
       if (lane == 0) {
         u = P;
-        ub = __ldg(rowptr + P);
-        ue = __ldg(rowptr + P + 1);
+        ub = __ldg(p.rowptr + P);
+        ue = __ldg(p.rowptr + P + 1);
       }
     }
     for (;;) {
-      solo_expand<kH>(p, sl, sw, wb, Q, t, u, ub, ue, lane);
+      solo_expand<kH>(p, sl, sw, wb, Q, s, t, u, ub, ue, lane);
       __syncwarp();
       if (Q.sh < Q.st) {
         const int cnt = min(32, Q.st - Q.sh);
@@ -938,11 +929,11 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       }
       if (Q.gh >= Q.gt && Q.spilled) {
         // the ring overflowed during this closure: move parked items (pend
-        // bits, all below clim) back into the ring, as many as fit
+        // bits, all below tmax) back into the ring, as many as fit
         Q.spilled = false;
         __syncwarp();
         fence_gpu();
-        const int pwords = (t.clim + 31) >> 5;
+        const int pwords = (t.tmax + 31) >> 5;
         for (int w0 = 0; w0 < pwords && !Q.spilled; w0 += 32) {
           const int wi = w0 + lane;
           uint32_t x = wi < pwords ? __ldcg(SL_PEND + wi) : 0u;
@@ -972,8 +963,8 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       u = lane < cnt ? (int)SL_QUEUE[(Q.gh + lane) & SL_QMASK] : -1;
       Q.gh += cnt;
       if (u >= 0) {
-        ub = __ldg(rowptr + u);
-        ue = __ldg(rowptr + u + 1);
+        ub = __ldg(p.rowptr + u);
+        ue = __ldg(p.rowptr + u + 1);
       }
     }
   }
@@ -1134,14 +1125,14 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
     fence_gpu();  // this warp's REDs are visible to its extraction
     __syncwarp();
     solo_stage_row(p, sl, s, g, lane);
-    // reset the touched words: reached | pend | thr (a threshold bit sits in
-    // the word of its reached bit), and the summaries
+    // reset the touched words: reached | pend (| thr in id order, where a
+    // threshold bit sits in the word of its reached bit), and the summaries
     for (int i0 = 0; i0 < Vs; i0 += 32) {
       const int i = i0 + lane;
       uint32_t x = i < Vs ? __ldcg(SL_RSUM + i) : 0u;
       if (x) {
         SL_RSUM[i] = 0u;
-        SL_TSUM[i] = 0u;
+        if (!kH) SL_TSUM[i] = 0u;
       }
       while (x) {
         const int b = __ffs(x) - 1;
@@ -1149,7 +1140,22 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
         const int wi = (i << 5) + b;
         SL_REACHED[wi] = 0u;
         SL_PEND[wi] = 0u;
-        SL_THR[wi] = 0u;
+        if (!kH) SL_THR[wi] = 0u;
+      }
+    }
+    if (kH) {
+      // height order: threshold bits sit at positions; the summary lists the
+      // global words written (window bits never reach global memory)
+      const int Ts = (int)(p.so_is - p.so_tsum);
+      for (int i0 = 0; i0 < Ts; i0 += 32) {
+        const int i = i0 + lane;
+        uint32_t x = i < Ts ? __ldcg(SL_TSUM + i) : 0u;
+        if (x) SL_TSUM[i] = 0u;
+        while (x) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1u;
+          SL_THR[(i << 5) + b] = 0u;
+        }
       }
     }
     // the clears are plain stores; the next source's atomics act at L2
@@ -1271,10 +1277,10 @@ int solo_ring(int64_t Vmax) {
 // [Ts] (summaries: one bit per word); is [nw], isum [ns] (structure over
 // [0, n)); the closure ring.  npos > 0: height order.  Returns the total.
 size_t solo_layout(int64_t Vmax, int64_t n, int64_t npos, StreamParams *p) {
-  // reached / pend / thr over vertex ids [0, Vmax), or positions [0, npos)
-  const int64_t V = npos > 0 ? npos : Vmax;
-  const size_t Vw = round4((size_t)((V + 31) / 32)), Vs = round4((Vw + 31) / 32);
-  const size_t Tw = Vw, Ts = Vs;
+  // reached / pend over vertex ids [0, Vmax); thr over ids [0, Vmax) or
+  // positions [0, npos) (height order)
+  const size_t Vw = round4((size_t)((Vmax + 31) / 32)), Vs = round4((Vw + 31) / 32);
+  const size_t Tw = npos > 0 ? round4((size_t)((npos + 31) / 32)) : Vw, Ts = round4((Tw + 31) / 32);
   const size_t nw = round4((size_t)((n + 31) / 32)), ns = round4((nw + 31) / 32);
   if (p) {
     p->so_pend = (uint32_t)Vw;
