@@ -25,15 +25,17 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "gp.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle.c with gcc (plain C, -O2, pthreads)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    """Compile oracle.c and gp.c with gcc (plain C, -O2, pthreads)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+            os.path.getmtime(f) for f in _SRCS):
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread",
-                               "-Wall", "-o", _LIB, _SRC])
+                               "-Wall", "-o", _LIB] + _SRCS)
     return _LIB
 
 
@@ -53,6 +55,10 @@ def _load():
         lib.oracle_supernodes.argtypes = [
             ctypes.c_int64, ctypes.c_int64, P(ctypes.c_int64), P(ctypes.c_int32),
             P(ctypes.c_int64), ctypes.c_int64, P(ctypes.c_int32)]
+        lib.oracle_gp.restype = ctypes.c_int
+        lib.oracle_gp.argtypes = [ctypes.c_int64, P(ctypes.c_int64), P(ctypes.c_int32),
+                                  P(P(ctypes.c_int64)), P(P(ctypes.c_int32)),
+                                  P(P(ctypes.c_int64)), P(P(ctypes.c_int32))]
         lib.oracle_free.restype = None
         lib.oracle_free.argtypes = [ctypes.c_void_p]
         _lib = lib
@@ -142,3 +148,41 @@ def symbolic(rowptr, colidx, chunk_size: int = 128, row_begin: int = 0,
              nnz_A_offdiag=nnz_a_off, fill_count=int(fill), row_begin=row_begin,
              row_end=row_end)
     return r
+
+
+def _cols_to_rows(cp, ri, n):
+    """Column-compressed pattern -> row-compressed (rows' columns ascending)."""
+    cols = np.repeat(np.arange(n, dtype=np.int64), np.diff(cp))
+    order = np.lexsort((cols, ri))                      # by row, then column
+    rows = ri[order].astype(np.int64)
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    return np.cumsum(rp), cols[order].astype(np.int32)
+
+
+def gp(rowptr, colidx):
+    """Second oracle: Gilbert-Peierls symbolic LU, column by
+    column; returned in the same row form as :func:`symbolic` (L strictly
+    lower, U with the diagonal first)."""
+    lib = _load()
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    n = rowptr.size - 1
+    P = ctypes.POINTER
+    lp, li, up, ui = P(ctypes.c_int64)(), P(ctypes.c_int32)(), P(ctypes.c_int64)(), P(ctypes.c_int32)()
+    cidx = colidx if colidx.size else np.zeros(1, np.int32)
+    rc = lib.oracle_gp(n, _ptr(rowptr, ctypes.c_int64), _ptr(cidx, ctypes.c_int32),
+                       ctypes.byref(lp), ctypes.byref(li), ctypes.byref(up), ctypes.byref(ui))
+    if rc != 0:
+        raise RuntimeError(f"oracle_gp failed rc={rc}")
+    try:
+        Lp = np.ctypeslib.as_array(lp, shape=(n + 1,)).copy()
+        Up = np.ctypeslib.as_array(up, shape=(n + 1,)).copy()
+        Li = np.ctypeslib.as_array(li, shape=(max(1, int(Lp[-1])),))[: int(Lp[-1])].copy()
+        Ui = np.ctypeslib.as_array(ui, shape=(max(1, int(Up[-1])),))[: int(Up[-1])].copy()
+    finally:
+        for q in (lp, li, up, ui):
+            lib.oracle_free(ctypes.cast(q, ctypes.c_void_p))
+    L_rowptr, L_colidx = _cols_to_rows(Lp, Li, n)
+    U_rowptr, U_colidx = _cols_to_rows(Up, Ui, n)
+    return dict(L_rowptr=L_rowptr, L_colidx=L_colidx, U_rowptr=U_rowptr, U_colidx=U_colidx)

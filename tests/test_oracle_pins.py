@@ -390,3 +390,53 @@ def test_supernodes_row_range_subset():
     # a chunk-aligned range reproduces the full partition restricted to it
     inside = [s for s in full["sn_start"].tolist() if 40 <= s < 100] + [100]
     assert part["sn_start"].tolist() == inside
+
+
+# ------------------------------------- the second oracle (Gilbert-Peierls) --
+# oracle.gp (oracle/gp.c): column-by-column reach through the columns of L
+# computed so far.  Independent of oracle.c (fill2 per row); both
+# are pinned to dense 0/1 Gaussian elimination here and to each other at mid
+# scale.
+
+def gp_dense(rowptr, colidx):
+    n = rowptr.size - 1
+    r = oracle.gp(rowptr, colidx)
+    M = np.zeros((n, n), dtype=bool)
+    for i in range(n):
+        Li = r["L_colidx"][r["L_rowptr"][i]:r["L_rowptr"][i + 1]]
+        Ui = r["U_colidx"][r["U_rowptr"][i]:r["U_rowptr"][i + 1]]
+        assert np.all(Li < i) and np.all(np.diff(Li) > 0)
+        assert Ui.size >= 1 and Ui[0] == i and np.all(np.diff(Ui) > 0)
+        M[i, Li] = True
+        M[i, Ui] = True
+    return M
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_gp_equals_dense_ge_random(seed):
+    rng = np.random.default_rng(70_000 + seed)
+    n = int(rng.integers(1, 65))
+    rp, ci = gen.random_graph(n, float(rng.uniform(0.02, 0.25)), seed=3000 + seed)
+    assert np.array_equal(gp_dense(rp, ci), dense_ge(rp, ci))
+
+
+def test_gp_paper_example():
+    """The worked example's row 8: L(8,:) = {1,2,3,4,5,7},
+    U(8,:) = {8,9}; fill (1,5) (P:229)."""
+    rp, ci = gen.paper_example()
+    r = oracle.gp(rp, ci)
+    L8 = r["L_colidx"][r["L_rowptr"][8]:r["L_rowptr"][9]].tolist()
+    U8 = r["U_colidx"][r["U_rowptr"][8]:r["U_rowptr"][9]].tolist()
+    assert L8 == [1, 2, 3, 4, 5, 7] and U8 == [8, 9]
+    assert 5 in r["U_colidx"][r["U_rowptr"][1]:r["U_rowptr"][2]].tolist()
+
+
+@pytest.mark.parametrize("name,scale", [("C1", None), ("C2", 16), ("C3", 4000), ("C4", 80),
+                                        ("C5", 20)])
+def test_gp_equals_fill2_mid_scale(name, scale):
+    """The two oracles agree element by element at mid scale (n up to 8k)."""
+    rp, ci = gen.config(name, scale)
+    a = oracle.gp(rp, ci)
+    b = oracle.rows(rp, ci)
+    for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx"):
+        assert np.array_equal(a[k], b[k]), k

@@ -504,3 +504,15 @@ def test_visit_stats(ctx, name, scale, monkeypatch):
     assert h["first_visits"] == t["first_visits"]
     assert h["source_expansions"] == h["first_visits"]
     assert h["edge_inspections"] == t["edge_inspections"]
+
+
+@pytest.mark.parametrize("name,scale", [("C2", 24), ("C3", 6000), ("C4", 150), ("C5", 24)])
+def test_second_oracle_gilbert_peierls(ctx, name, scale):
+    """The CUDA path against the independent second oracle (Gilbert-Peierls,
+    column by column) at mid scale, every schedule."""
+    rp, ci = gen.config(name, scale)
+    want = oracle.gp(rp, ci)
+    for sched in ("auto", "threshold", "height", "fifo"):
+        got = run(rp, ci, ctx, schedule=sched)
+        for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx"):
+            assert np.array_equal(got[k], want[k]), (sched, k)
