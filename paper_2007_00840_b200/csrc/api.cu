@@ -136,8 +136,8 @@ struct gsofa_context {
   int32_t *in_colidx = nullptr, *rowptr32 = nullptr;
   size_t in_rowptr_cap = 0, in_colidx_cap = 0, rowptr32_cap = 0;
   int64_t *h_small = nullptr;  // pinned host scratch
-  // height order (order.cu): heights | positions | inverse | per-position
-  // {height, segment end}, one grow-only buffer
+  // height order (order.cu): per-position records | heights | positions,
+  // one grow-only buffer
   int32_t *ord_buf = nullptr;
   size_t ord_cap = 0;
   HostBlock *hpool = nullptr;  // pinned storage reused by host-side results
@@ -960,9 +960,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       rp_h = hrp.data();
       ci_h = hci.data();
     }
-    std::vector<int32_t> hord((size_t)n * 5);  // hgt | pos | vert | pseg (2 per position)
-    gsofa::height_order(n, rp_h, ci_h, hord.data(), hord.data() + n, hord.data() + 2 * n,
-                        hord.data() + 3 * n);
+    std::vector<int32_t> hord((size_t)n * 6);  // posrec (4 per position) | hgt | pos
+    gsofa::height_order(n, rp_h, ci_h, hord.data() + 4 * n, hord.data() + 5 * n, hord.data());
     if ((rc = grow_device(&c->ord_buf, &c->ord_cap, hord.size(), st)) != GSOFA_OK) goto fail;
     CK(cudaMemcpyAsync(c->ord_buf, hord.data(), hord.size() * 4, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));  // the host vector goes out of scope
@@ -1136,10 +1135,9 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     gsofa::solo_layout(plan.Vmax, n, ord_npos, &sp);
     sp.hmode = ord_npos > 0;
     sp.npos = (int32_t)ord_npos;
-    sp.hgt = c->ord_buf;
-    sp.pos = c->ord_buf + n;
-    sp.vert = c->ord_buf + 2 * n;
-    sp.pseg = reinterpret_cast<const int2 *>(c->ord_buf + 3 * n);
+    sp.posrec = reinterpret_cast<const int4 *>(c->ord_buf);  // 16-byte aligned (buffer start)
+    sp.hgt = c->ord_buf + 4 * n;
+    sp.pos = c->ord_buf + 5 * n;
     if (plan.heavy > 0) {
       // the heaviest groups (top separator / hub rows) start on
       // the solo kernel: one per first-wave solo CTA (one per SM)

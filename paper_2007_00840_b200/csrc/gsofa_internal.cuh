@@ -98,10 +98,10 @@ struct StreamParams {
   // bitmaps then indexed by position (vertices sorted by (height, id), npos = n)
   int32_t hmode;
   int32_t npos;
+  const int4 *posrec;        // [n] per position: {vertex, rowptr, rowptr + 1, end of its
+                             //     height's segment of positions}
   const int32_t *hgt;        // [n] etree height of a vertex
   const int32_t *pos;        // [n] vertex -> position
-  const int32_t *vert;       // [n] position -> vertex
-  const int2 *pseg;          // [n] per position: {height, end of its height's segment}
   // solo slot layout: word offsets of its arrays (solo_layout)
   uint32_t so_pend, so_thr, so_rsum, so_tsum, so_is, so_isum, so_queue;
 };
@@ -118,10 +118,10 @@ int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos);
 size_t stream_smem_bytes(int64_t Vmax, int64_t npos);  // dynamic smem: threshold-word summary
 // order.cu (host): elimination tree of A + A^T and the height order
 void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *parent);
-// heights, positions (sorted by (height, id)), inverse, and per position
-// {height, segment end} (int2 as two int32) of the etree of A + A^T
+// etree heights, positions (sorted by (height, id)) and per position
+// {vertex, rowptr, rowptr + 1, segment end} (int4 as four int32)
 void height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *hgt,
-                  int32_t *pos, int32_t *vert, int32_t *pseg);
+                  int32_t *pos, int32_t *posrec);
 cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st);
 cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st);
 cudaError_t launch_gather(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,

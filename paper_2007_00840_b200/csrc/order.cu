@@ -81,11 +81,11 @@ void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t 
 }
 
 // Height order of the vertices (see the header comment), into caller
-// arrays of n entries: hgt (etree height), pos (vertex -> position, sorted by
-// (height, id)), vert (position -> vertex), pseg (per position, two int32:
-// its height and the end of that height's segment of positions).
+// arrays: hgt[n] (etree height), pos[n] (vertex -> position, sorted by
+// (height, id)), posrec[4n] (per position: vertex, rowptr[v], rowptr[v+1],
+// the end of v's height segment of positions).
 void height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *hgt,
-                  int32_t *pos, int32_t *vert, int32_t *pseg) {
+                  int32_t *pos, int32_t *posrec) {
   std::vector<int32_t> parent((size_t)n);
   etree_sym(n, rowptr, colidx, parent.data());
   int32_t H = 0;
@@ -101,9 +101,10 @@ void height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32
   for (int64_t v = 0; v < n; ++v) {
     const int64_t q = at[hgt[v]]++;
     pos[v] = (int32_t)q;
-    vert[q] = (int32_t)v;
-    pseg[2 * q] = hgt[v];
-    pseg[2 * q + 1] = (int32_t)seg[hgt[v] + 1];
+    posrec[4 * q + 0] = (int32_t)v;
+    posrec[4 * q + 1] = (int32_t)rowptr[v];
+    posrec[4 * q + 2] = (int32_t)rowptr[v + 1];
+    posrec[4 * q + 3] = (int32_t)seg[hgt[v] + 1];
   }
 }
 

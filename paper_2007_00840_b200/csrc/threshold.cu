@@ -713,7 +713,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
   // kSoloBatch batches of 32 (item, neighbour) pairs are in flight at once:
   // all their colidx loads, then all their atomics, then the pushes
   for (int f0 = 0; f0 < total; f0 += 32 * kSoloBatch) {
-    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch], hw[kSoloBatch];
+    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch], hw[kSoloBatch], qw[kSoloBatch];
     uint32_t ro[kSoloBatch];
     const int nb = min(kSoloBatch, (total - f0 + 31) >> 5);  // warp-uniform: skip empty batches
 #pragma unroll
@@ -742,6 +742,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       ro[k] = 1u;
       rb[k] = re[k] = 0;
       hw[k] = 0;
+      qw[k] = w[k];
       if (k >= nb) continue;
       const uint32_t bw = vbit(w[k]);
       // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds
@@ -757,8 +758,12 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
         rb[k] = __ldg(p.rowptr + w[k]);
         re[k] = __ldg(p.rowptr + w[k] + 1);
       }
-      // between the step's thresholds: its height decides (height order)
-      if (kH && w[k] > t.tmin && w[k] < t.tmax) hw[k] = __ldg(p.hgt + w[k]);
+      if (kH && w[k] > t.tmin && w[k] < s) {
+        // may be a fill: its threshold position travels with the atomic; between
+        // the step's thresholds its height decides (height order)
+        qw[k] = __ldg(p.pos + w[k]);
+        if (w[k] < t.tmax) hw[k] = __ldg(p.hgt + w[k]);
+      }
     }
 #pragma unroll
     for (int k = 0; k < kSoloBatch; ++k) {
@@ -777,7 +782,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
           // fill of L(s,:) (R4); w becomes a threshold of this source
           atomicOr(SL_IS + (wk >> 5), bw);  // RED
           red_sum(SL_ISUM, wk);
-          const int q = kH ? __ldg(p.pos + wk) : wk;  // its bitmap position
+          const int q = qw[k];  // its bitmap position
           const int d = (q >> 5) - wb;
           if (d < 32) {
             atomicOr(&sw.win[d], vbit(q));  // smem (d >= 0: after the step's thresholds)
@@ -868,10 +873,9 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       // the step: every threshold of h = height(P) in the window at or after
       // P, i.e. positions [P, min(seg_end(h), window end)); the first word's
       // items go to the lanes, the others to the worklist
-      const int2 hs = __ldg(p.pseg + P);  // {height, end of its segment}
-      t.h = hs.x;
-      const int lim = min(hs.y, (wb + 32) << 5);
-      int tmin = INT_MAX, tmax = -1;
+      // {vertex, rowptr, rowptr + 1, end of its height's segment}: one load
+      const int lim = min(__ldg(&p.posrec[P].w), (wb + 32) << 5);
+      int tmin = INT_MAX, tmax = -1, hh = 0;
       for (int wi = P >> 5; (wi << 5) < lim; ++wi) {
         uint32_t x = sw.win[wi - wb];
         if (wi == (P >> 5)) x &= kFull << (P & 31);
@@ -879,11 +883,13 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
         const bool has = (x >> lane) & 1u;
         int v = -1, vb = 0, ve = 0;
         if (has) {
-          v = __ldg(p.vert + (wi << 5) + lane);
-          vb = __ldg(p.rowptr + v);
-          ve = __ldg(p.rowptr + v + 1);
+          const int4 r = __ldg(p.posrec + (wi << 5) + lane);
+          v = r.x;
+          vb = r.y;
+          ve = r.z;
           tmin = min(tmin, v);
           tmax = max(tmax, v);
+          hh = __ldg(p.hgt + v);  // the step's height (used between tmin and tmax only)
         }
         if (wi == (P >> 5)) {
           // compact to the low lanes (the single-item fast path)
@@ -901,6 +907,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       }
       t.tmin = __reduce_min_sync(kFull, tmin);
       t.tmax = __reduce_max_sync(kFull, tmax);
+      t.h = __reduce_max_sync(kFull, hh);
       P = lim - 1;  // the next step starts after these positions
     } else {
       t.tmin = t.tmax = P;
