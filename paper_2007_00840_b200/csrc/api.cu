@@ -1107,6 +1107,16 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.failed_need = failed_need;
     sp.stats = c->stats;
     sp.group_trace = nullptr;
+    sp.src_trace = nullptr;
+    const char *src_trace_path = std::getenv("GSOFA_SRC_TRACE");  // dev: per-source trace dump
+    if (src_trace_path) {
+      if (cudaMallocAsync((void **)&sp.src_trace, (size_t)rows * 32, st) != cudaSuccess) {
+        cudaGetLastError();
+        sp.src_trace = nullptr;
+      } else {
+        cudaMemsetAsync(sp.src_trace, 0, (size_t)rows * 32, st);
+      }
+    }
     sp.debug = nullptr;
     if (std::getenv("GSOFA_CHECK_CLEAN")) {
       cudaMallocAsync((void **)&sp.debug, 256, st);
@@ -1216,6 +1226,16 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       grid = std::min<int64_t>(plan.light, nf);
       sp.abort_cycles = 0;  // retries run on the lockstep kernel alone
       sp.solo_top = 0;
+    }
+    if (sp.src_trace) {
+      std::vector<long long> h((size_t)rows * 4);
+      cudaMemcpyAsync(h.data(), sp.src_trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      if (FILE *f = std::fopen(src_trace_path, "wb")) {
+        std::fwrite(h.data(), 8, h.size(), f);
+        std::fclose(f);
+      }
+      cudaFreeAsync(sp.src_trace, st);
     }
     if (sp.group_trace) {
       std::vector<long long> h((size_t)ngroups * 8);

@@ -91,6 +91,7 @@ struct StreamParams {
   unsigned long long *failed_need;
   unsigned long long *stats; // items, edges, levels, thresholds, pairs
   long long *group_trace;    // optional [ngroups][8]: steps, levels, items, cycles, ...
+  long long *src_trace;      // optional [rows][4] (solo sources): start ns, end ns, steps, levels
   int *debug;                // optional dev checks
   // processing order of the solo kernel's thresholds (order.cu): hmode = 0:
   // increasing vertex id (one threshold per step); hmode = 1: increasing etree

@@ -1128,7 +1128,19 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
     if (g < 0) break;
     const int s = p.row_begin + 32 * g + k;
     if (s >= p.row_end) continue;  // tail of the last group
+    unsigned long long t0 = 0;
+    if (p.src_trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     solo_source<kH>(p, sl, s, lane, sw);
+    if (p.src_trace && lane == 0) {
+      // dev trace (GSOFA_SRC_TRACE): start / end ns, steps, levels of this source
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      long long *tr = p.src_trace + 4 * (size_t)(s - p.row_begin);
+      tr[0] = (long long)t0;
+      tr[1] = (long long)t1;
+      tr[2] = sw.steps;
+      tr[3] = sw.levels;
+    }
     fence_gpu();  // this warp's REDs are visible to its extraction
     __syncwarp();
     solo_stage_row(p, sl, s, g, lane);

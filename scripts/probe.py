@@ -49,3 +49,17 @@ if os.environ.get("GSOFA_GROUP_TRACE"):
     for q in (50, 90, 99, 99.9):
         print(f"  p{q}: ms={np.percentile(ms, q):.3f} steps={np.percentile(t[:,0], q):.0f} levels={np.percentile(t[:,1], q):.0f}")
     print(f"  sum traverse ms {t[:,4].sum()/1.965e6:.0f}  extract ms {t[:,5].sum()/1.965e6:.0f}  total {ms.sum():.0f}")
+if os.environ.get("GSOFA_SRC_TRACE"):
+    import numpy as np
+    t = np.fromfile(os.environ["GSOFA_SRC_TRACE"], dtype=np.int64).reshape(-1, 4)
+    solo = np.nonzero(t[:, 1])[0]
+    if solo.size:
+        t0 = t[solo, 0].min()
+        dur = (t[solo, 1] - t[solo, 0]) / 1e6
+        order = solo[np.argsort(-dur)]
+        print(f"solo sources {solo.size}; last end {(t[solo, 1].max() - t0) / 1e6:.1f} ms after the first start")
+        print("top sources: row  start_ms  dur_ms  steps  levels  us/level")
+        for r in order[:12]:
+            d = (t[r, 1] - t[r, 0]) / 1e6
+            print(f"  {r:8d} {(t[r, 0] - t0) / 1e6:9.2f} {d:8.2f} {t[r, 2]:7d} {t[r, 3]:8d} "
+                  f"{1e3 * d / max(1, t[r, 3]):8.2f}")
