@@ -221,7 +221,7 @@ bool make_plan(int schedule, int64_t n, int64_t rows, int64_t vb_max, int64_t cm
 // sources").
 // npos > 0: height order (threshold bitmaps over npos positions, order.cu)
 bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int device, Plan &p,
-                      int64_t npos) {
+                      int64_t npos, bool wide) {
   // the lockstep kernel runs id order (its slots do not depend on npos)
   if (gsofa::stream_smem_bytes(Vmax, 0) > 200 * 1024) return false;
   const size_t ws = gsofa::stream_ws_words(Vmax, 0), isw = gsofa::stream_is_words(n);
@@ -234,8 +234,8 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const int64_t ngroups = ceil_div(rows, 32);
   const int64_t wpc = gsofa::stream_warps_per_cta();  // lockstep slots (warps) per CTA
-  const int64_t res_light = gsofa::stream_max_blocks(device, Vmax, 0, npos) * wpc;
-  const int64_t res_heavy = gsofa::stream_max_blocks(device, Vmax, 1, npos);
+  const int64_t res_light = gsofa::stream_max_blocks(device, Vmax, 0, npos, wide) * wpc;
+  const int64_t res_heavy = gsofa::stream_max_blocks(device, Vmax, 1, npos, wide);
   if (res_light < 1) return false;
   // solo CTAs: one per SM is resident next to the lockstep CTAs from the
   // start; more become resident as lockstep CTAs finish (the grid is
@@ -247,7 +247,7 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
   (void)res_heavy;
   if (const char *e = std::getenv("GSOFA_SOLO_CTAS")) heavy = std::min<int64_t>(heavy, atoll(e));
   heavy = std::max<int64_t>(0, std::min<int64_t>(heavy, (int64_t)(((size_t)budget - fixed) / 2 / per_heavy)));
-  int64_t light = heavy > 0 ? (int64_t)sms * gsofa::stream_light_per_sm_with_solo(device, Vmax, npos) * wpc
+  int64_t light = heavy > 0 ? (int64_t)sms * gsofa::stream_light_per_sm_with_solo(device, Vmax, npos, wide) * wpc
                             : res_light;
   if (res_heavy < 1) heavy = 0;
   light = std::min<int64_t>(light, res_light);
@@ -489,7 +489,7 @@ int gsofa_context_create(int32_t device, int64_t mem_budget_bytes, gsofa_context
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  c->stream_blocks = gsofa::stream_max_blocks(device, 1 << 20, 0, 0);
+  c->stream_blocks = gsofa::stream_max_blocks(device, 1 << 20, 0, 0, false);
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&c->clock_khz, cudaDevAttrClockRate, device);
   c->max_blocks[0] = gsofa::traverse_max_blocks(device, 0);
@@ -876,6 +876,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   Plan plan;
   bool auto_fifo = false;
   int64_t ord_npos = 0;  // > 0: height order
+  // solo kernel shape: dev knob for now
+  const bool solo_wide = std::getenv("GSOFA_SOLO_WIDE") && atoi(std::getenv("GSOFA_SOLO_WIDE")) != 0;
 
   CK(cudaSetDevice(c->device));
   e_start = ev();
@@ -972,7 +974,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     const int64_t cmax_req =
         o.max_concurrent ? o.max_concurrent : 65536;  // FIFO: one batch when it fits (C3 -6% vs 16k)
     const int64_t budget_req = o.mem_budget_bytes ? o.mem_budget_bytes : c->budget;
-    int64_t key[7] = {o.schedule, n, rb, re, budget_req, cmax_req, ord_npos};
+    int64_t key[7] = {o.schedule, n, rb, re, budget_req, cmax_req, ord_npos * 2 + solo_wide};
     bool ok = true;
     if (std::equal(key, key + 7, c->plan_key)) {
       plan = c->plan_cache;
@@ -983,13 +985,13 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       ok = o.schedule == GSOFA_SCHEDULE_FIFO
                ? make_plan(o.schedule, n, rows, vb_max, cmax_req, budget, plan)
                : make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan,
-                                  ord_npos);
+                                  ord_npos, solo_wide);
       if (!ok && auto_fifo) {
         // AUTO picked FIFO but its smallest batch does not fit: threshold
         // order needs far less memory per source (no maxId labels)
         o.schedule = GSOFA_SCHEDULE_THRESHOLD;
         key[0] = o.schedule;
-        ok = make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan, 0);
+        ok = make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan, 0, solo_wide);
       }
       if (ok && !std::getenv("GSOFA_LIGHT_CTAS") && !std::getenv("GSOFA_SOLO_CTAS") &&
           !std::getenv("GSOFA_SOLO_RING")) {
@@ -1144,6 +1146,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.abort_cycles = 0;
     gsofa::solo_layout(plan.Vmax, n, ord_npos, &sp);
     sp.hmode = ord_npos > 0;
+    sp.wide = solo_wide;
     sp.npos = (int32_t)ord_npos;
     sp.posrec = reinterpret_cast<const int4 *>(c->ord_buf);  // 16-byte aligned (buffer start)
     sp.hgt = c->ord_buf + 4 * n;

@@ -5,10 +5,10 @@
 // finished structure, not part of the traversal.
 //
 //   1. expand the row pointers: row[e] = row_begin + r for every entry e of row r
-//   2. stable radix sort of (column, row) pairs by column (CUB): entries come in
-//      row-major order, so the rows of each column stay ascending
+//   2. stable radix sort of (column, row) pairs by column (radix.cu, 64-bit
+//      counts: C5's L has 2.2e9 entries): entries come in row-major order, so
+//      the rows of each column stay ascending
 //   3. col_ptr[j] = first position whose column is >= j (binary search)
-#include <cub/device/device_radix_sort.cuh>
 
 #include "gsofa_internal.cuh"
 
@@ -42,35 +42,43 @@ cudaError_t l_rows_to_csc(const int64_t *L_rowptr, const int32_t *L_colidx, int6
                           int64_t row_begin, int64_t n, int64_t nnz, int64_t *col_ptr,
                           int32_t *row_idx, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
-  int32_t *keys_in = nullptr, *keys_out = nullptr, *vals_in = nullptr;
-  void *tmp = nullptr;
-  size_t tmp_bytes = 0;
+  uint32_t *ka = nullptr, *kb = nullptr;
+  int32_t *vtmp = nullptr;
+  void *hist = nullptr;
   int bits = 1;
   while (bits < 31 && (int64_t(1) << bits) < n) ++bits;
+  const int passes = (bits + 7) / 8;
+  const int grid = radix_grid();
+  uint32_t *sorted = nullptr;
   if (nnz > 0) {
-    if ((e = cudaMallocAsync((void **)&keys_in, (size_t)nnz * 4, st)) != cudaSuccess) goto done;
-    if ((e = cudaMallocAsync((void **)&keys_out, (size_t)nnz * 4, st)) != cudaSuccess) goto done;
-    if ((e = cudaMallocAsync((void **)&vals_in, (size_t)nnz * 4, st)) != cudaSuccess) goto done;
-    if ((e = cudaMemcpyAsync(keys_in, L_colidx, (size_t)nnz * 4, cudaMemcpyDeviceToDevice, st)) !=
+    if ((e = cudaMallocAsync((void **)&ka, (size_t)nnz * 4, st)) != cudaSuccess) goto done;
+    if ((e = cudaMallocAsync((void **)&kb, (size_t)nnz * 4, st)) != cudaSuccess) goto done;
+    if ((e = cudaMallocAsync((void **)&vtmp, (size_t)nnz * 4, st)) != cudaSuccess) goto done;
+    if ((e = cudaMallocAsync(&hist, radix_hist_bytes(grid), st)) != cudaSuccess) goto done;
+    if ((e = cudaMemcpyAsync(ka, L_colidx, (size_t)nnz * 4, cudaMemcpyDeviceToDevice, st)) !=
         cudaSuccess)
       goto done;
-    row_expand_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(L_rowptr, rows, row_begin, vals_in);
-    if ((e = cudaGetLastError()) != cudaSuccess) goto done;
-    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, vals_in, row_idx,
-                                             nnz, 0, bits, st)) != cudaSuccess)
-      goto done;
-    if ((e = cudaMallocAsync(&tmp, tmp_bytes, st)) != cudaSuccess) goto done;
-    if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, row_idx, nnz,
-                                             0, bits, st)) != cudaSuccess)
-      goto done;
+    {
+      // the row values ping-pong between row_idx and vtmp: start where an
+      // odd / even number of passes makes them end in row_idx
+      int32_t *v0 = (passes & 1) ? vtmp : row_idx, *v1 = (passes & 1) ? row_idx : vtmp;
+      row_expand_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(L_rowptr, rows, row_begin, v0);
+      if ((e = cudaGetLastError()) != cudaSuccess) goto done;
+      bool in_tmp = false;
+      if ((e = radix_sort_pairs_u32(ka, v0, kb, v1, nnz, bits, hist, grid, st, &in_tmp)) !=
+          cudaSuccess)
+        goto done;
+      sorted = in_tmp ? kb : ka;
+    }
   }
-  colptr_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(keys_out, nnz, n, col_ptr);
+  colptr_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>((const int32_t *)sorted, nnz, n,
+                                                                 col_ptr);
   e = cudaGetLastError();
 done:
-  if (tmp) cudaFreeAsync(tmp, st);
-  if (keys_in) cudaFreeAsync(keys_in, st);
-  if (keys_out) cudaFreeAsync(keys_out, st);
-  if (vals_in) cudaFreeAsync(vals_in, st);
+  if (hist) cudaFreeAsync(hist, st);
+  if (ka) cudaFreeAsync(ka, st);
+  if (kb) cudaFreeAsync(kb, st);
+  if (vtmp) cudaFreeAsync(vtmp, st);
   return e;
 }
 
@@ -79,7 +87,8 @@ done:
 // ------------------------------------------------------------------ permute
 // B = P A P^T for the ordering perm (new vertex i = old vertex perm[i]):
 // B(i, j) != 0 iff A(perm[i], perm[j]) != 0.  Entries become 64-bit keys
-// (i << 32 | iperm[col]); one radix sort orders them by row, then column.
+// (i << bits | iperm[col]); one radix sort (radix.cu) orders them by row,
+// then column.
 namespace gsofa {
 namespace {
 
@@ -96,14 +105,14 @@ __global__ void iperm_kernel(const int32_t *perm, int64_t n, int32_t *iperm, int
 
 __global__ void perm_keys_kernel(const int64_t *rowptr, const int32_t *colidx, const int32_t *perm,
                                  const int32_t *iperm, int64_t n, const int64_t *new_rowptr,
-                                 unsigned long long *keys) {
+                                 int bits, unsigned long long *keys) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= n) return;
   const int32_t r = perm[i];
   const int64_t a = rowptr[r], b = rowptr[r + 1], o = new_rowptr[i];
   for (int64_t e = a + lane; e < b; e += 32)
-    keys[o + (e - a)] = ((unsigned long long)i << 32) | (uint32_t)iperm[colidx[e]];
+    keys[o + (e - a)] = ((unsigned long long)i << bits) | (uint32_t)iperm[colidx[e]];
 }
 
 __global__ void perm_degree_kernel(const int64_t *rowptr, const int32_t *perm, int64_t n,
@@ -112,9 +121,10 @@ __global__ void perm_degree_kernel(const int64_t *rowptr, const int32_t *perm, i
   if (i < n) deg[i] = (int32_t)(rowptr[perm[i] + 1] - rowptr[perm[i]]);
 }
 
-__global__ void perm_split_kernel(const unsigned long long *keys, int64_t nnz, int32_t *colidx) {
+__global__ void perm_split_kernel(const unsigned long long *keys, int64_t nnz, int bits,
+                                  int32_t *colidx) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < nnz) colidx[e] = (int32_t)(keys[e] & 0xFFFFFFFFull);
+  if (e < nnz) colidx[e] = (int32_t)(keys[e] & ((1ull << bits) - 1ull));
 }
 
 }  // namespace
@@ -141,27 +151,26 @@ cudaError_t permute_pattern(const int64_t *rowptr, const int32_t *colidx, const 
                             int32_t *new_colidx, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   unsigned long long *k0 = nullptr, *k1 = nullptr;
-  void *tmp = nullptr;
-  size_t tmp_bytes = 0;
+  void *hist = nullptr;
   int bits = 1;
   while (bits < 31 && (int64_t(1) << bits) < n) ++bits;
+  const int grid = radix_grid();
+  bool in_tmp = false;
   if (nnz == 0) return cudaSuccess;
   if ((e = cudaMallocAsync((void **)&k0, (size_t)nnz * 8, st)) != cudaSuccess) goto done;
   if ((e = cudaMallocAsync((void **)&k1, (size_t)nnz * 8, st)) != cudaSuccess) goto done;
+  if ((e = cudaMallocAsync(&hist, radix_hist_bytes(grid), st)) != cudaSuccess) goto done;
   perm_keys_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(rowptr, colidx, perm, iperm, n, new_rowptr,
-                                                             k0);
+                                                             bits, k0);
   if ((e = cudaGetLastError()) != cudaSuccess) goto done;
-  // one sort over row (high word) and column (low word) bits
-  if ((e = cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, k0, k1, nnz, 0, 32 + bits, st)) !=
-      cudaSuccess)
+  // one sort of (row << bits | column) keys: 2 * bits key bits
+  if ((e = radix_sort_keys_u64(k0, k1, nnz, 2 * bits, hist, grid, st, &in_tmp)) != cudaSuccess)
     goto done;
-  if ((e = cudaMallocAsync(&tmp, tmp_bytes, st)) != cudaSuccess) goto done;
-  if ((e = cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, k0, k1, nnz, 0, 32 + bits, st)) != cudaSuccess)
-    goto done;
-  perm_split_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(k1, nnz, new_colidx);
+  perm_split_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(in_tmp ? k1 : k0, nnz, bits,
+                                                                   new_colidx);
   e = cudaGetLastError();
 done:
-  if (tmp) cudaFreeAsync(tmp, st);
+  if (hist) cudaFreeAsync(hist, st);
   if (k0) cudaFreeAsync(k0, st);
   if (k1) cudaFreeAsync(k1, st);
   return e;

@@ -99,6 +99,7 @@ struct StreamParams {
   // bitmaps then indexed by position (vertices sorted by (height, id), npos = n)
   int32_t hmode;
   int32_t npos;
+  int32_t wide;              // solo kernel shape: 0 = throughput (48 warps/SM), 1 = latency (4 batches)
   const int4 *posrec;        // [n] per position: {vertex, rowptr, rowptr + 1, end of its
                              //     height's segment of positions}
   const int32_t *hgt;        // [n] etree height of a vertex
@@ -108,14 +109,14 @@ struct StreamParams {
 };
 size_t stream_ws_words(int64_t Vmax, int64_t npos);
 size_t stream_is_words(int64_t n);
-int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos);
+int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos, bool wide);
 int stream_heavy_ratio();  // warps of a solo CTA / warps of a lockstep CTA
 int stream_warps_per_cta();  // lockstep slots (one group per warp) per CTA
 size_t solo_ws_words(int64_t Vmax, int64_t n, int64_t npos);  // per solo slot (one warp, one source)
 size_t solo_layout(int64_t Vmax, int64_t n, int64_t npos, StreamParams *p);  // + offsets
 int solo_warps_per_cta();
 int solo_ring(int64_t Vmax);
-int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos);
+int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos, bool wide);
 size_t stream_smem_bytes(int64_t Vmax, int64_t npos);  // dynamic smem: threshold-word summary
 // order.cu (host): elimination tree of A + A^T and the height order
 void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *parent);
@@ -134,6 +135,18 @@ cudaError_t launch_gather(const int32_t *stage, const int64_t *row_off, const in
 cudaError_t l_rows_to_csc(const int64_t *L_rowptr, const int32_t *L_colidx, int64_t rows,
                           int64_t row_begin, int64_t n, int64_t nnz, int64_t *col_ptr,
                           int32_t *row_idx, cudaStream_t st);
+
+// radix.cu: stable LSD radix sort (8-bit digits, 64-bit counts); the result
+// is in the input or the tmp arrays (*result_in_tmp); hist scratch of
+// radix_hist_bytes(grid) bytes
+size_t radix_hist_bytes(int grid);
+inline int radix_grid() { return 296; }  // 2 persistent 1024-thread CTAs per SM
+cudaError_t radix_sort_pairs_u32(uint32_t *keys, int32_t *vals, uint32_t *keys_tmp, int32_t *vals_tmp,
+                                 int64_t n, int key_bits, void *hist, int grid, cudaStream_t st,
+                                 bool *result_in_tmp);
+cudaError_t radix_sort_keys_u64(unsigned long long *keys, unsigned long long *keys_tmp, int64_t n,
+                                int key_bits, void *hist, int grid, cudaStream_t st,
+                                bool *result_in_tmp);
 
 // csc.cu: symmetric permutation B = P A P^T of a pattern (device arrays)
 cudaError_t launch_iperm(const int32_t *perm, int64_t n, int32_t *iperm, int *bad, cudaStream_t st);

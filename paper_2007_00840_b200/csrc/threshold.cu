@@ -549,10 +549,6 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
 //   is[nw] isum[nw/32]             in-structure bitmap over [0, n) + touched words
 //   ring[R]                        closure overflow (vertex ids)
 constexpr int kSoloQ = 64;  // shared-memory closure worklist entries per warp
-#ifndef GSOFA_SOLO_BATCH
-#define GSOFA_SOLO_BATCH 1
-#endif
-constexpr int kSoloBatch = GSOFA_SOLO_BATCH;  // 32-pair batches a solo warp keeps in flight
 
 
 
@@ -682,7 +678,7 @@ __device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot 
 // of the current step t of source s.  Thresholds are kept at their bitmap
 // position: the vertex id (id order) or pos(w) (height order, loaded for
 // each new fill).
-template <bool kH>
+template <bool kH, int kB>
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
                                             SoloWarpSmem &sw, int wb, SoloQueue &Q, int s,
                                             const SoloStep &t, int u, int beg, int end,
@@ -710,14 +706,14 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       sw.levels += 1;
     }
   }
-  // kSoloBatch batches of 32 (item, neighbour) pairs are in flight at once:
+  // kB batches of 32 (item, neighbour) pairs are in flight at once:
   // all their colidx loads, then all their atomics, then the pushes
-  for (int f0 = 0; f0 < total; f0 += 32 * kSoloBatch) {
-    int w[kSoloBatch], rb[kSoloBatch], re[kSoloBatch], hw[kSoloBatch], qw[kSoloBatch];
-    uint32_t ro[kSoloBatch];
-    const int nb = min(kSoloBatch, (total - f0 + 31) >> 5);  // warp-uniform: skip empty batches
+  for (int f0 = 0; f0 < total; f0 += 32 * kB) {
+    int w[kB], rb[kB], re[kB], hw[kB], qw[kB];
+    uint32_t ro[kB];
+    const int nb = min(kB, (total - f0 + 31) >> 5);  // warp-uniform: skip empty batches
 #pragma unroll
-    for (int k = 0; k < kSoloBatch; ++k) {
+    for (int k = 0; k < kB; ++k) {
       w[k] = s;
       if (k >= nb) continue;
       const int f = f0 + 32 * k + lane;
@@ -738,7 +734,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       w[k] = f < total ? __ldg(p.colidx + ob + (f - oe)) : s;
     }
 #pragma unroll
-    for (int k = 0; k < kSoloBatch; ++k) {
+    for (int k = 0; k < kB; ++k) {
       ro[k] = 1u;
       rb[k] = re[k] = 0;
       hw[k] = 0;
@@ -766,7 +762,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       }
     }
 #pragma unroll
-    for (int k = 0; k < kSoloBatch; ++k) {
+    for (int k = 0; k < kB; ++k) {
       if (k >= nb) continue;
       const int wk = w[k];
       const uint32_t bw = vbit(wk);
@@ -836,7 +832,7 @@ __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const ui
 // position (vertices sorted by (height, id)) and a step takes every threshold
 // of one height within the 32-word window (order.cu); the graph, reached and
 // structure bitmaps stay in vertex ids (the ND order's locality)
-template <bool kH>
+template <bool kH, int kB>
 __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s,
                                             int lane, SoloWarpSmem &sw) {
   // threshold positions: below s (id order), anywhere in [0, n) (height order)
@@ -919,7 +915,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       }
     }
     for (;;) {
-      solo_expand<kH>(p, sl, sw, wb, Q, s, t, u, ub, ue, lane);
+      solo_expand<kH, kB>(p, sl, sw, wb, Q, s, t, u, ub, ue, lane);
       __syncwarp();
       if (Q.sh < Q.st) {
         const int cnt = min(32, Q.st - Q.sh);
@@ -1072,13 +1068,15 @@ __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const Solo
   return ok;
 }
 
-#ifndef GSOFA_SOLO_MINB
-// 48 warps per SM (40 registers, one 32-pair batch in flight): measured best
-// against 32 warps / 64 registers and 64 warps / 32 registers
-#define GSOFA_SOLO_MINB (48 / kSoloWarps)
-#endif
-template <bool kH>
-__global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(StreamParams p) {
+// Two shapes: kB = 1: 48 warps per SM (40 registers, one
+// 32-pair batch in flight per warp) -- the throughput shape, measured best
+// against 32 warps / 64 registers and 64 warps / 32 registers when sources
+// outnumber warps; kB = 4 ("wide"): 32 warps per SM, a level's first 128
+// pairs in flight at once -- the latency shape for chain-bound sources (few
+// heavy sources: C4's hub rows, the top-separator ranges of a multi-GPU split)
+template <bool kH, int kB>
+__global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 32 / kSoloWarps)
+    solo_kernel(StreamParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rows = p.row_end - p.row_begin;
   const size_t slot = (size_t)blockIdx.x * kSoloWarps + warp;
@@ -1130,7 +1128,7 @@ __global__ void __launch_bounds__(kSoloWarps * 32, GSOFA_SOLO_MINB) solo_kernel(
     if (s >= p.row_end) continue;  // tail of the last group
     unsigned long long t0 = 0;
     if (p.src_trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    solo_source<kH>(p, sl, s, lane, sw);
+    solo_source<kH, kB>(p, sl, s, lane, sw);
     if (p.src_trace && lane == 0) {
       // dev trace (GSOFA_SRC_TRACE): start / end ns, steps, levels of this source
       unsigned long long t1;
@@ -1231,17 +1229,18 @@ size_t stream_smem_bytes(int64_t Vmax, int64_t npos) {
 
 // kernel instances of the two threshold orders (kH = height order)
 const void *stream_fn(bool) { return (const void *)stream_kernel; }  // id order only
-const void *solo_fn(bool h) {
-  return h ? (const void *)solo_kernel<true> : (const void *)solo_kernel<false>;
+const void *solo_fn(bool h, bool wide) {
+  if (wide) return h ? (const void *)solo_kernel<true, 4> : (const void *)solo_kernel<false, 4>;
+  return h ? (const void *)solo_kernel<true, 1> : (const void *)solo_kernel<false, 1>;
 }
 
-int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos) {
+int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos, bool wide) {
   int sms = 0, per = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
   cudaError_t e;
   const bool h = npos > 0;
   if (heavy) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solo_fn(h), kSoloWarps * 32, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solo_fn(h, wide), kSoloWarps * 32, 0);
   } else {
     const size_t smem = stream_smem_bytes(Vmax, 0);  // the lockstep kernel runs id order
     if (smem > 48 * 1024 &&
@@ -1259,10 +1258,10 @@ int stream_heavy_ratio() { return kSoloWarps / kLightWarps; }
 int stream_warps_per_cta() { return 1; }  // slots are CTAs
 
 // lockstep CTAs that still fit on an SM next to one solo CTA
-int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos) {
+int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos, bool wide) {
   cudaFuncAttributes fs, fl;
   const bool h = npos > 0;
-  if (cudaFuncGetAttributes(&fs, solo_fn(h)) != cudaSuccess ||
+  if (cudaFuncGetAttributes(&fs, solo_fn(h, wide)) != cudaSuccess ||
       cudaFuncGetAttributes(&fl, stream_fn(h)) != cudaSuccess)
     return 0;
   int regs = 0, warps = 0, smem_sm = 0;
@@ -1332,8 +1331,13 @@ cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st) {
 
 cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st) {
   if (grid <= 0) return cudaSuccess;
-  if (p.hmode) solo_kernel<true><<<grid, kSoloWarps * 32, 0, st>>>(p);
-  else solo_kernel<false><<<grid, kSoloWarps * 32, 0, st>>>(p);
+  if (p.wide) {
+    if (p.hmode) solo_kernel<true, 4><<<grid, kSoloWarps * 32, 0, st>>>(p);
+    else solo_kernel<false, 4><<<grid, kSoloWarps * 32, 0, st>>>(p);
+  } else {
+    if (p.hmode) solo_kernel<true, 1><<<grid, kSoloWarps * 32, 0, st>>>(p);
+    else solo_kernel<false, 1><<<grid, kSoloWarps * 32, 0, st>>>(p);
+  }
   return cudaGetLastError();
 }
 
