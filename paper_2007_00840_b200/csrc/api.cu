@@ -876,6 +876,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   Plan plan;
   bool auto_fifo = false;
   int64_t ord_npos = 0;  // > 0: height order
+  std::vector<int64_t> ord_hrp;              // host copies of a device CSR (height order)
+  std::vector<int32_t> ord_hci, ord_host;    // ... and the order arrays before upload
   // solo kernel shape: dev knob for now
   const bool solo_wide = std::getenv("GSOFA_SOLO_WIDE") && atoi(std::getenv("GSOFA_SOLO_WIDE")) != 0;
 
@@ -946,28 +948,11 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     o.schedule = auto_fifo ? GSOFA_SCHEDULE_FIFO : GSOFA_SCHEDULE_THRESHOLD;
   }
   // ---------------------------------------------------- A2: height order
+  // positions are a permutation of [0, n): the plan does not depend on the
+  // tree, which is computed on the host while the lockstep kernel runs
   if (o.schedule == GSOFA_SCHEDULE_HEIGHT) {
-    // elimination tree of A + A^T, heights and (height, id) positions
-    // (order.cu): host computation of the plan, O(nnz alpha)
-    std::vector<int64_t> hrp;
-    std::vector<int32_t> hci;
-    const int64_t *rp_h = rowptr;
-    const int32_t *ci_h = colidx;
-    if (in_dev) {
-      hrp.resize((size_t)n + 1);
-      hci.resize((size_t)std::max<int64_t>(nnz, 1));
-      CK(cudaMemcpyAsync(hrp.data(), rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-      if (nnz) CK(cudaMemcpyAsync(hci.data(), colidx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      rp_h = hrp.data();
-      ci_h = hci.data();
-    }
-    std::vector<int32_t> hord((size_t)n * 6);  // posrec (4 per position) | hgt | pos
-    gsofa::height_order(n, rp_h, ci_h, hord.data() + 4 * n, hord.data() + 5 * n, hord.data());
-    if ((rc = grow_device(&c->ord_buf, &c->ord_cap, hord.size(), st)) != GSOFA_OK) goto fail;
-    CK(cudaMemcpyAsync(c->ord_buf, hord.data(), hord.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));  // the host vector goes out of scope
     ord_npos = n;
+    if ((rc = grow_device(&c->ord_buf, &c->ord_cap, (size_t)n * 6, st)) != GSOFA_OK) goto fail;
   }
   // ---------------------------------------------------- plan + arena
   {
@@ -1189,6 +1174,31 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
         CK(cudaEventRecord(ea, st));
         CK(gsofa::launch_stream(sp, (int)ceil_div(grid, gsofa::stream_warps_per_cta()), st));  // lockstep first
         CK(cudaStreamWaitEvent(c->stream2, ea, 0));
+        if (ord_npos > 0) {
+          // A2, height order: the elimination tree of A + A^T, heights and
+          // (height, id) positions on the host (order.cu; SURVEY §8(a) A2,
+          // O(nnz alpha)), while the lockstep kernel -- id order, no tree
+          // needed -- runs; then up to the solo kernel's stream
+          const int64_t *rp_h = rowptr;
+          const int32_t *ci_h = colidx;
+          if (in_dev) {
+            ord_hrp.resize((size_t)n + 1);
+            ord_hci.resize((size_t)std::max<int64_t>(nnz, 1));
+            CK(cudaMemcpyAsync(ord_hrp.data(), rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               c->stream2));
+            if (nnz)
+              CK(cudaMemcpyAsync(ord_hci.data(), colidx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                 c->stream2));
+            CK(cudaStreamSynchronize(c->stream2));
+            rp_h = ord_hrp.data();
+            ci_h = ord_hci.data();
+          }
+          ord_host.resize((size_t)n * 6);  // posrec (4 per position) | hgt | pos
+          gsofa::height_order(n, rp_h, ci_h, ord_host.data() + 4 * n, ord_host.data() + 5 * n,
+                              ord_host.data());
+          CK(cudaMemcpyAsync(c->ord_buf, ord_host.data(), ord_host.size() * 4, cudaMemcpyHostToDevice,
+                             c->stream2));
+        }
         CK(gsofa::launch_solo(sp, (int)plan.heavy, c->stream2));
         CK(cudaEventRecord(eb, c->stream2));
         CK(cudaStreamWaitEvent(st, eb, 0));

@@ -516,3 +516,50 @@ def test_second_oracle_gilbert_peierls(ctx, name, scale):
         got = run(rp, ci, ctx, schedule=sched)
         for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx"):
             assert np.array_equal(got[k], want[k]), (sched, k)
+
+
+def test_l_csc_C5_full(ctx):
+    """gsofa_result_l_csc at full C5 scale (nnz(L) ~ 2.2e9 > 2^31): the
+    column pointers equal the column histogram of the (oracle-checked, see
+    test_full_C5_exact) row form, every column's rows ascend, and per column
+    the count and two weighted sums of its rows match the row form (sums are
+    exact in float64 at these sizes)."""
+    rp, ci = gen.config("C5")
+    n = rp.size - 1
+    r = g.symbolic(rp, ci, ctx=ctx)
+    try:
+        arr = r.to_numpy(copy=False)
+        Lp, Li = arr["L_rowptr"], arr["L_colidx"]
+        assert r.nnz_L > (1 << 31)
+        csc = r.l_csc()
+    finally:
+        pass
+    cp, ri = csc["col_ptr"], csc["row_idx"]
+    assert cp.size == n + 1 and cp[0] == 0 and cp[-1] == r.nnz_L
+
+    def wsums(cols_of, rows_of, acc):
+        acc[0] += np.bincount(cols_of, minlength=n)
+        acc[1] += np.bincount(cols_of, weights=rows_of.astype(np.float64), minlength=n)
+        h = (rows_of.astype(np.uint64) * np.uint64(2654435761)) & np.uint64(0xFFFFFFFF)
+        acc[2] += np.bincount(cols_of, weights=h.astype(np.float64), minlength=n)
+
+    want = [np.zeros(n, np.int64), np.zeros(n), np.zeros(n)]
+    step = 1 << 16
+    for a in range(0, n, step):
+        b = min(n, a + step)
+        rows_of = np.repeat(np.arange(a, b, dtype=np.int64), np.diff(Lp[a:b + 1]))
+        wsums(Li[Lp[a]:Lp[b]], rows_of, want)
+    got = [np.zeros(n, np.int64), np.zeros(n), np.zeros(n)]
+    for a in range(0, n, step):
+        b = min(n, a + step)
+        seg = ri[cp[a]:cp[b]]
+        cols_of = np.repeat(np.arange(a, b, dtype=np.int64), np.diff(cp[a:b + 1]))
+        # ascending within each column: a descent may only occur at a column start
+        desc = np.nonzero(np.diff(seg) <= 0)[0] + 1
+        starts = set((cp[a:b] - cp[a]).tolist())
+        assert all(int(d) in starts for d in desc), f"rows not ascending in columns [{a},{b})"
+        wsums(cols_of, seg, got)
+    r.free()
+    assert np.array_equal(got[0], want[0])
+    assert np.array_equal(got[1], want[1])
+    assert np.array_equal(got[2], want[2])
