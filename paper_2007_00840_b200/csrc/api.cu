@@ -1131,7 +1131,9 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.abort_cycles = 0;
     gsofa::solo_layout(plan.Vmax, n, ord_npos, &sp);
     sp.hmode = ord_npos > 0;
-    sp.wide = solo_wide;
+    // the latency shape's bulk copies need a 16-byte aligned colidx
+    sp.wide = solo_wide && ((uintptr_t)d_colidx & 15) == 0;
+    sp.nnz = nnz;
     sp.npos = (int32_t)ord_npos;
     sp.posrec = reinterpret_cast<const int4 *>(c->ord_buf);  // 16-byte aligned (buffer start)
     sp.hgt = c->ord_buf + 4 * n;

@@ -100,6 +100,7 @@ struct StreamParams {
   int32_t hmode;
   int32_t npos;
   int32_t wide;              // solo kernel shape: 0 = throughput (48 warps/SM), 1 = latency (4 batches)
+  int64_t nnz;               // entries of colidx (the latency shape's bulk copies stay inside)
   const int4 *posrec;        // [n] per position: {vertex, rowptr, rowptr + 1, end of its
                              //     height's segment of positions}
   const int32_t *hgt;        // [n] etree height of a vertex

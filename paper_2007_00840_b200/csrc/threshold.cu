@@ -621,6 +621,45 @@ struct SoloWarpSmem {
   uint32_t fv;                           // first visits (vertices < s reached)
 };
 
+// Adjacency prefetch of the latency shape (kB > 1): when a closure member
+// enters the shared-memory worklist its row pointers are already known, so
+// its neighbour list is copied into shared memory right away with one bulk
+// async copy (cp.async.bulk, completion on a per-slot mbarrier); when the item
+// is expanded a level later its neighbours are read from shared memory, and
+// the colidx round trip leaves the chain's critical path.  Lists that do not
+// fit a 64-byte slot (with 16-byte alignment slack) are read from global
+// memory as before.
+constexpr int kAdj = 16;  // ints per slot: the 16-byte-aligned span of <= 13 neighbours
+struct SoloPF {
+  int adj[kSoloQ][kAdj];
+  unsigned long long bar[kSoloQ];
+  uint32_t phase[kSoloQ / 32];  // per slot: parity of its next completion
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void *q) {
+  return (uint32_t)__cvta_generic_to_shared(q);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch(int *dst, const int32_t *src, int bytes,
+                                              unsigned long long *b) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(b))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+
 struct SoloQueue {
   int sh, st;      // shared-memory worklist head / tail (warp-uniform)
   int gh, gt;      // global ring head / tail
@@ -646,9 +685,12 @@ struct SoloStep {
 
 // one closure item per lane into the worklist: shared memory, then the
 // global ring, then parked in pend (push = this lane has an item)
+// (pf: the latency shape's adjacency prefetch; qb's top bit marks a slot
+// whose neighbour list is on its way to shared memory)
+template <bool kPF>
 __device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot &sl,
-                                          SoloWarpSmem &sw, SoloQueue &Q, bool push, int wk,
-                                          int rb, int re, int lane) {
+                                          SoloWarpSmem &sw, SoloPF *pf, SoloQueue &Q, bool push,
+                                          int wk, int rb, int re, int lane) {
   const uint32_t pb = __ballot_sync(kFull, push);
   if (!pb) return;
   const int pos = Q.st + __popc(pb & lanemask_lt());
@@ -656,8 +698,15 @@ __device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot 
   if (push && in_s) {
     const int i = pos & (kSoloQ - 1);
     sw.qw[i] = wk;
-    sw.qb[i] = rb;
     sw.qe[i] = re;
+    if (kPF) {
+      const int a = rb & ~3, e = (re + 3) & ~3;  // 16-byte aligned span
+      const bool go = re > rb && e - a <= kAdj && e <= p.nnz;
+      if (go) bulk_prefetch(pf->adj[i], p.colidx + a, (e - a) * 4, &pf->bar[i]);
+      sw.qb[i] = go ? (rb | (int)0x80000000) : rb;
+    } else {
+      sw.qb[i] = rb;
+    }
   }
   const uint32_t sb = __ballot_sync(kFull, push && in_s);
   Q.st += __popc(sb);
@@ -680,9 +729,10 @@ __device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot 
 // each new fill).
 template <bool kH, int kB>
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
-                                            SoloWarpSmem &sw, int wb, SoloQueue &Q, int s,
-                                            const SoloStep &t, int u, int beg, int end,
-                                            int lane) {
+                                            SoloWarpSmem &sw, SoloPF *pf, int wb, SoloQueue &Q,
+                                            int s, const SoloStep &t, int u, int beg, int end,
+                                            int us, int lane) {
+  constexpr bool kPF = kB > 1;  // us: this lane's item's prefetch slot (-1: none)
   const int deg = u >= 0 ? end - beg : 0;
   // fast path (every threshold's level 0, most closure levels of a chain):
   // one item in lane 0 with at most 32 neighbours -- lane j takes neighbour
@@ -719,7 +769,12 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       const int f = f0 + 32 * k + lane;
       if (single) {
         const int b0 = __shfl_sync(kFull, beg, 0);
-        w[k] = f < total ? __ldg(p.colidx + b0 + f) : s;
+        if (kPF) {
+          const int s0 = __shfl_sync(kFull, us, 0);
+          w[k] = f < total ? (s0 >= 0 ? pf->adj[s0][(b0 & 3) + f] : __ldg(p.colidx + b0 + f)) : s;
+        } else {
+          w[k] = f < total ? __ldg(p.colidx + b0 + f) : s;
+        }
         continue;
       }
       int o = 0;
@@ -731,7 +786,13 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       }
       const int ob = __shfl_sync(kFull, beg, o);
       const int oe = __shfl_sync(kFull, excl, o);
-      w[k] = f < total ? __ldg(p.colidx + ob + (f - oe)) : s;
+      if (kPF) {
+        const int os = __shfl_sync(kFull, us, o);
+        w[k] = f < total ? (os >= 0 ? pf->adj[os][(ob & 3) + (f - oe)] : __ldg(p.colidx + ob + (f - oe)))
+                         : s;
+      } else {
+        w[k] = f < total ? __ldg(p.colidx + ob + (f - oe)) : s;
+      }
     }
 #pragma unroll
     for (int k = 0; k < kB; ++k) {
@@ -790,7 +851,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
           push = true;  // maxId(w) = T, not in the structure: continue with T
         }
       }
-      solo_push(p, sl, sw, Q, push, wk, rb[k], re[k], lane);
+      solo_push<kPF>(p, sl, sw, pf, Q, push, wk, rb[k], re[k], lane);
     }
   }
 }
@@ -834,7 +895,8 @@ __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const ui
 // structure bitmaps stay in vertex ids (the ND order's locality)
 template <bool kH, int kB>
 __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s,
-                                            int lane, SoloWarpSmem &sw) {
+                                            int lane, SoloWarpSmem &sw, SoloPF *pf) {
+  constexpr bool kPF = kB > 1;
   // threshold positions: below s (id order), anywhere in [0, n) (height order)
   const int tbw = kH ? (p.n + 31) >> 5 : (s + 31) >> 5;
   // seed: the out-neighbours of s are in the structure; the
@@ -898,7 +960,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
           ub = ok ? cb : 0;
           ue = ok ? ce : 0;
         } else {
-          solo_push(p, sl, sw, Q, has, v, vb, ve, lane);
+          solo_push<kPF>(p, sl, sw, pf, Q, has, v, vb, ve, lane);
         }
       }
       t.tmin = __reduce_min_sync(kFull, tmin);
@@ -914,17 +976,28 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
         ue = __ldg(p.rowptr + P + 1);
       }
     }
+    int us = -1;  // prefetch slot of this lane's item
     for (;;) {
-      solo_expand<kH, kB>(p, sl, sw, wb, Q, s, t, u, ub, ue, lane);
+      solo_expand<kH, kB>(p, sl, sw, pf, wb, Q, s, t, u, ub, ue, us, lane);
       __syncwarp();
+      us = -1;
       if (Q.sh < Q.st) {
         const int cnt = min(32, Q.st - Q.sh);
         u = -1;
+        int i = 0;
         if (lane < cnt) {
-          const int i = (Q.sh + lane) & (kSoloQ - 1);
+          i = (Q.sh + lane) & (kSoloQ - 1);
           u = sw.qw[i];
           ub = sw.qb[i];
           ue = sw.qe[i];
+          if (kPF && ub < 0) {
+            // its neighbour list was prefetched: wait for the bytes, then
+            // the slot's barrier is in its next phase
+            ub &= 0x7FFFFFFF;
+            us = i;
+            mbar_wait(&pf->bar[i], (pf->phase[i >> 5] >> (i & 31)) & 1u);
+            atomicXor(&pf->phase[i >> 5], 1u << (i & 31));
+          }
         }
         Q.sh += cnt;
         __syncwarp();
@@ -1084,6 +1157,14 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
   const int Vs = (int)(p.so_tsum - p.so_rsum);  // reached-word summary words
   __shared__ SoloWarpSmem s_sw[kSoloWarps];
   SoloWarpSmem &sw = s_sw[warp];
+  extern __shared__ __align__(128) unsigned char s_dyn[];  // latency shape: SoloPF per warp
+  SoloPF *pf = nullptr;
+  if (kB > 1) {
+    pf = reinterpret_cast<SoloPF *>(s_dyn) + warp;
+    for (int i = lane; i < kSoloQ; i += 32) mbar_init(&pf->bar[i]);
+    if (lane < kSoloQ / 32) pf->phase[lane] = 0u;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (lane == 0) sw.items = sw.pairs = sw.levels = sw.steps = sw.fv = 0u;
   __syncwarp();
   // first task: warp-major over the grid, so consecutive (heaviest) sources
@@ -1128,7 +1209,7 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
     if (s >= p.row_end) continue;  // tail of the last group
     unsigned long long t0 = 0;
     if (p.src_trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    solo_source<kH, kB>(p, sl, s, lane, sw);
+    solo_source<kH, kB>(p, sl, s, lane, sw, pf);
     if (p.src_trace && lane == 0) {
       // dev trace (GSOFA_SRC_TRACE): start / end ns, steps, levels of this source
       unsigned long long t1;
@@ -1234,13 +1315,20 @@ const void *solo_fn(bool h, bool wide) {
   return h ? (const void *)solo_kernel<true, 1> : (const void *)solo_kernel<false, 1>;
 }
 
+// dynamic shared memory of the solo kernel: the latency shape's prefetch slots
+size_t solo_dyn_smem(bool wide) { return wide ? sizeof(SoloPF) * kSoloWarps : 0; }
+
 int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos, bool wide) {
   int sms = 0, per = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
   cudaError_t e;
   const bool h = npos > 0;
   if (heavy) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solo_fn(h, wide), kSoloWarps * 32, 0);
+    const size_t dyn = solo_dyn_smem(wide);
+    if (dyn && cudaFuncSetAttribute(solo_fn(h, wide), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)dyn) != cudaSuccess)
+      return 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solo_fn(h, wide), kSoloWarps * 32, dyn);
   } else {
     const size_t smem = stream_smem_bytes(Vmax, 0);  // the lockstep kernel runs id order
     if (smem > 48 * 1024 &&
@@ -1274,7 +1362,8 @@ int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos, bool w
   const int by_regs = (regs - solo_regs) / light_regs;
   const int by_warps = (warps - kSoloWarps) / kLightWarps;
   const size_t light_smem = fl.sharedSizeBytes + stream_smem_bytes(Vmax, 0) + 1024;
-  const int by_smem = (int)((smem_sm - fs.sharedSizeBytes - 1024) / light_smem);
+  const int by_smem =
+      (int)((smem_sm - fs.sharedSizeBytes - solo_dyn_smem(wide) - 1024) / light_smem);
   return std::max(0, std::min(std::min(by_regs, by_warps), by_smem));
 }
 
@@ -1332,8 +1421,12 @@ cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st) {
 cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st) {
   if (grid <= 0) return cudaSuccess;
   if (p.wide) {
-    if (p.hmode) solo_kernel<true, 4><<<grid, kSoloWarps * 32, 0, st>>>(p);
-    else solo_kernel<false, 4><<<grid, kSoloWarps * 32, 0, st>>>(p);
+    const size_t dyn = solo_dyn_smem(true);
+    cudaError_t e = cudaFuncSetAttribute(solo_fn(p.hmode, true),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    if (p.hmode) solo_kernel<true, 4><<<grid, kSoloWarps * 32, dyn, st>>>(p);
+    else solo_kernel<false, 4><<<grid, kSoloWarps * 32, dyn, st>>>(p);
   } else {
     if (p.hmode) solo_kernel<true, 1><<<grid, kSoloWarps * 32, 0, st>>>(p);
     else solo_kernel<false, 1><<<grid, kSoloWarps * 32, 0, st>>>(p);

@@ -563,3 +563,27 @@ def test_l_csc_C5_full(ctx):
     assert np.array_equal(got[0], want[0])
     assert np.array_equal(got[1], want[1])
     assert np.array_equal(got[2], want[2])
+
+
+@pytest.mark.parametrize("wide", ["0", "1"])
+@pytest.mark.parametrize("schedule", ["threshold", "height"])
+def test_solo_shapes(schedule, wide, monkeypatch):
+    """Both shapes of the solo kernel (throughput; latency with the bulk-copy
+    adjacency prefetch) in both threshold orders, on every group (solo for
+    all groups), repeated on one context: the oracle's result each time."""
+    monkeypatch.setenv("GSOFA_SOLO_WIDE", wide)
+    monkeypatch.setenv("GSOFA_ABORT_MS", "0.00001")
+    cases = [gen.config("C4", 60), gen.config("C5", 14), gen.config("C2", 16), gen.config("C3", 2000)]
+    wants = [oracle.symbolic(rp, ci) for rp, ci in cases]
+    with g.Context(0) as c:
+        for rep in range(2):
+            for (rp, ci), want in zip(cases, wants):
+                assert_full_equal(run(rp, ci, c, schedule=schedule), want,
+                                  tag=f"{schedule} wide={wide} rep {rep} n={rp.size - 1}")
+    rng = np.random.default_rng(5)
+    with g.Context(0) as c:
+        for it in range(40):
+            n = int(rng.integers(1, 400))
+            rp, ci = gen.random_graph(n, float(rng.uniform(0.005, 0.1)), seed=int(rng.integers(1 << 30)))
+            assert_full_equal(run(rp, ci, c, schedule=schedule), oracle.symbolic(rp, ci),
+                              tag=f"random {it} n={n}")
