@@ -630,7 +630,7 @@ struct SoloWarpSmem {
 // fit a 64-byte slot (with 16-byte alignment slack) are read from global
 // memory as before.
 constexpr int kAdj = 16;  // ints per slot: the 16-byte-aligned span of <= 13 neighbours
-struct SoloPF {
+struct alignas(128) SoloPF {
   int adj[kSoloQ][kAdj];
   unsigned long long bar[kSoloQ];
   uint32_t phase[kSoloQ / 32];  // per slot: parity of its next completion
