@@ -664,6 +664,7 @@ struct SoloQueue {
   int sh, st;      // shared-memory worklist head / tail (warp-uniform)
   int gh, gt;      // global ring head / tail
   bool spilled;    // items parked in pend
+  int hold;        // slots below sh still being expanded (their prefetched lists are in use)
 };
 
 __device__ __forceinline__ uint32_t vbit(int v) { return 1u << (v & 31); }
@@ -694,7 +695,9 @@ __device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot 
   const uint32_t pb = __ballot_sync(kFull, push);
   if (!pb) return;
   const int pos = Q.st + __popc(pb & lanemask_lt());
-  const bool in_s = pos - Q.sh < kSoloQ;
+  // (with prefetch, the slots of the items being expanded stay reserved:
+  // their neighbour lists are read during this expansion)
+  const bool in_s = pos - (Q.sh - (kPF ? Q.hold : 0)) < kSoloQ;
   if (push && in_s) {
     const int i = pos & (kSoloQ - 1);
     sw.qw[i] = wk;
@@ -924,7 +927,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
     P = solo_next_threshold(SL_THR, SL_TSUM, tbw, P, wb, sw, lane);
     if (P == INT_MAX) break;
     if (lane == 0) sw.steps += 1;
-    SoloQueue Q = {0, 0, 0, 0, false};
+    SoloQueue Q = {0, 0, 0, 0, false, 0};
     int u = -1, ub = 0, ue = 0;
     SoloStep t;
     if (kH) {
@@ -981,8 +984,10 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       solo_expand<kH, kB>(p, sl, sw, pf, wb, Q, s, t, u, ub, ue, us, lane);
       __syncwarp();
       us = -1;
+      Q.hold = 0;
       if (Q.sh < Q.st) {
         const int cnt = min(32, Q.st - Q.sh);
+        Q.hold = cnt;
         u = -1;
         int i = 0;
         if (lane < cnt) {
