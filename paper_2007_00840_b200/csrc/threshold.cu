@@ -629,6 +629,12 @@ struct SoloWarpSmem {
 // the colidx round trip leaves the chain's critical path.  Lists that do not
 // fit a 64-byte slot (with 16-byte alignment slack) are read from global
 // memory as before.
+// Measured slower (profiles/r2/tma_bulk_prefetch_ab.txt: 1.5-1.8x on C4/C5),
+// so it is compiled only with -DGSOFA_ADJ_PREFETCH=1 (to reproduce the A/B).
+#ifndef GSOFA_ADJ_PREFETCH
+#define GSOFA_ADJ_PREFETCH 0
+#endif
+constexpr bool kAdjPrefetch = GSOFA_ADJ_PREFETCH != 0;
 constexpr int kAdj = 16;  // ints per slot: the 16-byte-aligned span of <= 13 neighbours
 struct alignas(128) SoloPF {
   int adj[kSoloQ][kAdj];
@@ -735,7 +741,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
                                             SoloWarpSmem &sw, SoloPF *pf, int wb, SoloQueue &Q,
                                             int s, const SoloStep &t, int u, int beg, int end,
                                             int us, int lane) {
-  constexpr bool kPF = kB > 1;  // us: this lane's item's prefetch slot (-1: none)
+  constexpr bool kPF = kB > 1 && kAdjPrefetch;  // us: this lane's prefetch slot (-1: none)
   const int deg = u >= 0 ? end - beg : 0;
   // fast path (every threshold's level 0, most closure levels of a chain):
   // one item in lane 0 with at most 32 neighbours -- lane j takes neighbour
@@ -899,7 +905,7 @@ __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const ui
 template <bool kH, int kB>
 __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s,
                                             int lane, SoloWarpSmem &sw, SoloPF *pf) {
-  constexpr bool kPF = kB > 1;
+  constexpr bool kPF = kB > 1 && kAdjPrefetch;
   // threshold positions: below s (id order), anywhere in [0, n) (height order)
   const int tbw = kH ? (p.n + 31) >> 5 : (s + 31) >> 5;
   // seed: the out-neighbours of s are in the structure; the
@@ -1164,7 +1170,7 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
   SoloWarpSmem &sw = s_sw[warp];
   extern __shared__ __align__(128) unsigned char s_dyn[];  // latency shape: SoloPF per warp
   SoloPF *pf = nullptr;
-  if (kB > 1) {
+  if (kB > 1 && kAdjPrefetch) {
     pf = reinterpret_cast<SoloPF *>(s_dyn) + warp;
     for (int i = lane; i < kSoloQ; i += 32) mbar_init(&pf->bar[i]);
     if (lane < kSoloQ / 32) pf->phase[lane] = 0u;
@@ -1321,7 +1327,7 @@ const void *solo_fn(bool h, bool wide) {
 }
 
 // dynamic shared memory of the solo kernel: the latency shape's prefetch slots
-size_t solo_dyn_smem(bool wide) { return wide ? sizeof(SoloPF) * kSoloWarps : 0; }
+size_t solo_dyn_smem(bool wide) { return wide && kAdjPrefetch ? sizeof(SoloPF) * kSoloWarps : 0; }
 
 int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos, bool wide) {
   int sms = 0, per = 0;
@@ -1427,9 +1433,11 @@ cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st) {
   if (grid <= 0) return cudaSuccess;
   if (p.wide) {
     const size_t dyn = solo_dyn_smem(true);
-    cudaError_t e = cudaFuncSetAttribute(solo_fn(p.hmode, true),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    if (e != cudaSuccess) return e;
+    if (dyn) {
+      cudaError_t e = cudaFuncSetAttribute(solo_fn(p.hmode, true),
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      if (e != cudaSuccess) return e;
+    }
     if (p.hmode) solo_kernel<true, 4><<<grid, kSoloWarps * 32, dyn, st>>>(p);
     else solo_kernel<false, 4><<<grid, kSoloWarps * 32, dyn, st>>>(p);
   } else {
