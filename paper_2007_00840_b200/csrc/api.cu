@@ -875,7 +875,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   int64_t baseL = 0, baseU = 0, nbatches = 0, maxC = 0;
   Plan plan;
   bool auto_fifo = false;
-  int64_t ord_npos = 0;  // > 0: height order
+  int64_t ord_npos = 0;  // > 0: height order possible (threshold bitmaps sized for n positions)
+  bool auto_order = false;  // AUTO: pick the threshold order from the tree's shape
   std::vector<int64_t> ord_hrp;              // host copies of a device CSR (height order)
   std::vector<int32_t> ord_hci, ord_host;    // ... and the order arrays before upload
   // solo kernel shape: dev knob for now
@@ -946,11 +947,14 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       auto_fifo = labels <= (double)budget;
     }
     o.schedule = auto_fifo ? GSOFA_SCHEDULE_FIFO : GSOFA_SCHEDULE_THRESHOLD;
+    // threshold family: the solo kernel's order (id or etree height) is
+    // chosen once the tree is known (below)
+    auto_order = !auto_fifo;
   }
   // ---------------------------------------------------- A2: height order
   // positions are a permutation of [0, n): the plan does not depend on the
   // tree, which is computed on the host while the lockstep kernel runs
-  if (o.schedule == GSOFA_SCHEDULE_HEIGHT) {
+  if (o.schedule == GSOFA_SCHEDULE_HEIGHT || auto_order) {
     ord_npos = n;
     if ((rc = grow_device(&c->ord_buf, &c->ord_cap, (size_t)n * 6, st)) != GSOFA_OK) goto fail;
   }
@@ -1130,9 +1134,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.light_slots = (int32_t)plan.light;
     sp.abort_cycles = 0;
     gsofa::solo_layout(plan.Vmax, n, ord_npos, &sp);
-    sp.hmode = ord_npos > 0;
-    // the latency shape's bulk copies need a 16-byte aligned colidx
-    sp.wide = solo_wide && ((uintptr_t)d_colidx & 15) == 0;
+    sp.hmode = o.schedule == GSOFA_SCHEDULE_HEIGHT;  // AUTO: decided at the solo launch
+    sp.wide = solo_wide;
     sp.nnz = nnz;
     sp.npos = (int32_t)ord_npos;
     sp.posrec = reinterpret_cast<const int4 *>(c->ord_buf);  // 16-byte aligned (buffer start)
@@ -1196,10 +1199,22 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
             ci_h = ord_hci.data();
           }
           ord_host.resize((size_t)n * 6);  // posrec (4 per position) | hgt | pos
-          gsofa::height_order(n, rp_h, ci_h, ord_host.data() + 4 * n, ord_host.data() + 5 * n,
-                              ord_host.data());
-          CK(cudaMemcpyAsync(c->ord_buf, ord_host.data(), ord_host.size() * 4, cudaMemcpyHostToDevice,
-                             c->stream2));
+          const gsofa::OrderShape shape = gsofa::height_order(
+              n, rp_h, ci_h, ord_host.data() + 4 * n, ord_host.data() + 5 * n, ord_host.data());
+          if (auto_order) {
+            // AUTO: height order when the last row's id-order chain (about
+            // |L(n-1,:)| threshold steps) is far longer than the tree is
+            // high (its rounds in height order) -- C4's hub rows: 577k vs
+            // 4.2k; 3D grids: 58k vs 38k keep id order, which is faster per
+            // step.  The chain-bound pattern also takes the latency shape.
+            const bool use_h = shape.last_row_chain > 4 * shape.height;
+            sp.hmode = use_h;
+            if (!std::getenv("GSOFA_SOLO_WIDE")) sp.wide = use_h;
+            o.schedule = use_h ? GSOFA_SCHEDULE_HEIGHT : GSOFA_SCHEDULE_THRESHOLD;
+          }
+          if (sp.hmode)
+            CK(cudaMemcpyAsync(c->ord_buf, ord_host.data(), ord_host.size() * 4,
+                               cudaMemcpyHostToDevice, c->stream2));
         }
         CK(gsofa::launch_solo(sp, (int)plan.heavy, c->stream2));
         CK(cudaEventRecord(eb, c->stream2));

@@ -120,11 +120,20 @@ int solo_ring(int64_t Vmax);
 int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos, bool wide);
 size_t stream_smem_bytes(int64_t Vmax, int64_t npos);  // dynamic smem: threshold-word summary
 // order.cu (host): elimination tree of A + A^T and the height order
-void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *parent);
+// last_row_subtree (optional): |struct(L(n-1,:))| of A + A^T
+void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *parent,
+               int64_t *last_row_subtree);
+// the tree's shape, for the AUTO choice of the threshold order: its height
+// (rounds of the last source in height order, at most) against the last
+// row's structure size (its threshold steps in id order, about)
+struct OrderShape {
+  int64_t height = 0;
+  int64_t last_row_chain = 0;
+};
 // etree heights, positions (sorted by (height, id)) and per position
 // {vertex, rowptr, rowptr + 1, segment end} (int4 as four int32)
-void height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *hgt,
-                  int32_t *pos, int32_t *posrec);
+OrderShape height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *hgt,
+                        int32_t *pos, int32_t *posrec);
 cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st);
 cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st);
 cudaError_t launch_gather(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,

@@ -44,7 +44,8 @@ namespace gsofa {
 // Row u's lower entries of A and of A^T (column u of A) are the edges
 // (x, u), x < u, of the symmetrised graph; each links the root of x's
 // current tree under u (Liu's algorithm; `anc` compresses paths).
-void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *parent) {
+void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *parent,
+               int64_t *last_row_subtree) {
   const int64_t nnz = rowptr[n];
   // lower entries of column u of A, i.e. rows x < u with A(x, u) != 0
   std::vector<int64_t> cp(n + 1, 0);
@@ -78,16 +79,34 @@ void etree_sym(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t 
       }
     }
   }
+  if (last_row_subtree && n > 0) {
+    // |struct(L(n-1,:))| of A + A^T: the row subtree of the last row, i.e.
+    // every vertex on a tree path from one of its lower neighbours up to it
+    // (anc is reused as the visited mark)
+    const int64_t s = n - 1;
+    int64_t cnt = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      const int64_t *P = pass ? cp.data() : rowptr;
+      const int32_t *I = pass ? cr.data() : colidx;
+      for (int64_t e = P[s]; e < P[s + 1]; ++e)
+        for (int32_t k = I[e]; k != -1 && k < s && anc[k] != -2; k = parent[k]) {
+          anc[k] = -2;
+          ++cnt;
+        }
+    }
+    *last_row_subtree = cnt;
+  }
 }
 
 // Height order of the vertices (see the header comment), into caller
 // arrays: hgt[n] (etree height), pos[n] (vertex -> position, sorted by
 // (height, id)), posrec[4n] (per position: vertex, rowptr[v], rowptr[v+1],
 // the end of v's height segment of positions).
-void height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *hgt,
-                  int32_t *pos, int32_t *posrec) {
+OrderShape height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *hgt,
+                        int32_t *pos, int32_t *posrec) {
   std::vector<int32_t> parent((size_t)n);
-  etree_sym(n, rowptr, colidx, parent.data());
+  OrderShape shape;
+  etree_sym(n, rowptr, colidx, parent.data(), &shape.last_row_chain);
   int32_t H = 0;
   for (int64_t v = 0; v < n; ++v) hgt[v] = 0;
   for (int64_t v = 0; v < n; ++v) {  // parents are larger: one ascending pass
@@ -106,6 +125,8 @@ void height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32
     posrec[4 * q + 2] = (int32_t)rowptr[v + 1];
     posrec[4 * q + 3] = (int32_t)seg[hgt[v] + 1];
   }
+  shape.height = H;
+  return shape;
 }
 
 }  // namespace gsofa

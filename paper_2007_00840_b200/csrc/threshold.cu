@@ -807,8 +807,10 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
     for (int k = 0; k < kB; ++k) {
       ro[k] = 1u;
       rb[k] = re[k] = 0;
-      hw[k] = 0;
-      qw[k] = w[k];
+      if (kH) {
+        hw[k] = 0;
+        qw[k] = w[k];
+      }
       if (k >= nb) continue;
       const uint32_t bw = vbit(w[k]);
       // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds
@@ -820,7 +822,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
         red_sum(SL_ISUM, w[k]);
       }
       // w < tmax may join the closure: its row pointers travel with the atomic
-      if (w[k] < t.tmax) {
+      if (w[k] < (kH ? t.tmax : t.tmin)) {  // (id order: the one threshold T = tmin)
         rb[k] = __ldg(p.rowptr + w[k]);
         re[k] = __ldg(p.rowptr + w[k] + 1);
       }
@@ -836,19 +838,14 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       if (k >= nb) continue;
       const int wk = w[k];
       const uint32_t bw = vbit(wk);
-      {
-        // first visits: the reached bit of w < s was clear (w >= s: ro = bw)
-        const uint32_t nv = __popc(__ballot_sync(kFull, !(ro[k] & bw)));
-        if (lane == 0) sw.fv += nv;
-      }
       bool push = false;
       if (!(ro[k] & bw)) {
         if (ro[k] == 0u) red_sum(SL_RSUM, wk);
-        if (wk > t.tmax || (kH && wk > t.tmin && hw[k] > t.h)) {
+        if (kH ? (wk > t.tmax || (wk > t.tmin && hw[k] > t.h)) : wk > t.tmin) {
           // fill of L(s,:) (R4); w becomes a threshold of this source
           atomicOr(SL_IS + (wk >> 5), bw);  // RED
           red_sum(SL_ISUM, wk);
-          const int q = qw[k];  // its bitmap position
+          const int q = kH ? qw[k] : wk;  // its bitmap position
           const int d = (q >> 5) - wb;
           if (d < 32) {
             atomicOr(&sw.win[d], vbit(q));  // smem (d >= 0: after the step's thresholds)
@@ -914,8 +911,6 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
   for (int j0 = beg; j0 < end; j0 += 32) {
     const int j = j0 + lane;
     const int w = j < end ? __ldg(p.colidx + j) : s;
-    const uint32_t nv = __popc(__ballot_sync(kFull, w < s));  // first visits of the seeds
-    if (lane == 0) sw.fv += nv;
     if (w == s) continue;
     const uint32_t bw = vbit(w);
     if (atomicOr(SL_IS + (w >> 5), bw) == 0u) red_sum(SL_ISUM, w);
@@ -977,23 +972,26 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       t.h = __reduce_max_sync(kFull, hh);
       P = lim - 1;  // the next step starts after these positions
     } else {
-      t.tmin = t.tmax = P;
-      t.h = 0;
+      t.tmin = P;  // the one threshold (tmax / h unused in id order)
       if (lane == 0) {
         u = P;
         ub = __ldg(p.rowptr + P);
         ue = __ldg(p.rowptr + P + 1);
       }
     }
+    // first visits (R11): every vertex newly reached below s is either a
+    // closure member (pushed once, counted here per step) or a structure
+    // member (a seed or a fill: |L(s,:)|, added when the row is staged)
+    const int pushed0 = Q.st + Q.gt;  // the step's own thresholds queued above
     int us = -1;  // prefetch slot of this lane's item
     for (;;) {
       solo_expand<kH, kB>(p, sl, sw, pf, wb, Q, s, t, u, ub, ue, us, lane);
       __syncwarp();
       us = -1;
-      Q.hold = 0;
+      if (kPF) Q.hold = 0;
       if (Q.sh < Q.st) {
         const int cnt = min(32, Q.st - Q.sh);
-        Q.hold = cnt;
+        if (kPF) Q.hold = cnt;
         u = -1;
         int i = 0;
         if (lane < cnt) {
@@ -1020,7 +1018,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
         Q.spilled = false;
         __syncwarp();
         fence_gpu();
-        const int pwords = (t.tmax + 31) >> 5;
+        const int pwords = ((kH ? t.tmax : t.tmin) + 31) >> 5;
         for (int w0 = 0; w0 < pwords && !Q.spilled; w0 += 32) {
           const int wi = w0 + lane;
           uint32_t x = wi < pwords ? __ldcg(SL_PEND + wi) : 0u;
@@ -1045,7 +1043,10 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
         }
         __syncwarp();
       }
-      if (Q.gh >= Q.gt) break;
+      if (Q.gh >= Q.gt) {
+        if (lane == 0) sw.fv += (uint32_t)(Q.st + Q.gt - pushed0);
+        break;
+      }
       const int cnt = min(32, Q.gt - Q.gh);
       u = lane < cnt ? (int)SL_QUEUE[(Q.gh + lane) & SL_QMASK] : -1;
       Q.gh += cnt;
@@ -1061,7 +1062,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
 // s then the bits above s, ascending; staged at one reservation; the bitmap
 // words read are zeroed.  Returns false if the staging area was full.
 __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const SoloSlot &sl, int s,
-                                               int g, int lane) {
+                                               int g, int lane, SoloWarpSmem &sw) {
   const int ns = (((p.n + 31) >> 5) + 31) >> 5;
   // count pass: lane handles summary words i0 + lane (1024 vertices each)
   uint32_t cl = 0, cu = 0;
@@ -1094,6 +1095,7 @@ __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const Solo
   if (lane == 0) {
     p.row_off[r] = ok ? (long long)base : -1;
     p.row_nL[r] = (int)cl;
+    sw.fv += cl;  // the seeds and fills below s: first visits too
     p.row_nU[r] = (int)cu + 1;
     if (ok) {
       p.stage[base + cl] = s;  // U(s,:) starts with the diagonal
@@ -1218,22 +1220,24 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
     if (g < 0) break;
     const int s = p.row_begin + 32 * g + k;
     if (s >= p.row_end) continue;  // tail of the last group
-    unsigned long long t0 = 0;
-    if (p.src_trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    solo_source<kH, kB>(p, sl, s, lane, sw, pf);
     if (p.src_trace && lane == 0) {
       // dev trace (GSOFA_SRC_TRACE): start / end ns, steps, levels of this source
+      unsigned long long t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      p.src_trace[4 * (size_t)(s - p.row_begin)] = (long long)t0;
+    }
+    solo_source<kH, kB>(p, sl, s, lane, sw, pf);
+    if (p.src_trace && lane == 0) {
       unsigned long long t1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
       long long *tr = p.src_trace + 4 * (size_t)(s - p.row_begin);
-      tr[0] = (long long)t0;
       tr[1] = (long long)t1;
       tr[2] = sw.steps;
       tr[3] = sw.levels;
     }
     fence_gpu();  // this warp's REDs are visible to its extraction
     __syncwarp();
-    solo_stage_row(p, sl, s, g, lane);
+    solo_stage_row(p, sl, s, g, lane, sw);
     // reset the touched words: reached | pend (| thr in id order, where a
     // threshold bit sits in the word of its reached bit), and the summaries
     for (int i0 = 0; i0 < Vs; i0 += 32) {
