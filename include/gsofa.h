@@ -258,6 +258,21 @@ int gsofa_result_l_csc(const gsofa_result *r, int32_t on_device, int64_t **col_p
 void gsofa_buffer_free(void *p, int32_t on_device);
 
 /*
+ * gsofa_result_supno -- the supernode partition in SuperLU's form: xsup is
+ * r->sn_start itself (first row of each supernode, then the sentinel), and
+ * supno[i - row_begin] = the index k of the supernode holding row i
+ * (xsup[k] <= i < xsup[k+1]); numeric factorization codes index their
+ * supernodal blocks by it.
+ *   r          a gsofa_symbolic result (after any gsofa_supernode_stitch)
+ *   on_device  1: *supno is device memory, 0: host (malloc)
+ *   supno      receives int32[row_end - row_begin]; release with
+ *              gsofa_buffer_free(p, on_device)
+ * Runs on the result's device (one thread per supernode).  Errors:
+ * GSOFA_EINVAL, GSOFA_ENOMEM, GSOFA_ECUDA.
+ */
+int gsofa_result_supno(const gsofa_result *r, int32_t on_device, int32_t **supno);
+
+/*
  * gsofa_permute -- symmetric permutation B = P A P^T of a pattern, for applying
  * a fill-reducing ordering computed elsewhere (ordering itself is out of
  * scope): new vertex i is old vertex perm[i], so

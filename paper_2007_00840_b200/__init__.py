@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = [
     "gsofa_symbolic", "gsofa_result_copy", "gsofa_result_free",
     "gsofa_partition_rows", "gsofa_strerror", "gsofa_last_error_detail",
     "gsofa_version", "gsofa_supernode_stitch", "gsofa_result_l_csc", "gsofa_buffer_free",
-    "gsofa_permute",
+    "gsofa_permute", "gsofa_result_supno",
 ]
 
 _I64, _I32 = ctypes.c_int64, ctypes.c_int32
@@ -103,6 +103,7 @@ def load():
                                          ctypes.c_void_p]
     lib.gsofa_supernode_stitch.argtypes = [_P(CResult), ctypes.c_void_p, ctypes.c_void_p]
     lib.gsofa_result_l_csc.argtypes = [_P(CResult), _I32, _P(_P(_I64)), _P(_P(_I32))]
+    lib.gsofa_result_supno.argtypes = [_P(CResult), _I32, _P(_P(_I32))]
     lib.gsofa_buffer_free.argtypes = [ctypes.c_void_p, _I32]
     lib.gsofa_buffer_free.restype = None
     lib.gsofa_permute.argtypes = [_I64] + [ctypes.c_void_p] * 5
@@ -252,6 +253,18 @@ class Result:
             lib.gsofa_buffer_free(ctypes.cast(cp, ctypes.c_void_p), 0)
             lib.gsofa_buffer_free(ctypes.cast(ri, ctypes.c_void_p), 0)
         return dict(col_ptr=col_ptr, row_idx=row_idx)
+
+    def supno(self):
+        """gsofa_result_supno: SuperLU's supno (xsup is sn_start): for each row
+        of the range, the index of its supernode (numpy int32)."""
+        lib = load()
+        q = _P(_I32)()
+        _check(lib.gsofa_result_supno(self._p, 0, ctypes.byref(q)), "gsofa_result_supno")
+        try:
+            return (np.ctypeslib.as_array(q, shape=(self.rows,)).copy() if self.rows
+                    else np.empty(0, np.int32))
+        finally:
+            lib.gsofa_buffer_free(ctypes.cast(q, ctypes.c_void_p), 0)
 
     def __getitem__(self, k):
         return self.to_numpy()[k]

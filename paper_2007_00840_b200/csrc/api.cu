@@ -684,6 +684,59 @@ done:
   return rc;
 }
 
+int gsofa_result_supno(const gsofa_result *r, int32_t on_device, int32_t **supno) {
+  if (!r || !supno) {
+    set_detail("NULL argument to gsofa_result_supno");
+    return GSOFA_EINVAL;
+  }
+  *supno = nullptr;
+  cudaError_t e = cudaSetDevice(r->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  const int64_t rows = r->row_end - r->row_begin;
+  int32_t *d_sn = nullptr, *d_out = nullptr;
+  cudaStream_t st = nullptr;
+  if (r->on_device) {
+    d_sn = r->sn_start;
+  } else {
+    if ((e = cudaMallocAsync((void **)&d_sn, (size_t)(r->nsuper + 1) * 4, st)) != cudaSuccess)
+      return cuda_fail(e, "cudaMallocAsync");
+    if ((e = cudaMemcpyAsync(d_sn, r->sn_start, (size_t)(r->nsuper + 1) * 4, cudaMemcpyHostToDevice,
+                             st)) != cudaSuccess) {
+      cudaFreeAsync(d_sn, st);
+      return cuda_fail(e, "cudaMemcpyAsync");
+    }
+  }
+  if ((e = cudaMallocAsync((void **)&d_out, (size_t)std::max<int64_t>(rows, 1) * 4, st)) == cudaSuccess)
+    e = gsofa::launch_supno(d_sn, r->nsuper, (int32_t)r->row_begin, d_out, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (!r->on_device) cudaFreeAsync(d_sn, st);
+  if (e != cudaSuccess) {
+    if (d_out) cudaFreeAsync(d_out, st);
+    cudaStreamSynchronize(st);
+    return cuda_fail(e, "supno");
+  }
+  if (on_device) {
+    *supno = d_out;
+    return GSOFA_OK;
+  }
+  int32_t *h = (int32_t *)std::malloc((size_t)std::max<int64_t>(rows, 1) * 4);
+  if (!h) {
+    cudaFreeAsync(d_out, st);
+    cudaStreamSynchronize(st);
+    set_detail("host allocation for supno failed");
+    return GSOFA_ENOMEM;
+  }
+  e = cudaMemcpy(h, d_out, (size_t)rows * 4, cudaMemcpyDeviceToHost);
+  cudaFreeAsync(d_out, st);
+  cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    std::free(h);
+    return cuda_fail(e, "cudaMemcpy");
+  }
+  *supno = h;
+  return GSOFA_OK;
+}
+
 void gsofa_buffer_free(void *p, int32_t on_device) {
   if (!p) return;
   if (on_device) {

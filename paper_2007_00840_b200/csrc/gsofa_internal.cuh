@@ -188,6 +188,8 @@ int extract_sub_columns();  // columns per extraction warp unit
 cudaError_t launch_validate(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
                             int64_t nnz, int32_t *rowptr32, int *err_flag, unsigned int *bw,
                             cudaStream_t st);
+cudaError_t launch_supno(const int32_t *sn_start, int64_t nsuper, int32_t row_begin, int32_t *supno,
+                         cudaStream_t st);
 cudaError_t launch_count_offdiag(const int32_t *rowptr, const int32_t *colidx, int32_t r0,
                                  int32_t r1, unsigned long long *out, cudaStream_t st);
 cudaError_t launch_supernode_flags(const int64_t *L_rowptr, const int32_t *L_colidx,

@@ -324,6 +324,23 @@ cudaError_t scan_exclusive_i32_i64(const int32_t *in, int64_t *out, int64_t coun
   return scan_rec<int32_t, int64_t>(in, out, count, total, (int64_t *)tmp, st);
 }
 
+// SuperLU-style supno (xsup = sn_start): supno[i - row_begin] = the index of
+// the supernode holding row i, i.e. k with sn_start[k] <= i < sn_start[k+1];
+// one thread per supernode writes its rows
+__global__ void supno_kernel(const int32_t *sn_start, int64_t nsuper, int32_t row_begin,
+                             int32_t *supno) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nsuper) return;
+  for (int32_t i = sn_start[k]; i < sn_start[k + 1]; ++i) supno[i - row_begin] = (int32_t)k;
+}
+
+cudaError_t launch_supno(const int32_t *sn_start, int64_t nsuper, int32_t row_begin, int32_t *supno,
+                         cudaStream_t st) {
+  if (nsuper <= 0) return cudaSuccess;
+  supno_kernel<<<(unsigned)((nsuper + 255) / 256), 256, 0, st>>>(sn_start, nsuper, row_begin, supno);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_validate(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
                             int64_t nnz, int32_t *rowptr32, int *err_flag, unsigned int *bw,
                             cudaStream_t st) {

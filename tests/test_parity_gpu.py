@@ -602,3 +602,20 @@ def test_auto_threshold_order_full(ctx, name, want):
     r.free()
     assert sched == want
     assert_full_equal(got, oracle.symbolic(rp, ci), tag=name)
+
+
+@pytest.mark.parametrize("name,scale,rb", [("C5", 14, 0), ("C4", 60, 777), ("C1", None, 0)])
+def test_supno(ctx, name, scale, rb):
+    """gsofa_result_supno (SuperLU's supno, xsup = sn_start) equals the row ->
+    supernode map of the oracle's partition."""
+    rp, ci = gen.config(name, scale)
+    n = rp.size - 1
+    want = oracle.symbolic(rp, ci, row_begin=rb, row_end=n)
+    r = g.symbolic(rp, ci, ctx=ctx, row_begin=rb)
+    if rb % 128:
+        r.stitch(None)  # a range start with no predecessor starts a block
+    got = r.supno()
+    r.free()
+    sn = want["sn_start"]
+    ref = np.repeat(np.arange(sn.size - 1, dtype=np.int32), np.diff(sn))
+    assert np.array_equal(got, ref)
