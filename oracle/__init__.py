@@ -55,6 +55,8 @@ def _load():
         lib.oracle_supernodes.argtypes = [
             ctypes.c_int64, ctypes.c_int64, P(ctypes.c_int64), P(ctypes.c_int32),
             P(ctypes.c_int64), ctypes.c_int64, P(ctypes.c_int32)]
+        lib.oracle_supernodes_cap.restype = ctypes.c_int64
+        lib.oracle_supernodes_cap.argtypes = lib.oracle_supernodes.argtypes
         lib.oracle_gp.restype = ctypes.c_int
         lib.oracle_gp.argtypes = [ctypes.c_int64, P(ctypes.c_int64), P(ctypes.c_int32),
                                   P(P(ctypes.c_int64)), P(P(ctypes.c_int32)),
@@ -109,9 +111,12 @@ def rows(rowptr, colidx, rows=None, nthreads: int | None = None):
     return dict(L_rowptr=Lp, L_colidx=Li, U_rowptr=Up, U_colidx=Ui, visits=int(visits.value))
 
 
-def supernodes(row_begin: int, L_rowptr, L_colidx, U_rowptr, chunk_size: int = 128):
+def supernodes(row_begin: int, L_rowptr, L_colidx, U_rowptr, chunk_size: int = 128,
+               cap_only: bool = False):
     """Greedy T3 scan (Def. def:T3) over consecutive rows starting
-    at ``row_begin``; returns sn_start (leading rows + sentinel)."""
+    at ``row_begin``; returns sn_start (leading rows + sentinel).  Forced
+    breaks at multiples of chunk_size, or with ``cap_only`` only a
+    maximum supernode size of chunk_size rows."""
     lib = _load()
     Lp = np.ascontiguousarray(L_rowptr, dtype=np.int64)
     Li = np.ascontiguousarray(L_colidx, dtype=np.int32)
@@ -119,7 +124,8 @@ def supernodes(row_begin: int, L_rowptr, L_colidx, U_rowptr, chunk_size: int = 1
     m = Lp.size - 1
     out = np.zeros(m + 1, dtype=np.int32)
     Li_ = Li if Li.size else np.zeros(1, np.int32)
-    ns = lib.oracle_supernodes(int(row_begin), m, _ptr(Lp, ctypes.c_int64),
+    fn = lib.oracle_supernodes_cap if cap_only else lib.oracle_supernodes
+    ns = fn(int(row_begin), m, _ptr(Lp, ctypes.c_int64),
                                _ptr(Li_, ctypes.c_int32), _ptr(Up, ctypes.c_int64),
                                int(chunk_size), _ptr(out, ctypes.c_int32))
     if ns < 0:
@@ -128,7 +134,7 @@ def supernodes(row_begin: int, L_rowptr, L_colidx, U_rowptr, chunk_size: int = 1
 
 
 def symbolic(rowptr, colidx, chunk_size: int = 128, row_begin: int = 0,
-             row_end: int | None = None, nthreads: int | None = None):
+             row_end: int | None = None, nthreads: int | None = None, cap_only: bool = False):
     """Full oracle result over rows [row_begin, row_end): L/U CSR, sn_start,
     nnz counts and fill count (nnz_offdiag(L+U) - nnz_offdiag(A))."""
     rowptr = np.asarray(rowptr, dtype=np.int64)
@@ -137,7 +143,7 @@ def symbolic(rowptr, colidx, chunk_size: int = 128, row_begin: int = 0,
     row_end = n if row_end is None else row_end
     rr = np.arange(row_begin, row_end, dtype=np.int64)
     r = rows(rowptr, colidx, rr, nthreads)
-    sn = supernodes(row_begin, r["L_rowptr"], r["L_colidx"], r["U_rowptr"], chunk_size)
+    sn = supernodes(row_begin, r["L_rowptr"], r["L_colidx"], r["U_rowptr"], chunk_size, cap_only)
     rows_a = np.repeat(rr, np.diff(rowptr[row_begin:row_end + 1]))
     cols_a = colidx[rowptr[row_begin]:rowptr[row_end]]
     nnz_a_off = int(np.count_nonzero(cols_a != rows_a))

@@ -296,3 +296,36 @@ int64_t oracle_supernodes(int64_t row_begin, int64_t nrows, const int64_t *Lptr,
 }
 
 void oracle_free(void *p) { free(p); }
+
+/*
+ * oracle_supernodes_cap: the cap-only variant of the T3 partition (SURVEY.md
+ * §8(f) NEXT-3).  chunkSize is read only as "the size of the user defined
+ * maximum supernode" (default 128 P:1011), without the forced break at
+ * multiples of chunk_size: the greedy left-to-right scan of Definition def:T3
+ * from row_begin, where row s joins the supernode of leader r iff
+ *   s - r < cap                       (the supernode would not exceed cap rows)
+ *   nnz(U(s,:)) = nnz(U(s-1,:)) - 1   (requirement (i))
+ *   L(s, r) != 0                      (requirement (ii))
+ * and otherwise starts a new supernode.  Arguments as oracle_supernodes.
+ */
+int64_t oracle_supernodes_cap(int64_t row_begin, int64_t nrows, const int64_t *Lptr,
+                              const int32_t *Lidx, const int64_t *Uptr,
+                              int64_t cap, int32_t *sn_start) {
+    if (nrows < 0 || cap < 1 || !sn_start) return -2;
+    int64_t ns = 0, r = -1;
+    for (int64_t k = 0; k < nrows; ++k) {
+        int64_t s = row_begin + k;
+        int joins = 0;
+        if (k > 0 && s - r < cap) {
+            int64_t nnz_s = Uptr[k + 1] - Uptr[k];
+            int64_t nnz_prev = Uptr[k] - Uptr[k - 1];
+            if (nnz_s == nnz_prev - 1) {              /* requirement (i) */
+                for (int64_t e = Lptr[k]; e < Lptr[k + 1]; ++e)
+                    if (Lidx[e] == r) { joins = 1; break; }  /* (ii) L(s,r) != 0 */
+            }
+        }
+        if (!joins) { r = s; sn_start[ns++] = (int32_t)s; }
+    }
+    sn_start[ns] = (int32_t)(row_begin + nrows);
+    return ns;
+}

@@ -440,3 +440,72 @@ def test_gp_equals_fill2_mid_scale(name, scale):
     b = oracle.rows(rp, ci)
     for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx"):
         assert np.array_equal(a[k], b[k]), k
+
+
+# ------------------------------------ cap-only supernodes (§8(f) NEXT-3) ----
+# chunk_size read only as the maximum supernode size, no forced
+# breaks at its multiples.
+
+def _diag_then_dense(p, m):
+    """p diagonal-only rows, then an m x m dense block: rows p..p+m-1 hold
+    every column of the block."""
+    n = p + m
+    rows, cols = [], []
+    for i in range(p, n):
+        for j in range(p, n):
+            if i != j:
+                rows.append(i)
+                cols.append(j)
+    return gen.csr_from_edges(n, np.array(rows, np.int64), np.array(cols, np.int64))
+
+
+@pytest.mark.parametrize("p,m,cap", [(5, 40, 8), (3, 17, 4), (0, 30, 7), (6, 10, 128), (1, 9, 1)])
+def test_cap_only_closed_form(p, m, cap):
+    """Diagonal prefix + dense block (no fill): the prefix rows are singletons
+    (nnzU = 1 each), the block's rows satisfy Def. def:T3 against any earlier
+    block row (nnzU drops by one, L dense), so the cap-only blocks start at
+    p, p + cap, p + 2 cap, ...; the forced-break partition instead breaks at
+    the multiples of cap."""
+    rp, ci = _diag_then_dense(p, m)
+    n = p + m
+    r = oracle.symbolic(rp, ci, chunk_size=cap, cap_only=True)
+    assert r["fill_count"] == 0
+    want = list(range(p)) + list(range(p, n, cap)) + [n]
+    assert r["sn_start"].tolist() == want
+    f = oracle.symbolic(rp, ci, chunk_size=cap)["sn_start"].tolist()
+    want_f = sorted(set(range(p)) | {p} | {k for k in range(p, n) if k % cap == 0}) + [n]
+    assert f == want_f
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_cap_only_def1_and_maximality(seed):
+    """Every cap-only block satisfies Def. def:T3 and the cap; every leader
+    after the first either follows a full block or fails (i) or (ii) against
+    the previous leader (the greedy scan never splits a joinable row); with a
+    cap of at least n both partitions are the uncapped greedy scan."""
+    rng = np.random.default_rng(9100 + seed)
+    if seed % 3 == 0:
+        rp, ci = gen.grid3d(4, p=0.25, seed=seed, order="nd")
+    else:
+        rp, ci = gen.random_graph(int(rng.integers(10, 90)), float(rng.uniform(0.03, 0.3)),
+                                  seed=9300 + seed)
+    n = rp.size - 1
+    for cap in (1, 2, 3, 5, 128):
+        r = oracle.symbolic(rp, ci, chunk_size=cap, cap_only=True)
+        nnzU = np.diff(r["U_rowptr"]).tolist()
+        Ls = [set(row_sets(r, i)[0].tolist()) for i in range(n)]
+        sn = r["sn_start"].tolist()
+        assert sn[0] == 0 and sn[-1] == n and all(a < b for a, b in zip(sn, sn[1:]))
+        for b in range(len(sn) - 1):
+            lead = sn[b]
+            assert sn[b + 1] - lead <= cap
+            for s in range(lead + 1, sn[b + 1]):
+                assert nnzU[s] == nnzU[s - 1] - 1 and lead in Ls[s]
+            if b > 0 and lead - sn[b - 1] < cap:
+                prev = sn[b - 1]
+                assert not (nnzU[lead] == nnzU[lead - 1] - 1 and prev in Ls[lead])
+        if cap == 1:
+            assert sn == list(range(n + 1))
+    big = oracle.symbolic(rp, ci, chunk_size=n + 1, cap_only=True)["sn_start"]
+    assert np.array_equal(big, oracle.symbolic(rp, ci, chunk_size=n + 1)["sn_start"])
+
