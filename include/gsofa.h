@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define GSOFA_VERSION 1
+#define GSOFA_VERSION 2
 
 /* ---------------------------------------------------------- error codes -- */
 #define GSOFA_OK            0
@@ -114,6 +114,16 @@ typedef struct gsofa_opts {
    * GSOFA_EINTERNAL with the failed checks in gsofa_last_error_detail().
    * Costs one extra pass over the output; default 0. */
   int32_t checked;
+  /* Supernode rule.  0 (default): forced break at
+   * every multiple of chunk_size (chunks never share a supernode).
+   * 1: cap-only -- chunk_size is only "the size of the user defined maximum
+   * supernode": the greedy Def. def:T3 scan lets row s
+   * join the block of leader r iff s - r < chunk_size and (i), (ii) hold,
+   * so blocks may cross multiples of chunk_size.  A range's provisional head
+   * blocks can then change up to the first row where the stitched scan meets
+   * one of its own leaders (gsofa_supernode_stitch); the tail record's
+   * leader carries the running block length (row - leader + 1). */
+  int32_t sn_cap_only;
 } gsofa_opts;
 
 /* ------------------------------------------------------------ statistics -- */
@@ -220,8 +230,11 @@ typedef struct gsofa_tail {
  *         of chunk_size) are recomputed by the greedy Def. def:T3 scan
  *         starting from *prev (row s joins the block of leader r iff
  *         nnz(U(s,:)) = nnz(U(s-1,:)) - 1 and L(s, r) != 0).  Blocks after
- *         that chunk boundary are unchanged.  The scan runs in a CUDA kernel
- *         (host results are read through their pinned mapping).
+ *         that chunk boundary are unchanged.  With sn_cap_only the re-scan
+ *         (also requiring s - r < chunk_size) runs until it starts a block at
+ *         a row that already leads one (from there on the scans agree), or to
+ *         row_end.  The scan runs in a CUDA kernel (host results are read
+ *         through their pinned mapping).
  *   prev  tail of the range ending at row_begin - 1 (else GSOFA_EINVAL);
  *         NULL: row_begin truly starts a block (e.g. row_begin = 0), nothing
  *         changes.

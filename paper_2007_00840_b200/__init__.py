@@ -38,7 +38,8 @@ class Opts(ctypes.Structure):
     _fields_ = [("chunk_size", _I32), ("max_concurrent", _I32), ("mem_budget_bytes", _I64),
                 ("fill_first", _I32), ("schedule", _I32), ("row_begin", _I64),
                 ("row_end", _I64), ("device", _I32), ("outputs_on_device", _I32),
-                ("stream", ctypes.c_void_p), ("checked", _I32)]
+                ("stream", ctypes.c_void_p), ("checked", _I32),
+                ("sn_cap_only", _I32)]
 
 
 class Stats(ctypes.Structure):
@@ -285,13 +286,15 @@ def symbolic(rowptr, colidx, *, ctx: Context | None = None, chunk_size: int = 12
              max_concurrent: int = 0, mem_budget_bytes: int = 0, fill_first: bool = False,
              row_begin: int = 0, row_end: int = -1, device: int = 0,
              outputs_on_device: bool = False, stream=None, schedule: str = "auto",
-             checked: bool = False) -> Result:
+             checked: bool = False, sn_cap_only: bool = False) -> Result:
     """gsofa_symbolic: L/U patterns, supernodes and fill count of the pattern
     (rowptr int64[n+1], colidx int32[nnz]) for rows [row_begin, row_end).
     Inputs: numpy (host) or torch tensors (host or CUDA).  ``stream``: a
     torch.cuda.Stream or raw cudaStream_t integer.  ``schedule``:
     "auto" (default: FIFO for banded dense patterns, else threshold),
-    "threshold" or "fifo" (the paper's all-frontiers order)."""
+    "threshold" or "fifo" (the paper's all-frontiers order).  ``sn_cap_only``:
+    chunk_size bounds the supernode size only (no forced breaks at its
+    multiples)."""
     lib = load()
     rp, _, krp = _ptr(rowptr)
     ci, _, kci = _ptr(colidx)
@@ -306,6 +309,7 @@ def symbolic(rowptr, colidx, *, ctx: Context | None = None, chunk_size: int = 12
     o.outputs_on_device = int(bool(outputs_on_device))
     o.schedule = SCHEDULES[schedule]
     o.checked = int(bool(checked))
+    o.sn_cap_only = int(bool(sn_cap_only))
     if stream is not None:
         o.stream = ctypes.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
     if ci == 0:  # empty colidx: pass a valid dummy pointer

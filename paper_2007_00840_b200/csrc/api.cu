@@ -84,6 +84,7 @@ struct ResultImpl {
   gsofa_result r;
   HostBlock *block;  // pinned host storage of the arrays (host results)
   int32_t chunk_size;  // of the call (supernode stitch); sn_start has room for rows+1
+  int32_t cap_only;    // supernode rule of the call (gsofa_opts.sn_cap_only)
 };
 
 // ------------------------------------------------------------------ context
@@ -815,22 +816,34 @@ int gsofa_supernode_stitch(gsofa_result *r, const gsofa_tail *prev, gsofa_tail *
   }
   cudaError_t e = cudaSetDevice(r->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
-  if (prev && rb % chunk != 0) {
-    // provisional head blocks [rb, he): re-scan from the predecessor's tail
+  const bool cap = impl->cap_only != 0;
+  if (prev && (cap || rb % chunk != 0)) {
+    // provisional head blocks: re-scan from the predecessor's tail -- over
+    // [rb, next chunk start) under the forced-break rule, until the scan
+    // meets a provisional leader under the cap-only rule
     const int64_t he = std::min<int64_t>(re, (rb / chunk + 1) * chunk);
+    const int64_t cap_out = cap ? rows + 3 : chunk + 2;
     int32_t *d_out = nullptr;
-    if ((e = cudaMalloc((void **)&d_out, (size_t)(chunk + 2) * 4)) != cudaSuccess)
+    if ((e = cudaMalloc((void **)&d_out, (size_t)cap_out * 4)) != cudaSuccess)
       return cuda_fail(e, "cudaMalloc(stitch)");
-    std::vector<int32_t> h((size_t)chunk + 2);
-    e = gsofa::launch_supernode_stitch(r->U_rowptr, r->L_rowptr, r->L_colidx, (int32_t)rb,
-                                       (int32_t)he, prev->nnzU, (int32_t)prev->leader, r->sn_start,
-                                       r->nsuper, d_out, nullptr);
-    if (e == cudaSuccess) e = cudaMemcpy(h.data(), d_out, h.size() * 4, cudaMemcpyDeviceToHost);
+    int32_t hdr[3] = {0, 0, 0};
+    if (cap) {
+      e = gsofa::launch_supernode_stitch_cap(r->U_rowptr, r->L_rowptr, r->L_colidx, (int32_t)rb,
+                                             (int32_t)re, chunk, prev->nnzU, (int32_t)prev->leader,
+                                             r->sn_start, r->nsuper, d_out, nullptr);
+      if (e == cudaSuccess) e = cudaMemcpy(hdr, d_out, 12, cudaMemcpyDeviceToHost);
+    } else {
+      e = gsofa::launch_supernode_stitch(r->U_rowptr, r->L_rowptr, r->L_colidx, (int32_t)rb,
+                                         (int32_t)he, prev->nnzU, (int32_t)prev->leader, r->sn_start,
+                                         r->nsuper, d_out, nullptr);
+      if (e == cudaSuccess) e = cudaMemcpy(hdr, d_out, 8, cudaMemcpyDeviceToHost);
+    }
     if (e != cudaSuccess) {
       cudaFree(d_out);
       return cuda_fail(e, "supernode stitch");
     }
-    const int64_t nc = h[0], oc = h[1], tail = r->nsuper + 1 - oc;  // tail incl. the sentinel
+    const int64_t nc = hdr[0], oc = hdr[1], tail = r->nsuper + 1 - oc;  // tail incl. the sentinel
+    const int32_t *d_new = d_out + (cap ? 3 : 2);                        // the new head leaders
     if (r->on_device) {
       if (nc != oc && tail > 0) {
         int32_t *tmp = nullptr;
@@ -840,10 +853,10 @@ int gsofa_supernode_stitch(gsofa_result *r, const gsofa_tail *prev, gsofa_tail *
         cudaFree(tmp);
       }
       if (e == cudaSuccess && nc)
-        e = cudaMemcpy(r->sn_start, d_out + 2, (size_t)nc * 4, cudaMemcpyDeviceToDevice);
+        e = cudaMemcpy(r->sn_start, d_new, (size_t)nc * 4, cudaMemcpyDeviceToDevice);
     } else {
       std::memmove(r->sn_start + nc, r->sn_start + oc, (size_t)tail * 4);
-      std::memcpy(r->sn_start, h.data() + 2, (size_t)nc * 4);
+      if (nc) e = cudaMemcpy(r->sn_start, d_new, (size_t)nc * 4, cudaMemcpyDeviceToHost);
     }
     cudaFree(d_out);
     if (e != cudaSuccess) return cuda_fail(e, "supernode stitch copy");
@@ -881,7 +894,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   if (o.row_end < 0) o.row_end = n;
   if (o.chunk_size < 1 || o.row_begin < 0 || o.row_end > n || o.row_begin >= o.row_end ||
       o.max_concurrent < 0 || o.max_concurrent % 32 != 0 ||
-      o.mem_budget_bytes < 0 || o.schedule < 0 || o.schedule > GSOFA_SCHEDULE_HEIGHT) {
+      o.mem_budget_bytes < 0 || o.schedule < 0 || o.schedule > GSOFA_SCHEDULE_HEIGHT ||
+      o.sn_cap_only < 0 || o.sn_cap_only > 1) {
     set_detail("bad opts: chunk=%d rows=[%lld,%lld) C=%d budget=%lld", o.chunk_size,
                (long long)o.row_begin, (long long)o.row_end, o.max_concurrent,
                (long long)o.mem_budget_bytes);
@@ -1518,7 +1532,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     int32_t *flags = sn_scratch;                 // [2 rows]: Phase-I bits, leaders
     int32_t *pos = sn_scratch + 2 * rows;        // [rows]
     int32_t *total = (int32_t *)c->totals + 4;   // scratch int
-    CK(gsofa::launch_supernode_flags(Lrp, Lci, Urp, (int32_t)rb, (int32_t)re, o.chunk_size, flags, st));
+    CK(gsofa::launch_supernode_flags(Lrp, Lci, Urp, (int32_t)rb, (int32_t)re, o.chunk_size,
+                                     o.sn_cap_only, flags, st));
     CK(gsofa::scan_exclusive_i32(flags + rows, pos, rows, total, scan_tmp, tmpb, st));
     CK(gsofa::launch_supernode_scatter(flags + rows, pos, (int32_t)rb, (int32_t)re, total, sn, st));
     launches += 4;
@@ -1538,7 +1553,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       CK(cudaStreamSynchronize(st));
     }
     CK(gsofa::launch_audit(c->rowptr32, d_colidx, Lrp, Lci, Urp, Uci, sn, (int32_t *)c->totals + 4,
-                           (int32_t)rb, (int32_t)rows, (int32_t)n, o.chunk_size, c->err, st));
+                           (int32_t)rb, (int32_t)rows, (int32_t)n, o.chunk_size, o.sn_cap_only, c->err, st));
     ++launches;
     int bad = 0;
     CK(cudaMemcpyAsync(&bad, c->err, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1574,6 +1589,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     res->device = c->device;
     res->schedule = o.schedule;
     reinterpret_cast<ResultImpl *>(res)->chunk_size = o.chunk_size;
+    reinterpret_cast<ResultImpl *>(res)->cap_only = o.sn_cap_only;
     res->stats.frontier_items = (int64_t)hs[0];
     res->stats.edge_inspections = (int64_t)hs[1];
     res->stats.rounds = (int64_t)hs[2];

@@ -192,9 +192,11 @@ cudaError_t launch_supno(const int32_t *sn_start, int64_t nsuper, int32_t row_be
                          cudaStream_t st);
 cudaError_t launch_count_offdiag(const int32_t *rowptr, const int32_t *colidx, int32_t r0,
                                  int32_t r1, unsigned long long *out, cudaStream_t st);
+// flags: [3 rows] scratch; [0, rows) Phase-I bits, [rows, 2 rows) leaders,
+// [2 rows, 3 rows) the cap-only successor table (free again on return)
 cudaError_t launch_supernode_flags(const int64_t *L_rowptr, const int32_t *L_colidx,
                                    const int64_t *U_rowptr, int32_t row_begin, int32_t row_end,
-                                   int32_t chunk, int32_t *flags, cudaStream_t st);
+                                   int32_t chunk, int32_t cap_only, int32_t *flags, cudaStream_t st);
 // exclusive scans (int32 -> int32 / int32 -> int64); total -> *total
 cudaError_t scan_exclusive_i32(const int32_t *in, int32_t *out, int64_t count, int32_t *total,
                                void *tmp, size_t tmp_bytes, cudaStream_t st);
@@ -205,10 +207,18 @@ cudaError_t launch_supernode_stitch(const int64_t *U_rowptr, const int64_t *L_ro
                                     const int32_t *L_colidx, int32_t rb, int32_t he,
                                     int64_t prev_nnzU, int32_t prev_leader, const int32_t *sn_start,
                                     int64_t nsuper, int32_t *out, cudaStream_t st);
+// cap-only rule: re-scan from rb until the scan starts a block at a row that
+// already leads one (or row_end); out [3 + rows]: [0] new leaders, [1] old
+// leaders below the meeting row, [2] the meeting row, [3..] the new leaders
+cudaError_t launch_supernode_stitch_cap(const int64_t *U_rowptr, const int64_t *L_rowptr,
+                                        const int32_t *L_colidx, int32_t rb, int32_t re, int32_t cap,
+                                        int64_t prev_nnzU, int32_t prev_leader,
+                                        const int32_t *sn_start, int64_t nsuper, int32_t *out,
+                                        cudaStream_t st);
 cudaError_t launch_audit(const int32_t *A_rowptr, const int32_t *A_colidx, const int64_t *L_rowptr,
                          const int32_t *L_colidx, const int64_t *U_rowptr, const int32_t *U_colidx,
                          const int32_t *sn_start, const int32_t *nsuper, int32_t row_begin, int32_t rows,
-                         int32_t n, int32_t chunk, int *err, cudaStream_t st);
+                         int32_t n, int32_t chunk, int32_t cap_only, int *err, cudaStream_t st);
 cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, int32_t row_begin,
                                      int32_t row_end, const int32_t *total, int32_t *sn_start,
                                      cudaStream_t st);

@@ -95,14 +95,15 @@ __device__ __forceinline__ bool row_contains(const int32_t *cols, int64_t a, int
   return false;
 }
 
-// Phase I: flags[s] = 1 (Phase-I leader, bit 0) or 0 (bit 1)
+// Phase I: bit[k] = 1 iff row s = row_begin + k satisfies requirement (i)
+// against s - 1 (and, under the forced-break rule, s is not a chunk start)
 __global__ void sn_phase1_kernel(const int64_t *U_rowptr, int32_t row_begin, int32_t row_end,
-                                 int32_t chunk, int32_t *bit) {
+                                 int32_t chunk, int32_t cap_only, int32_t *bit) {
   const int32_t s = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= row_end) return;
   const int k = s - row_begin;
   int b = 0;
-  if (s != row_begin && s % chunk != 0) {
+  if (s != row_begin && (cap_only || s % chunk != 0)) {
     const int64_t nu = U_rowptr[k + 1] - U_rowptr[k];
     const int64_t np = U_rowptr[k] - U_rowptr[k - 1];
     b = (nu == np - 1);
@@ -128,6 +129,120 @@ __global__ void sn_phase2_kernel(const int64_t *L_rowptr, const int32_t *L_colid
       leader[kt] = 1;  // rejected: starts a new supernode
       r = t;
     }
+  }
+}
+
+// Cap-only rule: chunk_size bounds the block size but
+// forces no break, so a run of bit-1 rows may be longer than the cap and the
+// greedy scan inside it is a chain of leaders.  Two steps keep the chain off
+// the binary searches:
+//   sn_next_kernel (one warp per row r as a would-be leader): nxt[r] = the
+//     first row t in (r, r + cap] that cannot join r's block -- t = r + cap,
+//     t = row_end, bit[t] = 0, or L(t, r) = 0 -- 32 candidate rows per probe;
+//     also clears leader[r]
+//   sn_walk_kernel (one thread per Phase-I leader, i.e. bit 0): follows
+//     r -> nxt[r] through its run and marks every leader on the way; the
+//     walk ends at the next Phase-I leader (that thread's run) or row_end.
+__global__ void sn_next_kernel(const int64_t *L_rowptr, const int32_t *L_colidx, int32_t row_begin,
+                               int32_t row_end, int32_t cap, const int32_t *bit, int32_t *nxt,
+                               int32_t *leader) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int32_t rows = row_end - row_begin;
+  if (k >= rows) return;
+  const int32_t r = row_begin + (int32_t)k;
+  const int32_t lim = (int32_t)min((int64_t)row_end, (int64_t)r + cap);
+  int32_t res = lim;
+  for (int32_t t0 = r + 1; t0 < lim; t0 += 32) {
+    const int32_t t = t0 + lane;
+    bool fail = false;
+    if (t < lim) {
+      const int kt = t - row_begin;
+      fail = !bit[kt] || !row_contains(L_colidx, L_rowptr[kt], L_rowptr[kt + 1], r);
+    }
+    const uint32_t b = __ballot_sync(kFull, fail);
+    if (b) {
+      res = t0 + __ffs(b) - 1;
+      break;
+    }
+  }
+  if (lane == 0) {
+    nxt[k] = res - row_begin;
+    leader[k] = 0;
+  }
+}
+
+__global__ void sn_walk_kernel(int32_t rows, const int32_t *bit, const int32_t *nxt,
+                               int32_t *leader) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= rows || bit[k]) return;
+  int32_t r = k;
+  leader[r] = 1;
+  for (;;) {
+    const int32_t t = nxt[r];
+    if (t >= rows || !bit[t]) break;  // the next run (its own thread) or the end
+    leader[t] = 1;
+    r = t;
+  }
+}
+
+// Cap-only stitch: one warp re-runs the greedy scan over [rb, re) from the
+// predecessor's tail, testing 32 rows per probe against the current leader r
+// (t - r < cap, requirement (i) against row t - 1, L(t, r) != 0).  The first
+// row that cannot join becomes a leader; if it already leads a provisional
+// block the two scans agree from there on (same leader, same rows) and the
+// re-scan stops.  out: [0] new leaders, [1] provisional leaders below the
+// meeting row, [2] the meeting row, [3..] the new leaders.
+__global__ void sn_stitch_cap_kernel(const int64_t *U_rowptr, const int64_t *L_rowptr,
+                                     const int32_t *L_colidx, int32_t rb, int32_t re, int32_t cap,
+                                     int64_t prev_nnzU, int32_t prev_leader,
+                                     const int32_t *sn_start, int64_t nsuper, int32_t *out) {
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  int32_t r = prev_leader, s = rb, meet = re;
+  int nc = 0;
+  while (s < re) {
+    const int32_t t = s + lane;
+    bool fail = false;
+    if (t < re) {
+      const int k = t - rb;
+      const int64_t nu = U_rowptr[k + 1] - U_rowptr[k];
+      const int64_t np = k == 0 ? prev_nnzU : U_rowptr[k] - U_rowptr[k - 1];
+      fail = !((int64_t)t - r < cap && nu == np - 1 &&
+               row_contains(L_colidx, L_rowptr[k], L_rowptr[k + 1], r));
+    }
+    const uint32_t b = __ballot_sync(kFull, fail);
+    if (!b) {
+      s += 32;
+      continue;
+    }
+    const int32_t lead = s + __ffs(b) - 1;
+    // does lead already start a provisional block?  (binary search)
+    int64_t lo = 0, hi = nsuper;
+    while (lo < hi) {
+      const int64_t m = (lo + hi) >> 1;
+      if (sn_start[m] < lead) lo = m + 1;
+      else hi = m;
+    }
+    if (lo < nsuper && sn_start[lo] == lead) {
+      meet = lead;
+      break;
+    }
+    if (lane == 0) out[3 + nc] = lead;
+    ++nc;
+    r = lead;
+    s = lead + 1;
+  }
+  if (lane == 0) {
+    int64_t lo = 0, hi = nsuper;  // provisional leaders below meet
+    while (lo < hi) {
+      const int64_t m = (lo + hi) >> 1;
+      if (sn_start[m] < meet) lo = m + 1;
+      else hi = m;
+    }
+    out[0] = nc;
+    out[1] = (int32_t)lo;
+    out[2] = meet;
   }
 }
 
@@ -173,7 +288,7 @@ __global__ void sn_stitch_kernel(const int64_t *U_rowptr, const int64_t *L_rowpt
 __global__ void audit_kernel(const int32_t *A_rowptr, const int32_t *A_colidx, const int64_t *L_rowptr,
                              const int32_t *L_colidx, const int64_t *U_rowptr, const int32_t *U_colidx,
                              const int32_t *sn_start, const int32_t *nsuper_p, int32_t row_begin,
-                             int32_t rows, int32_t n, int32_t chunk, int *err) {
+                             int32_t rows, int32_t n, int32_t chunk, int32_t cap_only, int *err) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
@@ -207,8 +322,9 @@ __global__ void audit_kernel(const int32_t *A_rowptr, const int32_t *A_colidx, c
     const int32_t lead = sn_start[lo];
     if (s != lead) {
       const int64_t nu = ub - ua, np = ua - U_rowptr[r - 1];
-      if (s % chunk == 0 || nu != np - 1 || !row_contains(L_colidx, la, lb, lead)) bad |= 8;
-    } else if (s != row_begin && s % chunk != 0) {
+      const bool brk = cap_only ? s - lead >= chunk : s % chunk == 0;
+      if (brk || nu != np - 1 || !row_contains(L_colidx, la, lb, lead)) bad |= 8;
+    } else if (s != row_begin && (cap_only || s % chunk != 0)) {
       int32_t lo2 = 0, hi2 = ns;  // leader of s - 1
       while (hi2 - lo2 > 1) {
         const int32_t m = (lo2 + hi2) >> 1;
@@ -216,7 +332,8 @@ __global__ void audit_kernel(const int32_t *A_rowptr, const int32_t *A_colidx, c
         else hi2 = m;
       }
       const int64_t nu = ub - ua, np = ua - U_rowptr[r - 1];
-      if (nu == np - 1 && row_contains(L_colidx, la, lb, sn_start[lo2])) bad |= 16;
+      const bool room = !cap_only || s - sn_start[lo2] < chunk;
+      if (room && nu == np - 1 && row_contains(L_colidx, la, lb, sn_start[lo2])) bad |= 16;
     }
   }
   bad = __reduce_or_sync(0xFFFFFFFFu, bad);
@@ -358,14 +475,21 @@ cudaError_t launch_count_offdiag(const int32_t *rowptr, const int32_t *colidx, i
 
 cudaError_t launch_supernode_flags(const int64_t *L_rowptr, const int32_t *L_colidx,
                                    const int64_t *U_rowptr, int32_t row_begin, int32_t row_end,
-                                   int32_t chunk, int32_t *flags, cudaStream_t st) {
-  // flags has room for 2 * rows: [0, rows) = Phase-I bits, [rows, 2 rows) = leaders
+                                   int32_t chunk, int32_t cap_only, int32_t *flags, cudaStream_t st) {
+  // flags has room for 3 * rows: [0, rows) = Phase-I bits, [rows, 2 rows) =
+  // leaders, [2 rows, 3 rows) = cap-only successor table
   const int32_t rows = row_end - row_begin;
   if (rows <= 0) return cudaSuccess;
   const unsigned nb = (unsigned)((rows + 255) / 256);
-  sn_phase1_kernel<<<nb, 256, 0, st>>>(U_rowptr, row_begin, row_end, chunk, flags);
-  sn_phase2_kernel<<<nb, 256, 0, st>>>(L_rowptr, L_colidx, row_begin, row_end, flags,
-                                       flags + rows);
+  sn_phase1_kernel<<<nb, 256, 0, st>>>(U_rowptr, row_begin, row_end, chunk, cap_only, flags);
+  if (cap_only) {
+    sn_next_kernel<<<(unsigned)(((int64_t)rows * 32 + 255) / 256), 256, 0, st>>>(
+        L_rowptr, L_colidx, row_begin, row_end, chunk, flags, flags + 2 * rows, flags + rows);
+    sn_walk_kernel<<<nb, 256, 0, st>>>(rows, flags, flags + 2 * rows, flags + rows);
+  } else {
+    sn_phase2_kernel<<<nb, 256, 0, st>>>(L_rowptr, L_colidx, row_begin, row_end, flags,
+                                         flags + rows);
+  }
   return cudaGetLastError();
 }
 
@@ -387,14 +511,24 @@ cudaError_t launch_supernode_stitch(const int64_t *U_rowptr, const int64_t *L_ro
   return cudaGetLastError();
 }
 
+cudaError_t launch_supernode_stitch_cap(const int64_t *U_rowptr, const int64_t *L_rowptr,
+                                        const int32_t *L_colidx, int32_t rb, int32_t re, int32_t cap,
+                                        int64_t prev_nnzU, int32_t prev_leader,
+                                        const int32_t *sn_start, int64_t nsuper, int32_t *out,
+                                        cudaStream_t st) {
+  sn_stitch_cap_kernel<<<1, 32, 0, st>>>(U_rowptr, L_rowptr, L_colidx, rb, re, cap, prev_nnzU,
+                                         prev_leader, sn_start, nsuper, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_audit(const int32_t *A_rowptr, const int32_t *A_colidx, const int64_t *L_rowptr,
                          const int32_t *L_colidx, const int64_t *U_rowptr, const int32_t *U_colidx,
                          const int32_t *sn_start, const int32_t *nsuper, int32_t row_begin, int32_t rows,
-                         int32_t n, int32_t chunk, int *err, cudaStream_t st) {
+                         int32_t n, int32_t chunk, int32_t cap_only, int *err, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   audit_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(A_rowptr, A_colidx, L_rowptr, L_colidx,
                                                            U_rowptr, U_colidx, sn_start, nsuper,
-                                                           row_begin, rows, n, chunk, err);
+                                                           row_begin, rows, n, chunk, cap_only, err);
   return cudaGetLastError();
 }
 

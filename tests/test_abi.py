@@ -69,7 +69,7 @@ int main(void) {
 
 def test_version_and_strings(g):
     lib = g.load()
-    assert lib.gsofa_version() == 1
+    assert lib.gsofa_version() == 2
     assert lib.gsofa_strerror(-2).decode() == "malformed CSR input"
 
 

@@ -619,3 +619,52 @@ def test_supno(ctx, name, scale, rb):
     sn = want["sn_start"]
     ref = np.repeat(np.arange(sn.size - 1, dtype=np.int32), np.diff(sn))
     assert np.array_equal(got, ref)
+
+
+# ---------------------------- cap-only supernodes ----
+
+@pytest.mark.parametrize("name,scale,chunk", [("C1", None, 128), ("C1", None, 4), ("C3", 3000, 128),
+                                              ("C3", 3000, 16), ("C2", 16, 32), ("C5", 14, 128),
+                                              ("C4", 60, 64)])
+def test_supernodes_cap_only(ctx, name, scale, chunk):
+    """chunk_size as the maximum supernode size only (no forced breaks at its
+    multiples): the whole structure and the cap-only partition equal the
+    oracle's cap-only scan; checked mode (Def. def:T3 + maximality under the
+    cap rule) passes on the GPU output."""
+    rp, ci = gen.config(name, scale)
+    want = oracle.symbolic(rp, ci, chunk_size=chunk, cap_only=True)
+    got = run(rp, ci, ctx, chunk_size=chunk, sn_cap_only=True, checked=True)
+    assert_full_equal(got, want, f"{name} cap-only chunk={chunk}")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_supernodes_cap_only_random(ctx, seed):
+    rng = np.random.default_rng(4400 + seed)
+    n = int(rng.integers(40, 600))
+    rp, ci = gen.random_graph(n, float(rng.uniform(0.005, 0.08)), seed=4500 + seed)
+    for chunk in (1, 3, 8, 1000):
+        want = oracle.symbolic(rp, ci, chunk_size=chunk, cap_only=True)
+        assert_full_equal(run(rp, ci, ctx, chunk_size=chunk, sn_cap_only=True), want, f"chunk={chunk}")
+
+
+@pytest.mark.parametrize("name,scale,chunk", [("C3", 3000, 128), ("C2", 12, 16), ("C5", 14, 64)])
+@pytest.mark.parametrize("on_device", [False, True])
+def test_supernode_stitch_cap_only(ctx, name, scale, chunk, on_device):
+    """Cap-only ranges cut inside blocks, inside long joinable runs and one
+    row wide: the stitch chain re-scans each head until it meets one of the
+    range's own leaders and reproduces the whole-matrix cap-only partition."""
+    rp, ci = gen.config(name, scale)
+    n = rp.size - 1
+    full = oracle.symbolic(rp, ci, chunk_size=chunk, cap_only=True)
+    sn = full["sn_start"]
+    inside = [int(a) + 1 for a, b in zip(sn[:-1], sn[1:]) if b - a >= 3]
+    rng = np.random.default_rng(11)
+    cuts = set(rng.integers(1, n, 6).tolist()) | set(inside[:: max(1, len(inside) // 8)][:8])
+    cuts |= {c + 1 for c in list(cuts)[:3]}  # one-row ranges
+    bounds = [0] + sorted(c for c in cuts if 0 < c < n) + [n]
+    asm, tails = _stitched_ranges(rp, ci, ctx, bounds, chunk, outputs_on_device=on_device,
+                                  sn_cap_only=True)
+    for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start"):
+        assert np.array_equal(asm[k], full[k]), k
+    for (rb, re), t in zip(zip(bounds[:-1], bounds[1:]), tails):
+        assert t[2] == sn[np.searchsorted(sn, re - 1, side="right") - 1]
