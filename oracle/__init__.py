@@ -25,13 +25,13 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
-_SRCS = [_SRC, os.path.join(_HERE, "gp.c")]
+_SRCS = [_SRC, os.path.join(_HERE, "gp.c"), os.path.join(_HERE, "etree.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle.c and gp.c with gcc (plain C, -O2, pthreads)."""
+    """Compile oracle.c, gp.c and etree.c with gcc (plain C, -O2, pthreads)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
             os.path.getmtime(f) for f in _SRCS):
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread",
@@ -61,6 +61,9 @@ def _load():
         lib.oracle_gp.argtypes = [ctypes.c_int64, P(ctypes.c_int64), P(ctypes.c_int32),
                                   P(P(ctypes.c_int64)), P(P(ctypes.c_int32)),
                                   P(P(ctypes.c_int64)), P(P(ctypes.c_int32))]
+        lib.oracle_etree_rows.restype = ctypes.c_int
+        lib.oracle_etree_rows.argtypes = [ctypes.c_int64, P(ctypes.c_int64), P(ctypes.c_int32),
+                                          ctypes.c_int, P(P(ctypes.c_int64)), P(P(ctypes.c_int32))]
         lib.oracle_free.restype = None
         lib.oracle_free.argtypes = [ctypes.c_void_p]
         _lib = lib
@@ -192,3 +195,39 @@ def gp(rowptr, colidx):
     L_rowptr, L_colidx = _cols_to_rows(Lp, Li, n)
     U_rowptr, U_colidx = _cols_to_rows(Up, Ui, n)
     return dict(L_rowptr=L_rowptr, L_colidx=L_colidx, U_rowptr=U_rowptr, U_colidx=U_colidx)
+
+
+def etree_rows(rowptr, colidx, nthreads: int | None = None):
+    """Third comparator, symmetric patterns only: L by rows from the
+    elimination tree's row subtrees (oracle/etree.c); U = L^T + diagonal.
+    Returns dict(L_rowptr, L_colidx, U_rowptr, U_colidx); raises ValueError
+    if the pattern is not structurally symmetric."""
+    lib = _load()
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    n = rowptr.size - 1
+    P = ctypes.POINTER
+    lp, li = P(ctypes.c_int64)(), P(ctypes.c_int32)()
+    cidx = colidx if colidx.size else np.zeros(1, np.int32)
+    rc = lib.oracle_etree_rows(n, _ptr(rowptr, ctypes.c_int64), _ptr(cidx, ctypes.c_int32),
+                               int(nthreads or default_threads()), ctypes.byref(lp), ctypes.byref(li))
+    if rc == -3:
+        raise ValueError("pattern is not structurally symmetric")
+    if rc != 0:
+        raise RuntimeError(f"oracle_etree_rows failed rc={rc}")
+    try:
+        Lp = np.ctypeslib.as_array(lp, shape=(n + 1,)).copy()
+        Li = np.ctypeslib.as_array(li, shape=(max(1, int(Lp[-1])),))[: int(Lp[-1])].copy()
+    finally:
+        for q in (lp, li):
+            lib.oracle_free(ctypes.cast(q, ctypes.c_void_p))
+    # U(i,:) = {i} + column i of L (symmetric pattern), ascending
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(Lp))
+    cols = Li.astype(np.int64)
+    key_r = np.concatenate([cols, np.arange(n, dtype=np.int64)])
+    key_c = np.concatenate([rows, np.arange(n, dtype=np.int64)])
+    order = np.lexsort((key_c, key_r))
+    Up = np.zeros(n + 1, np.int64)
+    np.add.at(Up, key_r + 1, 1)
+    return dict(L_rowptr=Lp, L_colidx=Li, U_rowptr=np.cumsum(Up),
+                U_colidx=key_c[order].astype(np.int32))

@@ -509,3 +509,45 @@ def test_cap_only_def1_and_maximality(seed):
     big = oracle.symbolic(rp, ci, chunk_size=n + 1, cap_only=True)["sn_start"]
     assert np.array_equal(big, oracle.symbolic(rp, ci, chunk_size=n + 1)["sn_start"])
 
+
+
+# ------------------- third comparator: etree row subtrees (§8(f) NEXT-4) ----
+# oracle.etree_rows (oracle/etree.c): symmetric patterns only.
+
+@pytest.mark.parametrize("seed", range(40))
+def test_etree_rows_equals_dense_ge(seed):
+    rng = np.random.default_rng(81_000 + seed)
+    n = int(rng.integers(1, 70))
+    rp, ci = symmetrize(*gen.random_graph(n, float(rng.uniform(0.01, 0.2)), seed=82_000 + seed))
+    r = oracle.etree_rows(rp, ci)
+    M = np.zeros((n, n), dtype=bool)
+    for i in range(n):
+        M[i, r["L_colidx"][r["L_rowptr"][i]:r["L_rowptr"][i + 1]]] = True
+        M[i, r["U_colidx"][r["U_rowptr"][i]:r["U_rowptr"][i + 1]]] = True
+    assert np.array_equal(M, dense_ge(rp, ci))
+
+
+@pytest.mark.parametrize("k", [1, 2, 5, 12, 32])
+def test_etree_rows_grid_closed_form(k):
+    """2D k x k 5-point grid, natural order, no dropout: nnz(L) = (k-1)(k^2+1)."""
+    rp, ci = gen.grid2d(k, p=0.0, seed=0, order="natural")
+    r = oracle.etree_rows(rp, ci)
+    assert int(r["L_rowptr"][-1]) == (k - 1) * (k * k + 1)
+    assert int(r["U_rowptr"][-1]) - k * k == (k - 1) * (k * k + 1)
+
+
+def test_etree_rows_rejects_nonsymmetric():
+    rp, ci = gen.config("C1")  # p = 0.25 dropout per direction
+    with pytest.raises(ValueError):
+        oracle.etree_rows(rp, ci)
+
+
+@pytest.mark.parametrize("name,scale", [("C4", 120), ("C4", None)])
+def test_etree_rows_equal_fill2_symmetric_configs(name, scale):
+    """C4 is structurally symmetric (G3_circuit is): the etree comparator and
+    fill2 agree element by element (full size: 1.6M rows, a few seconds)."""
+    rp, ci = gen.config(name, scale)
+    a = oracle.etree_rows(rp, ci)
+    b = oracle.rows(rp, ci)
+    for key in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx"):
+        assert np.array_equal(a[key], b[key]), key

@@ -668,3 +668,22 @@ def test_supernode_stitch_cap_only(ctx, name, scale, chunk, on_device):
         assert np.array_equal(asm[k], full[k]), k
     for (rb, re), t in zip(zip(bounds[:-1], bounds[1:]), tails):
         assert t[2] == sn[np.searchsorted(sn, re - 1, side="right") - 1]
+
+
+# ----------------------- symmetric comparator --
+
+@pytest.mark.parametrize("case", ["C4_full", "grid3d_nd_p0", "C4_60"])
+def test_symmetric_etree_comparator(ctx, case):
+    """Structurally symmetric patterns: the GPU's L and U equal the Cholesky
+    structure from the elimination tree's row subtrees (oracle.etree_rows),
+    a comparator independent of fill2; C4 at its full size."""
+    if case == "C4_full":
+        rp, ci = gen.config("C4")
+    elif case == "C4_60":
+        rp, ci = gen.config("C4", 60)
+    else:
+        rp, ci = gen.grid3d(40, p=0.0, seed=0, order="nd")
+    want = oracle.etree_rows(rp, ci)
+    got = run(rp, ci, ctx)
+    for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx"):
+        assert np.array_equal(got[k], want[k]), k
