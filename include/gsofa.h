@@ -153,6 +153,11 @@ typedef struct gsofa_stats {
    * kernel abandons to the solo kernel count once (their redo). */
   int64_t first_visits;
   int64_t source_expansions;
+  /* External frontier management (FIFO order): frontier queue
+   * items written to pinned host memory because the HBM part of the queue
+   * (1/8 of its worst case when the memory budget is short, else all of it)
+   * was full.  0 when everything fit on the GPU. */
+  int64_t frontier_spilled;
 } gsofa_stats;
 
 /* --------------------------------------------------------------- result -- */

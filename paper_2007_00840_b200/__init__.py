@@ -49,7 +49,7 @@ class Stats(ctypes.Structure):
                 ("ms_total", ctypes.c_double), ("ms_traverse", ctypes.c_double),
                 ("ms_extract", ctypes.c_double), ("ms_supernode", ctypes.c_double),
                 ("ms_transfer", ctypes.c_double), ("first_visits", _I64),
-                ("source_expansions", _I64)]
+                ("source_expansions", _I64), ("frontier_spilled", _I64)]
 
 
 class CResult(ctypes.Structure):

@@ -94,6 +94,9 @@ struct Plan {
   size_t work_bytes, is_words, cnt_words;
   int64_t nsub;
   size_t total;
+  // FIFO: the queues hold 1 / 2^qfl of their worst case in HBM; the rest
+  // goes to pinned host memory (external frontier management)
+  int qfl = 0;
   // streaming (threshold) schedule
   int64_t slots = 0, heavy = 0, light = 0, Vmax = 0;
   size_t ws_words = 0, slot_is_words = 0, hws_words = 0;
@@ -112,6 +115,7 @@ struct gsofa_context {
   int64_t Cmax = 0, Gmax = 0;
   int gbits = 0;
   size_t work_bytes = 0, is_words = 0;
+  int qfl = 0;               // FIFO queue fraction in HBM: 1 / 2^qfl (Plan::qfl)
   int work_state = 0;        // WorkState
   uint64_t layout_sig = 0;   // streaming slot layout of the last call (Vmax, ws_words)
   int stream_blocks = 0;     // resident CTAs of the streaming kernel
@@ -142,6 +146,10 @@ struct gsofa_context {
   int32_t *ord_buf = nullptr;
   size_t ord_cap = 0;
   HostBlock *hpool = nullptr;  // pinned storage reused by host-side results
+  // external frontier (FIFO queue overflow) in mapped pinned host memory,
+  // grow-only; spill_dev is its device address
+  uint32_t *spill = nullptr, *spill_dev = nullptr;
+  size_t spill_cap = 0;  // words
 };
 
 namespace {
@@ -161,23 +169,47 @@ size_t small_bytes(int64_t Cmax) {
 
 // Traversal working set of a batch of C sources whose labels cover Vb
 // vertices (Table tab:complexity, after bubble removal):
-//   FIFO:      maxId labels C*Vb*4 B + 2 frontier masks + 2 queues (G*Vb words each)
+//   FIFO:      maxId labels C*Vb*4 B + 2 frontier masks (G*Vb words each) +
+//              2 queues (G*Vb words each, of which 1 / 2^qfl in HBM)
 //   threshold: per 32-source group reached/pend/list0/list1 (Vb words each)
 //              + a threshold bitmap (Vb/32 words)
-size_t work_need(int schedule, int64_t C, int64_t Vb) {
+size_t work_need(int schedule, int64_t C, int64_t Vb, int qfl = 0) {
   const int64_t G = C / 32;
-  if (schedule == GSOFA_SCHEDULE_FIFO) return (size_t)C * Vb * 4 + (size_t)G * Vb * 16;
+  if (schedule == GSOFA_SCHEDULE_FIFO)
+    return (size_t)C * Vb * 4 + (size_t)G * Vb * 8 + (((size_t)G * Vb) >> qfl) * 8;
   return (size_t)G * gsofa::stream_ws_words(Vb, 0) * 4;
 }
 
 // FIFO keeps its label region apart from masks/queues so that every label
 // cell only ever holds epoch-encoded values (P:573 requires stale values to
-// decode as "uninitialised").
-size_t fifo_label_bytes(size_t work) { return (size_t)((double)work * 4.0 / 4.5) / 512 * 512; }
+// decode as "uninitialised").  Per (group, vertex) cell: 128 B of labels,
+// 8 B of masks, 8 / 2^qfl B of queues in HBM.
+size_t fifo_label_bytes(size_t work, int qfl) {
+  return (size_t)((double)work * 128.0 / (136.0 + 8.0 / (double)(1 << qfl))) / 512 * 512;
+}
+// mask capacity (words per mask array) and HBM queue capacity (items per queue)
+void fifo_caps(size_t work, int qfl, size_t &Qm, size_t &Qq) {
+  const size_t lab = fifo_label_bytes(work, qfl);
+  Qm = (size_t)((double)(work - lab) / (8.0 + 8.0 / (double)(1 << qfl)));
+  Qq = Qm >> qfl;
+}
 
 bool make_plan(int schedule, int64_t n, int64_t rows, int64_t vb_max, int64_t cmax_req,
                int64_t budget, Plan &p) {
   const int64_t sub = gsofa::extract_sub_columns();
+  // external frontier management first, then fewer concurrent sources
+  // (P:780-784): when the budget cannot hold the whole batch with its full
+  // queues, only 1/8 of each queue stays in HBM (the paper measured peak
+  // frontier usage up to 25% and far less on average, Table tab:FQ_usage)
+  int qfl = 0;
+  if (schedule == GSOFA_SCHEDULE_FIFO) {
+    const int64_t C0 = std::max<int64_t>(32, round_up(std::min<int64_t>(cmax_req, round_up(rows, 32)), 32));
+    const int64_t G0 = C0 / 32;
+    const size_t full = work_need(schedule, C0, vb_max) + (size_t)G0 * n * 4 +
+                        2 * (size_t)G0 * ceil_div(n, sub) * 32 * 4 + small_bytes(C0) + 8192 + 4096;
+    if ((int64_t)full > budget) qfl = 3;
+    if (const char *e = std::getenv("GSOFA_FRONTIER_FRAC_LOG")) qfl = std::max(0, std::min(20, atoi(e)));
+  }
   int64_t Cmax = std::min<int64_t>(cmax_req, round_up(rows, 32));
   Cmax = std::max<int64_t>(32, round_up(Cmax, 32));
   for (; Cmax >= 32; Cmax = (Cmax / 2 / 32) * 32) {
@@ -189,14 +221,15 @@ bool make_plan(int schedule, int64_t n, int64_t rows, int64_t vb_max, int64_t cm
     const size_t is_words = (size_t)G * n;
     const size_t cnt_words = (size_t)G * nsub * 32;
     const size_t fixed = is_words * 4 + 2 * cnt_words * 4 + small_bytes(Cmax) + 8192;
-    const size_t need_max = work_need(schedule, Cmax, vb_max) + 4096;
-    const size_t need_min = work_need(schedule, 32, vb_max) + 4096;
+    const size_t need_max = work_need(schedule, Cmax, vb_max, qfl) + 4096;
+    const size_t need_min = work_need(schedule, 32, vb_max, qfl) + 4096;
     if ((int64_t)(fixed + need_min) > budget) continue;
     size_t work = std::min<size_t>(need_max, (size_t)budget - fixed);
     work = (work + 4095) / 4096 * 4096;
     p.Cmax = Cmax;
     p.Gmax = G;
     p.gbits = gb;
+    p.qfl = qfl;
     p.work_bytes = work;
     p.is_words = is_words;
     p.cnt_words = cnt_words;
@@ -275,16 +308,18 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
 }
 
 // largest multiple of 32 <= cap whose working set fits `work` bytes
-int64_t fit_batch(int schedule, int64_t n, int64_t s0, int64_t cap, size_t work) {
+int64_t fit_batch(int schedule, int64_t n, int64_t s0, int64_t cap, size_t work, int qfl) {
   int64_t lo = 0, hi = cap / 32;  // in groups
   while (lo < hi) {
     const int64_t mid = (lo + hi + 1) / 2;
     const int64_t C = mid * 32;
     const int64_t vb = std::min<int64_t>(n, s0 + C);
-    size_t need = work_need(schedule, C, vb);
+    size_t need = work_need(schedule, C, vb, qfl);
     if (schedule == GSOFA_SCHEDULE_FIFO) {
-      const size_t lab = fifo_label_bytes(work);
-      if ((size_t)C * vb * 4 > lab || (size_t)(C / 32) * vb > (work - lab) / 16) need = work + 1;
+      // labels and masks must fit; the queues overflow into host memory
+      size_t Qm, Qq;
+      fifo_caps(work, qfl, Qm, Qq);
+      need = ((size_t)C * vb * 4 > fifo_label_bytes(work, qfl) || (size_t)(C / 32) * vb > Qm) ? work + 1 : 0;
     }
     if (need <= work) lo = mid;
     else hi = mid - 1;
@@ -297,7 +332,7 @@ enum WorkState { kWorkZero = 0, kWorkFifo = 1, kWorkDirty = 2 };
 int ensure_arena(gsofa_context *c, int64_t n, const Plan &p, cudaStream_t st) {
   int rc = GSOFA_OK;
   if (c->arena && c->key_n == n && c->Cmax == p.Cmax && c->work_bytes == p.work_bytes &&
-      c->is_words == p.is_words)
+      c->is_words == p.is_words && c->qfl == p.qfl)
     return rc;
   release_arena(c);
   {
@@ -334,6 +369,7 @@ int ensure_arena(gsofa_context *c, int64_t n, const Plan &p, cudaStream_t st) {
   c->gbits = p.gbits;
   c->work_bytes = p.work_bytes;
   c->is_words = p.is_words;
+  c->qfl = p.qfl;
   c->nsub = p.nsub;
   c->layout_sig = 0;
   CK(cudaMemsetAsync(c->work, 0, p.work_bytes, st));
@@ -351,7 +387,7 @@ int prepare_work(gsofa_context *c, int schedule, cudaStream_t st) {
   int rc = GSOFA_OK;
   if (schedule == GSOFA_SCHEDULE_FIFO) {
     if (c->work_state != kWorkFifo) {
-      const size_t lab = fifo_label_bytes(c->work_bytes);
+      const size_t lab = fifo_label_bytes(c->work_bytes, c->qfl);
       CK(cudaMemsetAsync(c->work, 0xFF, lab, st));                    // labels: above every epoch
       CK(cudaMemsetAsync((char *)c->work + lab, 0, c->work_bytes - lab, st));  // masks, queues
       c->floor = 0xFFFFFFFFu;
@@ -518,6 +554,7 @@ void gsofa_context_destroy(gsofa_context *c) {
   if (c->stage) cudaFree(c->stage);
   if (c->ord_buf) cudaFree(c->ord_buf);
   if (c->h_small) cudaFreeHost(c->h_small);
+  if (c->spill) cudaFreeHost(c->spill);
   host_block_release(c->hpool);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->stream2) cudaStreamDestroy(c->stream2);
@@ -1050,7 +1087,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
         ok = make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan, 0, solo_wide);
       }
       if (ok && !std::getenv("GSOFA_LIGHT_CTAS") && !std::getenv("GSOFA_SOLO_CTAS") &&
-          !std::getenv("GSOFA_SOLO_RING")) {
+          !std::getenv("GSOFA_SOLO_RING") && !std::getenv("GSOFA_FRONTIER_FRAC_LOG")) {
         c->plan_cache = plan;
         std::copy(key, key + 7, c->plan_key);
       }
@@ -1426,7 +1463,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     // working set fits the work region ("dynamic space allocation",
     // P:768-778; "reduce the number of concurrent sources")
     const int64_t C = fit_batch(o.schedule, n, s0, std::min<int64_t>(c->Cmax, round_up(re - s0, 32)),
-                                c->work_bytes);
+                                c->work_bytes, c->qfl);
     if (C < 32) {
       set_detail("work region too small for a 32-source group at s0=%lld", (long long)s0);
       rc = GSOFA_EINFEASIBLE;
@@ -1439,16 +1476,36 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     if (o.schedule == GSOFA_SCHEDULE_FIFO) {
       // epoch: a fresh value range below every value written so far
       if (c->floor < (uint32_t)(n + 2) + 1u) {
-        CK(cudaMemsetAsync(c->work, 0xFF, fifo_label_bytes(c->work_bytes), st));
+        CK(cudaMemsetAsync(c->work, 0xFF, fifo_label_bytes(c->work_bytes, c->qfl), st));
         c->floor = 0xFFFFFFFFu;
       }
       const uint32_t base = c->floor - (uint32_t)(n + 2);
       c->floor = base;
-      // masks and queues at FIXED offsets (capacity Q words each): a mask
-      // array must never land on memory a previous batch used as a queue
-      const size_t lab_b = fifo_label_bytes(c->work_bytes);
-      const size_t Q = (c->work_bytes - lab_b) / 16;
+      // masks and queues at FIXED offsets (capacity Qm words per mask, Qq
+      // items per queue in HBM): a mask array must never land on memory a
+      // previous batch used as a queue
+      const size_t lab_b = fifo_label_bytes(c->work_bytes, c->qfl);
+      size_t Qm, Qq;
+      fifo_caps(c->work_bytes, c->qfl, Qm, Qq);
       uint32_t *fmq = (uint32_t *)((char *)c->work + lab_b);
+      // external frontier: queue items past Qq go to mapped pinned host
+      // memory, at most G * vb - Qq per queue
+      const size_t ext = (size_t)G * vb > Qq ? (size_t)G * vb - Qq : 0;
+      if (ext && 2 * ext > c->spill_cap) {
+        CK(cudaStreamSynchronize(st));
+        if (c->spill) cudaFreeHost(c->spill);
+        c->spill = c->spill_dev = nullptr;
+        c->spill_cap = 0;
+        cudaError_t e2 = cudaHostAlloc((void **)&c->spill, 2 * ext * 4, cudaHostAllocMapped);
+        if (e2 == cudaSuccess) e2 = cudaHostGetDevicePointer((void **)&c->spill_dev, c->spill, 0);
+        if (e2 != cudaSuccess) {
+          cudaGetLastError();
+          set_detail("external frontier: cudaHostAlloc(%zu bytes) failed", 2 * ext * 4);
+          rc = GSOFA_ENOMEM;
+          goto fail;
+        }
+        c->spill_cap = 2 * ext;
+      }
       gsofa::BatchParams bp;
       bp.rowptr = c->rowptr32;
       bp.colidx = d_colidx;
@@ -1461,9 +1518,12 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       bp.base = base;
       bp.lab = c->work;
       bp.fm0 = fmq;
-      bp.fm1 = fmq + Q;
-      bp.q0 = fmq + 2 * Q;
-      bp.q1 = fmq + 3 * Q;
+      bp.fm1 = fmq + Qm;
+      bp.q0 = fmq + 2 * Qm;
+      bp.q1 = fmq + 2 * Qm + Qq;
+      bp.qcap = (uint32_t)std::min<size_t>(Qq, (size_t)G * vb);
+      bp.qx0 = ext ? c->spill_dev : nullptr;
+      bp.qx1 = ext ? c->spill_dev + ext : nullptr;
       bp.qcount = c->qcount;
       bp.is = c->is;
       bp.stats = c->stats;
@@ -1597,6 +1657,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     res->stats.item_edges = (int64_t)hs[4];
     res->stats.first_visits = (int64_t)hs[8];
     res->stats.source_expansions = (int64_t)hs[9];
+    res->stats.frontier_spilled = (int64_t)hs[10];
     res->stats.batches = nbatches;
     res->stats.max_batch = maxC;
     res->stats.kernel_launches = launches;

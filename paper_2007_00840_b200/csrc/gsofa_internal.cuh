@@ -40,7 +40,10 @@ struct BatchParams {
   uint32_t base;           // epoch base: enc(m) = base + m + 1
   uint32_t *lab;           // [G][Vb][32]
   uint32_t *fm0, *fm1;     // [G][Vb]
-  uint32_t *q0, *q1;       // queues
+  uint32_t *q0, *q1;       // queues: items [0, qcap) in HBM ...
+  uint32_t *qx0, *qx1;     // ... the rest in mapped host memory (external
+                           // frontier; NULL when nothing spills)
+  uint32_t qcap;
   uint32_t *qcount;        // [3] rotating item counters
   uint32_t *is;            // [G][n]
   unsigned long long *stats;  // [4]: items, edge inspections, rounds, pushes

@@ -33,6 +33,18 @@ namespace gsofa {
 namespace {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
+// queue slot i: the first qcap items live in HBM, the rest in mapped host
+// memory (external frontier management)
+__device__ __forceinline__ uint32_t q_load(const uint32_t *q, const uint32_t *qx, uint32_t qcap,
+                                           uint32_t i) {
+  return i < qcap ? __ldcg(q + i) : __ldcv(qx + (i - qcap));
+}
+__device__ __forceinline__ void q_store(uint32_t *q, uint32_t *qx, uint32_t qcap, uint32_t i,
+                                        uint32_t v) {
+  if (i < qcap) q[i] = v;
+  else __stcg(qx + (i - qcap), v);
+}
+
 // Seed: every out-neighbour w != src of each source is in the structure;
 // the smaller ones get maxId = -1 and form the first frontier.
 __global__ void __launch_bounds__(256) seed_kernel(BatchParams p) {
@@ -56,7 +68,7 @@ __global__ void __launch_bounds__(256) seed_kernel(BatchParams p) {
       labg[(size_t)w * 32] = p.base;  // enc(-1)
       if (atomicOr(fmg + w, bit) == 0u) {
         const uint32_t pos = atomicAdd(p.qcount, 1u);
-        p.q0[pos] = ((uint32_t)w << p.gbits) | (uint32_t)g;
+        q_store(p.q0, p.qx0, p.qcap, pos, ((uint32_t)w << p.gbits) | (uint32_t)g);
       }
     }
   }
@@ -73,7 +85,7 @@ constexpr int kFifoInflight = GSOFA_FIFO_INFLIGHT;
 template <bool kFillFirst>
 __device__ __forceinline__ void expand_item(const BatchParams &p, uint32_t u, uint32_t g,
                                             uint32_t *fmc, uint32_t *fmn, uint32_t *nq,
-                                            uint32_t *ncount, uint32_t *buf, int &nb,
+                                            uint32_t *nqx, uint32_t *ncount, uint32_t *buf, int &nb,
                                             int lane, unsigned long long &st_items,
                                             unsigned long long &st_edges,
                                             unsigned long long &st_pairs,
@@ -154,7 +166,7 @@ __device__ __forceinline__ void expand_item(const BatchParams &p, uint32_t u, ui
         uint32_t b = 0;
         if (lane == 0) b = atomicAdd(ncount, 32u);
         b = __shfl_sync(kFull, b, 0);
-        nq[b + lane] = buf[lane];
+        q_store(nq, nqx, p.qcap, b + lane, buf[lane]);
         __syncwarp();
         if (lane < nb - 32) buf[lane] = buf[32 + lane];
         __syncwarp();
@@ -178,20 +190,25 @@ __global__ void __launch_bounds__(kTraverseThreads, 2) traverse_kernel(BatchPara
   for (;; ++round) {
     const uint32_t *q = (round & 1) ? p.q1 : p.q0;
     uint32_t *nq = (round & 1) ? p.q0 : p.q1;
+    const uint32_t *qx = (round & 1) ? p.qx1 : p.qx0;
+    uint32_t *nqx = (round & 1) ? p.qx0 : p.qx1;
     uint32_t *fmc = (round & 1) ? p.fm1 : p.fm0;
     uint32_t *fmn = (round & 1) ? p.fm0 : p.fm1;
     uint32_t *ncount = p.qcount + (round + 1) % 3;
     const uint32_t qn = __ldcg(p.qcount + round % 3);
-    if (blockIdx.x == 0 && threadIdx.x == 0) p.qcount[(round + 2) % 3] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.qcount[(round + 2) % 3] = 0u;
+      if (round == 0 && qn > p.qcap) atomicAdd(p.stats + 10, (unsigned long long)(qn - p.qcap));
+    }
     uint32_t per = (qn + nw - 1) / nw;
     per = per < 1u ? 1u : (per > 32u ? 32u : per);
     int nb = 0;
     for (uint32_t b0 = gw * per; b0 < qn; b0 += nw * per) {
       const uint32_t cnt = min(per, qn - b0);
-      const uint32_t my = lane < (int)cnt ? __ldcg(q + b0 + lane) : 0u;
+      const uint32_t my = lane < (int)cnt ? q_load(q, qx, p.qcap, b0 + lane) : 0u;
       for (uint32_t t = 0; t < cnt; ++t) {
         const uint32_t item = __shfl_sync(kFull, my, t);
-        expand_item<kFillFirst>(p, item >> p.gbits, item & gmask, fmc, fmn, nq, ncount, buf,
+        expand_item<kFillFirst>(p, item >> p.gbits, item & gmask, fmc, fmn, nq, nqx, ncount, buf,
                                 nb, lane, st_items, st_edges, st_pairs, st_fv, st_sx);
       }
     }
@@ -199,10 +216,14 @@ __global__ void __launch_bounds__(kTraverseThreads, 2) traverse_kernel(BatchPara
       uint32_t b = 0;
       if (lane == 0) b = atomicAdd(ncount, (uint32_t)nb);
       b = __shfl_sync(kFull, b, 0);
-      if (lane < nb) nq[b + lane] = buf[lane];
+      if (lane < nb) q_store(nq, nqx, p.qcap, b + lane, buf[lane]);
     }
     grid.sync();
-    if (__ldcg(ncount) == 0u) break;
+    const uint32_t nn = __ldcg(ncount);
+    // items of the next frontier that went to host memory
+    if (blockIdx.x == 0 && threadIdx.x == 0 && nn > p.qcap)
+      atomicAdd(p.stats + 10, (unsigned long long)(nn - p.qcap));
+    if (nn == 0u) break;
   }
   if (lane == 0 && st_items) {
     atomicAdd(p.stats + 0, st_items);

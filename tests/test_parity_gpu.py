@@ -687,3 +687,39 @@ def test_symmetric_etree_comparator(ctx, case):
     got = run(rp, ci, ctx)
     for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx"):
         assert np.array_equal(got[k], want[k]), k
+
+
+# ------------- external frontier management --
+
+@pytest.mark.parametrize("name,scale,qfl", [("C3", 3000, 6), ("C1", None, 4), ("C2", 12, 8),
+                                            ("C3", 6000, 12)])
+def test_external_frontier_spill(name, scale, qfl, monkeypatch):
+    """FIFO queues with only 1/2^qfl of their worst case in HBM: the overflow
+    goes to mapped pinned host memory and comes back the next iteration; the
+    output is byte-identical to the oracle and the spill is counted."""
+    monkeypatch.setenv("GSOFA_FRONTIER_FRAC_LOG", str(qfl))
+    rp, ci = gen.config(name, scale)
+    c = g.Context(0)
+    try:
+        got = run(rp, ci, c, schedule="fifo")
+    finally:
+        c.close()
+    assert_full_equal(got, oracle.symbolic(rp, ci), f"{name} qfl={qfl}")
+    assert got["stats"]["frontier_spilled"] > 0
+
+
+@pytest.mark.parametrize("budget_mb", [64, 256])
+def test_external_frontier_budget(budget_mb):
+    """A budget below the full FIFO working set turns on external frontier
+    management (1/8 of the queues in HBM) before #C shrinks; the
+    result does not change."""
+    rp, ci = gen.config("C3", 6000)
+    c = g.Context(0, mem_budget_bytes=budget_mb << 20)
+    try:
+        got = run(rp, ci, c, schedule="fifo")
+        again = run(rp, ci, c, schedule="fifo")
+    finally:
+        c.close()
+    want = oracle.symbolic(rp, ci)
+    assert_full_equal(got, want)
+    assert_full_equal(again, want)
