@@ -1320,7 +1320,15 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
             CK(cudaMemcpyAsync(c->ord_buf, ord_host.data(), ord_host.size() * 4,
                                cudaMemcpyHostToDevice, c->stream2));
         }
-        CK(gsofa::launch_solo(sp, (int)plan.heavy, c->stream2));
+        // the solo kernel's first tasks are static per CTA, so every CTA of
+        // its grid must be able to become resident: AUTO may have switched
+        // the order / shape after the plan, so clamp to the residency of the
+        // variant actually launched
+        int64_t hgrid = plan.heavy;
+        const int64_t hres =
+            gsofa::stream_max_blocks(c->device, plan.Vmax, 1, sp.hmode ? ord_npos : 0, sp.wide);
+        if (hres > 0) hgrid = std::min<int64_t>(hgrid, hres);
+        CK(gsofa::launch_solo(sp, (int)hgrid, c->stream2));
         CK(cudaEventRecord(eb, c->stream2));
         CK(cudaStreamWaitEvent(st, eb, 0));
         cudaEventDestroy(ea);
