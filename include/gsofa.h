@@ -90,9 +90,13 @@ typedef struct gsofa_opts {
    *     revisits -- measured 1.3-2.9x faster there) and one batch of labels
    *     (min(rows, 65536) x n x 4 B) fits the memory budget of the call;
    *     threshold otherwise (ND orders, hubs: 15x the inspections in FIFO),
-   *     and also when the FIFO plan turns out infeasible.  The bandwidth is
-   *     measured by the CSR validation pass.  gsofa_result.schedule reports
-   *     the choice. */
+   *     and also when the FIFO plan turns out infeasible.  Within the
+   *     threshold family, patterns with hub rows (largest row > 32x the
+   *     mean row length) get the elimination tree computed on the host; the
+   *     height order is taken when the last row's id-order chain exceeds 4x
+   *     the tree height (C4's hubs), else id order.  The bandwidth and the
+   *     largest row are measured by the CSR validation pass.
+   *     gsofa_result.schedule reports the choice. */
   int32_t schedule;
   /* source rows [row_begin, row_end); row_end = -1 means n.  Any row_begin:
    * if it is not a multiple of chunk_size, the supernodes of the head rows

@@ -1025,11 +1025,11 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   // reads the input; the same pass measures the bandwidth for AUTO
   if ((rc = grow_device(&c->rowptr32, &c->rowptr32_cap, (size_t)n + 1, st)) != GSOFA_OK) goto fail;
   if (!c->bw_dev) CK(cudaMalloc((void **)&c->bw_dev, 64));
-  CK(cudaMemsetAsync(c->bw_dev, 0, 8, st));  // [0] bandwidth, [1] error flags
+  CK(cudaMemsetAsync(c->bw_dev, 0, 12, st));  // [0] bandwidth, [1] error flags, [2] max degree
   CK(gsofa::launch_validate(d_rowptr64, d_colidx, n, nnz, c->rowptr32, (int *)(c->bw_dev + 1),
                             o.schedule == GSOFA_SCHEDULE_AUTO ? c->bw_dev : nullptr, st));
   ++launches;
-  CK(cudaMemcpyAsync(c->h_small, c->bw_dev, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->h_small, c->bw_dev, 12, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (const int f = ((int *)c->h_small)[1]) {
     set_detail("CSR check failed:%s%s%s", (f & 1) ? " bad rowptr" : "",
@@ -1052,8 +1052,14 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     }
     o.schedule = auto_fifo ? GSOFA_SCHEDULE_FIFO : GSOFA_SCHEDULE_THRESHOLD;
     // threshold family: the solo kernel's order (id or etree height) is
-    // chosen once the tree is known (below)
-    auto_order = !auto_fifo;
+    // chosen once the tree is known (below).  The tree is a host pass
+    // (O(nnz alpha) plus a copy of A) on the solo kernel's critical path, so
+    // it is computed only for patterns with hub rows (largest row > 32x the
+    // mean), where height order was measured to win (C4: 1.19 s -> 0.45 s);
+    // on grids it would only delay the solo kernel (C5: ~5%)
+    const unsigned int maxdeg = ((unsigned int *)c->h_small)[2];
+    const int64_t mean = std::max<int64_t>(1, nnz / std::max<int64_t>(1, n));
+    auto_order = !auto_fifo && (int64_t)maxdeg > 32 * mean;
   }
   // ---------------------------------------------------- A2: height order
   // positions are a permutation of [0, n): the plan does not depend on the

@@ -21,13 +21,13 @@ namespace {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 // CSR checks + int64 -> int32 row pointers; with bw != NULL also the
-// bandwidth max |i - j| of A (GSOFA_SCHEDULE_AUTO), taken only from rows that
-// passed the row-pointer check, so a malformed rowptr never leads to a read
-// outside colidx
+// bandwidth max |i - j| of A (bw[0]) and the largest row length (bw[2]) for
+// GSOFA_SCHEDULE_AUTO, taken only from rows that passed the row-pointer
+// check, so a malformed rowptr never leads to a read outside colidx
 __global__ void validate_kernel(const int64_t *rowptr64, const int32_t *colidx, int64_t n,
                                 int64_t nnz, int32_t *rowptr32, int *err, unsigned int *bw) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned int m = 0;
+  unsigned int m = 0, dg = 0;
   if (i <= n) {
     const int64_t a = rowptr64[i];
     rowptr32[i] = (int32_t)a;
@@ -39,6 +39,7 @@ __global__ void validate_kernel(const int64_t *rowptr64, const int32_t *colidx, 
       if (b < a || a < 0 || b > nnz) {
         atomicOr(err, 1);
       } else {
+        dg = (unsigned int)(b - a > INT32_MAX ? INT32_MAX : b - a);
         int32_t prev = -1;
         for (int64_t e = a; e < b; ++e) {
           const int32_t c = colidx[e];
@@ -58,7 +59,9 @@ __global__ void validate_kernel(const int64_t *rowptr64, const int32_t *colidx, 
   }
   if (bw) {
     m = __reduce_max_sync(0xFFFFFFFFu, m);
+    dg = __reduce_max_sync(0xFFFFFFFFu, dg);
     if ((threadIdx.x & 31) == 0 && m) atomicMax(bw, m);
+    if ((threadIdx.x & 31) == 0 && dg) atomicMax(bw + 2, dg);
   }
 }
 
