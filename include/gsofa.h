@@ -53,6 +53,27 @@ extern "C" {
 #define GSOFA_SCHEDULE_AUTO      2
 #define GSOFA_SCHEDULE_HEIGHT    3
 
+/* Row interleave: the paper's source scheduling
+ * across GPUs -- consecutive chunks of rows dealt round-robin to the
+ * compute nodes and rows interleaved across the GPUs of a node to balance
+ * the work (measured 1.6x and a further 3.3x there).  A
+ * call with nparts > 1 computes only the units u = 0, 1, ... of unit_rows
+ * rows, counted from row_begin, with u % nparts == part; its result holds
+ * those rows in ascending order (local row k is the k-th of them).
+ *   unit_rows a multiple of chunk_size: every unit starts a chunk, so the
+ *     supernodes are unit-local and complete after the call;
+ *   otherwise (finer interleave): the supernodes need the neighbouring
+ *     rows of other parts -- nsuper is -1 after the call, and each part
+ *     exports its per-row Def. def:T3 data (gsofa_result_rowinfo), the parts
+ *     all-gather it and every part calls gsofa_supernodes_gathered.
+ * nparts <= 1: no interleave (all rows of [row_begin, row_end)). */
+typedef struct gsofa_interleave {
+  int32_t nparts;     /* N: number of parts (GPUs) */
+  int32_t part;       /* q in [0, N): this call's part */
+  int32_t unit_rows;  /* U: rows per unit, a multiple of 32 */
+  int32_t reserved;
+} gsofa_interleave;
+
 /* -------------------------------------------------------------- options -- */
 typedef struct gsofa_opts {
   /* chunkSize = user-defined maximum supernode size; a supernode never crosses
@@ -128,6 +149,10 @@ typedef struct gsofa_opts {
    * one of its own leaders (gsofa_supernode_stitch); the tail record's
    * leader carries the running block length (row - leader + 1). */
   int32_t sn_cap_only;
+  /* row interleave (see gsofa_interleave); all zero = off.  Needs the
+   * threshold family of schedules (AUTO then never picks FIFO), row_begin a
+   * multiple of chunk_size and the forced-break supernode rule. */
+  gsofa_interleave interleave;
 } gsofa_opts;
 
 /* ------------------------------------------------------------ statistics -- */
@@ -186,6 +211,11 @@ typedef struct gsofa_result {
   gsofa_stats stats;
   int32_t schedule;       /* the schedule that ran (THRESHOLD or FIFO) */
   int32_t reserved;
+  /* rows held: row_end - row_begin, or the rows of this part under a row
+   * interleave (the arrays above are indexed by local row k; sn_start holds
+   * global leading rows, its sentinel is one past the last row held) */
+  int64_t rows;
+  gsofa_interleave interleave;
 } gsofa_result;
 
 typedef struct gsofa_context gsofa_context;
@@ -308,6 +338,34 @@ int gsofa_result_supno(const gsofa_result *r, int32_t on_device, int32_t **supno
  */
 int gsofa_permute(int64_t n, const int64_t *rowptr, const int32_t *colidx, const int32_t *perm,
                   int64_t *out_rowptr, int32_t *out_colidx);
+
+/*
+ * gsofa_result_rowinfo -- what the supernode detection of the rows after this
+ * part's rows needs from it (finer-than-chunk row interleave, see
+ * gsofa_interleave): for each local row k (global row s):
+ *   nnzU[k]              nnz(U(s,:)) including the diagonal (Def. def:T3 (i))
+ *   lmask[k * W + d / 32] bit d % 32 set iff L(s, s - d) != 0, for
+ *                        1 <= d <= s % chunk_size (candidate leaders inside
+ *                        s's chunk, Def. def:T3 (ii)); W = (chunk_size + 31) / 32
+ * Both arrays are caller-allocated DEVICE memory on the result's device
+ * (int32[rows], uint32[rows * W]); r must be a device result.  One kernel on
+ * the result's device, synchronous.  Errors: GSOFA_EINVAL, GSOFA_ECUDA.
+ */
+int gsofa_result_rowinfo(const gsofa_result *r, int32_t *nnzU, uint32_t *lmask);
+
+/*
+ * gsofa_supernodes_gathered -- the supernodes of an interleaved part from
+ * every part's rowinfo (all-gathered, part-major: part p's local row k at
+ * index p * stride + k of nnzU_all, and at (p * stride + k) * W of
+ * lmask_all; device memory).  The greedy Def. def:T3 scan runs
+ * once per chunk (forced break at every multiple of chunk_size) over
+ * the rows of all parts; r keeps the leaders among its own rows: sn_start
+ * and nsuper are written in place (the union over parts is the supernode
+ * partition of [row_begin, row_end)).  Synchronous.  Errors: GSOFA_EINVAL
+ * (r not interleaved, or not a device result), GSOFA_ECUDA.
+ */
+int gsofa_supernodes_gathered(gsofa_result *r, const int32_t *nnzU_all, const uint32_t *lmask_all,
+                              int64_t stride);
 
 /* Frees every array of r (host or device) and r itself.  NULL is a no-op. */
 void gsofa_result_free(gsofa_result *r);

@@ -27,11 +27,17 @@ EXPORTED_SYMBOLS = [
     "gsofa_symbolic", "gsofa_result_copy", "gsofa_result_free",
     "gsofa_partition_rows", "gsofa_strerror", "gsofa_last_error_detail",
     "gsofa_version", "gsofa_supernode_stitch", "gsofa_result_l_csc", "gsofa_buffer_free",
-    "gsofa_permute", "gsofa_result_supno",
+    "gsofa_permute", "gsofa_result_supno", "gsofa_result_rowinfo", "gsofa_supernodes_gathered",
 ]
 
 _I64, _I32 = ctypes.c_int64, ctypes.c_int32
 _P = ctypes.POINTER
+
+
+class Interleave(ctypes.Structure):
+    """gsofa_interleave: units of unit_rows rows dealt round-robin to nparts
+    parts; this call computes part `part`."""
+    _fields_ = [("nparts", _I32), ("part", _I32), ("unit_rows", _I32), ("reserved", _I32)]
 
 
 class Opts(ctypes.Structure):
@@ -39,7 +45,7 @@ class Opts(ctypes.Structure):
                 ("fill_first", _I32), ("schedule", _I32), ("row_begin", _I64),
                 ("row_end", _I64), ("device", _I32), ("outputs_on_device", _I32),
                 ("stream", ctypes.c_void_p), ("checked", _I32),
-                ("sn_cap_only", _I32)]
+                ("sn_cap_only", _I32), ("interleave", Interleave)]
 
 
 class Stats(ctypes.Structure):
@@ -59,7 +65,8 @@ class CResult(ctypes.Structure):
                 ("nsuper", _I64), ("sn_start", _P(_I32)),
                 ("nnz_L", _I64), ("nnz_U", _I64), ("nnz_A_offdiag", _I64),
                 ("fill_count", _I64), ("on_device", _I32), ("device", _I32),
-                ("stats", Stats), ("schedule", _I32), ("reserved", _I32)]
+                ("stats", Stats), ("schedule", _I32), ("reserved", _I32),
+                ("rows", _I64), ("interleave", Interleave)]
 
 
 class Tail(ctypes.Structure):
@@ -108,6 +115,8 @@ def load():
     lib.gsofa_buffer_free.argtypes = [ctypes.c_void_p, _I32]
     lib.gsofa_buffer_free.restype = None
     lib.gsofa_permute.argtypes = [_I64] + [ctypes.c_void_p] * 5
+    lib.gsofa_result_rowinfo.argtypes = [_P(CResult), ctypes.c_void_p, ctypes.c_void_p]
+    lib.gsofa_supernodes_gathered.argtypes = [_P(CResult), ctypes.c_void_p, ctypes.c_void_p, _I64]
     lib.gsofa_strerror.restype = ctypes.c_char_p
     lib.gsofa_strerror.argtypes = [ctypes.c_int]
     lib.gsofa_last_error_detail.restype = ctypes.c_char_p
@@ -178,10 +187,14 @@ class Result:
         self._p = cres_ptr
         r = cres_ptr.contents
         self.n, self.row_begin, self.row_end = r.n, r.row_begin, r.row_end
-        self.rows = r.row_end - r.row_begin
+        self.rows = r.rows
+        iv = r.interleave
+        self.interleave = (iv.nparts, iv.part, iv.unit_rows) if iv.nparts > 1 else None
         self.nnz_L, self.nnz_U, self.nsuper = r.nnz_L, r.nnz_U, r.nsuper
         self.nnz_A_offdiag, self.fill_count = r.nnz_A_offdiag, r.fill_count
         self.on_device = bool(r.on_device)
+        self.device = r.device
+        self.chunk_size = 128  # set by symbolic()
         self.schedule = SCHEDULE_NAMES.get(r.schedule, str(r.schedule))
         s = r.stats
         self.stats = {f: getattr(s, f) for f, _ in Stats._fields_}
@@ -238,6 +251,29 @@ class Result:
         self._arrays = None
         return out
 
+    def rowinfo(self):
+        """gsofa_result_rowinfo (device results): per local row nnz(U(s,:))
+        (int32 tensor [rows]) and the candidate-leader L mask (int32 tensor
+        [rows, W], W = ceil(chunk_size / 32), bit d: L(s, s - d) != 0)."""
+        import torch
+        lib = load()
+        W = (self.chunk_size + 31) // 32
+        nnzU = torch.empty(max(self.rows, 1), dtype=torch.int32, device=f"cuda:{self.device}")
+        mask = torch.empty((max(self.rows, 1), W), dtype=torch.int32, device=f"cuda:{self.device}")
+        _check(lib.gsofa_result_rowinfo(self._p, ctypes.c_void_p(nnzU.data_ptr()),
+                                        ctypes.c_void_p(mask.data_ptr())), "gsofa_result_rowinfo")
+        return nnzU[: self.rows], mask[: self.rows]
+
+    def supernodes_gathered(self, nnzU_all, mask_all, stride: int):
+        """gsofa_supernodes_gathered: this part's supernodes from every
+        part's rowinfo, gathered part-major with `stride` rows per part
+        (device tensors)."""
+        _check(load().gsofa_supernodes_gathered(self._p, ctypes.c_void_p(nnzU_all.data_ptr()),
+                                                ctypes.c_void_p(mask_all.data_ptr()), int(stride)),
+               "gsofa_supernodes_gathered")
+        self.nsuper = self._p.contents.nsuper
+        self._arrays = None
+
     def l_csc(self):
         """gsofa_result_l_csc: L in compressed sparse column form, as numpy
         arrays col_ptr int64[n+1] (columns [0, n)) and row_idx int32[nnz_L]
@@ -286,7 +322,7 @@ def symbolic(rowptr, colidx, *, ctx: Context | None = None, chunk_size: int = 12
              max_concurrent: int = 0, mem_budget_bytes: int = 0, fill_first: bool = False,
              row_begin: int = 0, row_end: int = -1, device: int = 0,
              outputs_on_device: bool = False, stream=None, schedule: str = "auto",
-             checked: bool = False, sn_cap_only: bool = False) -> Result:
+             checked: bool = False, sn_cap_only: bool = False, interleave=None) -> Result:
     """gsofa_symbolic: L/U patterns, supernodes and fill count of the pattern
     (rowptr int64[n+1], colidx int32[nnz]) for rows [row_begin, row_end).
     Inputs: numpy (host) or torch tensors (host or CUDA).  ``stream``: a
@@ -294,7 +330,8 @@ def symbolic(rowptr, colidx, *, ctx: Context | None = None, chunk_size: int = 12
     "auto" (default: FIFO for banded dense patterns, else threshold),
     "threshold" or "fifo" (the paper's all-frontiers order).  ``sn_cap_only``:
     chunk_size bounds the supernode size only (no forced breaks at its
-    multiples)."""
+    multiples).  ``interleave=(nparts, part, unit_rows)``:
+    only this part's units of rows (gsofa_interleave)."""
     lib = load()
     rp, _, krp = _ptr(rowptr)
     ci, _, kci = _ptr(colidx)
@@ -310,6 +347,8 @@ def symbolic(rowptr, colidx, *, ctx: Context | None = None, chunk_size: int = 12
     o.schedule = SCHEDULES[schedule]
     o.checked = int(bool(checked))
     o.sn_cap_only = int(bool(sn_cap_only))
+    if interleave is not None:
+        o.interleave.nparts, o.interleave.part, o.interleave.unit_rows = (int(x) for x in interleave)
     if stream is not None:
         o.stream = ctypes.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
     if ci == 0:  # empty colidx: pass a valid dummy pointer
@@ -319,7 +358,9 @@ def symbolic(rowptr, colidx, *, ctx: Context | None = None, chunk_size: int = 12
     _check(lib.gsofa_symbolic(ctx.handle if ctx else None, n, ctypes.c_void_p(rp),
                               ctypes.c_void_p(ci), ctypes.byref(o), ctypes.byref(out)),
            "gsofa_symbolic")
-    return Result(out)
+    res = Result(out)
+    res.chunk_size = int(chunk_size)
+    return res
 
 
 def partition_rows(rowptr, colidx, nparts: int, align: int = 1) -> np.ndarray:

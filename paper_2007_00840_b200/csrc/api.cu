@@ -569,6 +569,10 @@ int gsofa_result_l_csc(const gsofa_result *r, int32_t on_device, int64_t **col_p
   }
   *col_ptr = nullptr;
   *row_idx = nullptr;
+  if (r->interleave.nparts > 1) {
+    set_detail("gsofa_result_l_csc: an interleaved part's rows are not a range");
+    return GSOFA_EINVAL;
+  }
   cudaError_t e = cudaSetDevice(r->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   const int64_t n = r->n, rows = r->row_end - r->row_begin, nnz = r->nnz_L;
@@ -728,6 +732,10 @@ int gsofa_result_supno(const gsofa_result *r, int32_t on_device, int32_t **supno
     return GSOFA_EINVAL;
   }
   *supno = nullptr;
+  if (r->interleave.nparts > 1) {
+    set_detail("gsofa_result_supno: an interleaved part's rows are not a range");
+    return GSOFA_EINVAL;
+  }
   cudaError_t e = cudaSetDevice(r->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   const int64_t rows = r->row_end - r->row_begin;
@@ -795,7 +803,7 @@ int gsofa_result_copy(const gsofa_result *r, int64_t *L_rowptr, int32_t *L_colid
     cudaError_t e = cudaSetDevice(r->device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   }
-  const int64_t rows = r->row_end - r->row_begin;
+  const int64_t rows = r->rows;
   struct {
     void *dst;
     const void *src;
@@ -814,6 +822,65 @@ int gsofa_result_copy(const gsofa_result *r, int64_t *L_rowptr, int32_t *L_colid
       std::memcpy(c.dst, c.src, c.bytes);
     }
   }
+  return GSOFA_OK;
+}
+
+namespace {
+gsofa::RowMap result_map(const gsofa_result *r) {
+  gsofa::RowMap m;
+  m.rb = (int32_t)r->row_begin;
+  m.re = (int32_t)r->row_end;
+  if (r->interleave.nparts > 1) {
+    m.N = r->interleave.nparts;
+    m.q = r->interleave.part;
+    m.U = r->interleave.unit_rows;
+  }
+  return m;
+}
+}  // namespace
+
+int gsofa_result_rowinfo(const gsofa_result *r, int32_t *nnzU, uint32_t *lmask) {
+  if (!r || !nnzU || !lmask || !r->on_device) {
+    set_detail("gsofa_result_rowinfo: NULL argument or a host result");
+    return GSOFA_EINVAL;
+  }
+  cudaError_t e = cudaSetDevice(r->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  const int32_t chunk = reinterpret_cast<const ResultImpl *>(r)->chunk_size;
+  e = gsofa::launch_rowinfo(r->L_rowptr, r->L_colidx, r->U_rowptr, result_map(r), (int32_t)r->rows,
+                            chunk, nnzU, lmask, nullptr);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+  return e == cudaSuccess ? GSOFA_OK : cuda_fail(e, "gsofa_result_rowinfo");
+}
+
+int gsofa_supernodes_gathered(gsofa_result *r, const int32_t *nnzU_all, const uint32_t *lmask_all,
+                              int64_t stride) {
+  if (!r || !nnzU_all || !lmask_all || !r->on_device || r->interleave.nparts <= 1 ||
+      stride < r->rows) {
+    set_detail("gsofa_supernodes_gathered: needs an interleaved device result and stride >= rows");
+    return GSOFA_EINVAL;
+  }
+  cudaError_t e = cudaSetDevice(r->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  const int32_t chunk = reinterpret_cast<const ResultImpl *>(r)->chunk_size;
+  const int64_t rows = r->rows;
+  const gsofa::RowMap m = result_map(r);
+  cudaStream_t st = nullptr;
+  const size_t tmpb = gsofa::scan_tmp_bytes(rows);
+  char *scr = nullptr;
+  if ((e = cudaMallocAsync((void **)&scr, (size_t)rows * 8 + 64 + tmpb, st)) != cudaSuccess)
+    return cuda_fail(e, "cudaMallocAsync");
+  int32_t *leader = (int32_t *)scr, *pos = leader + rows, *total = pos + rows;
+  void *tmp = scr + (size_t)rows * 8 + 64;
+  int32_t ns = 0;
+  e = gsofa::launch_supernode_gathered(m, chunk, nnzU_all, lmask_all, stride, leader, st);
+  if (e == cudaSuccess) e = gsofa::scan_exclusive_i32(leader, pos, rows, total, tmp, tmpb, st);
+  if (e == cudaSuccess) e = gsofa::launch_supernode_scatter(leader, pos, m, (int32_t)rows, total, r->sn_start, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&ns, total, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(scr, st);
+  if (e != cudaSuccess) return cuda_fail(e, "gsofa_supernodes_gathered");
+  r->nsuper = ns;
   return GSOFA_OK;
 }
 
@@ -845,6 +912,10 @@ int gsofa_supernode_stitch(gsofa_result *r, const gsofa_tail *prev, gsofa_tail *
   }
   ResultImpl *impl = reinterpret_cast<ResultImpl *>(r);
   const int64_t rb = r->row_begin, re = r->row_end, rows = re - rb;
+  if (r->interleave.nparts > 1) {
+    set_detail("gsofa_supernode_stitch: interleaved parts use gsofa_supernodes_gathered");
+    return GSOFA_EINVAL;
+  }
   const int32_t chunk = impl->chunk_size;
   if (prev && (prev->row != rb - 1 || prev->leader < 0 || prev->leader > prev->row || prev->nnzU < 1)) {
     set_detail("stitch tail {row %lld, nnzU %lld, leader %lld} does not precede row_begin %lld",
@@ -938,6 +1009,31 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
                (long long)o.mem_budget_bytes);
     return GSOFA_EINVAL;
   }
+  // row interleave (gsofa_interleave): the units of this part
+  gsofa::RowMap rmap;
+  rmap.rb = (int32_t)o.row_begin;
+  rmap.re = (int32_t)o.row_end;
+  const bool ilv = o.interleave.nparts > 1;
+  if (ilv) {
+    const gsofa_interleave &iv = o.interleave;
+    if (iv.part < 0 || iv.part >= iv.nparts || iv.unit_rows < 32 || iv.unit_rows % 32 != 0 ||
+        o.sn_cap_only || o.schedule == GSOFA_SCHEDULE_FIFO || o.row_begin % o.chunk_size != 0) {
+      set_detail("bad interleave: parts=%d part=%d unit_rows=%d (multiple of 32; threshold "
+                 "schedules, forced-break supernodes, row_begin a multiple of chunk_size)",
+                 iv.nparts, iv.part, iv.unit_rows);
+      return GSOFA_EINVAL;
+    }
+    rmap.N = iv.nparts;
+    rmap.q = iv.part;
+    rmap.U = iv.unit_rows;
+    if (rmap.count() < 1) {
+      set_detail("interleave part %d of %d holds no rows of [%lld, %lld)", iv.part, iv.nparts,
+                 (long long)o.row_begin, (long long)o.row_end);
+      return GSOFA_EINVAL;
+    }
+  }
+  // finer than a chunk: supernodes wait for the parts' exchange
+  const bool sn_deferred = ilv && o.interleave.unit_rows % o.chunk_size != 0;
   bool own_ctx = false;
   int rc = GSOFA_OK;
   if (!ctx) {
@@ -969,7 +1065,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     return (int)evs.size() - 1;
   };
 #define ev() ev_at(__LINE__)
-  const int64_t rb = o.row_begin, re = o.row_end, rows = re - rb;
+  const int64_t rb = o.row_begin, re = o.row_end, rows = rmap.count();
   int64_t nnz = 0;
   bool in_dev;
   const int64_t *d_rowptr64;
@@ -1043,7 +1139,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     // one batch of maxId labels (sources x vertices x 4 B) to fit the budget
     // the plan will use: FIFO in many small batches loses its edge.
     const unsigned int bw = ((unsigned int *)c->h_small)[0];
-    auto_fifo = (int64_t)bw * 8 <= n && nnz >= 8 * n;
+    auto_fifo = (int64_t)bw * 8 <= n && nnz >= 8 * n && !ilv;
     if (auto_fifo) {
       int64_t budget = o.mem_budget_bytes ? o.mem_budget_bytes : c->budget;
       if (!budget) budget = auto_budget(c->device) + (int64_t)c->arena_bytes;
@@ -1073,7 +1169,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     const int64_t cmax_req =
         o.max_concurrent ? o.max_concurrent : 65536;  // FIFO: one batch when it fits (C3 -6% vs 16k)
     const int64_t budget_req = o.mem_budget_bytes ? o.mem_budget_bytes : c->budget;
-    int64_t key[7] = {o.schedule, n, rb, re, budget_req, cmax_req, ord_npos * 2 + solo_wide};
+    int64_t key[7] = {o.schedule, n, rb, re ^ ((int64_t)rmap.q << 32) ^ ((int64_t)rmap.N << 40),
+                      budget_req, cmax_req, ord_npos * 2 + solo_wide};
     bool ok = true;
     if (std::equal(key, key + 7, c->plan_key)) {
       plan = c->plan_cache;
@@ -1185,6 +1282,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.n = (int32_t)n;
     sp.row_begin = (int32_t)rb;
     sp.row_end = (int32_t)re;
+    sp.map = rmap;
+    sp.nrows = (int32_t)rows;
     sp.ngroups = (int32_t)ngroups;
     sp.Vmax = (int32_t)plan.Vmax;
     sp.ws = c->work;
@@ -1606,13 +1705,16 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     int32_t *flags = sn_scratch;                 // [2 rows]: Phase-I bits, leaders
     int32_t *pos = sn_scratch + 2 * rows;        // [rows]
     int32_t *total = (int32_t *)c->totals + 4;   // scratch int
-    CK(gsofa::launch_supernode_flags(Lrp, Lci, Urp, (int32_t)rb, (int32_t)re, o.chunk_size,
-                                     o.sn_cap_only, flags, st));
+    if (!sn_deferred)
+      CK(gsofa::launch_supernode_flags(Lrp, Lci, Urp, rmap, (int32_t)rows, o.chunk_size,
+                                       o.sn_cap_only, flags, st));
+    else  // no leaders yet (gsofa_supernodes_gathered); the sentinel only
+      CK(cudaMemsetAsync(flags + rows, 0, (size_t)rows * 4, st));
     CK(gsofa::scan_exclusive_i32(flags + rows, pos, rows, total, scan_tmp, tmpb, st));
-    CK(gsofa::launch_supernode_scatter(flags + rows, pos, (int32_t)rb, (int32_t)re, total, sn, st));
+    CK(gsofa::launch_supernode_scatter(flags + rows, pos, rmap, (int32_t)rows, total, sn, st));
     launches += 4;
     unsigned long long *offd = c->stats + 5;
-    CK(gsofa::launch_count_offdiag(c->rowptr32, d_colidx, (int32_t)rb, (int32_t)re, offd, st));
+    CK(gsofa::launch_count_offdiag(c->rowptr32, d_colidx, rmap, (int32_t)rows, offd, st));
     ++launches;
   }
   e_sn1 = ev();
@@ -1626,8 +1728,9 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       if (inj[0] == 'U' && baseU > 0) CK(cudaMemsetAsync(Uci, 0xFF, 4, st));
       CK(cudaStreamSynchronize(st));
     }
-    CK(gsofa::launch_audit(c->rowptr32, d_colidx, Lrp, Lci, Urp, Uci, sn, (int32_t *)c->totals + 4,
-                           (int32_t)rb, (int32_t)rows, (int32_t)n, o.chunk_size, o.sn_cap_only, c->err, st));
+    CK(gsofa::launch_audit(c->rowptr32, d_colidx, Lrp, Lci, Urp, Uci, sn,
+                           sn_deferred ? nullptr : (int32_t *)c->totals + 4, rmap, (int32_t)rows,
+                           (int32_t)n, o.chunk_size, o.sn_cap_only, c->err, st));
     ++launches;
     int bad = 0;
     CK(cudaMemcpyAsync(&bad, c->err, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1657,7 +1760,9 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     res->row_end = re;
     res->nnz_L = baseL;
     res->nnz_U = baseU;
-    res->nsuper = *(int32_t *)(c->h_small + 16);
+    res->nsuper = sn_deferred ? -1 : *(int32_t *)(c->h_small + 16);
+    res->rows = rows;
+    res->interleave = ilv ? o.interleave : gsofa_interleave{0, 0, 0, 0};
     res->nnz_A_offdiag = (int64_t)hs[5];
     res->fill_count = baseL + (baseU - rows) - res->nnz_A_offdiag;
     res->device = c->device;

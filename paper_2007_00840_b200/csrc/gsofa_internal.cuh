@@ -26,6 +26,29 @@
 namespace gsofa {
 
 constexpr int kWarp = 32;
+
+// The source rows of a call: [rb, re), or -- row interleave across GPUs, the
+// paper's source scheduling -- only the
+// units u = 0, 1, ... of U rows counted from rb with u % N == q.  Local row r
+// (0 .. count-1, ascending) is global row row(r); groups of 32 local rows
+// are 32 consecutive global rows (U is a multiple of 32).
+struct RowMap {
+  int32_t rb = 0, re = 0, N = 1, q = 0, U = 32;
+  __host__ __device__ __forceinline__ int32_t row(int32_t r) const {
+    if (N <= 1) return rb + r;
+    const int32_t u = r / U;
+    return rb + (u * N + q) * U + (r - u * U);
+  }
+  // host: number of local rows
+  int64_t count() const {
+    if (N <= 1) return (int64_t)re - rb;
+    const int64_t len = (int64_t)re - rb, nu = (len + U - 1) / U;
+    if (nu <= q) return 0;
+    const int64_t mine = (nu - q + N - 1) / N;         // units q, q + N, ... < nu
+    const int64_t last = q + (mine - 1) * N;            // my last unit
+    return mine * U - (last == nu - 1 ? nu * U - len : 0);
+  }
+};
 constexpr int kTraverseThreads = 512;   // 16 warps
 
 struct BatchParams {
@@ -62,6 +85,8 @@ struct StreamParams {
   const int32_t *rowptr;
   const int32_t *colidx;
   int32_t n, row_begin, row_end, ngroups, Vmax;
+  RowMap map;                // local row -> global row (row interleave)
+  int32_t nrows;             // local rows (= row_end - row_begin without interleave)
   uint32_t *ws;              // [slots][ws_words]
   size_t ws_words;
   uint32_t *is;              // [slots][is_words]: is[n] | isum[n/1024]
@@ -193,12 +218,12 @@ cudaError_t launch_validate(const int64_t *rowptr64, const int32_t *colidx, int6
                             cudaStream_t st);
 cudaError_t launch_supno(const int32_t *sn_start, int64_t nsuper, int32_t row_begin, int32_t *supno,
                          cudaStream_t st);
-cudaError_t launch_count_offdiag(const int32_t *rowptr, const int32_t *colidx, int32_t r0,
-                                 int32_t r1, unsigned long long *out, cudaStream_t st);
+cudaError_t launch_count_offdiag(const int32_t *rowptr, const int32_t *colidx, const RowMap &m,
+                                 int32_t rows, unsigned long long *out, cudaStream_t st);
 // flags: [3 rows] scratch; [0, rows) Phase-I bits, [rows, 2 rows) leaders,
 // [2 rows, 3 rows) the cap-only successor table (free again on return)
 cudaError_t launch_supernode_flags(const int64_t *L_rowptr, const int32_t *L_colidx,
-                                   const int64_t *U_rowptr, int32_t row_begin, int32_t row_end,
+                                   const int64_t *U_rowptr, const RowMap &m, int32_t rows,
                                    int32_t chunk, int32_t cap_only, int32_t *flags, cudaStream_t st);
 // exclusive scans (int32 -> int32 / int32 -> int64); total -> *total
 cudaError_t scan_exclusive_i32(const int32_t *in, int32_t *out, int64_t count, int32_t *total,
@@ -220,10 +245,16 @@ cudaError_t launch_supernode_stitch_cap(const int64_t *U_rowptr, const int64_t *
                                         cudaStream_t st);
 cudaError_t launch_audit(const int32_t *A_rowptr, const int32_t *A_colidx, const int64_t *L_rowptr,
                          const int32_t *L_colidx, const int64_t *U_rowptr, const int32_t *U_colidx,
-                         const int32_t *sn_start, const int32_t *nsuper, int32_t row_begin, int32_t rows,
+                         const int32_t *sn_start, const int32_t *nsuper, const RowMap &m, int32_t rows,
                          int32_t n, int32_t chunk, int32_t cap_only, int *err, cudaStream_t st);
-cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, int32_t row_begin,
-                                     int32_t row_end, const int32_t *total, int32_t *sn_start,
+cudaError_t launch_rowinfo(const int64_t *L_rowptr, const int32_t *L_colidx, const int64_t *U_rowptr,
+                          const RowMap &m, int32_t rows, int32_t chunk, int32_t *nnzU,
+                          uint32_t *lmask, cudaStream_t st);
+cudaError_t launch_supernode_gathered(const RowMap &m, int32_t chunk, const int32_t *nnzU_all,
+                                      const uint32_t *lmask_all, int64_t stride, int32_t *leader,
+                                      cudaStream_t st);
+cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, const RowMap &m,
+                                     int32_t rows, const int32_t *total, int32_t *sn_start,
                                      cudaStream_t st);
 
 // ------------------------------------------------------------- helpers

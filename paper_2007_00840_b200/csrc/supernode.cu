@@ -65,12 +65,13 @@ __global__ void validate_kernel(const int64_t *rowptr64, const int32_t *colidx, 
   }
 }
 
-__global__ void offdiag_kernel(const int32_t *rowptr, const int32_t *colidx, int32_t r0,
-                               int32_t r1, unsigned long long *out) {
+__global__ void offdiag_kernel(const int32_t *rowptr, const int32_t *colidx, RowMap m,
+                               int32_t rows, unsigned long long *out) {
   __shared__ unsigned long long ws[32];
-  const int i = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long c = 0;
-  if (i < r1) {
+  if (k < rows) {
+    const int i = m.row(k);
     const int a = rowptr[i], b = rowptr[i + 1];
     c = (unsigned long long)(b - a);
     for (int e = a; e < b; ++e) c -= (colidx[e] == i);
@@ -100,13 +101,15 @@ __device__ __forceinline__ bool row_contains(const int32_t *cols, int64_t a, int
 
 // Phase I: bit[k] = 1 iff row s = row_begin + k satisfies requirement (i)
 // against s - 1 (and, under the forced-break rule, s is not a chunk start)
-__global__ void sn_phase1_kernel(const int64_t *U_rowptr, int32_t row_begin, int32_t row_end,
+__global__ void sn_phase1_kernel(const int64_t *U_rowptr, RowMap m, int32_t rows,
                                  int32_t chunk, int32_t cap_only, int32_t *bit) {
-  const int32_t s = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= row_end) return;
-  const int k = s - row_begin;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= rows) return;
+  const int32_t s = m.row(k);
   int b = 0;
-  if (s != row_begin && (cap_only || s % chunk != 0)) {
+  // (interleaved rows: units start at multiples of chunk, so row k - 1 is
+  // row s - 1 whenever s is not a chunk start)
+  if (k != 0 && (cap_only || s % chunk != 0)) {
     const int64_t nu = U_rowptr[k + 1] - U_rowptr[k];
     const int64_t np = U_rowptr[k] - U_rowptr[k - 1];
     b = (nu == np - 1);
@@ -115,22 +118,19 @@ __global__ void sn_phase1_kernel(const int64_t *U_rowptr, int32_t row_begin, int
 }
 
 // Phase II: each Phase-I leader grows through its run of bit-1 rows
-__global__ void sn_phase2_kernel(const int64_t *L_rowptr, const int32_t *L_colidx,
-                                 int32_t row_begin, int32_t row_end, const int32_t *bit,
-                                 int32_t *leader) {
-  const int32_t s = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= row_end) return;
-  const int k = s - row_begin;
+__global__ void sn_phase2_kernel(const int64_t *L_rowptr, const int32_t *L_colidx, RowMap m,
+                                 int32_t rows, const int32_t *bit, int32_t *leader) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= rows) return;
   if (bit[k]) return;  // not a Phase-I leader
   leader[k] = 1;
-  int32_t r = s;
-  for (int32_t t = s + 1; t < row_end && bit[t - row_begin]; ++t) {
-    const int kt = t - row_begin;
+  int32_t r = m.row(k);  // (a run of bit-1 rows never leaves its unit)
+  for (int kt = k + 1; kt < rows && bit[kt]; ++kt) {
     if (row_contains(L_colidx, L_rowptr[kt], L_rowptr[kt + 1], r)) {
       leader[kt] = 0;  // joins the supernode led by r (Def. def:T3 (ii))
     } else {
       leader[kt] = 1;  // rejected: starts a new supernode
-      r = t;
+      r = m.row(kt);
     }
   }
 }
@@ -249,6 +249,59 @@ __global__ void sn_stitch_cap_kernel(const int64_t *U_rowptr, const int64_t *L_r
   }
 }
 
+// ---- finer-than-chunk row interleave (gsofa_interleave): the parts
+// exchange what Def. def:T3 needs about each row, then every part runs the
+// greedy scan per chunk over all rows and keeps its own leaders.
+// rowinfo (one thread per local row k, global row s): nnz(U(s,:)) and the
+// mask of candidate leaders r = s - d inside s's chunk with L(s, r) != 0.
+__global__ void rowinfo_kernel(const int64_t *L_rowptr, const int32_t *L_colidx,
+                               const int64_t *U_rowptr, RowMap m, int32_t rows, int32_t chunk,
+                               int32_t W, int32_t *nnzU, uint32_t *lmask) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= rows) return;
+  const int32_t s = m.row(k), cs = s - s % chunk;
+  nnzU[k] = (int32_t)(U_rowptr[k + 1] - U_rowptr[k]);
+  uint32_t *mk = lmask + (size_t)k * W;
+  for (int w = 0; w < W; ++w) mk[w] = 0u;
+  int64_t a = L_rowptr[k], b = L_rowptr[k + 1];
+  while (a < b) {  // first entry >= cs
+    const int64_t mid = (a + b) >> 1;
+    if (L_colidx[mid] < cs) a = mid + 1;
+    else b = mid;
+  }
+  for (int64_t e = a; e < L_rowptr[k + 1]; ++e) {
+    const int32_t d = s - L_colidx[e];  // 1 .. s - cs
+    mk[d >> 5] |= 1u << (d & 31);
+  }
+}
+
+// one thread per chunk: the greedy Def. def:T3 scan over the
+// chunk's rows, wherever they live (part p = unit % N, local index from the
+// unit); leader[local] for this part's rows
+__global__ void sn_gathered_kernel(RowMap m, int32_t chunk, int32_t W, const int32_t *nnzU_all,
+                                   const uint32_t *lmask_all, int64_t stride, int32_t *leader) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t cs64 = (int64_t)m.rb + c * chunk;
+  if (cs64 >= m.re) return;
+  const int32_t cs = (int32_t)cs64, ce = (int32_t)min((int64_t)m.re, cs64 + chunk);
+  int32_t r = cs;
+  int64_t pn = 0;
+  for (int32_t s = cs; s < ce; ++s) {
+    const int32_t off = s - m.rb, u = off / m.U;
+    const int32_t part = u % m.N;
+    const int64_t idx = (int64_t)part * stride + (int64_t)(u / m.N) * m.U + (off - u * m.U);
+    const int64_t nu = nnzU_all[idx];
+    bool join = false;
+    if (s != cs) {
+      const int32_t d = s - r;
+      join = nu == pn - 1 && ((lmask_all[idx * W + (d >> 5)] >> (d & 31)) & 1u);
+    }
+    if (!join) r = s;
+    if (part == m.q) leader[idx - (int64_t)part * stride] = join ? 0 : 1;
+    pn = nu;
+  }
+}
+
 // Supernode-boundary stitch (multi-range runs): the head rows [rb, he) of a
 // range that starts inside a chunk were scanned as if rb started a block;
 // re-run the greedy Def. def:T3 scan over them from the
@@ -290,12 +343,12 @@ __global__ void sn_stitch_kernel(const int64_t *U_rowptr, const int64_t *L_rowpt
 //      previous block (the greedy scan would not have split there)
 __global__ void audit_kernel(const int32_t *A_rowptr, const int32_t *A_colidx, const int64_t *L_rowptr,
                              const int32_t *L_colidx, const int64_t *U_rowptr, const int32_t *U_colidx,
-                             const int32_t *sn_start, const int32_t *nsuper_p, int32_t row_begin,
+                             const int32_t *sn_start, const int32_t *nsuper_p, RowMap m,
                              int32_t rows, int32_t n, int32_t chunk, int32_t cap_only, int *err) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
-  const int32_t s = row_begin + r;
+  const int32_t s = m.row(r);
   const int64_t la = L_rowptr[r], lb = L_rowptr[r + 1], ua = U_rowptr[r], ub = U_rowptr[r + 1];
   int bad = 0;
   for (int64_t e = la + lane; e < lb; e += 32) {
@@ -313,7 +366,7 @@ __global__ void audit_kernel(const int32_t *A_rowptr, const int32_t *A_colidx, c
     const bool found = c < s ? row_contains(L_colidx, la, lb, c) : row_contains(U_colidx, ua + 1, ub, c);
     if (!found) bad |= 4;
   }
-  if (lane == 0) {
+  if (lane == 0 && nsuper_p) {  // (no supernodes yet: deferred to the exchange)
     // leader of s: the last sn_start entry <= s
     const int32_t ns = *nsuper_p;
     int32_t lo = 0, hi = ns;
@@ -327,7 +380,7 @@ __global__ void audit_kernel(const int32_t *A_rowptr, const int32_t *A_colidx, c
       const int64_t nu = ub - ua, np = ua - U_rowptr[r - 1];
       const bool brk = cap_only ? s - lead >= chunk : s % chunk == 0;
       if (brk || nu != np - 1 || !row_contains(L_colidx, la, lb, lead)) bad |= 8;
-    } else if (s != row_begin && (cap_only || s % chunk != 0)) {
+    } else if (r != 0 && (cap_only || s % chunk != 0)) {
       int32_t lo2 = 0, hi2 = ns;  // leader of s - 1
       while (hi2 - lo2 > 1) {
         const int32_t m = (lo2 + hi2) >> 1;
@@ -343,13 +396,12 @@ __global__ void audit_kernel(const int32_t *A_rowptr, const int32_t *A_colidx, c
   if (lane == 0 && bad) atomicOr(err, bad);
 }
 
-__global__ void sn_scatter_kernel(const int32_t *flags, const int32_t *pos, int32_t row_begin,
-                                  int32_t row_end, const int32_t *total, int32_t *sn_start) {
-  const int32_t s = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
-  if (s == row_begin) sn_start[*total] = row_end;  // sentinel
-  if (s >= row_end) return;
-  const int k = s - row_begin;
-  if (flags[k]) sn_start[pos[k]] = s;
+__global__ void sn_scatter_kernel(const int32_t *flags, const int32_t *pos, RowMap m, int32_t rows,
+                                  const int32_t *total, int32_t *sn_start) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k == 0) sn_start[*total] = rows > 0 ? m.row(rows - 1) + 1 : m.rb;  // sentinel: after the last row
+  if (k >= rows) return;
+  if (flags[k]) sn_start[pos[k]] = m.row(k);
 }
 
 // ---- exclusive scan, 4096 items per block, recursive on block sums
@@ -469,39 +521,37 @@ cudaError_t launch_validate(const int64_t *rowptr64, const int32_t *colidx, int6
   return cudaGetLastError();
 }
 
-cudaError_t launch_count_offdiag(const int32_t *rowptr, const int32_t *colidx, int32_t r0,
-                                 int32_t r1, unsigned long long *out, cudaStream_t st) {
-  if (r1 <= r0) return cudaSuccess;
-  offdiag_kernel<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, st>>>(rowptr, colidx, r0, r1, out);
+cudaError_t launch_count_offdiag(const int32_t *rowptr, const int32_t *colidx, const RowMap &m,
+                                 int32_t rows, unsigned long long *out, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  offdiag_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(rowptr, colidx, m, rows, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_supernode_flags(const int64_t *L_rowptr, const int32_t *L_colidx,
-                                   const int64_t *U_rowptr, int32_t row_begin, int32_t row_end,
+                                   const int64_t *U_rowptr, const RowMap &m, int32_t rows,
                                    int32_t chunk, int32_t cap_only, int32_t *flags, cudaStream_t st) {
   // flags has room for 3 * rows: [0, rows) = Phase-I bits, [rows, 2 rows) =
-  // leaders, [2 rows, 3 rows) = cap-only successor table
-  const int32_t rows = row_end - row_begin;
+  // leaders, [2 rows, 3 rows) = cap-only successor table (cap-only rows are
+  // never interleaved: m.row(k) = rb + k)
   if (rows <= 0) return cudaSuccess;
   const unsigned nb = (unsigned)((rows + 255) / 256);
-  sn_phase1_kernel<<<nb, 256, 0, st>>>(U_rowptr, row_begin, row_end, chunk, cap_only, flags);
+  sn_phase1_kernel<<<nb, 256, 0, st>>>(U_rowptr, m, rows, chunk, cap_only, flags);
   if (cap_only) {
     sn_next_kernel<<<(unsigned)(((int64_t)rows * 32 + 255) / 256), 256, 0, st>>>(
-        L_rowptr, L_colidx, row_begin, row_end, chunk, flags, flags + 2 * rows, flags + rows);
+        L_rowptr, L_colidx, m.rb, m.rb + rows, chunk, flags, flags + 2 * rows, flags + rows);
     sn_walk_kernel<<<nb, 256, 0, st>>>(rows, flags, flags + 2 * rows, flags + rows);
   } else {
-    sn_phase2_kernel<<<nb, 256, 0, st>>>(L_rowptr, L_colidx, row_begin, row_end, flags,
-                                         flags + rows);
+    sn_phase2_kernel<<<nb, 256, 0, st>>>(L_rowptr, L_colidx, m, rows, flags, flags + rows);
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, int32_t row_begin,
-                                     int32_t row_end, const int32_t *total, int32_t *sn_start,
+cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, const RowMap &m,
+                                     int32_t rows, const int32_t *total, int32_t *sn_start,
                                      cudaStream_t st) {
-  const int32_t rows = row_end - row_begin;
-  sn_scatter_kernel<<<(unsigned)((rows + 255) / 256 + 1), 256, 0, st>>>(flags, pos, row_begin,
-                                                                        row_end, total, sn_start);
+  sn_scatter_kernel<<<(unsigned)((rows + 255) / 256 + 1), 256, 0, st>>>(flags, pos, m, rows, total,
+                                                                        sn_start);
   return cudaGetLastError();
 }
 
@@ -524,14 +574,33 @@ cudaError_t launch_supernode_stitch_cap(const int64_t *U_rowptr, const int64_t *
   return cudaGetLastError();
 }
 
+cudaError_t launch_rowinfo(const int64_t *L_rowptr, const int32_t *L_colidx, const int64_t *U_rowptr,
+                          const RowMap &m, int32_t rows, int32_t chunk, int32_t *nnzU,
+                          uint32_t *lmask, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  rowinfo_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(
+      L_rowptr, L_colidx, U_rowptr, m, rows, chunk, (chunk + 31) / 32, nnzU, lmask);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_supernode_gathered(const RowMap &m, int32_t chunk, const int32_t *nnzU_all,
+                                      const uint32_t *lmask_all, int64_t stride, int32_t *leader,
+                                      cudaStream_t st) {
+  const int64_t nch = ((int64_t)m.re - m.rb + chunk - 1) / chunk;
+  if (nch <= 0) return cudaSuccess;
+  sn_gathered_kernel<<<(unsigned)((nch + 127) / 128), 128, 0, st>>>(m, chunk, (chunk + 31) / 32,
+                                                                    nnzU_all, lmask_all, stride, leader);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_audit(const int32_t *A_rowptr, const int32_t *A_colidx, const int64_t *L_rowptr,
                          const int32_t *L_colidx, const int64_t *U_rowptr, const int32_t *U_colidx,
-                         const int32_t *sn_start, const int32_t *nsuper, int32_t row_begin, int32_t rows,
+                         const int32_t *sn_start, const int32_t *nsuper, const RowMap &m, int32_t rows,
                          int32_t n, int32_t chunk, int32_t cap_only, int *err, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   audit_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(A_rowptr, A_colidx, L_rowptr, L_colidx,
                                                            U_rowptr, U_colidx, sn_start, nsuper,
-                                                           row_begin, rows, n, chunk, cap_only, err);
+                                                           m, rows, n, chunk, cap_only, err);
   return cudaGetLastError();
 }
 

@@ -262,7 +262,7 @@ __device__ __forceinline__ void stage_rows(const StreamParams &p, uint32_t *is, 
         const long long off = (long long)base + inc - sz;
         s_rowoff[lane] = off;
         s_nL[lane] = (int)nl;
-        const int r = s_lane - p.row_begin;
+        const int r = 32 * g + lane;  // local row
         p.row_off[r] = ok ? off : -1;
         p.row_nL[r] = (int)nl;
         p.row_nU[r] = (int)nu;
@@ -368,8 +368,8 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
     const unsigned long long st0 = c.steps, lv0 = c.levels, it0 = c.items, pr0 = c.pairs;
     const unsigned long long fv0 = c.fv, sx0 = c.sx;
     long long t_trav = 0, t_ext = 0;
-    const int s0g = p.row_begin + 32 * g;
-    const int nsrc = min(32, p.row_end - s0g);
+    const int s0g = p.map.row(32 * g);  // the group's 32 rows are consecutive
+    const int nsrc = min(32, p.nrows - 32 * g);
     const int Vb = min(n, s0g + nsrc);  // maxId only below the largest source
     const int tbw = (Vb + 31) >> 5;
     for (int i = tid; i < ((tbw + 31) >> 5); i += kThreads) s_tsum[i] = 0u;
@@ -1062,7 +1062,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
 // s then the bits above s, ascending; staged at one reservation; the bitmap
 // words read are zeroed.  Returns false if the staging area was full.
 __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const SoloSlot &sl, int s,
-                                               int g, int lane, SoloWarpSmem &sw) {
+                                               int r, int g, int lane, SoloWarpSmem &sw) {
   const int ns = (((p.n + 31) >> 5) + 31) >> 5;
   // count pass: lane handles summary words i0 + lane (1024 vertices each)
   uint32_t cl = 0, cu = 0;
@@ -1091,7 +1091,6 @@ __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const Solo
   if (lane == 0) base = atomicAdd(p.stage_cursor, tot);
   base = __shfl_sync(kFull, base, 0);
   const bool ok = base + tot <= p.stage_cap;
-  const int r = s - p.row_begin;
   if (lane == 0) {
     p.row_off[r] = ok ? (long long)base : -1;
     p.row_nL[r] = (int)cl;
@@ -1164,7 +1163,7 @@ template <bool kH, int kB>
 __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 32 / kSoloWarps)
     solo_kernel(StreamParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rows = p.row_end - p.row_begin;
+  const int rows = p.nrows;
   const size_t slot = (size_t)blockIdx.x * kSoloWarps + warp;
   const SoloSlot sl = solo_slot(p, slot);
   const int Vs = (int)(p.so_tsum - p.so_rsum);  // reached-word summary words
@@ -1218,26 +1217,27 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
     }
     g = __shfl_sync(kFull, g, 0);
     if (g < 0) break;
-    const int s = p.row_begin + 32 * g + k;
-    if (s >= p.row_end) continue;  // tail of the last group
+    const int r = 32 * g + k;  // local row
+    if (r >= rows) continue;   // tail of the last group
+    const int s = p.map.row(r);
     if (p.src_trace && lane == 0) {
       // dev trace (GSOFA_SRC_TRACE): start / end ns, steps, levels of this source
       unsigned long long t0;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-      p.src_trace[4 * (size_t)(s - p.row_begin)] = (long long)t0;
+      p.src_trace[4 * (size_t)r] = (long long)t0;
     }
     solo_source<kH, kB>(p, sl, s, lane, sw, pf);
     if (p.src_trace && lane == 0) {
       unsigned long long t1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      long long *tr = p.src_trace + 4 * (size_t)(s - p.row_begin);
+      long long *tr = p.src_trace + 4 * (size_t)r;
       tr[1] = (long long)t1;
       tr[2] = sw.steps;
       tr[3] = sw.levels;
     }
     fence_gpu();  // this warp's REDs are visible to its extraction
     __syncwarp();
-    solo_stage_row(p, sl, s, g, lane, sw);
+    solo_stage_row(p, sl, s, r, g, lane, sw);
     // reset the touched words: reached | pend (| thr in id order, where a
     // threshold bit sits in the word of its reached bit), and the summaries
     for (int i0 = 0; i0 < Vs; i0 += 32) {

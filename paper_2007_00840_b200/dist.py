@@ -13,6 +13,16 @@ kernel) and forwards its own tail.  Then one allgather of per-rank counts
 (nnz_L, nnz_U, fill, nsuper, nnz_A_offdiag) gives every rank the global CSR
 offsets of its slice.  Both are tiny messages over NCCL (NVLink/NVSwitch on a
 B200 box); nothing else crosses GPUs.
+
+Row interleave (the paper's source scheduling,
+P:632-647): instead of contiguous ranges, units of U rows are dealt
+round-robin to the ranks (symbolic_interleaved).  With U a multiple of
+chunk_size every unit starts a chunk, supernodes are unit-local and no
+exchange is needed; with a finer U each rank exports 4 + 4 W bytes per row
+(nnz(U(s,:)) and the candidate-leader L mask, gsofa_result_rowinfo), one
+all_gather over NCCL moves them, and every rank runs the per-chunk Def. T3
+scan over the gathered rows (gsofa_supernodes_gathered) -- the B200 analogue
+of the paper's unified-memory remote reads.
 """
 from __future__ import annotations
 
@@ -147,3 +157,87 @@ def assemble(slices_arrays, n: int):
     return dict(L_rowptr=np.concatenate(Lp), L_colidx=np.concatenate(Li).astype(np.int32),
                 U_rowptr=np.concatenate(Up), U_colidx=np.concatenate(Ui).astype(np.int32),
                 sn_start=np.concatenate(sn).astype(np.int32))
+
+
+# ------------------------------------------------------------ row interleave
+
+def interleave_rows(row_begin: int, row_end: int, nparts: int, part: int, unit_rows: int) -> np.ndarray:
+    """Global rows of `part` under the round-robin unit deal (ascending)."""
+    u = np.arange(part, (row_end - row_begin + unit_rows - 1) // unit_rows, nparts, dtype=np.int64)
+    rows = (row_begin + u[:, None] * unit_rows + np.arange(unit_rows, dtype=np.int64)[None, :]).ravel()
+    return rows[rows < row_end]
+
+
+def _rowinfo_gpu(res):
+    return res.rowinfo()
+
+
+def _gathered_gpu(res, nnzU_all, mask_all, stride):
+    res.supernodes_gathered(nnzU_all, mask_all, stride)
+
+
+def symbolic_interleaved(rowptr, colidx, *, rank: int, unit_rows: int = 128, chunk_size: int = 128,
+                         row_begin: int = 0, row_end: int | None = None, compute_fn=None,
+                         rowinfo_fn=None, gathered_fn=None, group=None, device=None, **kw):
+    """This rank's units of rows (round-robin deal of unit_rows-row units,
+    SURVEY §8(f) NEXT-2); supernodes completed by the rowinfo all_gather when
+    unit_rows is not a multiple of chunk_size; then the count allgather.
+
+    compute_fn(rowptr, colidx, interleave=(N, q, U), chunk_size=..., ...) ->
+    result with rows/nsuper/counts; rowinfo_fn(result) -> (nnzU [rows],
+    mask [rows, W]) tensors; gathered_fn(result, nnzU_all, mask_all, stride)
+    completes its supernodes.  Defaults: the CUDA library; tests inject CPU
+    versions to check the host logic on gloo.  Returns (result, counts)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    n = (rowptr.size if isinstance(rowptr, np.ndarray) else rowptr.numel()) - 1
+    row_end = n if row_end is None else row_end
+    if compute_fn is None:
+        from . import symbolic as compute_fn
+    rowinfo_fn = rowinfo_fn or _rowinfo_gpu
+    gathered_fn = gathered_fn or _gathered_gpu
+    res = compute_fn(rowptr, colidx, interleave=(world, rank, unit_rows), chunk_size=chunk_size,
+                     row_begin=row_begin, row_end=row_end, **kw)
+    if res.nsuper < 0:
+        # Def. def:T3 data of every row, part-major, padded to the largest part
+        stride = max(interleave_rows(row_begin, row_end, world, p, unit_rows).size for p in range(world))
+        nnzU, mask = rowinfo_fn(res)
+        W = mask.shape[1]
+        pad_n = torch.zeros(stride, dtype=torch.int32, device=nnzU.device)
+        pad_m = torch.zeros((stride, W), dtype=torch.int32, device=mask.device)
+        pad_n[: nnzU.numel()] = nnzU
+        pad_m[: mask.shape[0]] = mask
+        all_n = torch.empty(world * stride, dtype=torch.int32, device=nnzU.device)
+        all_m = torch.empty((world * stride, W), dtype=torch.int32, device=mask.device)
+        dist.all_gather_into_tensor(all_n, pad_n, group=group)
+        dist.all_gather_into_tensor(all_m, pad_m, group=group)
+        gathered_fn(res, all_n, all_m, stride)
+    local = np.array([res.nnz_L, res.nnz_U, res.fill_count, res.nsuper, res.nnz_A_offdiag, res.rows],
+                     np.int64)
+    counts = allgather_counts(local, group=group, device=device)
+    return res, counts
+
+
+def assemble_interleaved(parts, row_begin: int, row_end: int, unit_rows: int, n: int):
+    """Global CSR + supernodes from the parts' host arrays (verification
+    helper): rows dealt back in order, sn_start = union of the parts'
+    leaders."""
+    N = len(parts)
+    rows_of = [interleave_rows(row_begin, row_end, N, q, unit_rows) for q in range(N)]
+    m = row_end - row_begin
+    nL = np.zeros(m, np.int64)
+    nU = np.zeros(m, np.int64)
+    for q, a in enumerate(parts):
+        nL[rows_of[q] - row_begin] = np.diff(a["L_rowptr"])
+        nU[rows_of[q] - row_begin] = np.diff(a["U_rowptr"])
+    Lp = np.concatenate([[0], np.cumsum(nL)]).astype(np.int64)
+    Up = np.concatenate([[0], np.cumsum(nU)]).astype(np.int64)
+    Li = np.empty(int(Lp[-1]), np.int32)
+    Ui = np.empty(int(Up[-1]), np.int32)
+    for q, a in enumerate(parts):
+        for k, s in enumerate(rows_of[q] - row_begin):
+            Li[Lp[s]:Lp[s + 1]] = a["L_colidx"][a["L_rowptr"][k]:a["L_rowptr"][k + 1]]
+            Ui[Up[s]:Up[s + 1]] = a["U_colidx"][a["U_rowptr"][k]:a["U_rowptr"][k + 1]]
+    sn = np.sort(np.concatenate([a["sn_start"][:-1] for a in parts] + [np.array([row_end])]))
+    return dict(L_rowptr=Lp, L_colidx=Li, U_rowptr=Up, U_colidx=Ui, sn_start=sn.astype(np.int32))

@@ -4,7 +4,14 @@ rank owns a whole B200 in the real run), and report per-range device times.
 The N-GPU step time is max over ranges (+ the two tiny collectives, ~0.1 ms);
 speedup = full single-GPU time / that max.
 
+With --mode interleave the rows are dealt round-robin in units of --unit
+rows (the paper's source scheduling) instead of
+contiguous work-balanced ranges; for units finer than chunk_size each part's
+time includes its gsofa_result_rowinfo and gsofa_supernodes_gathered calls
+(the NCCL all_gather between them is not in the emulation).
+
 usage: python scripts/scaling_emulation.py --config C5 --gpus 2 4 8 [--reps 2]
+       python scripts/scaling_emulation.py --config C5 --mode interleave --unit 128
 """
 import argparse
 import json
@@ -22,6 +29,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C5")
 ap.add_argument("--gpus", type=int, nargs="+", default=[2, 4, 8])
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--mode", default="ranges", choices=["ranges", "interleave"])
+ap.add_argument("--unit", type=int, default=128)
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
 
@@ -29,13 +38,29 @@ rp, ci = gen.config(a.config)
 n = rp.size - 1
 
 
-def timed(rb, re):
+def timed(rb, re, il=None):
     # a fresh context per range, as each rank owns its GPU; best of reps
+    import time
+
+    import torch
     ctx = g.Context(0)
     best = None
     for _ in range(a.reps):
-        r = g.symbolic(rp, ci, ctx=ctx, row_begin=rb, row_end=re, outputs_on_device=True)
+        r = g.symbolic(rp, ci, ctx=ctx, row_begin=rb, row_end=re, outputs_on_device=True,
+                       interleave=il)
         ms = r.stats["ms_total"]
+        if r.nsuper < 0:
+            # the part's side of the exchange (rowinfo export + the per-chunk
+            # scan over gathered rows; its own rows stand in for the others')
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            nn, mm = r.rowinfo()
+            stride = r.rows
+            all_n = nn.repeat(il[0])
+            all_m = mm.repeat(il[0], 1)
+            r.supernodes_gathered(all_n, all_m, stride)
+            torch.cuda.synchronize()
+            ms += (time.perf_counter() - t0) * 1e3
         fill = r.fill_count
         r.free()
         best = ms if best is None else min(best, ms)
@@ -45,13 +70,17 @@ def timed(rb, re):
 
 full_ms, full_fill = timed(0, n)
 print(f"{a.config}: 1 GPU {full_ms:.1f} ms, fill {full_fill}", flush=True)
-report = {"config": a.config, "n": n, "one_gpu_ms": full_ms, "fill": full_fill, "runs": []}
+report = {"config": a.config, "n": n, "one_gpu_ms": full_ms, "fill": full_fill, "mode": a.mode,
+          "unit": a.unit if a.mode == "interleave" else None, "runs": []}
 for N in a.gpus:
-    bounds = gd.partition(rp, ci, N)
+    bounds = gd.partition(rp, ci, N) if a.mode == "ranges" else np.array([0, n])
     per = []
     fills = 0
     for r in range(N):
-        ms, f = timed(int(bounds[r]), int(bounds[r + 1]))
+        if a.mode == "ranges":
+            ms, f = timed(int(bounds[r]), int(bounds[r + 1]))
+        else:
+            ms, f = timed(0, n, (N, r, a.unit))
         per.append(ms)
         fills += f
     assert fills == full_fill

@@ -156,3 +156,129 @@ def test_stitch_chain_oracle(name, scale, chunk):
     from paper_2007_00840_b200 import dist as gd
     asm = gd.assemble(parts, n)
     assert np.array_equal(asm["sn_start"], full["sn_start"])
+
+
+# ------------------------------------------------------------ row interleave
+# dist.symbolic_interleaved: round-robin units of rows,
+# and for finer-than-chunk units the all_gather of per-row Def. def:T3 data.
+# Compute, rowinfo and the per-chunk scan are injected CPU stand-ins (the
+# product path calls the CUDA library); under test are the deal, the padding
+# and part-major layout of the gathered rows, and the count allgather.
+
+def _il_compute(rowptr, colidx, interleave, chunk_size, row_begin, row_end):
+    from paper_2007_00840_b200 import dist as gd
+    N, q, U = interleave
+    rows = gd.interleave_rows(row_begin, row_end, N, q, U)
+    r = oracle.rows(rowptr, colidx, rows, 1)
+    ns = types.SimpleNamespace(rows=rows.size, glob=rows, chunk=chunk_size, il=interleave)
+    ns.arrays = {k: r[k] for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx")}
+    ns.nnz_L, ns.nnz_U = int(r["L_rowptr"][-1]), int(r["U_rowptr"][-1])
+    offd = sum(int(np.count_nonzero(colidx[rowptr[s]:rowptr[s + 1]] != s)) for s in rows)
+    ns.nnz_A_offdiag = offd
+    ns.fill_count = ns.nnz_L + ns.nnz_U - rows.size - offd
+    if U % chunk_size == 0:  # unit-local supernodes: the oracle scan per unit
+        lead = []
+        for u0 in range(0, rows.size, U):
+            sl = slice(u0, min(rows.size, u0 + U))
+            Lp = r["L_rowptr"][sl.start:sl.stop + 1] - r["L_rowptr"][sl.start]
+            Up = r["U_rowptr"][sl.start:sl.stop + 1] - r["U_rowptr"][sl.start]
+            Li = r["L_colidx"][r["L_rowptr"][sl.start]:r["L_rowptr"][sl.stop]]
+            lead += oracle.supernodes(int(rows[u0]), Lp, Li, Up, chunk_size)[:-1].tolist()
+        ns.arrays["sn_start"] = np.array(lead + [int(rows[-1]) + 1], np.int32)
+        ns.nsuper = len(lead)
+    else:
+        ns.nsuper = -1
+    return ns
+
+
+def _il_rowinfo(res):
+    import torch
+    a, W = res.arrays, (res.chunk + 31) // 32
+    nnzU = torch.tensor(np.diff(a["U_rowptr"]), dtype=torch.int32)
+    mask = np.zeros((res.rows, W), np.uint32)
+    for k, s in enumerate(res.glob):
+        for c in a["L_colidx"][a["L_rowptr"][k]:a["L_rowptr"][k + 1]]:
+            d = int(s - c)
+            if d <= s % res.chunk:
+                mask[k, d // 32] |= np.uint32(1 << (d % 32))
+    return nnzU, torch.tensor(mask.view(np.int32))
+
+
+def _il_gathered(res, all_n, all_m, stride):
+    """Per chunk, the greedy Def. def:T3 scan over the gathered rows; this
+    part keeps its own leaders."""
+    N, q, U = res.il
+    nn, mm = all_n.numpy(), all_m.numpy().view(np.uint32)
+    end = int(res.glob[-1]) + 1
+    n_rows = max(end, 0)
+    mine, lead = set(res.glob.tolist()), []
+
+    def at(s):
+        u = s // U
+        return (u % N) * stride + (u // N) * U + s % U
+
+    total_rows = res.total_rows
+    for cs in range(0, total_rows, res.chunk):
+        r, pn = cs, 0
+        for s in range(cs, min(total_rows, cs + res.chunk)):
+            i = at(s)
+            nu, d = int(nn[i]), s - r
+            join = s != cs and nu == pn - 1 and (int(mm[i, d // 32]) >> (d % 32)) & 1
+            if not join:
+                r = s
+                if s in mine:
+                    lead.append(s)
+            pn = nu
+    res.arrays["sn_start"] = np.array(lead + [n_rows], np.int32)
+    res.nsuper = len(lead)
+
+
+def _il_worker(rank, world, port, name, scale, chunk, U, q):
+    import torch.distributed as dist
+
+    from paper_2007_00840_b200 import dist as gd
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rp, ci = gen.config(name, scale)
+
+        def compute(rowptr, colidx, **kw):
+            r = _il_compute(rowptr, colidx, **kw)
+            r.total_rows = rowptr.size - 1
+            return r
+        res, counts = gd.symbolic_interleaved(rp, ci, rank=rank, unit_rows=U, chunk_size=chunk,
+                                              compute_fn=compute, rowinfo_fn=_il_rowinfo,
+                                              gathered_fn=_il_gathered)
+        q.put((rank, counts.tolist(), res.arrays))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,name,scale,chunk,U", [
+    (2, "C1", None, 128, 32), (3, "C2", 10, 64, 96), (2, "C3", 1500, 128, 256), (3, "C4", 40, 64, 64)])
+def test_interleave_host_logic_gloo(world, name, scale, chunk, U):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_il_worker, args=(r, world, port, name, scale, chunk, U, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    outs.sort(key=lambda t: t[0])
+    rp, ci = gen.config(name, scale)
+    n = rp.size - 1
+    full = oracle.symbolic(rp, ci, chunk_size=chunk)
+    counts = np.array(outs[0][1])
+    assert all(np.array_equal(np.array(o[1]), counts) for o in outs)
+    tot = counts.sum(axis=0)
+    assert tot[0] == full["nnz_L"] and tot[1] == full["nnz_U"] and tot[2] == full["fill_count"]
+    assert tot[3] == full["nsuper"] and tot[5] == n
+    from paper_2007_00840_b200 import dist as gd
+    asm = gd.assemble_interleaved([o[2] for o in outs], 0, n, U, n)
+    for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start"):
+        assert np.array_equal(asm[k], full[k]), k

@@ -723,3 +723,65 @@ def test_external_frontier_budget(budget_mb):
     want = oracle.symbolic(rp, ci)
     assert_full_equal(got, want)
     assert_full_equal(again, want)
+
+
+# ------------------------------ row interleave --
+
+def _run_interleaved(rp, ci, ctx, N, U, chunk, **kw):
+    """Every part through the C-ABI in one process (each part is one GPU's
+    call in the multi-GPU layer); finer-than-chunk units complete their
+    supernodes from the parts' gathered rowinfo, as dist.symbolic_interleaved
+    does over NCCL."""
+    import torch
+    from paper_2007_00840_b200 import dist as gd
+    n = rp.size - 1
+    res = [g.symbolic(rp, ci, ctx=ctx, chunk_size=chunk, interleave=(N, q, U),
+                      outputs_on_device=True, **kw) for q in range(N)]
+    if res[0].nsuper < 0:
+        stride = max(r.rows for r in res)
+        infos = [r.rowinfo() for r in res]
+        W = infos[0][1].shape[1]
+        all_n = torch.zeros(N * stride, dtype=torch.int32, device="cuda")
+        all_m = torch.zeros((N * stride, W), dtype=torch.int32, device="cuda")
+        for q, (a, m) in enumerate(infos):
+            all_n[q * stride: q * stride + a.numel()] = a
+            all_m[q * stride: q * stride + m.shape[0]] = m
+        for r in res:
+            r.supernodes_gathered(all_n, all_m, stride)
+    parts = []
+    for q, r in enumerate(res):
+        assert r.rows == gd.interleave_rows(0, n, N, q, U).size
+        parts.append({k: v.copy() for k, v in r.to_numpy().items()})
+        parts[-1]["counts"] = (r.nnz_L, r.nnz_U, r.fill_count, r.nsuper, r.nnz_A_offdiag)
+        r.free()
+    return gd.assemble_interleaved(parts, 0, n, U, n), parts
+
+
+@pytest.mark.parametrize("name,scale,N,U,chunk", [
+    ("C1", None, 2, 128, 128), ("C1", None, 3, 32, 128), ("C3", 3000, 4, 64, 128),
+    ("C2", 16, 8, 32, 128), ("C2", 16, 3, 256, 128), ("C5", 14, 8, 128, 64),
+    ("C5", 14, 5, 96, 64), ("C4", 60, 8, 32, 128), ("C4", 60, 2, 1024, 128)])
+def test_interleave_parts(ctx, name, scale, N, U, chunk):
+    """Round-robin units of U rows over N parts: the parts' rows reassembled in
+    order, and the union of their leaders, equal the oracle's whole-matrix
+    result; per-part counts add up."""
+    rp, ci = gen.config(name, scale)
+    want = oracle.symbolic(rp, ci, chunk_size=chunk)
+    asm, parts = _run_interleaved(rp, ci, ctx, N, U, chunk)
+    for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start"):
+        assert np.array_equal(asm[k], want[k]), k
+    tot = np.array([p["counts"] for p in parts]).sum(axis=0)
+    assert tuple(int(x) for x in tot) == (want["nnz_L"], want["nnz_U"], want["fill_count"],
+                                          want["nsuper"], want["nnz_A_offdiag"])
+
+
+def test_interleave_checked_and_errors(ctx):
+    rp, ci = gen.config("C2", 12)
+    got, _ = _run_interleaved(rp, ci, ctx, 3, 64, 128, checked=True)
+    assert np.array_equal(got["L_colidx"], oracle.symbolic(rp, ci)["L_colidx"])
+    for bad in (dict(interleave=(2, 2, 64)), dict(interleave=(2, 0, 48)),
+                dict(interleave=(2, 0, 64), schedule="fifo"),
+                dict(interleave=(2, 0, 64), sn_cap_only=True),
+                dict(interleave=(2, 0, 64), row_begin=5)):
+        with pytest.raises(g.GsofaError):
+            g.symbolic(rp, ci, ctx=ctx, **bad)
