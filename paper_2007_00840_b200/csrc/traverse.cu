@@ -86,11 +86,8 @@ template <bool kFillFirst>
 __device__ __forceinline__ void expand_item(const BatchParams &p, uint32_t u, uint32_t g,
                                             uint32_t *fmc, uint32_t *fmn, uint32_t *nq,
                                             uint32_t *nqx, uint32_t *ncount, uint32_t *buf, int &nb,
-                                            int lane, unsigned long long &st_items,
-                                            unsigned long long &st_edges,
-                                            unsigned long long &st_pairs,
-                                            unsigned long long &st_fv,
-                                            unsigned long long &st_sx) {
+                                            int lane, unsigned long long *wst,
+                                            uint32_t &st_fv) {
   const size_t row = (size_t)g * p.Vb + u;
   uint32_t mask = 0;
   if (lane == 0) {
@@ -106,10 +103,12 @@ __device__ __forceinline__ void expand_item(const BatchParams &p, uint32_t u, ui
   const uint32_t encc = p.base + (uint32_t)c + 1u;
   const int beg = __ldg(p.rowptr + u), end = __ldg(p.rowptr + u + 1);
   if (lane == 0) {
-    st_items += 1;
-    st_sx += (unsigned long long)__popc(mask);
-    st_edges += (unsigned long long)__popc(mask) * (unsigned long long)(end - beg);
-    st_pairs += (unsigned long long)(end - beg);
+    // this warp's counters live in shared memory (registers are at the
+    // 64-per-thread budget of 2 CTAs x 512 threads)
+    wst[0] += 1;
+    wst[1] += (unsigned long long)__popc(mask) * (unsigned long long)(end - beg);
+    wst[2] += (unsigned long long)(end - beg);
+    wst[3] += (unsigned long long)__popc(mask);
   }
   uint32_t *labg = p.lab + (size_t)g * p.Vb * 32 + lane;
   uint32_t *isg = p.is + (size_t)g * p.n;
@@ -141,8 +140,8 @@ __device__ __forceinline__ void expand_item(const BatchParams &p, uint32_t u, ui
       for (int i = 0; i < kFifoInflight; ++i) {
         // first visit of (s, w): the old label is not of this batch's epoch
         // (values of the epoch are base .. base + n + 1)
-        const uint32_t nv = __popc(__ballot_sync(kFull, lo[i] && old[i] > p.base + (uint32_t)p.n + 1u));
-        if (lane == 0) st_fv += nv;
+        // (counted per lane, summed over the warp once at the end)
+        st_fv += (lo[i] && old[i] > p.base + (uint32_t)p.n + 1u) ? 1u : 0u;
         const bool enq = lo[i] && encc < old[i] && old[i] > p.base + (uint32_t)w[i] + 1u;
         const bool fill = enq && c < w[i];
         const uint32_t ib = __ballot_sync(kFull, up[i] || fill);
@@ -185,7 +184,13 @@ __global__ void __launch_bounds__(kTraverseThreads, 2) traverse_kernel(BatchPara
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
   const uint32_t gmask = (1u << p.gbits) - 1u;
   uint32_t *buf = sbuf[wib];
-  unsigned long long st_items = 0, st_edges = 0, st_pairs = 0, st_fv = 0, st_sx = 0;
+  // per warp: items, (source, edge) inspections, (item, neighbour) pairs,
+  // source expansions
+  __shared__ unsigned long long s_st[kTraverseThreads / 32][4];
+  unsigned long long *wst = s_st[wib];
+  if (lane < 4) wst[lane] = 0ull;
+  __syncwarp();
+  uint32_t st_fv = 0;  // this lane's first visits
   int round = 0;
   for (;; ++round) {
     const uint32_t *q = (round & 1) ? p.q1 : p.q0;
@@ -209,7 +214,7 @@ __global__ void __launch_bounds__(kTraverseThreads, 2) traverse_kernel(BatchPara
       for (uint32_t t = 0; t < cnt; ++t) {
         const uint32_t item = __shfl_sync(kFull, my, t);
         expand_item<kFillFirst>(p, item >> p.gbits, item & gmask, fmc, fmn, nq, nqx, ncount, buf,
-                                nb, lane, st_items, st_edges, st_pairs, st_fv, st_sx);
+                                nb, lane, wst, st_fv);
       }
     }
     if (nb > 0) {
@@ -225,12 +230,15 @@ __global__ void __launch_bounds__(kTraverseThreads, 2) traverse_kernel(BatchPara
       atomicAdd(p.stats + 10, (unsigned long long)(nn - p.qcap));
     if (nn == 0u) break;
   }
-  if (lane == 0 && st_items) {
-    atomicAdd(p.stats + 0, st_items);
-    atomicAdd(p.stats + 1, st_edges);
-    atomicAdd(p.stats + 4, st_pairs);
-    atomicAdd(p.stats + 8, st_fv);
-    atomicAdd(p.stats + 9, st_sx);
+  unsigned long long fv = st_fv;
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) fv += __shfl_xor_sync(kFull, fv, d);
+  if (lane == 0 && wst[0]) {
+    atomicAdd(p.stats + 0, wst[0]);
+    atomicAdd(p.stats + 1, wst[1]);
+    atomicAdd(p.stats + 4, wst[2]);
+    atomicAdd(p.stats + 8, fv);
+    atomicAdd(p.stats + 9, wst[3]);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.stats + 2, (unsigned long long)(round + 1));
 }
