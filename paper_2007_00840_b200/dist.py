@@ -208,11 +208,14 @@ def symbolic_interleaved(rowptr, colidx, *, rank: int, unit_rows: int = 128, chu
         pad_m = torch.zeros((stride, W), dtype=torch.int32, device=mask.device)
         pad_n[: nnzU.numel()] = nnzU
         pad_m[: mask.shape[0]] = mask
-        all_n = torch.empty(world * stride, dtype=torch.int32, device=nnzU.device)
-        all_m = torch.empty((world * stride, W), dtype=torch.int32, device=mask.device)
-        dist.all_gather_into_tensor(all_n, pad_n, group=group)
-        dist.all_gather_into_tensor(all_m, pad_m, group=group)
-        gathered_fn(res, all_n, all_m, stride)
+        # NCCL gathers device tensors in place; gloo (tests, shared-GPU
+        # smoke runs) goes through host memory
+        cdev = pad_n.device if dist.get_backend(group) != "gloo" else torch.device("cpu")
+        all_n = torch.empty(world * stride, dtype=torch.int32, device=cdev)
+        all_m = torch.empty((world * stride, W), dtype=torch.int32, device=cdev)
+        dist.all_gather_into_tensor(all_n, pad_n.to(cdev), group=group)
+        dist.all_gather_into_tensor(all_m, pad_m.to(cdev), group=group)
+        gathered_fn(res, all_n.to(nnzU.device), all_m.to(mask.device), stride)
     local = np.array([res.nnz_L, res.nnz_U, res.fill_count, res.nsuper, res.nnz_A_offdiag, res.rows],
                      np.int64)
     counts = allgather_counts(local, group=group, device=device)
