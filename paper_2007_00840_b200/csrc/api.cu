@@ -145,6 +145,9 @@ struct gsofa_context {
   // one grow-only buffer
   int32_t *ord_buf = nullptr;
   size_t ord_cap = 0;
+  // ELL copy of the adjacency (solo kernel, id order, rows <= 8 entries)
+  int32_t *ell = nullptr;
+  size_t ell_cap = 0;
   HostBlock *hpool = nullptr;  // pinned storage reused by host-side results
   // external frontier (FIFO queue overflow) in mapped pinned host memory,
   // grow-only; spill_dev is its device address
@@ -553,6 +556,7 @@ void gsofa_context_destroy(gsofa_context *c) {
   if (c->bw_dev) cudaFree(c->bw_dev);
   if (c->stage) cudaFree(c->stage);
   if (c->ord_buf) cudaFree(c->ord_buf);
+  if (c->ell) cudaFree(c->ell);
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->spill) cudaFreeHost(c->spill);
   host_block_release(c->hpool);
@@ -1075,6 +1079,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   int64_t baseL = 0, baseU = 0, nbatches = 0, maxC = 0;
   Plan plan;
   bool auto_fifo = false;
+  unsigned int maxdeg = 0;  // largest row of A (validation pass)
   int64_t ord_npos = 0;  // > 0: height order possible (threshold bitmaps sized for n positions)
   bool auto_order = false;  // AUTO: pick the threshold order from the tree's shape
   std::vector<int64_t> ord_hrp;              // host copies of a device CSR (height order)
@@ -1123,7 +1128,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   if (!c->bw_dev) CK(cudaMalloc((void **)&c->bw_dev, 64));
   CK(cudaMemsetAsync(c->bw_dev, 0, 12, st));  // [0] bandwidth, [1] error flags, [2] max degree
   CK(gsofa::launch_validate(d_rowptr64, d_colidx, n, nnz, c->rowptr32, (int *)(c->bw_dev + 1),
-                            o.schedule == GSOFA_SCHEDULE_AUTO ? c->bw_dev : nullptr, st));
+                            c->bw_dev, st));
   ++launches;
   CK(cudaMemcpyAsync(c->h_small, c->bw_dev, 12, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1133,6 +1138,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     rc = GSOFA_EBADCSR;
     goto fail;
   }
+  maxdeg = ((unsigned int *)c->h_small)[2];  // largest row of A
   if (o.schedule == GSOFA_SCHEDULE_AUTO) {
     // banded and dense -> the paper's FIFO order (few rounds, no revisits);
     // otherwise threshold order (DESIGN.md §8 "Schedule").  FIFO also needs
@@ -1153,7 +1159,6 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     // it is computed only for patterns with hub rows (largest row > 32x the
     // mean), where height order was measured to win (C4: 1.19 s -> 0.45 s);
     // on grids it would only delay the solo kernel (C5: ~5%)
-    const unsigned int maxdeg = ((unsigned int *)c->h_small)[2];
     const int64_t mean = std::max<int64_t>(1, nnz / std::max<int64_t>(1, n));
     auto_order = !auto_fifo && (int64_t)maxdeg > 32 * mean;
   }
@@ -1350,6 +1355,15 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.posrec = reinterpret_cast<const int4 *>(c->ord_buf);  // 16-byte aligned (buffer start)
     sp.hgt = c->ord_buf + 4 * n;
     sp.pos = c->ord_buf + 5 * n;
+    sp.ell = nullptr;
+    if (maxdeg <= 8 && !sp.wide && !sp.hmode && !(std::getenv("GSOFA_ELL") && atoi(std::getenv("GSOFA_ELL")) == 0)) {
+      // id-order solo sources read neighbour lists from an ELL copy (every
+      // row fits 8 entries): one dependent round trip less per closure level
+      if ((rc = grow_device(&c->ell, &c->ell_cap, (size_t)n * 8, st)) != GSOFA_OK) goto fail;
+      CK(gsofa::launch_ell_build(c->rowptr32, d_colidx, (int32_t)n, c->ell, st));
+      ++launches;
+      sp.ell = c->ell;
+    }
     if (plan.heavy > 0) {
       // the heaviest groups (top separator / hub rows) start on
       // the solo kernel: one per first-wave solo CTA (one per SM)

@@ -133,6 +133,7 @@ struct StreamParams {
                              //     height's segment of positions}
   const int32_t *hgt;        // [n] etree height of a vertex
   const int32_t *pos;        // [n] vertex -> position
+  const int32_t *ell;        // [8 n] ELL adjacency (id order, rows <= 8 entries), or NULL
   // solo slot layout: word offsets of its arrays (solo_layout)
   uint32_t so_pend, so_thr, so_rsum, so_tsum, so_is, so_isum, so_queue;
 };
@@ -256,6 +257,11 @@ cudaError_t launch_supernode_gathered(const RowMap &m, int32_t chunk, const int3
 cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, const RowMap &m,
                                      int32_t rows, const int32_t *total, int32_t *sn_start,
                                      cudaStream_t st);
+
+// ELL copy of the adjacency for the solo kernel's id order (rows <= 8
+// entries): ell[8 v + j] = j-th neighbour of v, -1 padded
+cudaError_t launch_ell_build(const int32_t *rowptr, const int32_t *colidx, int32_t n, int32_t *ell,
+                             cudaStream_t st);
 
 // ------------------------------------------------------------- helpers
 // Row `lane` of a 32x32 bit matrix in, column `lane` out (bit j of the result

@@ -862,6 +862,66 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
   }
 }
 
+// ELL adjacency (id order, every row <= kEll entries): the neighbours of v
+// are ell[kEll v .. kEll v + kEll), padded with -1, so a closure member's
+// neighbour list depends on its id alone -- it is prefetched into L1 when
+// the member is reached (in flight together with the reached atomic) and the
+// next level reads it without waiting for row pointers.  Items map to lanes
+// statically (4 items x 8 slots per 32-lane batch): no prefix sum or owner
+// search.
+constexpr int kEll = 8;
+
+__device__ __forceinline__ void prefetch_l1(const void *q) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+}
+
+__device__ __forceinline__ void solo_expand_ell(const StreamParams &p, const SoloSlot &sl,
+                                                SoloWarpSmem &sw, int wb, SoloQueue &Q, int s,
+                                                int T, int u, int lane) {
+  const int nitems = __popc(__ballot_sync(kFull, u >= 0));  // items sit in lanes 0 .. nitems-1
+  uint32_t npairs = 0;
+  for (int b0 = 0; b0 < nitems; b0 += 32 / kEll) {
+    const int i = b0 + lane / kEll;
+    const int ui = __shfl_sync(kFull, u, i & 31);
+    int w = i < nitems ? __ldg(p.ell + (size_t)ui * kEll + (lane & (kEll - 1))) : -1;
+    if (w < 0) w = s;  // padding: no pair
+    npairs += __popc(__ballot_sync(kFull, w != s));
+    const uint32_t bw = vbit(w);
+    // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds iff
+    // the source has not reached w yet (line 10 of fig:alg)
+    const uint32_t ro = w < s ? atomicOr(SL_REACHED + (w >> 5), bw) : bw;
+    if (w > s) {
+      atomicOr(SL_IS + (w >> 5), bw);  // RED
+      red_sum(SL_ISUM, w);
+    }
+    if (w < T) prefetch_l1(p.ell + (size_t)w * kEll);  // a possible closure member
+    bool push = false;
+    if (!(ro & bw)) {
+      if (ro == 0u) red_sum(SL_RSUM, w);
+      if (w > T) {
+        // fill of L(s,:) (R4); w becomes a threshold of this source
+        atomicOr(SL_IS + (w >> 5), bw);  // RED
+        red_sum(SL_ISUM, w);
+        const int d = (w >> 5) - wb;
+        if (d < 32) {
+          atomicOr(&sw.win[d], bw);  // smem
+        } else {
+          atomicOr(SL_THR + (w >> 5), bw);  // RED
+          red_sum(SL_TSUM, w);
+        }
+      } else {
+        push = true;  // maxId(w) = T, not in the structure: continue with T
+      }
+    }
+    solo_push<false>(p, sl, sw, nullptr, Q, push, w, -1, -1, lane);
+  }
+  if (lane == 0) {
+    sw.items += (uint32_t)nitems;
+    sw.pairs += npairs;
+    sw.levels += 1;
+  }
+}
+
 // Next threshold of the source above T.  Inside the window: shared memory
 // only.  Past it: publish this warp's global threshold REDs, scan the global
 // bitmap (summary-guided) and load a new window at the found threshold.
@@ -899,7 +959,7 @@ __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const ui
 // position (vertices sorted by (height, id)) and a step takes every threshold
 // of one height within the 32-word window (order.cu); the graph, reached and
 // structure bitmaps stay in vertex ids (the ND order's locality)
-template <bool kH, int kB>
+template <bool kH, int kB, bool kE = false>
 __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s,
                                             int lane, SoloWarpSmem &sw, SoloPF *pf) {
   constexpr bool kPF = kB > 1 && kAdjPrefetch;
@@ -975,8 +1035,10 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       t.tmin = P;  // the one threshold (tmax / h unused in id order)
       if (lane == 0) {
         u = P;
-        ub = __ldg(p.rowptr + P);
-        ue = __ldg(p.rowptr + P + 1);
+        if (!kE) {  // (ELL: the neighbour list needs no row pointers)
+          ub = __ldg(p.rowptr + P);
+          ue = __ldg(p.rowptr + P + 1);
+        }
       }
     }
     // first visits (R11): every vertex newly reached below s is either a
@@ -985,7 +1047,8 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
     const int pushed0 = Q.st + Q.gt;  // the step's own thresholds queued above
     int us = -1;  // prefetch slot of this lane's item
     for (;;) {
-      solo_expand<kH, kB>(p, sl, sw, pf, wb, Q, s, t, u, ub, ue, us, lane);
+      if (kE) solo_expand_ell(p, sl, sw, wb, Q, s, t.tmin, u, lane);
+      else solo_expand<kH, kB>(p, sl, sw, pf, wb, Q, s, t, u, ub, ue, us, lane);
       __syncwarp();
       us = -1;
       if (kPF) Q.hold = 0;
@@ -997,8 +1060,10 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
         if (lane < cnt) {
           i = (Q.sh + lane) & (kSoloQ - 1);
           u = sw.qw[i];
-          ub = sw.qb[i];
-          ue = sw.qe[i];
+          if (!kE) {
+            ub = sw.qb[i];
+            ue = sw.qe[i];
+          }
           if (kPF && ub < 0) {
             // its neighbour list was prefetched: wait for the bytes, then
             // the slot's barrier is in its next phase
@@ -1050,7 +1115,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
       const int cnt = min(32, Q.gt - Q.gh);
       u = lane < cnt ? (int)SL_QUEUE[(Q.gh + lane) & SL_QMASK] : -1;
       Q.gh += cnt;
-      if (u >= 0) {
+      if (u >= 0 && !kE) {
         ub = __ldg(p.rowptr + u);
         ue = __ldg(p.rowptr + u + 1);
       }
@@ -1159,7 +1224,7 @@ __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const Solo
 // outnumber warps; kB = 4 ("wide"): 32 warps per SM, a level's first 128
 // pairs in flight at once -- the latency shape for chain-bound sources (few
 // heavy sources: C4's hub rows, the top-separator ranges of a multi-GPU split)
-template <bool kH, int kB>
+template <bool kH, int kB, bool kE = false>
 __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 32 / kSoloWarps)
     solo_kernel(StreamParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1226,7 +1291,7 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
       p.src_trace[4 * (size_t)r] = (long long)t0;
     }
-    solo_source<kH, kB>(p, sl, s, lane, sw, pf);
+    solo_source<kH, kB, kE>(p, sl, s, lane, sw, pf);
     if (p.src_trace && lane == 0) {
       unsigned long long t1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
@@ -1446,6 +1511,7 @@ cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st) {
     else solo_kernel<false, 4><<<grid, kSoloWarps * 32, dyn, st>>>(p);
   } else {
     if (p.hmode) solo_kernel<true, 1><<<grid, kSoloWarps * 32, 0, st>>>(p);
+    else if (p.ell) solo_kernel<false, 1, true><<<grid, kSoloWarps * 32, 0, st>>>(p);
     else solo_kernel<false, 1><<<grid, kSoloWarps * 32, 0, st>>>(p);
   }
   return cudaGetLastError();
@@ -1457,6 +1523,28 @@ cudaError_t launch_gather(const int32_t *stage, const int64_t *row_off, const in
   if (rows <= 0) return cudaSuccess;
   gather_kernel<<<(rows + 7) / 8, 256, 0, st>>>(stage, row_off, row_nL, L_rowptr, U_rowptr, rows,
                                                 L_out, U_out);
+  return cudaGetLastError();
+}
+
+namespace {
+__global__ void ell_build_kernel(const int32_t *rowptr, const int32_t *colidx, int32_t n,
+                                 int32_t *ell) {
+  const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int32_t a = rowptr[v], d = rowptr[v + 1] - a;
+  int r[kEll];
+#pragma unroll
+  for (int j = 0; j < kEll; ++j) r[j] = j < d ? colidx[a + j] : -1;
+  int4 *o = reinterpret_cast<int4 *>(ell + (size_t)v * kEll);
+  o[0] = make_int4(r[0], r[1], r[2], r[3]);
+  o[1] = make_int4(r[4], r[5], r[6], r[7]);
+}
+}  // namespace
+
+cudaError_t launch_ell_build(const int32_t *rowptr, const int32_t *colidx, int32_t n, int32_t *ell,
+                             cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ell_build_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rowptr, colidx, n, ell);
   return cudaGetLastError();
 }
 

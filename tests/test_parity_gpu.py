@@ -785,3 +785,36 @@ def test_interleave_checked_and_errors(ctx):
                 dict(interleave=(2, 0, 64), row_begin=5)):
         with pytest.raises(g.GsofaError):
             g.symbolic(rp, ci, ctx=ctx, **bad)
+
+
+# --------------------------- ELL neighbour lists of the id-order solo kernel --
+
+@pytest.mark.parametrize("ell", ["0", "1"])
+@pytest.mark.parametrize("case", ["C2_24", "C5_20", "C1", "rand_sparse", "all_solo"])
+def test_solo_ell_path(case, ell, monkeypatch):
+    """Rows of at most 8 entries: the solo kernel reads neighbour lists from
+    the ELL copy (GSOFA_ELL=1, default) or the CSR (0); both equal the oracle
+    (also with every group on the solo kernel)."""
+    monkeypatch.setenv("GSOFA_ELL", ell)
+    if case == "C2_24":
+        rp, ci = gen.config("C2", 24)
+    elif case == "C5_20":
+        rp, ci = gen.config("C5", 20)
+    elif case == "C1":
+        rp, ci = gen.config("C1")
+    elif case == "rand_sparse":
+        rp, ci = gen.random_graph(3000, 0.0012, seed=77)
+        keep = np.diff(rp) <= 8
+        rows = np.repeat(np.arange(rp.size - 1), np.diff(rp))
+        m = keep[rows]
+        rp, ci = gen.csr_from_edges(rp.size - 1, rows[m], ci[m].astype(np.int64))
+    else:
+        monkeypatch.setenv("GSOFA_ABORT_MS", "0.001")
+        rp, ci = gen.config("C2", 20)
+    assert np.diff(rp).max() <= 8
+    c = g.Context(0)
+    try:
+        got = run(rp, ci, c, schedule="threshold")
+    finally:
+        c.close()
+    assert_full_equal(got, oracle.symbolic(rp, ci), f"{case} ell={ell}")
