@@ -1356,9 +1356,12 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.hgt = c->ord_buf + 4 * n;
     sp.pos = c->ord_buf + 5 * n;
     sp.ell = nullptr;
-    if (maxdeg <= 8 && !sp.wide && !sp.hmode && !(std::getenv("GSOFA_ELL") && atoi(std::getenv("GSOFA_ELL")) == 0)) {
-      // id-order solo sources read neighbour lists from an ELL copy (every
-      // row fits 8 entries): one dependent round trip less per closure level
+    if (maxdeg <= 8 && !sp.wide && !sp.hmode && std::getenv("GSOFA_ELL") && atoi(std::getenv("GSOFA_ELL")) != 0) {
+      // dev A/B (GSOFA_ELL=1): id-order solo sources read neighbour lists from
+      // an ELL copy (every row fits 8 entries) -- one dependent round trip
+      // less per closure level, but measured slower (C5 3.41 -> 3.61 s, top
+      // range 4.4 -> 4.6 us per level: the reached atomic, not the list
+      // load, is the wait; profiles/r2/ell_ab.txt), so off by default
       if ((rc = grow_device(&c->ell, &c->ell_cap, (size_t)n * 8, st)) != GSOFA_OK) goto fail;
       CK(gsofa::launch_ell_build(c->rowptr32, d_colidx, (int32_t)n, c->ell, st));
       ++launches;

@@ -793,7 +793,7 @@ def test_interleave_checked_and_errors(ctx):
 @pytest.mark.parametrize("case", ["C2_24", "C5_20", "C1", "rand_sparse", "all_solo"])
 def test_solo_ell_path(case, ell, monkeypatch):
     """Rows of at most 8 entries: the solo kernel reads neighbour lists from
-    the ELL copy (GSOFA_ELL=1, default) or the CSR (0); both equal the oracle
+    the ELL copy (GSOFA_ELL=1, dev A/B) or the CSR (0, default); both equal the oracle
     (also with every group on the solo kernel)."""
     monkeypatch.setenv("GSOFA_ELL", ell)
     if case == "C2_24":
