@@ -1278,8 +1278,9 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     int32_t *nfailed = (int32_t *)(c->qcount + 1);
     unsigned long long *cursor = (unsigned long long *)c->totals;
     unsigned long long *failed_need = cursor + 1;
-    // qcount: [0] group_ctr, [1] nfailed, [2] hq_head, [3] hq_tail, [4] done
-    CK(cudaMemsetAsync(c->qcount, 0, 32, st));
+    // qcount: [0] group_ctr, [1] nfailed, [2] hq_head, [3] hq_tail, [4] done,
+    // [5] solo_ctr, [6..7] task_ctr, [8] live lockstep CTAs
+    CK(cudaMemsetAsync(c->qcount, 0, 36, st));
     CK(cudaMemsetAsync(c->totals, 0, 16, st));
     gsofa::StreamParams sp;
     sp.rowptr = c->rowptr32;
@@ -1341,6 +1342,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.hq_head = c->qcount + 2;
     sp.hq_tail = c->qcount + 3;
     sp.done = c->qcount + 4;
+    sp.light_live = c->qcount + 8;  // zeroed with qcount[0..8] below
     sp.task_ctr = (unsigned long long *)(c->qcount + 6);  // qcount[6..7]
     sp.hws = c->work + (size_t)plan.light * plan.ws_words;
     sp.hws_words = plan.hws_words;

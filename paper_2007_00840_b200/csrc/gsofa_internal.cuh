@@ -101,6 +101,7 @@ struct StreamParams {
   unsigned int *hq_head, *hq_tail;
   int32_t *hq_ready;         // [ngroups] publication flags
   unsigned int *done;        // rows completed (both kernels)
+  unsigned int *light_live;  // lockstep CTAs running (NULL: solo warps wait for `done`)
   unsigned long long *task_ctr;  // solo kernel: next dynamic source task
   uint32_t *hws;             // [solo slots = solo CTAs x warps][hws_words] per-source workspaces
   size_t hws_words;

@@ -344,6 +344,9 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
   __shared__ int s_nL[32];
   __shared__ int s_ok, s_abort;
   Counters c = {0, 0, 0, 0, 0, 0, 0, 0u};
+  // live lockstep CTAs: while any runs, it may still abandon a group to the
+  // solo kernel's queue (idle solo warps wait only as long as that can happen)
+  if (tid == 0 && p.light_live) atomicAdd(p.light_live, 1u);
 
   for (;;) {
     if (tid == 0) {
@@ -528,6 +531,10 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
     atomicAdd(p.stats + 3, c.steps);
   }
   if (p.n < 0) p.stats[7] = c.sink;  // never true; keeps the returning atomics
+  if (tid == 0 && p.light_live) {
+    __threadfence();  // this CTA's queue pushes are visible before it leaves
+    atomicSub(p.light_live, 1u);
+  }
 }
 
 // ---------------------------------------------------------------- solo kernel
@@ -1277,7 +1284,16 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
           }
         }
         if (*(volatile unsigned *)p.done >= (unsigned)rows) break;
-        __nanosleep(1000);
+        // no lockstep CTA left to abandon a group and every fresh group
+        // claimed: entry e can no longer appear, so this warp is done (idle
+        // polling took ~40% of issue slots in chain-bound tails, ncu)
+        if (p.light_live && *(volatile unsigned *)p.light_live == 0u &&
+            *(volatile unsigned *)p.group_ctr >= (unsigned)nfresh) {
+          __threadfence();
+          if (e >= *(volatile unsigned *)p.hq_tail) break;
+          continue;
+        }
+        __nanosleep(2000);
       }
     }
     g = __shfl_sync(kFull, g, 0);
