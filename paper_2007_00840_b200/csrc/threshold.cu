@@ -704,7 +704,8 @@ struct SoloStep {
 template <bool kPF>
 __device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot &sl,
                                           SoloWarpSmem &sw, SoloPF *pf, SoloQueue &Q, bool push,
-                                          int wk, int rb, int re, int lane) {
+                                          int wk, int rb, int re, int lane, uint32_t *ring,
+                                          int rmask) {
   const uint32_t pb = __ballot_sync(kFull, push);
   if (!pb) return;
   const int pos = Q.st + __popc(pb & lanemask_lt());
@@ -729,9 +730,9 @@ __device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot 
   const uint32_t gb = pb & ~sb;
   if (gb) {
     const int gpos = Q.gt + __popc(gb & lanemask_lt());
-    const bool in_g = gpos - Q.gh <= SL_QMASK;
+    const bool in_g = gpos - Q.gh <= rmask;
     if (push && !in_s) {
-      if (in_g) SL_QUEUE[gpos & SL_QMASK] = (uint32_t)wk;
+      if (in_g) ring[gpos & rmask] = (uint32_t)wk;
       else atomicOr(SL_PEND + (wk >> 5), vbit(wk));  // RED
     }
     Q.gt += __popc(__ballot_sync(kFull, push && !in_s && in_g));
@@ -747,7 +748,8 @@ template <bool kH, int kB>
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
                                             SoloWarpSmem &sw, SoloPF *pf, int wb, SoloQueue &Q,
                                             int s, const SoloStep &t, int u, int beg, int end,
-                                            int us, int lane) {
+                                            int us, int lane, uint32_t *win, uint32_t *ring,
+                                            int rmask) {
   constexpr bool kPF = kB > 1 && kAdjPrefetch;  // us: this lane's prefetch slot (-1: none)
   const int deg = u >= 0 ? end - beg : 0;
   // fast path (every threshold's level 0, most closure levels of a chain):
@@ -855,7 +857,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
           const int q = kH ? qw[k] : wk;  // its bitmap position
           const int d = (q >> 5) - wb;
           if (d < 32) {
-            atomicOr(&sw.win[d], vbit(q));  // smem (d >= 0: after the step's thresholds)
+            atomicOr(&win[d], vbit(q));  // smem (d >= 0: after the step's thresholds)
           } else {
             atomicOr(SL_THR + (q >> 5), vbit(q));  // RED
             red_sum(SL_TSUM, q);
@@ -864,7 +866,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
           push = true;  // maxId(w) = T, not in the structure: continue with T
         }
       }
-      solo_push<kPF>(p, sl, sw, pf, Q, push, wk, rb[k], re[k], lane);
+      solo_push<kPF>(p, sl, sw, pf, Q, push, wk, rb[k], re[k], lane, ring, rmask);
     }
   }
 }
@@ -920,7 +922,7 @@ __device__ __forceinline__ void solo_expand_ell(const StreamParams &p, const Sol
         push = true;  // maxId(w) = T, not in the structure: continue with T
       }
     }
-    solo_push<false>(p, sl, sw, nullptr, Q, push, w, -1, -1, lane);
+    solo_push<false>(p, sl, sw, nullptr, Q, push, w, -1, -1, lane, SL_QUEUE, SL_QMASK);
   }
   if (lane == 0) {
     sw.items += (uint32_t)nitems;
@@ -933,13 +935,13 @@ __device__ __forceinline__ void solo_expand_ell(const StreamParams &p, const Sol
 // only.  Past it: publish this warp's global threshold REDs, scan the global
 // bitmap (summary-guided) and load a new window at the found threshold.
 __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const uint32_t *tsum,
-                                                   int tbw, int T, int &wb, SoloWarpSmem &sw,
+                                                   int tbw, int T, int &wb, uint32_t *win,
                                                    int lane) {
   if (wb >= 0) {
     const int d0 = (T + 1) >> 5;  // first candidate word
     const int rel = d0 - wb;
     if (rel < 32) {
-      uint32_t x = lane >= rel ? sw.win[lane] : 0u;
+      uint32_t x = lane >= rel ? win[lane] : 0u;
       if (lane == rel) x &= kFull << ((T + 1) & 31);
       const uint32_t b = __ballot_sync(kFull, x != 0u);
       if (b) {
@@ -956,7 +958,7 @@ __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const ui
   if (t == INT_MAX) return INT_MAX;
   wb = t >> 5;
   __syncwarp();
-  sw.win[lane] = wb + lane < tbw ? __ldcg(thr + wb + lane) : 0u;
+  win[lane] = wb + lane < tbw ? __ldcg(thr + wb + lane) : 0u;
   __syncwarp();
   return t;
 }
@@ -992,7 +994,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
   int wb = -1;  // no window yet
   int P = -1;   // the last threshold (position) taken
   for (;;) {
-    P = solo_next_threshold(SL_THR, SL_TSUM, tbw, P, wb, sw, lane);
+    P = solo_next_threshold(SL_THR, SL_TSUM, tbw, P, wb, sw.win, lane);
     if (P == INT_MAX) break;
     if (lane == 0) sw.steps += 1;
     SoloQueue Q = {0, 0, 0, 0, false, 0};
@@ -1031,7 +1033,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
           ub = ok ? cb : 0;
           ue = ok ? ce : 0;
         } else {
-          solo_push<kPF>(p, sl, sw, pf, Q, has, v, vb, ve, lane);
+          solo_push<kPF>(p, sl, sw, pf, Q, has, v, vb, ve, lane, SL_QUEUE, SL_QMASK);
         }
       }
       t.tmin = __reduce_min_sync(kFull, tmin);
@@ -1055,7 +1057,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
     int us = -1;  // prefetch slot of this lane's item
     for (;;) {
       if (kE) solo_expand_ell(p, sl, sw, wb, Q, s, t.tmin, u, lane);
-      else solo_expand<kH, kB>(p, sl, sw, pf, wb, Q, s, t, u, ub, ue, us, lane);
+      else solo_expand<kH, kB>(p, sl, sw, pf, wb, Q, s, t, u, ub, ue, us, lane, sw.win, SL_QUEUE, SL_QMASK);
       __syncwarp();
       us = -1;
       if (kPF) Q.hold = 0;
@@ -1253,8 +1255,8 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
   __syncwarp();
   // first task: warp-major over the grid, so consecutive (heaviest) sources
   // start on different SMs; then the global task counter
-  long long t = (long long)warp * gridDim.x + blockIdx.x;
-  const long long t_static = (long long)kSoloWarps * gridDim.x;
+  long long t = (long long)warp * gridDim.x + blockIdx.x + p.task_base;
+  const long long t_static = (long long)kSoloWarps * gridDim.x + p.task_base;
   for (bool first = true;; first = false) {
     if (!first) {
       if (lane == 0) t = t_static + (long long)atomicAdd(p.task_ctr, 1ull);
@@ -1367,6 +1369,252 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
       sw.items = sw.pairs = sw.levels = sw.steps = sw.fv = 0u;
     }
     __syncwarp();
+  }
+}
+
+
+// ---------------------------------------------------------------- team kernel
+// Height order only (order.cu).  The heaviest sources of a hub pattern (C4's
+// hub rows, ordered last) are chains of at most tree-height steps whose steps
+// hold many same-height thresholds with DISJOINT closures.  A team of
+// kTeamWarps warps (one CTA, one source at a time, its own solo-layout slot)
+// deals every step's threshold words to its warps; each warp closes its
+// thresholds' closures with its own worklist (shared memory, a 1/kTeamWarps
+// share of the slot's ring, then the shared pend bitmap, reloaded by
+// claiming whole words); the CTA meets at a barrier before the next step.
+// Fills found inside the source's 32-word threshold window go to the CTA's
+// shared window, the others to the global threshold bitmap.  The team takes
+// the first team_tasks source tasks of the solo queue (the pre-enqueued top
+// groups); the solo kernel starts after them (task_base).
+constexpr int kTeamWarps = 16;
+
+struct TeamCtl {
+  uint32_t win[32];  // the source's threshold window (all warps)
+  int P, wb, lim, h, tmin, tmax;
+  long long task;
+};
+
+__device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlot &sl, int s,
+                                            int warp, int lane, SoloWarpSmem &sw, TeamCtl &ctl) {
+  const int tbw = (p.n + 31) >> 5;  // threshold positions over [0, n)
+  const int rshare = p.solo_ring / kTeamWarps;
+  uint32_t *ring = SL_QUEUE + (size_t)warp * rshare;
+  const int rmask = rshare - 1;
+  // seed: the warps share the neighbour list of s
+  const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
+  for (int j0 = beg + 32 * warp; j0 < end; j0 += 32 * kTeamWarps) {
+    const int j = j0 + lane;
+    const int w = j < end ? __ldg(p.colidx + j) : s;
+    if (w == s) continue;
+    const uint32_t bw = vbit(w);
+    if (atomicOr(SL_IS + (w >> 5), bw) == 0u) red_sum(SL_ISUM, w);
+    if (w < s) {
+      if (atomicOr(SL_REACHED + (w >> 5), bw) == 0u) red_sum(SL_RSUM, w);
+      const int q = __ldg(p.pos + w);
+      atomicOr(SL_THR + (q >> 5), vbit(q));  // RED
+      red_sum(SL_TSUM, q);
+    }
+  }
+  fence_gpu();
+  if (warp == 0 && lane == 0) {
+    ctl.P = -1;
+    ctl.wb = -1;
+  }
+  __syncthreads();
+  for (;;) {
+    if (warp == 0) {
+      // the next step: thresholds of height h = height(P) in the window,
+      // positions [P, min(seg_end(h), window end))
+      int wb = ctl.wb;
+      const int P = solo_next_threshold(SL_THR, SL_TSUM, tbw, ctl.P, wb, ctl.win, lane);
+      if (lane == 0) {
+        ctl.P = P;
+        ctl.wb = wb;
+        if (P != INT_MAX) {
+          const int4 r = __ldg(p.posrec + P);
+          ctl.lim = min(r.w, (wb + 32) << 5);
+          ctl.h = __ldg(p.hgt + r.x);
+          ctl.tmin = INT_MAX;
+          ctl.tmax = -1;
+          sw.steps += 1;
+        }
+      }
+    }
+    __syncthreads();
+    const int P = ctl.P;
+    if (P == INT_MAX) break;
+    const int wb = ctl.wb, lim = ctl.lim;
+    SoloQueue Q = {0, 0, 0, 0, false, 0};
+    int u = -1, ub = 0, ue = 0;
+    int tmin = INT_MAX, tmax = -1;
+    bool first = true;
+    for (int wi = (P >> 5) + warp; (wi << 5) < lim; wi += kTeamWarps) {
+      uint32_t x = ctl.win[wi - wb];
+      if (wi == (P >> 5)) x &= kFull << (P & 31);
+      if (lim - (wi << 5) < 32) x &= (1u << (lim - (wi << 5))) - 1u;
+      const bool has = (x >> lane) & 1u;
+      int v = -1, vb = 0, ve = 0;
+      if (has) {
+        const int4 r = __ldg(p.posrec + (wi << 5) + lane);
+        v = r.x;
+        vb = r.y;
+        ve = r.z;
+        tmin = min(tmin, v);
+        tmax = max(tmax, v);
+      }
+      if (first) {
+        // this warp's first word: its thresholds to the low lanes
+        const uint32_t b = __ballot_sync(kFull, has);
+        const int src = __fns(b, 0, lane + 1) & 31;
+        const int cu = __shfl_sync(kFull, v, src), cb = __shfl_sync(kFull, vb, src),
+                  ce = __shfl_sync(kFull, ve, src);
+        const bool ok = lane < __popc(b);
+        u = ok ? cu : -1;
+        ub = ok ? cb : 0;
+        ue = ok ? ce : 0;
+        first = false;
+      } else {
+        solo_push<false>(p, sl, sw, nullptr, Q, has, v, vb, ve, lane, ring, rmask);
+      }
+    }
+    tmin = __reduce_min_sync(kFull, tmin);
+    tmax = __reduce_max_sync(kFull, tmax);
+    if (lane == 0 && tmax >= 0) {
+      atomicMin(&ctl.tmin, tmin);
+      atomicMax(&ctl.tmax, tmax);
+    }
+    __syncthreads();
+    SoloStep t;
+    t.tmin = ctl.tmin;
+    t.tmax = ctl.tmax;
+    t.h = ctl.h;
+    const int pushed0 = Q.st + Q.gt;
+    for (;;) {
+      solo_expand<true, 1>(p, sl, sw, nullptr, wb, Q, s, t, u, ub, ue, -1, lane, ctl.win, ring, rmask);
+      __syncwarp();
+      if (Q.sh < Q.st) {
+        const int cnt = min(32, Q.st - Q.sh);
+        u = -1;
+        if (lane < cnt) {
+          const int i = (Q.sh + lane) & (kSoloQ - 1);
+          u = sw.qw[i];
+          ub = sw.qb[i];
+          ue = sw.qe[i];
+        }
+        Q.sh += cnt;
+        __syncwarp();
+        continue;
+      }
+      if (Q.gh >= Q.gt && Q.spilled) {
+        // parked closure items (pend bits, all below tmax, any warp's): claim
+        // whole words and move their items into this warp's ring
+        Q.spilled = false;
+        __syncwarp();
+        fence_gpu();
+        const int pwords = (t.tmax + 31) >> 5;
+        for (int w0 = 0; w0 < pwords && !Q.spilled; w0 += 32) {
+          const int wi = w0 + lane;
+          uint32_t x = 0u;
+          if (wi < pwords && __ldcg(SL_PEND + wi)) x = atomicExch(SL_PEND + wi, 0u);
+          for (;;) {
+            const bool has = x != 0u;
+            const uint32_t hb = __ballot_sync(kFull, has);
+            if (!hb) break;
+            const int pos = Q.gt + __popc(hb & lanemask_lt());
+            const bool fits = pos - Q.gh <= rmask;
+            if (has && fits) {
+              const int b = __ffs(x) - 1;
+              x &= x - 1u;
+              ring[pos & rmask] = (uint32_t)((wi << 5) + b);
+            }
+            Q.gt += __popc(__ballot_sync(kFull, has && fits));
+            if (__ballot_sync(kFull, has && !fits)) {
+              if (x) atomicOr(SL_PEND + wi, x);  // back to pend; rescan later
+              Q.spilled = true;
+              break;
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (Q.gh >= Q.gt) {
+        if (lane == 0) sw.fv += (uint32_t)(Q.st + Q.gt - pushed0);
+        break;
+      }
+      const int cnt = min(32, Q.gt - Q.gh);
+      u = lane < cnt ? (int)ring[(Q.gh + lane) & rmask] : -1;
+      Q.gh += cnt;
+      if (u >= 0) {
+        ub = __ldg(p.rowptr + u);
+        ue = __ldg(p.rowptr + u + 1);
+      }
+    }
+    fence_gpu();  // this warp's REDs (fills, thresholds) before the next step's scan
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kTeamWarps * 32, 1) team_kernel(StreamParams p) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ SoloWarpSmem s_sw[kTeamWarps];
+  __shared__ TeamCtl ctl;
+  SoloWarpSmem &sw = s_sw[warp];
+  const SoloSlot sl = SoloSlot{p.team_ws + (size_t)blockIdx.x * p.hws_words};
+  const int Vs = (int)(p.so_tsum - p.so_rsum), Ts = (int)(p.so_is - p.so_tsum);
+  if (lane == 0) sw.items = sw.pairs = sw.levels = sw.steps = sw.fv = 0u;
+  for (;;) {
+    if (threadIdx.x == 0) ctl.task = (long long)atomicAdd(p.team_ctr, 1u);
+    __syncthreads();
+    const long long k = ctl.task;
+    if (k >= p.team_tasks) break;
+    const int g = *(volatile int *)(p.hq + (k >> 5));  // pre-enqueued before the launch
+    const int r = 32 * g + (int)(k & 31);
+    if (r < p.nrows) {
+      const int s = p.map.row(r);
+      team_source(p, sl, s, warp, lane, sw, ctl);
+      fence_gpu();
+      __syncthreads();
+      if (warp == 0) solo_stage_row(p, sl, s, r, g, lane, sw);
+      __syncthreads();
+      // reset the touched reached | pend words and (height order) the global
+      // threshold words, split over the warps
+      for (int i0 = 32 * warp; i0 < Vs; i0 += 32 * kTeamWarps) {
+        const int i = i0 + lane;
+        uint32_t x = i < Vs ? __ldcg(SL_RSUM + i) : 0u;
+        if (x) SL_RSUM[i] = 0u;
+        while (x) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1u;
+          const int wi = (i << 5) + b;
+          SL_REACHED[wi] = 0u;
+          SL_PEND[wi] = 0u;
+        }
+      }
+      for (int i0 = 32 * warp; i0 < Ts; i0 += 32 * kTeamWarps) {
+        const int i = i0 + lane;
+        uint32_t x = i < Ts ? __ldcg(SL_TSUM + i) : 0u;
+        if (x) SL_TSUM[i] = 0u;
+        while (x) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1u;
+          SL_THR[(i << 5) + b] = 0u;
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      if (lane == 0) {
+        atomicAdd(p.stats + 0, (unsigned long long)sw.items);
+        atomicAdd(p.stats + 1, (unsigned long long)sw.pairs);
+        atomicAdd(p.stats + 4, (unsigned long long)sw.pairs);
+        atomicAdd(p.stats + 2, (unsigned long long)sw.levels);
+        atomicAdd(p.stats + 3, (unsigned long long)sw.steps);
+        atomicAdd(p.stats + 8, (unsigned long long)sw.fv);
+        atomicAdd(p.stats + 9, (unsigned long long)sw.items);
+        sw.items = sw.pairs = sw.levels = sw.steps = sw.fv = 0u;
+      }
+      if (threadIdx.x == 0) atomicAdd(p.done, 1u);
+    }
+    __syncthreads();
   }
 }
 
@@ -1530,6 +1778,12 @@ cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st) {
     else if (p.ell) solo_kernel<false, 1, true><<<grid, kSoloWarps * 32, 0, st>>>(p);
     else solo_kernel<false, 1><<<grid, kSoloWarps * 32, 0, st>>>(p);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_team(const StreamParams &p, int grid, cudaStream_t st) {
+  if (grid <= 0 || p.team_tasks <= 0) return cudaSuccess;
+  team_kernel<<<grid, kTeamWarps * 32, 0, st>>>(p);
   return cudaGetLastError();
 }
 
