@@ -9,6 +9,7 @@ import csv
 import io
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -63,7 +64,7 @@ def main():
     lines = []
     for rep in sys.argv[4:]:
         for d in raw(rep):
-            name = d["Kernel Name"][0].split("(")[0].split("::")[-1]
+            name = re.sub(r"<[^<>]*>$", "", d["Kernel Name"][0].split("(")[0]).split("::")[-1]
             b = val(d, "dram__bytes_read.sum") + val(d, "dram__bytes_write.sum")
             t = val(d, "gpu__time_duration.sum")
             ent["kernels"][name] = {"dram_bytes": b, "duration_s": t}
