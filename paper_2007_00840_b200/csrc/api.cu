@@ -1473,12 +1473,18 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
         sp.team_tasks = 0;
         sp.task_base = 0;
         if (sp.hmode && sp.solo_top > 0 && sp.solo_ring >= 64) {
-          int64_t trows = 3 * (int64_t)c->sms;
+          // dev A/B (GSOFA_TEAM_ROWS): measured slower on C4 (0.42 s ->
+          // 0.83 s with 448 team rows: a hub source's steps are too narrow
+          // for 16 warps, so a team runs one source about as fast as one
+          // warp while the solo kernel runs all of them at once;
+          // profiles/r2/team_ab.txt) -- off by default
+          int64_t trows = 0;
           if (const char *e = std::getenv("GSOFA_TEAM_ROWS")) trows = atoll(e);
           const int64_t tg = std::min<int64_t>(sp.solo_top, ceil_div(std::max<int64_t>(trows, 0), 32));
           if (tg > 0) {
-            const size_t words = (size_t)c->sms * plan.hws_words;
-            const uint64_t sig = ((uint64_t)plan.hws_words << 20) ^ (uint64_t)plan.Vmax;
+            const size_t words = (size_t)c->sms * gsofa::team_slot_words(sp);
+            const uint64_t sig = ((uint64_t)plan.hws_words << 20) ^ (uint64_t)plan.Vmax ^
+                                 ((uint64_t)sp.solo_ring << 44);
             if (c->team_words < words) {
               if (c->team_ws) cudaFree(c->team_ws);
               c->team_ws = nullptr;

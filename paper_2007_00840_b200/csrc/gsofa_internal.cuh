@@ -269,6 +269,7 @@ cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, c
 // ELL copy of the adjacency for the solo kernel's id order (rows <= 8
 // entries): ell[8 v + j] = j-th neighbour of v, -1 padded
 cudaError_t launch_team(const StreamParams &p, int grid, cudaStream_t st);
+size_t team_slot_words(const StreamParams &p);  // words per team slot
 cudaError_t launch_ell_build(const int32_t *rowptr, const int32_t *colidx, int32_t n, int32_t *ell,
                              cudaStream_t st);
 

@@ -1379,13 +1379,18 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
 // hold many same-height thresholds with DISJOINT closures.  A team of
 // kTeamWarps warps (one CTA, one source at a time, its own solo-layout slot)
 // deals every step's threshold words to its warps; each warp closes its
-// thresholds' closures with its own worklist (shared memory, a 1/kTeamWarps
-// share of the slot's ring, then the shared pend bitmap, reloaded by
+// thresholds' closures with its own worklist (shared memory, then its own
+// ring of solo_ring entries past the slot's solo layout -- a 1/kTeamWarps
+// share of one ring overflowed constantly on hub closures and every overflow
+// rescans pend, 9x slower on C4 -- then the shared pend bitmap, reloaded by
 // claiming whole words); the CTA meets at a barrier before the next step.
 // Fills found inside the source's 32-word threshold window go to the CTA's
 // shared window, the others to the global threshold bitmap.  The team takes
 // the first team_tasks source tasks of the solo queue (the pre-enqueued top
 // groups); the solo kernel starts after them (task_base).
+// Measured slower than the solo kernel on C4's hub rows (0.42 -> 0.83 s at
+// 448 team rows; profiles/r2/team_ab.txt): their height steps are too narrow
+// to occupy 16 warps.  Off by default (GSOFA_TEAM_ROWS enables it).
 constexpr int kTeamWarps = 16;
 
 struct TeamCtl {
@@ -1397,9 +1402,8 @@ struct TeamCtl {
 __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlot &sl, int s,
                                             int warp, int lane, SoloWarpSmem &sw, TeamCtl &ctl) {
   const int tbw = (p.n + 31) >> 5;  // threshold positions over [0, n)
-  const int rshare = p.solo_ring / kTeamWarps;
-  uint32_t *ring = SL_QUEUE + (size_t)warp * rshare;
-  const int rmask = rshare - 1;
+  uint32_t *ring = sl.base + p.hws_words + (size_t)warp * p.solo_ring;
+  const int rmask = p.solo_ring - 1;
   // seed: the warps share the neighbour list of s
   const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
   for (int j0 = beg + 32 * warp; j0 < end; j0 += 32 * kTeamWarps) {
@@ -1426,7 +1430,9 @@ __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlo
       // the next step: thresholds of height h = height(P) in the window,
       // positions [P, min(seg_end(h), window end))
       int wb = ctl.wb;
-      const int P = solo_next_threshold(SL_THR, SL_TSUM, tbw, ctl.P, wb, ctl.win, lane);
+      // the search starts after the previous step's positions
+      const int T0 = ctl.P < 0 ? -1 : ctl.lim - 1;
+      const int P = solo_next_threshold(SL_THR, SL_TSUM, tbw, T0, wb, ctl.win, lane);
       if (lane == 0) {
         ctl.P = P;
         ctl.wb = wb;
@@ -1559,7 +1565,8 @@ __global__ void __launch_bounds__(kTeamWarps * 32, 1) team_kernel(StreamParams p
   __shared__ SoloWarpSmem s_sw[kTeamWarps];
   __shared__ TeamCtl ctl;
   SoloWarpSmem &sw = s_sw[warp];
-  const SoloSlot sl = SoloSlot{p.team_ws + (size_t)blockIdx.x * p.hws_words};
+  // team slot: the solo layout, then kTeamWarps rings of solo_ring entries
+  const SoloSlot sl = SoloSlot{p.team_ws + (size_t)blockIdx.x * (p.hws_words + (size_t)kTeamWarps * p.solo_ring)};
   const int Vs = (int)(p.so_tsum - p.so_rsum), Ts = (int)(p.so_is - p.so_tsum);
   if (lane == 0) sw.items = sw.pairs = sw.levels = sw.steps = sw.fv = 0u;
   for (;;) {
@@ -1779,6 +1786,10 @@ cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st) {
     else solo_kernel<false, 1><<<grid, kSoloWarps * 32, 0, st>>>(p);
   }
   return cudaGetLastError();
+}
+
+size_t team_slot_words(const StreamParams &p) {
+  return p.hws_words + (size_t)kTeamWarps * p.solo_ring;
 }
 
 cudaError_t launch_team(const StreamParams &p, int grid, cudaStream_t st) {

@@ -825,7 +825,7 @@ def test_solo_ell_path(case, ell, monkeypatch):
 @pytest.mark.parametrize("rows", ["0", "32", "448", "100000"])
 @pytest.mark.parametrize("case", ["C4_70", "C5_16", "C2_20", "rand"])
 def test_team_kernel(case, rows, monkeypatch):
-    """Height order: the heaviest pre-enqueued groups run on the team kernel
+    """Height order, dev path (off by default): the heaviest pre-enqueued groups run on the team kernel
     (one source per 16-warp CTA, step thresholds dealt to the warps) -- none,
     one group, the default share, or every pre-enqueued group; the result
     equals the oracle."""
