@@ -244,3 +244,59 @@ def assemble_interleaved(parts, row_begin: int, row_end: int, unit_rows: int, n:
             Ui[Up[s]:Up[s + 1]] = a["U_colidx"][a["U_rowptr"][k]:a["U_rowptr"][k + 1]]
     sn = np.sort(np.concatenate([a["sn_start"][:-1] for a in parts] + [np.array([row_end])]))
     return dict(L_rowptr=Lp, L_colidx=Li, U_rowptr=Up, U_colidx=Ui, sn_start=sn.astype(np.int32))
+
+
+# ---------------------------------------------------- dynamic block stealing
+# SURVEY §8(f) NEXT-2, the third variant: instead of a fixed assignment, the
+# ranks claim chunk-aligned row blocks (equal estimated work, heaviest --
+# highest rows -- first) from one shared atomic counter until none is left.
+# Blocks start at multiples of chunk_size, so their supernodes are complete
+# and nothing is stitched; one all_gather of per-block counts gives
+# every rank the global CSR offsets.  The counter here is the process group's
+# store (an atomic add over TCP); a device-side counter in one GPU's memory
+# mapped by its peers (CUDA IPC over NVLink) would make a claim ~10 us instead
+# of ~50-100 us -- at a few dozen claims per call either is noise.
+
+def steal_blocks(rowptr, colidx, nblocks: int, chunk_size: int = 128, partition_fn=None):
+    """Chunk-aligned blocks of equal estimated work, in claim order
+    (descending rows): list of (row_begin, row_end)."""
+    b = partition(rowptr, colidx, nblocks, align=chunk_size, partition_fn=partition_fn)
+    blocks = [(int(b[i]), int(b[i + 1])) for i in range(len(b) - 1) if b[i + 1] > b[i]]
+    return blocks[::-1]
+
+
+def symbolic_stealing(rowptr, colidx, *, rank: int, blocks_per_rank: int = 4, chunk_size: int = 128,
+                      compute_fn=None, store=None, key: str = "gsofa_steal", group=None, device=None,
+                      **kw):
+    """Claim blocks from the shared counter until they run out; returns
+    (list of (block index, row_begin, row_end, result), counts [nblocks, 6]
+    gathered from all ranks: each block's counts come from the rank that
+    computed it)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if compute_fn is None:
+        from . import symbolic as compute_fn
+    if store is None:
+        from torch.distributed import distributed_c10d as c10d
+        store = c10d._get_default_store()
+    blocks = steal_blocks(rowptr, colidx, world * blocks_per_rank, chunk_size)
+    dist.barrier(group=group)
+    mine = []
+    local = np.zeros((len(blocks), len(COUNT_FIELDS)), np.int64)
+    while True:
+        k = int(store.add(key, 1)) - 1  # atomic fetch-and-add: this rank's next block
+        if k >= len(blocks):
+            break
+        rb, re = blocks[k]
+        res = compute_fn(rowptr, colidx, row_begin=rb, row_end=re, chunk_size=chunk_size, **kw)
+        local[k] = [res.nnz_L, res.nnz_U, res.fill_count, res.nsuper, res.nnz_A_offdiag, re - rb]
+        mine.append((k, rb, re, res))
+    # every block was computed by exactly one rank: the element-wise sum over
+    # ranks is the full table
+    counts = allgather_counts(local.ravel(), group=group, device=device)
+    counts = counts.reshape(world, len(blocks), len(COUNT_FIELDS)).sum(axis=0)
+    dist.barrier(group=group)
+    if rank == 0:
+        store.add(key, -int(store.add(key, 0)))  # reset for the next call
+    dist.barrier(group=group)
+    return mine, counts, blocks

@@ -10,6 +10,12 @@ contiguous work-balanced ranges; for units finer than chunk_size each part's
 time includes its gsofa_result_rowinfo and gsofa_supernodes_gathered calls
 (the NCCL all_gather between them is not in the emulation).
 
+With --mode steal the rows are cut into chunk-aligned blocks of equal
+estimated work (--blocks-per-rank per rank) claimed heaviest first from a
+shared counter (dist.symbolic_stealing): every block is timed alone on a warm
+context and the claims are replayed as list scheduling (the next block goes to
+the rank that frees up first); the N-GPU time is the last rank's finish.
+
 usage: python scripts/scaling_emulation.py --config C5 --gpus 2 4 8 [--reps 2]
        python scripts/scaling_emulation.py --config C5 --mode interleave --unit 128
 """
@@ -29,7 +35,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C5")
 ap.add_argument("--gpus", type=int, nargs="+", default=[2, 4, 8])
 ap.add_argument("--reps", type=int, default=2)
-ap.add_argument("--mode", default="ranges", choices=["ranges", "interleave"])
+ap.add_argument("--mode", default="ranges", choices=["ranges", "interleave", "steal"])
+ap.add_argument("--blocks-per-rank", type=int, default=4)
 ap.add_argument("--unit", type=int, default=128)
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
@@ -73,6 +80,33 @@ print(f"{a.config}: 1 GPU {full_ms:.1f} ms, fill {full_fill}", flush=True)
 report = {"config": a.config, "n": n, "one_gpu_ms": full_ms, "fill": full_fill, "mode": a.mode,
           "unit": a.unit if a.mode == "interleave" else None, "runs": []}
 for N in a.gpus:
+    if a.mode == "steal":
+        blocks = gd.steal_blocks(rp, ci, N * a.blocks_per_rank, 128)
+        ctx = g.Context(0)
+        bt = []
+        fills = 0
+        for rb, re in blocks:
+            best = None
+            for _ in range(a.reps):
+                r = g.symbolic(rp, ci, ctx=ctx, row_begin=rb, row_end=re, outputs_on_device=True)
+                best = r.stats["ms_total"] if best is None else min(best, r.stats["ms_total"])
+                f = r.fill_count
+                r.free()
+            bt.append(best)
+            fills += f
+        ctx.close()
+        assert fills == full_fill
+        free = [0.0] * N
+        for t in bt:  # claim order = heaviest first; the first free rank claims
+            i = min(range(N), key=lambda j: free[j])
+            free[i] += t
+        mx = max(free)
+        print(f"  N={N}: {len(blocks)} blocks, block ms {[round(x, 1) for x in bt]}\n"
+              f"        rank finish ms {[round(x, 1) for x in free]} -> max {mx:.1f} ms, "
+              f"speedup {full_ms / mx:.2f}x", flush=True)
+        report["runs"].append({"gpus": N, "blocks": blocks, "block_ms": bt, "rank_ms": free,
+                               "max_ms": mx, "speedup": full_ms / mx})
+        continue
     bounds = gd.partition(rp, ci, N) if a.mode == "ranges" else np.array([0, n])
     per = []
     fills = 0

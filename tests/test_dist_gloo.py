@@ -282,3 +282,60 @@ def test_interleave_host_logic_gloo(world, name, scale, chunk, U):
     asm = gd.assemble_interleaved([o[2] for o in outs], 0, n, U, n)
     for k in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start"):
         assert np.array_equal(asm[k], full[k]), k
+
+
+# ---------------------------------------------------- dynamic block stealing
+
+def _steal_worker(rank, world, port, name, scale, chunk, q):
+    import torch.distributed as dist
+
+    from paper_2007_00840_b200 import dist as gd
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rp, ci = gen.config(name, scale)
+
+        def compute(rowptr, colidx, row_begin, row_end, chunk_size):
+            return _oracle_compute(rowptr, colidx, row_begin, row_end, chunk_size)
+        import paper_2007_00840_b200 as g
+        for rep in range(2):  # the counter is reset between calls
+            mine, counts, blocks = gd.symbolic_stealing(rp, ci, rank=rank, chunk_size=chunk,
+                                                        compute_fn=compute)
+        q.put((rank, [(k, rb, re, r.arrays) for k, rb, re, r in mine], counts.tolist(), blocks))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,name,scale,chunk", [(2, "C2", 10, 16), (3, "C4", 40, 64), (2, "C3", 1500, 128)])
+def test_stealing_host_logic_gloo(world, name, scale, chunk):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_steal_worker, args=(r, world, port, name, scale, chunk, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rp, ci = gen.config(name, scale)
+    n = rp.size - 1
+    full = oracle.symbolic(rp, ci, chunk_size=chunk)
+    blocks = outs[0][3]
+    assert all(o[3] == blocks for o in outs)
+    assert all(rb % chunk == 0 for rb, _ in blocks) and sorted(blocks)[0][0] == 0
+    got = {}
+    for o in outs:
+        for k, rb, re, arr in o[1]:
+            assert k not in got  # claimed exactly once
+            got[k] = (rb, re, arr)
+    assert sorted(got) == list(range(len(blocks)))
+    counts = np.array(outs[0][2])
+    assert counts[:, 2].sum() == full["fill_count"] and counts[:, 3].sum() == full["nsuper"]
+    from paper_2007_00840_b200 import dist as gd
+    parts = [got[k][2] for k in sorted(got, key=lambda k: got[k][0])]
+    asm = gd.assemble(parts, n)
+    for key in ("L_rowptr", "L_colidx", "U_rowptr", "U_colidx", "sn_start"):
+        assert np.array_equal(asm[key], full[key]), key
