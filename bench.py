@@ -230,9 +230,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--layout", default="ranges", choices=["ranges", "interleave"],
-                    help="N > 1: contiguous work-balanced ranges (default) or round-robin "
-                         "units of --unit rows (SURVEY §8(f) NEXT-2)")
+    ap.add_argument("--layout", default="ranges", choices=["ranges", "interleave", "steal"],
+                    help="N > 1: contiguous work-balanced ranges (default), round-robin "
+                         "units of --unit rows, or chunk-aligned blocks claimed from a shared "
+                         "counter (SURVEY §8(f) NEXT-2)")
     ap.add_argument("--unit", type=int, default=128)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -292,7 +293,15 @@ def main():
         kw = dict(ctx=ctx, chunk_size=chunk, schedule=args.schedule,
                   max_concurrent=args.max_concurrent, stream=stream)
         src = (h_rp, h_ci) if host else (d_rp, d_ci)
-        if world > 1 and args.layout == "interleave":
+        if world > 1 and args.layout == "steal":
+            kw2 = {k: v for k, v in kw.items() if k != "chunk_size"}
+            mine, counts, _ = gd.symbolic_stealing(*src, rank=rank, chunk_size=chunk, device=coll_dev,
+                                                   outputs_on_device=not host, **kw2)
+            fills = int(counts[:, 2].sum())
+            for _, _, _, r_ in mine[1:]:
+                r_.free()
+            res = mine[0][3] if mine else None  # (the step's first block stands for the stats)
+        elif world > 1 and args.layout == "interleave":
             # this rank's units, per-row Def. T3 all_gather if finer than a chunk
             kw2 = {k: v for k, v in kw.items() if k != "chunk_size"}
             res, counts = gd.symbolic_interleaved(*src, rank=rank, unit_rows=args.unit, chunk_size=chunk,
@@ -450,8 +459,9 @@ def main():
                           "per_rank_ms": per_rank_ms,
                           "fill_ins": fills_step, "schedule": sched_used,
                           "parallelism": (f"rows split over {world} GPU(s)"
-                                          + (f", interleaved units of {args.unit}" if args.layout == "interleave"
-                                             else ", work-balanced ranges")) if world > 1 else "1 GPU",
+                                          + {"interleave": f", interleaved units of {args.unit}",
+                                             "steal": ", blocks claimed from a shared counter"}.get(
+                                              args.layout, ", work-balanced ranges")) if world > 1 else "1 GPU",
                           "l2": "flushed between timed steps (256 MiB write, untimed)"},
                "e2e": {"value": fills_step / (e2e_step / 1e3), "unit": UNIT,
                        "ms_per_step": e2e_step, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
