@@ -427,6 +427,12 @@ def main():
                      "dram_frac": gbs / peak}
         roofline["traffic"] = tot_b  # dram read + write of the traversal kernels, per launch
         roofline["ncu"] = {"kernels": nk, "source": ksrc}
+        # what HBM actually does during the traversal (north_star: "achieved
+        # HBM GB/s from ncu"): the kernels' DRAM bytes over their ncu time
+        dur = sum(v["ncu_ms"] for v in nk.values()) / 1e3
+        if dur > 0:
+            roofline["ncu_dram_gbs"] = tot_b / dur / 1e9
+            roofline["ncu_dram_frac"] = roofline["ncu_dram_gbs"] / peak
         roofline["limiter"] = ("latency of dependent L2 atomics (ncu: long-scoreboard stalls "
                                "dominate, DRAM well below peak; see roofline.ncu)")
     # the unit operation of the traversal is a random 4-byte atomic (one per
