@@ -621,6 +621,15 @@ __device__ __forceinline__ int solo_scan_next(const uint32_t *thr, const uint32_
 //   q*[kSoloQ] closure worklist: (w, rowptr[w], rowptr[w+1]); the row
 //             pointers were loaded together with the atomic that reached w.
 //             Overflow goes to the global ring (vertex only), then to pend.
+// Reached-word cache (kC): a per-warp direct-mapped shared-memory table of
+// reached-bitmap words known for the current source: {word index + 1, bits
+// known set}.  Bits only get set during a source (the table is cleared when
+// the next one starts), so a hit proves w was reached and its atomic can be
+// skipped -- 78% of the (item, neighbour) atomics of C5 find w already
+// reached (first visits 7.7e10 of 3.4e11 pairs).  Measured slower (C5 +7%,
+// C2 +18%; profiles/r2/reached_cache_ab.txt): dev A/B only (GSOFA_RCACHE=1).
+constexpr int kRC = 128;
+
 struct SoloWarpSmem {
   uint32_t win[32];
   int qw[kSoloQ], qb[kSoloQ], qe[kSoloQ];
@@ -744,12 +753,12 @@ __device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot 
 // of the current step t of source s.  Thresholds are kept at their bitmap
 // position: the vertex id (id order) or pos(w) (height order, loaded for
 // each new fill).
-template <bool kH, int kB>
+template <bool kH, int kB, bool kC = false>
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
                                             SoloWarpSmem &sw, SoloPF *pf, int wb, SoloQueue &Q,
                                             int s, const SoloStep &t, int u, int beg, int end,
                                             int us, int lane, uint32_t *win, uint32_t *ring,
-                                            int rmask) {
+                                            int rmask, uint2 *rc = nullptr) {
   constexpr bool kPF = kB > 1 && kAdjPrefetch;  // us: this lane's prefetch slot (-1: none)
   const int deg = u >= 0 ? end - beg : 0;
   // fast path (every threshold's level 0, most closure levels of a chain):
@@ -824,7 +833,12 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       const uint32_t bw = vbit(w[k]);
       // w > s: entry of U; w < s: atomicMin(maxId(w), T) succeeds
       // iff the source has not reached w yet (line 10 of fig:alg)
-      ro[k] = w[k] < s ? atomicOr(SL_REACHED + (w[k] >> 5), bw) : bw;
+      bool known = false;
+      if (kC && w[k] < s) {
+        const uint2 e = rc[(w[k] >> 5) & (kRC - 1)];
+        known = e.x == (uint32_t)(w[k] >> 5) + 1u && (e.y & bw);
+      }
+      ro[k] = w[k] < s && !known ? atomicOr(SL_REACHED + (w[k] >> 5), bw) : bw;
       if (w[k] > s) {
         // U entry: nothing waits for it -- two REDs (the summary bit is idempotent)
         atomicOr(SL_IS + (w[k] >> 5), bw);
@@ -847,6 +861,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
       if (k >= nb) continue;
       const int wk = w[k];
       const uint32_t bw = vbit(wk);
+      if (kC && wk < s) rc[(wk >> 5) & (kRC - 1)] = make_uint2((uint32_t)(wk >> 5) + 1u, ro[k] | bw);
       bool push = false;
       if (!(ro[k] & bw)) {
         if (ro[k] == 0u) red_sum(SL_RSUM, wk);
@@ -968,9 +983,15 @@ __device__ __forceinline__ int solo_next_threshold(const uint32_t *thr, const ui
 // position (vertices sorted by (height, id)) and a step takes every threshold
 // of one height within the 32-word window (order.cu); the graph, reached and
 // structure bitmaps stay in vertex ids (the ND order's locality)
-template <bool kH, int kB, bool kE = false>
+template <bool kH, int kB, bool kE = false, bool kC = false>
 __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlot &sl, int s,
-                                            int lane, SoloWarpSmem &sw, SoloPF *pf) {
+                                            int lane, SoloWarpSmem &sw, SoloPF *pf,
+                                            uint2 *rc = nullptr) {
+  if (kC) {
+    // a new source: nothing is known reached yet
+    for (int i = lane; i < kRC; i += 32) rc[i] = make_uint2(0u, 0u);
+    __syncwarp();
+  }
   constexpr bool kPF = kB > 1 && kAdjPrefetch;
   // threshold positions: below s (id order), anywhere in [0, n) (height order)
   const int tbw = kH ? (p.n + 31) >> 5 : (s + 31) >> 5;
@@ -1057,7 +1078,7 @@ __device__ __forceinline__ void solo_source(const StreamParams &p, const SoloSlo
     int us = -1;  // prefetch slot of this lane's item
     for (;;) {
       if (kE) solo_expand_ell(p, sl, sw, wb, Q, s, t.tmin, u, lane);
-      else solo_expand<kH, kB>(p, sl, sw, pf, wb, Q, s, t, u, ub, ue, us, lane, sw.win, SL_QUEUE, SL_QMASK);
+      else solo_expand<kH, kB, kC>(p, sl, sw, pf, wb, Q, s, t, u, ub, ue, us, lane, sw.win, SL_QUEUE, SL_QMASK, rc);
       __syncwarp();
       us = -1;
       if (kPF) Q.hold = 0;
@@ -1233,7 +1254,7 @@ __device__ __forceinline__ bool solo_stage_row(const StreamParams &p, const Solo
 // outnumber warps; kB = 4 ("wide"): 32 warps per SM, a level's first 128
 // pairs in flight at once -- the latency shape for chain-bound sources (few
 // heavy sources: C4's hub rows, the top-separator ranges of a multi-GPU split)
-template <bool kH, int kB, bool kE = false>
+template <bool kH, int kB, bool kE = false, bool kC = false>
 __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 32 / kSoloWarps)
     solo_kernel(StreamParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1243,6 +1264,8 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
   const int Vs = (int)(p.so_tsum - p.so_rsum);  // reached-word summary words
   __shared__ SoloWarpSmem s_sw[kSoloWarps];
   SoloWarpSmem &sw = s_sw[warp];
+  __shared__ uint2 s_rc[kC ? kSoloWarps * kRC : 1];  // reached-word caches (kC)
+  uint2 *rc = kC ? s_rc + warp * kRC : nullptr;
   extern __shared__ __align__(128) unsigned char s_dyn[];  // latency shape: SoloPF per warp
   SoloPF *pf = nullptr;
   if (kB > 1 && kAdjPrefetch) {
@@ -1309,7 +1332,7 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
       p.src_trace[4 * (size_t)r] = (long long)t0;
     }
-    solo_source<kH, kB, kE>(p, sl, s, lane, sw, pf);
+    solo_source<kH, kB, kE, kC>(p, sl, s, lane, sw, pf, rc);
     if (p.src_trace && lane == 0) {
       unsigned long long t1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
@@ -1783,6 +1806,8 @@ cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st) {
   } else {
     if (p.hmode) solo_kernel<true, 1><<<grid, kSoloWarps * 32, 0, st>>>(p);
     else if (p.ell) solo_kernel<false, 1, true><<<grid, kSoloWarps * 32, 0, st>>>(p);
+    else if (std::getenv("GSOFA_RCACHE") && atoi(std::getenv("GSOFA_RCACHE")) != 0)  // A/B
+      solo_kernel<false, 1, false, true><<<grid, kSoloWarps * 32, 0, st>>>(p);
     else solo_kernel<false, 1><<<grid, kSoloWarps * 32, 0, st>>>(p);
   }
   return cudaGetLastError();
