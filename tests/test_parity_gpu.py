@@ -841,3 +841,21 @@ def test_team_kernel(case, rows, monkeypatch):
     finally:
         c.close()
     assert_full_equal(got, oracle.symbolic(rp, ci), f"{case} team rows={rows}")
+
+
+@pytest.mark.parametrize("case", ["C2_24", "C5_20", "rand"])
+def test_solo_reached_cache(case, monkeypatch):
+    """Dev variant (off by default): the per-warp reached-word cache skips
+    atomics on words known reached for the current source; result unchanged."""
+    monkeypatch.setenv("GSOFA_RCACHE", "1")
+    if case == "rand":
+        rp, ci = gen.random_graph(2000, 0.003, seed=93)
+    else:
+        name, scale = case.split("_")
+        rp, ci = gen.config(name, int(scale))
+    c = g.Context(0)
+    try:
+        got = run(rp, ci, c, schedule="threshold")
+    finally:
+        c.close()
+    assert_full_equal(got, oracle.symbolic(rp, ci), f"{case} rcache")
