@@ -1401,7 +1401,10 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
 // hub rows, ordered last) are chains of at most tree-height steps whose steps
 // hold many same-height thresholds with DISJOINT closures.  A team of
 // kTeamWarps warps (one CTA, one source at a time, its own solo-layout slot)
-// deals every step's threshold words to its warps; each warp closes its
+// deals every step's threshold words -- every threshold of one height, the
+// whole segment of positions, found through the summary -- to its warps
+// (threshold bits are read from the global bitmap: a team has no window);
+// each warp closes its
 // thresholds' closures with its own worklist (shared memory, then its own
 // ring of solo_ring entries past the slot's solo layout -- a 1/kTeamWarps
 // share of one ring overflowed constantly on hub closures and every overflow
@@ -1443,25 +1446,23 @@ __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlo
     }
   }
   fence_gpu();
-  if (warp == 0 && lane == 0) {
-    ctl.P = -1;
-    ctl.wb = -1;
-  }
+  if (warp == 0 && lane == 0) ctl.P = -1;
   __syncthreads();
+  // no shared window: every fill goes to the global threshold bitmap (a
+  // window base far below any position sends solo_expand there)
+  const int wb = -(1 << 29);
   for (;;) {
     if (warp == 0) {
-      // the next step: thresholds of height h = height(P) in the window,
-      // positions [P, min(seg_end(h), window end))
-      int wb = ctl.wb;
-      // the search starts after the previous step's positions
+      // the next step: EVERY threshold of height h = height(P), i.e. the
+      // set bits of the whole segment [P, seg_end(h)) of positions -- they
+      // are final (fills are ancestors: strictly greater height)
       const int T0 = ctl.P < 0 ? -1 : ctl.lim - 1;
-      const int P = solo_next_threshold(SL_THR, SL_TSUM, tbw, T0, wb, ctl.win, lane);
+      const int P = solo_scan_next(SL_THR, SL_TSUM, tbw, T0, lane);
       if (lane == 0) {
         ctl.P = P;
-        ctl.wb = wb;
         if (P != INT_MAX) {
           const int4 r = __ldg(p.posrec + P);
-          ctl.lim = min(r.w, (wb + 32) << 5);
+          ctl.lim = r.w;
           ctl.h = __ldg(p.hgt + r.x);
           ctl.tmin = INT_MAX;
           ctl.tmax = -1;
@@ -1472,37 +1473,32 @@ __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlo
     __syncthreads();
     const int P = ctl.P;
     if (P == INT_MAX) break;
-    const int wb = ctl.wb, lim = ctl.lim;
+    const int lim = ctl.lim;
     SoloQueue Q = {0, 0, 0, 0, false, 0};
-    int u = -1, ub = 0, ue = 0;
     int tmin = INT_MAX, tmax = -1;
-    bool first = true;
-    for (int wi = (P >> 5) + warp; (wi << 5) < lim; wi += kTeamWarps) {
-      uint32_t x = ctl.win[wi - wb];
-      if (wi == (P >> 5)) x &= kFull << (P & 31);
-      if (lim - (wi << 5) < 32) x &= (1u << (lim - (wi << 5))) - 1u;
-      const bool has = (x >> lane) & 1u;
-      int v = -1, vb = 0, ve = 0;
-      if (has) {
-        const int4 r = __ldg(p.posrec + (wi << 5) + lane);
-        v = r.x;
-        vb = r.y;
-        ve = r.z;
-        tmin = min(tmin, v);
-        tmax = max(tmax, v);
-      }
-      if (first) {
-        // this warp's first word: its thresholds to the low lanes
-        const uint32_t b = __ballot_sync(kFull, has);
-        const int src = __fns(b, 0, lane + 1) & 31;
-        const int cu = __shfl_sync(kFull, v, src), cb = __shfl_sync(kFull, vb, src),
-                  ce = __shfl_sync(kFull, ve, src);
-        const bool ok = lane < __popc(b);
-        u = ok ? cu : -1;
-        ub = ok ? cb : 0;
-        ue = ok ? ce : 0;
-        first = false;
-      } else {
+    // the segment's threshold words, by summary word (32 words each) dealt
+    // round-robin to the warps; each warp queues its thresholds
+    const int w0 = P >> 5, w1 = (lim - 1) >> 5;
+    for (int si = (w0 >> 5) + warp; si <= (w1 >> 5); si += kTeamWarps) {
+      const uint32_t sm = __ldcg(SL_TSUM + si);
+      const int wi = (si << 5) + lane;
+      uint32_t x = ((sm >> lane) & 1u) && wi >= w0 && wi <= w1 ? __ldcg(SL_THR + wi) : 0u;
+      if (wi == w0) x &= kFull << (P & 31);
+      if (wi == w1 && (lim & 31)) x &= (1u << (lim & 31)) - 1u;
+      for (;;) {
+        const bool has = x != 0u;
+        if (!__ballot_sync(kFull, has)) break;
+        int v = -1, vb = 0, ve = 0;
+        if (has) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1u;
+          const int4 r = __ldg(p.posrec + (wi << 5) + b);
+          v = r.x;
+          vb = r.y;
+          ve = r.z;
+          tmin = min(tmin, v);
+          tmax = max(tmax, v);
+        }
         solo_push<false>(p, sl, sw, nullptr, Q, has, v, vb, ve, lane, ring, rmask);
       }
     }
@@ -1517,10 +1513,13 @@ __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlo
     t.tmin = ctl.tmin;
     t.tmax = ctl.tmax;
     t.h = ctl.h;
-    const int pushed0 = Q.st + Q.gt;
-    for (;;) {
-      solo_expand<true, 1>(p, sl, sw, nullptr, wb, Q, s, t, u, ub, ue, -1, lane, ctl.win, ring, rmask);
-      __syncwarp();
+    const int pushed0 = Q.st + Q.gt;  // the step's own thresholds (counted at staging, as |L(s,:)|)
+    int u = -1, ub = 0, ue = 0;
+    for (bool expand_now = false;; expand_now = true) {
+      if (expand_now) {
+        solo_expand<true, 1>(p, sl, sw, nullptr, wb, Q, s, t, u, ub, ue, -1, lane, ctl.win, ring, rmask);
+        __syncwarp();
+      }
       if (Q.sh < Q.st) {
         const int cnt = min(32, Q.st - Q.sh);
         u = -1;
@@ -1541,10 +1540,10 @@ __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlo
         __syncwarp();
         fence_gpu();
         const int pwords = (t.tmax + 31) >> 5;
-        for (int w0 = 0; w0 < pwords && !Q.spilled; w0 += 32) {
-          const int wi = w0 + lane;
+        for (int p0 = 0; p0 < pwords && !Q.spilled; p0 += 32) {
+          const int pi = p0 + lane;
           uint32_t x = 0u;
-          if (wi < pwords && __ldcg(SL_PEND + wi)) x = atomicExch(SL_PEND + wi, 0u);
+          if (pi < pwords && __ldcg(SL_PEND + pi)) x = atomicExch(SL_PEND + pi, 0u);
           for (;;) {
             const bool has = x != 0u;
             const uint32_t hb = __ballot_sync(kFull, has);
@@ -1554,11 +1553,11 @@ __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlo
             if (has && fits) {
               const int b = __ffs(x) - 1;
               x &= x - 1u;
-              ring[pos & rmask] = (uint32_t)((wi << 5) + b);
+              ring[pos & rmask] = (uint32_t)((pi << 5) + b);
             }
             Q.gt += __popc(__ballot_sync(kFull, has && fits));
             if (__ballot_sync(kFull, has && !fits)) {
-              if (x) atomicOr(SL_PEND + wi, x);  // back to pend; rescan later
+              if (x) atomicOr(SL_PEND + pi, x);  // back to pend; rescan later
               Q.spilled = true;
               break;
             }
