@@ -1,0 +1,216 @@
+#!/bin/bash
+# Round-2 GPU passes, one function per pass (usage: bash scripts/dev/round2_passes.sh N);
+# README.md maps each pass to the numbers it produced.  Run through gpurun from the repo root.
+set -u
+
+pass1() {
+  set -x
+  python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/p1_smoke.log 2>&1
+  timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/p1_tests.log 2>&1; tail -5 gpurun_out/p1_tests.log
+  for c in C2 C3 C4 C5; do timeout 600 python scripts/probe.py --config $c --reps 2; done > gpurun_out/p1_probe.log 2>&1
+  cat gpurun_out/p1_probe.log
+  timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/p1_bench.json 2> gpurun_out/p1_bench.log; tail -c 4000 gpurun_out/p1_bench.json
+  for c in C5 C4 C2; do timeout 1200 python scripts/scaling_emulation.py --config $c --gpus 2 4 8 --out gpurun_out/p1_scal_$c.json; done > gpurun_out/p1_scal.log 2>&1
+  cat gpurun_out/p1_scal.log
+}
+
+pass2() {
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  echo "== C4 auto"; timeout 120 python scripts/probe.py --config C4 --reps 2 2>&1 | tail -2
+  timeout 2700 python -m pytest tests -m gpu -q -x --durations=50 > gpurun_out/p2_tests.log 2>&1; echo "pytest rc=$?"
+  tail -75 gpurun_out/p2_tests.log
+}
+
+pass3() {
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 900 python -m pytest tests -m gpu -q -x -k "interleave or cap_only or external or etree" > gpurun_out/p3_tests.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/p3_tests.log
+  for c in C2 C5; do GSOFA_TIMELINE=1 timeout 300 python scripts/probe.py --config $c --reps 2 2>&1 | tail -22; done > gpurun_out/p3_probe.log 2>&1
+  grep "^rep" gpurun_out/p3_probe.log
+  timeout 900 python scripts/scaling_emulation.py --config C5 --gpus 2 4 8 --out gpurun_out/p3_scal_C5_ranges.json 2>&1 | tail -8
+  timeout 900 python scripts/scaling_emulation.py --config C5 --gpus 8 --mode interleave --unit 128 --out gpurun_out/p3_scal_C5_il128.json 2>&1 | tail -4
+  timeout 900 python scripts/scaling_emulation.py --config C5 --gpus 8 --mode interleave --unit 32 --out gpurun_out/p3_scal_C5_il32.json 2>&1 | tail -4
+  timeout 600 python scripts/scaling_emulation.py --config C4 --gpus 8 --out gpurun_out/p3_scal_C4_ranges.json 2>&1 | tail -4
+  timeout 600 python scripts/scaling_emulation.py --config C4 --gpus 8 --mode interleave --unit 128 --out gpurun_out/p3_scal_C4_il128.json 2>&1 | tail -4
+  timeout 600 python scripts/scaling_emulation.py --config C2 --gpus 8 --out gpurun_out/p3_scal_C2_ranges.json 2>&1 | tail -4
+  timeout 600 python scripts/scaling_emulation.py --config C2 --gpus 8 --mode interleave --unit 128 --out gpurun_out/p3_scal_C2_il128.json 2>&1 | tail -4
+}
+
+pass4() {
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for a in 0.85 0.90 0.97; do echo "== alpha $a"; GSOFA_PART_ALPHA=$a timeout 600 python scripts/scaling_emulation.py --config C5 --gpus 8 --reps 1 2>&1 | tail -3; done
+  echo "== wide all ranks"; GSOFA_SOLO_WIDE=1 timeout 600 python scripts/scaling_emulation.py --config C5 --gpus 8 --reps 1 2>&1 | tail -3
+  echo "== src trace C5 full"; GSOFA_SRC_TRACE=/tmp/st.bin timeout 300 python scripts/probe.py --config C5 --reps 1 2>&1 | tail -16
+  echo "== src trace C5 top range"; GSOFA_SRC_TRACE=/tmp/st2.bin timeout 300 python scripts/probe.py --config C5 --reps 1 --rows 2092230:2097152 2>&1 | tail -16
+}
+
+pass5() {
+  # A/B of builds on one box (old trees built in-tree under ab_*/), then one
+  # ncu --set full capture of the solo kernel on C5's top range (chain-bound)
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for t in ab_a4fd076 ab_fe8ee4c .; do
+    for c in C5 C2 C3; do
+      echo "== $t $c"; (cd $t && timeout 300 python scripts/probe.py --config $c --reps 3 2>&1 | grep "^rep 2")
+    done
+  done
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:solo_kernel -c 1 \
+    -o gpurun_out/prof_solo_C5top_r2 -f python scripts/probe.py --config C5 --reps 1 --rows 2092230:2097152 > gpurun_out/ncu_solo_top.log 2>&1
+  echo "ncu rc=$?"; tail -3 gpurun_out/ncu_solo_top.log
+}
+
+pass6() {
+  # bisect the C5/C2 regression since round 1: each tree is an in-place git
+  # archive with its own build and probe (one box, same clocks)
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for t in ab_a4fd076 ab_e866041 ab_07bd247 ab_fe8ee4c ab_e49e006 ab_b88768e ab_0524b72 ab_90ed60b ab_6e59a6b ab_89c6d7c ab_17e566f . ab_a4fd076; do
+    for c in C5 C2; do
+      r=$(cd $t && timeout 300 python scripts/probe.py --config $c --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+      echo "$t $c $r"
+    done
+  done
+}
+
+pass7() {
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 600 python -m pytest tests -m gpu -q -x -k "ell or random_graphs or full_config_exact" > gpurun_out/p7_tests.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/p7_tests.log
+  for e in 0 1; do for c in C5 C2; do
+    r=$(GSOFA_ELL=$e timeout 300 python scripts/probe.py --config $c --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "ELL=$e $c $r"
+  done; done
+  echo "== top range ELL=1"; GSOFA_SRC_TRACE=/tmp/st2.bin timeout 300 python scripts/probe.py --config C5 --reps 2 --rows 2092230:2097152 2>&1 | grep -A4 "^rep 1\|top sources"
+  timeout 900 python scripts/scaling_emulation.py --config C5 --gpus 8 --out gpurun_out/p7_scal_C5.json 2>&1 | tail -3
+}
+
+pass8() {
+  # round-2 measurement pass: C5 (default bench config) through scripts/measure.sh,
+  # bench lines of C2/C3/C4, FIFO budget sweep with external-frontier counts
+  bash scripts/measure.sh r2 C5
+  for c in C2 C3 C4; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 --cpu-seconds 10 > gpurun_out/bench_r2_$c.json 2> gpurun_out/bench_r2_$c.log; tail -c 600 gpurun_out/bench_r2_$c.json; echo; done
+  timeout 900 python scripts/budget_sweep.py --config C3 --schedule fifo --budgets-gb 0.25 1 5 16 0 --chunks 128 --out gpurun_out/budget_fifo_C3.json 2>&1 | tail -8
+}
+
+pass9() {
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 900 python -m pytest tests -m gpu -q -x -k "team or overflow or auto_threshold_order or solo_shapes or stream_paths" > gpurun_out/p9_tests.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/p9_tests.log
+  for tr in 0 448 1024 2048; do
+    r=$(GSOFA_TEAM_ROWS=$tr timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C4 team_rows=$tr $r"
+  done
+  for c in C5 C2; do r=$(timeout 300 python scripts/probe.py --config $c --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "$c $r"; done
+  timeout 900 python scripts/scaling_emulation.py --config C4 --gpus 2 4 8 --out gpurun_out/p9_scal_C4.json 2>&1 | tail -8
+}
+
+pass10() {
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for tr in 0 448 1024; do
+    r=$(GSOFA_TEAM_ROWS=$tr timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C4 team_rows=$tr $r"
+  done
+  timeout 600 python -m pytest tests -m gpu -q -x -k "team" 2>&1 | tail -2
+}
+
+pass11() {
+  python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/p11_smoke.log 2>&1; tail -1 gpurun_out/p11_smoke.log
+  timeout 1500 python -m pytest tests -m gpu -q -x --durations=15 > gpurun_out/p11_tests.log 2>&1; echo "pytest rc=$?"; tail -22 gpurun_out/p11_tests.log
+  timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/p11_bench.json 2> gpurun_out/p11_bench.log; python -c "
+  import json; d=json.load(open('gpurun_out/p11_bench.json')); print('bench C5', d['value'], d['ms_per_step'], d['e2e']['value'], d['roofline']['frac'], d['roofline']['ncu']['kernels']['solo_kernel']['dram_gbs'], d['clocks'])"
+  timeout 600 python bench.py --gpus 2 --config C2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/p11_n2_ranges.json 2> gpurun_out/p11_n2_ranges.log; tail -c 400 gpurun_out/p11_n2_ranges.json
+  timeout 600 python bench.py --gpus 2 --config C2 --steps 2 --warmup 3 --no-cpu-baseline --layout interleave --unit 32 > gpurun_out/p11_n2_il.json 2> gpurun_out/p11_n2_il.log; tail -c 400 gpurun_out/p11_n2_il.json
+}
+
+pass12() {
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for v in 0 1 0 1; do for c in C5 C2; do
+    r=$(GSOFA_ID_R1=$v timeout 300 python scripts/probe.py --config $c --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "ID_R1=$v $c $r"
+  done; done
+  for v in 0 1; do r=$(GSOFA_ID_R1=$v timeout 300 python scripts/probe.py --config C5 --reps 3 --rows 2092230:2097152 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "ID_R1=$v C5top $r"; done
+  GSOFA_ID_R1=1 timeout 600 python -m pytest tests -m gpu -q -x -k "random_graphs and threshold or full_config_exact or overflow" 2>&1 | tail -2
+}
+
+pass13() {
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for c in C5 C4 C2 C3; do timeout 1200 python scripts/scaling_emulation.py --config $c --gpus 2 4 8 --out gpurun_out/p13_scal_$c.json 2>&1 | tail -7; done
+  bash scripts/measure.sh r2 C2 > gpurun_out/p13_measure_C2.log 2>&1; tail -3 gpurun_out/p13_measure_C2.log
+  cat profiles/traffic.json
+}
+
+pass14() {
+  # per-chain time of C5 top-separator sources: narrow (48 w/SM, 1 batch) vs wide (32 w/SM, 4 batches)
+  # with the range small enough for one wave of the wide shape (4736 slots)
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for rows in 2092230:2097152 2093056:2097152 2094080:2097152 2095104:2097152; do for w in 0 1; do
+    r=$(GSOFA_SOLO_WIDE=$w timeout 300 python scripts/probe.py --config C5 --reps 2 --rows $rows 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "rows $rows wide=$w $r"
+  done; done
+}
+
+pass15() {
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 1200 python scripts/scaling_emulation.py --config C5 --gpus 8 --mode steal --blocks-per-rank 4 --out gpurun_out/p15_steal_C5_4.json 2>&1 | tail -4
+  timeout 1200 python scripts/scaling_emulation.py --config C5 --gpus 8 --mode steal --blocks-per-rank 2 --out gpurun_out/p15_steal_C5_2.json 2>&1 | tail -4
+  timeout 600 python scripts/scaling_emulation.py --config C4 --gpus 8 --mode steal --out gpurun_out/p15_steal_C4.json 2>&1 | tail -4
+  timeout 600 python scripts/scaling_emulation.py --config C2 --gpus 8 --mode steal --out gpurun_out/p15_steal_C2.json 2>&1 | tail -4
+}
+
+pass17() {
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for l in default 592 296 148; do for c in C5 C2 C4; do
+    if [ "$l" = "default" ]; then unset GSOFA_LIGHT_CTAS; else export GSOFA_LIGHT_CTAS=$l; fi
+    r=$(timeout 300 python scripts/probe.py --config $c --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "light=$l $c $r"
+  done; done
+}
+
+pass18() {
+  # reached-word cache (GSOFA_RCACHE=1) A/B and parity
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  GSOFA_RCACHE=1 timeout 900 python -m pytest tests -m gpu -q -x -k "random_graphs or full_config_exact or overflow or config_shapes or stream_paths" 2>&1 | tail -2
+  for v in 0 1 0 1; do for c in C5 C2; do
+    r=$(GSOFA_RCACHE=$v timeout 300 python scripts/probe.py --config $c --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*edges \([0-9.e+]*\).*/dev \1 trav \2/')
+    echo "RCACHE=$v $c $r"
+  done; done
+  for v in 0 1; do r=$(GSOFA_RCACHE=$v timeout 300 python scripts/probe.py --config C5 --reps 3 --rows 2092230:2097152 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "RCACHE=$v C5top $r"; done
+}
+
+pass19() {
+  # final verification of the round's code: build + smoke, full GPU suite, default bench, reference arm
+  python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/p19_smoke.log 2>&1; tail -1 gpurun_out/p19_smoke.log
+  timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/p19_tests.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/p19_tests.log
+  timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/p19_bench.json 2> gpurun_out/p19_bench.log; python -c "
+  import json; d=json.load(open('gpurun_out/p19_bench.json')); r=d['roofline']
+  print('bench', d['config']['workload'][:20], '%.4g'%d['value'], '%.1f ms'%d['ms_per_step'], 'e2e %.4g'%d['e2e']['value'], 'frac %.3f'%r['frac'], 'ncu_dram_frac %.4f'%r.get('ncu_dram_frac', -1), 'atomic %.3f'%r['atomic']['frac'], d['clocks'], 'launches', d['gpu_launches'])"
+  time (timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/p19_ref.json 2> gpurun_out/p19_ref.log); tail -c 300 gpurun_out/p19_ref.json
+}
+
+pass20() {
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 600 python -m pytest tests -m gpu -q -x -k "team" 2>&1 | tail -2
+  for tr in 0 448 1024; do
+    r=$(GSOFA_TEAM_ROWS=$tr timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C4 team_rows=$tr $r"
+  done
+  for tr in 0 448; do r=$(GSOFA_TEAM_ROWS=$tr timeout 300 python scripts/probe.py --config C4 --reps 3 --rows 1584915:1585478 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "C4 hub rank team_rows=$tr $r"; done
+}
+
+case "${1:-}" in
+  1) pass1 ;;
+  2) pass2 ;;
+  3) pass3 ;;
+  4) pass4 ;;
+  5) pass5 ;;
+  6) pass6 ;;
+  7) pass7 ;;
+  8) pass8 ;;
+  9) pass9 ;;
+  10) pass10 ;;
+  11) pass11 ;;
+  12) pass12 ;;
+  13) pass13 ;;
+  14) pass14 ;;
+  15) pass15 ;;
+  17) pass17 ;;
+  18) pass18 ;;
+  19) pass19 ;;
+  20) pass20 ;;
+  *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
+esac
