@@ -1484,7 +1484,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
           if (tg > 0) {
             const size_t words = (size_t)c->sms * gsofa::team_slot_words(sp);
             const uint64_t sig = ((uint64_t)plan.hws_words << 20) ^ (uint64_t)plan.Vmax ^
-                                 ((uint64_t)sp.solo_ring << 44);
+                                 ((uint64_t)n << 40);
             if (c->team_words < words) {
               if (c->team_ws) cudaFree(c->team_ws);
               c->team_ws = nullptr;
@@ -1857,6 +1857,9 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     res->stats.first_visits = (int64_t)hs[8];
     res->stats.source_expansions = (int64_t)hs[9];
     res->stats.frontier_spilled = (int64_t)hs[10];
+    if (std::getenv("GSOFA_TEAM_DEBUG") && hs[13])
+      std::fprintf(stderr, "[team] per-step pairs: busiest warp %llu, all warps %llu -> balance %.2f of 16\n",
+                   (unsigned long long)hs[12], (unsigned long long)hs[13], (double)hs[13] / (double)hs[12]);
     res->stats.batches = nbatches;
     res->stats.max_batch = maxC;
     res->stats.kernel_launches = launches;

@@ -749,16 +749,34 @@ __device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot 
   }
 }
 
+// CTA-shared work queue of a team (team kernel): entries[i] = vertex + 1 (0 =
+// not written yet / consumed); every vertex is queued at most once per
+// source (its reached bit), so indices never wrap within a source.
+struct TeamQ {
+  uint32_t *entries;
+  unsigned int *qt;  // shared memory: next index to fill
+};
+
+__device__ __forceinline__ void team_push(const TeamQ &tq, bool push, int wk, int lane) {
+  const uint32_t pb = __ballot_sync(kFull, push);
+  if (!pb) return;
+  unsigned int base = 0;
+  if (lane == 0) base = atomicAdd(tq.qt, (unsigned int)__popc(pb));
+  base = __shfl_sync(kFull, base, 0);
+  if (push) __stcg(tq.entries + base + __popc(pb & lanemask_lt()), (uint32_t)wk + 1u);
+}
+
 // expand the closure items u (one per lane, -1 = none; beg/end = adjacency)
 // of the current step t of source s.  Thresholds are kept at their bitmap
 // position: the vertex id (id order) or pos(w) (height order, loaded for
 // each new fill).
-template <bool kH, int kB, bool kC = false>
+template <bool kH, int kB, bool kC = false, bool kT = false>
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
                                             SoloWarpSmem &sw, SoloPF *pf, int wb, SoloQueue &Q,
                                             int s, const SoloStep &t, int u, int beg, int end,
                                             int us, int lane, uint32_t *win, uint32_t *ring,
-                                            int rmask, uint2 *rc = nullptr) {
+                                            int rmask, uint2 *rc = nullptr,
+                                            const TeamQ *tq = nullptr) {
   constexpr bool kPF = kB > 1 && kAdjPrefetch;  // us: this lane's prefetch slot (-1: none)
   const int deg = u >= 0 ? end - beg : 0;
   // fast path (every threshold's level 0, most closure levels of a chain):
@@ -881,7 +899,8 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
           push = true;  // maxId(w) = T, not in the structure: continue with T
         }
       }
-      solo_push<kPF>(p, sl, sw, pf, Q, push, wk, rb[k], re[k], lane, ring, rmask);
+      if constexpr (kT) team_push(*tq, push, wk, lane);  // the team's shared queue
+      else solo_push<kPF>(p, sl, sw, pf, Q, push, wk, rb[k], re[k], lane, ring, rmask);
     }
   }
 }
@@ -1420,16 +1439,20 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
 constexpr int kTeamWarps = 16;
 
 struct TeamCtl {
-  uint32_t win[32];  // the source's threshold window (all warps)
+  uint32_t win[32];  // (unused window of solo_expand's signature)
   int P, wb, lim, h, tmin, tmax;
   long long task;
+  unsigned int maxw, sumw;  // dev balance statistics of the current step
+  unsigned int qh, qt;      // the team queue: next index to take / to fill
+  unsigned int idle;        // warps of the team with nothing to do
 };
 
 __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlot &sl, int s,
                                             int warp, int lane, SoloWarpSmem &sw, TeamCtl &ctl) {
   const int tbw = (p.n + 31) >> 5;  // threshold positions over [0, n)
-  uint32_t *ring = sl.base + p.hws_words + (size_t)warp * p.solo_ring;
-  const int rmask = p.solo_ring - 1;
+  TeamQ tq;
+  tq.entries = sl.base + p.hws_words;  // n entries past the solo layout
+  tq.qt = &ctl.qt;
   // seed: the warps share the neighbour list of s
   const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
   for (int j0 = beg + 32 * warp; j0 < end; j0 += 32 * kTeamWarps) {
@@ -1446,11 +1469,16 @@ __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlo
     }
   }
   fence_gpu();
-  if (warp == 0 && lane == 0) ctl.P = -1;
+  if (warp == 0 && lane == 0) {
+    ctl.P = -1;
+    ctl.maxw = ctl.sumw = 0u;
+    ctl.qh = ctl.qt = 0u;
+  }
   __syncthreads();
   // no shared window: every fill goes to the global threshold bitmap (a
   // window base far below any position sends solo_expand there)
   const int wb = -(1 << 29);
+  SoloQueue Q = {0, 0, 0, 0, false, 0};  // (unused: the team queue replaces it)
   for (;;) {
     if (warp == 0) {
       // the next step: EVERY threshold of height h = height(P), i.e. the
@@ -1460,6 +1488,7 @@ __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlo
       const int P = solo_scan_next(SL_THR, SL_TSUM, tbw, T0, lane);
       if (lane == 0) {
         ctl.P = P;
+        ctl.idle = 0u;
         if (P != INT_MAX) {
           const int4 r = __ldg(p.posrec + P);
           ctl.lim = r.w;
@@ -1474,11 +1503,11 @@ __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlo
     const int P = ctl.P;
     if (P == INT_MAX) break;
     const int lim = ctl.lim;
-    SoloQueue Q = {0, 0, 0, 0, false, 0};
     int tmin = INT_MAX, tmax = -1;
     // the segment's threshold words, by summary word (32 words each) dealt
-    // round-robin to the warps; each warp queues its thresholds
+    // round-robin to the warps; the thresholds go to the team queue
     const int w0 = P >> 5, w1 = (lim - 1) >> 5;
+    const unsigned int q0 = ctl.qt;  // (the step's first queue index)
     for (int si = (w0 >> 5) + warp; si <= (w1 >> 5); si += kTeamWarps) {
       const uint32_t sm = __ldcg(SL_TSUM + si);
       const int wi = (si << 5) + lane;
@@ -1488,18 +1517,15 @@ __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlo
       for (;;) {
         const bool has = x != 0u;
         if (!__ballot_sync(kFull, has)) break;
-        int v = -1, vb = 0, ve = 0;
+        int v = -1;
         if (has) {
           const int b = __ffs(x) - 1;
           x &= x - 1u;
-          const int4 r = __ldg(p.posrec + (wi << 5) + b);
-          v = r.x;
-          vb = r.y;
-          ve = r.z;
+          v = __ldg(p.posrec + (wi << 5) + b).x;
           tmin = min(tmin, v);
           tmax = max(tmax, v);
         }
-        solo_push<false>(p, sl, sw, nullptr, Q, has, v, vb, ve, lane, ring, rmask);
+        team_push(tq, has, v, lane);
       }
     }
     tmin = __reduce_min_sync(kFull, tmin);
@@ -1513,72 +1539,78 @@ __device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlo
     t.tmin = ctl.tmin;
     t.tmax = ctl.tmax;
     t.h = ctl.h;
-    const int pushed0 = Q.st + Q.gt;  // the step's own thresholds (counted at staging, as |L(s,:)|)
-    int u = -1, ub = 0, ue = 0;
-    for (bool expand_now = false;; expand_now = true) {
-      if (expand_now) {
-        solo_expand<true, 1>(p, sl, sw, nullptr, wb, Q, s, t, u, ub, ue, -1, lane, ctl.win, ring, rmask);
-        __syncwarp();
-      }
-      if (Q.sh < Q.st) {
-        const int cnt = min(32, Q.st - Q.sh);
-        u = -1;
-        if (lane < cnt) {
-          const int i = (Q.sh + lane) & (kSoloQ - 1);
-          u = sw.qw[i];
-          ub = sw.qb[i];
-          ue = sw.qe[i];
-        }
-        Q.sh += cnt;
-        __syncwarp();
-        continue;
-      }
-      if (Q.gh >= Q.gt && Q.spilled) {
-        // parked closure items (pend bits, all below tmax, any warp's): claim
-        // whole words and move their items into this warp's ring
-        Q.spilled = false;
-        __syncwarp();
-        fence_gpu();
-        const int pwords = (t.tmax + 31) >> 5;
-        for (int p0 = 0; p0 < pwords && !Q.spilled; p0 += 32) {
-          const int pi = p0 + lane;
-          uint32_t x = 0u;
-          if (pi < pwords && __ldcg(SL_PEND + pi)) x = atomicExch(SL_PEND + pi, 0u);
+    const unsigned int nthr = ctl.qt - q0;  // the step's own thresholds (counted at staging)
+    const uint32_t pairs0 = sw.pairs;        // (dev balance statistics)
+    // cooperative closure: warps take up to 32 queued items at a time; the
+    // step ends when every warp is idle and nothing is queued.  A warp leaves
+    // the idle count BEFORE it claims, so an all-idle count proves that no
+    // claimed item is still being expanded.
+    bool idle = false;
+    for (;;) {
+      if (!idle) {
+        unsigned int k = 0, cnt = 0;
+        if (lane == 0) {
           for (;;) {
-            const bool has = x != 0u;
-            const uint32_t hb = __ballot_sync(kFull, has);
-            if (!hb) break;
-            const int pos = Q.gt + __popc(hb & lanemask_lt());
-            const bool fits = pos - Q.gh <= rmask;
-            if (has && fits) {
-              const int b = __ffs(x) - 1;
-              x &= x - 1u;
-              ring[pos & rmask] = (uint32_t)((pi << 5) + b);
-            }
-            Q.gt += __popc(__ballot_sync(kFull, has && fits));
-            if (__ballot_sync(kFull, has && !fits)) {
-              if (x) atomicOr(SL_PEND + pi, x);  // back to pend; rescan later
-              Q.spilled = true;
+            const unsigned int h = *(volatile unsigned int *)&ctl.qh;
+            const unsigned int tt = *(volatile unsigned int *)&ctl.qt;
+            if (h >= tt) break;
+            const unsigned int c = min(32u, tt - h);
+            if (atomicCAS(&ctl.qh, h, h + c) == h) {
+              k = h;
+              cnt = c;
               break;
             }
           }
         }
-        __syncwarp();
+        k = __shfl_sync(kFull, k, 0);
+        cnt = __shfl_sync(kFull, cnt, 0);
+        if (cnt) {
+          int u = -1, ub = 0, ue = 0;
+          if (lane < (int)cnt) {
+            uint32_t v;
+            while ((v = __ldcg(tq.entries + k + lane)) == 0u) {
+            }  // its producer is writing it
+            __stcg(tq.entries + k + lane, 0u);
+            u = (int)v - 1;
+            ub = __ldg(p.rowptr + u);
+            ue = __ldg(p.rowptr + u + 1);
+          }
+          solo_expand<true, 1, false, true>(p, sl, sw, nullptr, wb, Q, s, t, u, ub, ue, -1, lane,
+                                            ctl.win, nullptr, 0, nullptr, &tq);
+          __syncwarp();
+          continue;
+        }
+        if (lane == 0) atomicAdd(&ctl.idle, 1u);
+        idle = true;
       }
-      if (Q.gh >= Q.gt) {
-        if (lane == 0) sw.fv += (uint32_t)(Q.st + Q.gt - pushed0);
-        break;
+      int go = 0;  // 1: work appeared, 2: the step is done
+      if (lane == 0) {
+        if (*(volatile unsigned int *)&ctl.idle == (unsigned int)kTeamWarps &&
+            *(volatile unsigned int *)&ctl.qh >= *(volatile unsigned int *)&ctl.qt)
+          go = 2;
+        else if (*(volatile unsigned int *)&ctl.qh < *(volatile unsigned int *)&ctl.qt)
+          go = 1;
+        if (go == 1) atomicSub(&ctl.idle, 1u);
+        if (go == 0) __nanosleep(100);
       }
-      const int cnt = min(32, Q.gt - Q.gh);
-      u = lane < cnt ? (int)ring[(Q.gh + lane) & rmask] : -1;
-      Q.gh += cnt;
-      if (u >= 0) {
-        ub = __ldg(p.rowptr + u);
-        ue = __ldg(p.rowptr + u + 1);
-      }
+      go = __shfl_sync(kFull, go, 0);
+      if (go == 2) break;
+      if (go == 1) idle = false;
+    }
+    if (lane == 0) {
+      if (warp == 0) sw.fv += ctl.qt - q0 - nthr;  // closure members (first visits below s)
+      const uint32_t mine = sw.pairs - pairs0;    // this warp's (item, neighbour) pairs in the step
+      atomicMax(&ctl.maxw, mine);
+      atomicAdd(&ctl.sumw, mine);
     }
     fence_gpu();  // this warp's REDs (fills, thresholds) before the next step's scan
     __syncthreads();
+    if (threadIdx.x == 0) {
+      // dev: sum over steps of the busiest warp's pairs vs of all pairs / warps
+      atomicAdd(p.stats + 12, (unsigned long long)ctl.maxw);
+      atomicAdd(p.stats + 13, (unsigned long long)ctl.sumw);
+      ctl.maxw = ctl.sumw = 0u;
+    }
   }
 }
 
@@ -1587,8 +1619,9 @@ __global__ void __launch_bounds__(kTeamWarps * 32, 1) team_kernel(StreamParams p
   __shared__ SoloWarpSmem s_sw[kTeamWarps];
   __shared__ TeamCtl ctl;
   SoloWarpSmem &sw = s_sw[warp];
-  // team slot: the solo layout, then kTeamWarps rings of solo_ring entries
-  const SoloSlot sl = SoloSlot{p.team_ws + (size_t)blockIdx.x * (p.hws_words + (size_t)kTeamWarps * p.solo_ring)};
+  // team slot: the solo layout, then the team queue (one entry per vertex)
+  const SoloSlot sl =
+      SoloSlot{p.team_ws + (size_t)blockIdx.x * (p.hws_words + (((size_t)p.n + 31) & ~(size_t)31))};
   const int Vs = (int)(p.so_tsum - p.so_rsum), Ts = (int)(p.so_is - p.so_tsum);
   if (lane == 0) sw.items = sw.pairs = sw.levels = sw.steps = sw.fv = 0u;
   for (;;) {
@@ -1812,8 +1845,8 @@ cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-size_t team_slot_words(const StreamParams &p) {
-  return p.hws_words + (size_t)kTeamWarps * p.solo_ring;
+size_t team_slot_words(const StreamParams &p) {  // (as team_kernel computes it)
+  return p.hws_words + (((size_t)p.n + 31) & ~(size_t)31);
 }
 
 cudaError_t launch_team(const StreamParams &p, int grid, cudaStream_t st) {
