@@ -387,6 +387,26 @@ void gsofa_result_free(gsofa_result *r);
 int gsofa_partition_rows(int64_t n, const int64_t *rowptr, const int32_t *colidx,
                          int32_t nparts, int32_t align, int64_t *bounds);
 
+/*
+ * gsofa_height_order -- plan step A2 of the height-ordered threshold schedule
+ * (elimination tree; R18), the host pass
+ * gsofa_symbolic runs for hub patterns: the elimination tree of the
+ * symmetrised pattern A + A^T (Liu's algorithm, split over host threads:
+ * GSOFA_HOST_THREADS, default the hardware threads for n >= 65536), each
+ * vertex's height in it, and its position when the vertices are sorted by
+ * (height, id).
+ *   parent: out int32[n], -1 for roots     hgt: out int32[n]
+ *   pos:    out int32[n], a permutation    (any of the three may be NULL)
+ *   height: out, the tree height           last_row_chain: out, the number of
+ *           vertices of the last row's subtree path union (|struct(L(n-1,:))|
+ *           of A + A^T, the AUTO order choice's chain estimate); may be NULL
+ * Host pointers only, borrowed; the same CSR rules as gsofa_symbolic (rowptr
+ * monotone from 0, columns in [0,n) strictly increasing per row).  Errors:
+ * GSOFA_EINVAL (bad arguments, device pointers), GSOFA_EBADCSR.
+ */
+int gsofa_height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *parent,
+                       int32_t *hgt, int32_t *pos, int64_t *height, int64_t *last_row_chain);
+
 /* Static strings for an error code; thread-local detail of the last error. */
 const char *gsofa_strerror(int code);
 const char *gsofa_last_error_detail(void);

@@ -19,7 +19,7 @@ import numpy as np
 
 from .build import LIB_PATH, build  # noqa: F401
 
-__all__ = ["Context", "Result", "Tail", "symbolic", "permute", "partition_rows", "load", "GsofaError",
+__all__ = ["Context", "Result", "Tail", "symbolic", "permute", "partition_rows", "height_order", "load", "GsofaError",
            "EXPORTED_SYMBOLS", "build", "LIB_PATH"]
 
 EXPORTED_SYMBOLS = [
@@ -28,6 +28,7 @@ EXPORTED_SYMBOLS = [
     "gsofa_partition_rows", "gsofa_strerror", "gsofa_last_error_detail",
     "gsofa_version", "gsofa_supernode_stitch", "gsofa_result_l_csc", "gsofa_buffer_free",
     "gsofa_permute", "gsofa_result_supno", "gsofa_result_rowinfo", "gsofa_supernodes_gathered",
+    "gsofa_height_order",
 ]
 
 _I64, _I32 = ctypes.c_int64, ctypes.c_int32
@@ -109,6 +110,7 @@ def load():
     lib.gsofa_result_free.restype = None
     lib.gsofa_partition_rows.argtypes = [_I64, ctypes.c_void_p, ctypes.c_void_p, _I32, _I32,
                                          ctypes.c_void_p]
+    lib.gsofa_height_order.argtypes = [_I64, ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_void_p] * 5
     lib.gsofa_supernode_stitch.argtypes = [_P(CResult), ctypes.c_void_p, ctypes.c_void_p]
     lib.gsofa_result_l_csc.argtypes = [_P(CResult), _I32, _P(_P(_I64)), _P(_P(_I32))]
     lib.gsofa_result_supno.argtypes = [_P(CResult), _I32, _P(_P(_I32))]
@@ -376,6 +378,25 @@ def partition_rows(rowptr, colidx, nparts: int, align: int = 1) -> np.ndarray:
                                     int(nparts), int(align), b.ctypes.data),
            "gsofa_partition_rows")
     return b
+
+
+def height_order(rowptr, colidx) -> dict:
+    """gsofa_height_order (host computation, plan step A2): elimination tree
+    of A + A^T ("parent"), heights ("hgt"), (height, id) positions ("pos"),
+    the tree "height" and the AUTO chain estimate "last_row_chain"."""
+    lib = load()
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    if colidx.size == 0:
+        colidx = np.zeros(1, np.int32)
+    n = rowptr.size - 1
+    out = {k: np.zeros(n, np.int32) for k in ("parent", "hgt", "pos")}
+    h, c = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib.gsofa_height_order(n, rowptr.ctypes.data, colidx.ctypes.data, out["parent"].ctypes.data,
+                                  out["hgt"].ctypes.data, out["pos"].ctypes.data, ctypes.byref(h),
+                                  ctypes.byref(c)), "gsofa_height_order")
+    out["height"], out["last_row_chain"] = h.value, c.value
+    return out
 
 
 def permute(rowptr, colidx, perm):

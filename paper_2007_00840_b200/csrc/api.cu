@@ -146,6 +146,11 @@ struct gsofa_context {
   // one grow-only buffer
   int32_t *ord_buf = nullptr;
   size_t ord_cap = 0;
+  // ... their host side: the tree pass's scratch, and one grow-only pinned
+  // block for the order arrays and (device inputs) the host copy of the CSR
+  gsofa::OrderScratch *ord_scratch = nullptr;
+  char *ord_pin = nullptr;
+  size_t ord_pin_cap = 0;
   // ELL copy of the adjacency (solo kernel, id order, rows <= 8 entries)
   int32_t *ell = nullptr;
   size_t ell_cap = 0;
@@ -562,6 +567,8 @@ void gsofa_context_destroy(gsofa_context *c) {
   if (c->bw_dev) cudaFree(c->bw_dev);
   if (c->stage) cudaFree(c->stage);
   if (c->ord_buf) cudaFree(c->ord_buf);
+  if (c->ord_pin) cudaFreeHost(c->ord_pin);
+  gsofa::order_scratch_free(c->ord_scratch);
   if (c->ell) cudaFree(c->ell);
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->spill) cudaFreeHost(c->spill);
@@ -1090,8 +1097,6 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   unsigned int maxdeg = 0;  // largest row of A (validation pass)
   int64_t ord_npos = 0;  // > 0: height order possible (threshold bitmaps sized for n positions)
   bool auto_order = false;  // AUTO: pick the threshold order from the tree's shape
-  std::vector<int64_t> ord_hrp;              // host copies of a device CSR (height order)
-  std::vector<int32_t> ord_hci, ord_host;    // ... and the order arrays before upload
   // solo kernel shape: dev knob for now
   const bool solo_wide = std::getenv("GSOFA_SOLO_WIDE") && atoi(std::getenv("GSOFA_SOLO_WIDE")) != 0;
 
@@ -1426,23 +1431,37 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
           // (height, id) positions on the host (order.cu; SURVEY §8(a) A2,
           // O(nnz alpha)), while the lockstep kernel -- id order, no tree
           // needed -- runs; then up to the solo kernel's stream
+          const size_t ob = ((size_t)n * 6 * 4 + 15) & ~(size_t)15;  // posrec | hgt | pos
+          const size_t need = ob + (in_dev ? ((size_t)n + 1) * 8 + (size_t)std::max<int64_t>(nnz, 1) * 4 : 0);
+          if (c->ord_pin_cap < need) {
+            if (c->ord_pin) cudaFreeHost(c->ord_pin);
+            c->ord_pin = nullptr;
+            c->ord_pin_cap = 0;
+            CK(cudaMallocHost((void **)&c->ord_pin, need));
+            c->ord_pin_cap = need;
+          }
+          if (!c->ord_scratch) c->ord_scratch = gsofa::order_scratch_new();
+          int32_t *ord_host = (int32_t *)c->ord_pin;
           const int64_t *rp_h = rowptr;
           const int32_t *ci_h = colidx;
           if (in_dev) {
-            ord_hrp.resize((size_t)n + 1);
-            ord_hci.resize((size_t)std::max<int64_t>(nnz, 1));
-            CK(cudaMemcpyAsync(ord_hrp.data(), rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                               c->stream2));
-            if (nnz)
-              CK(cudaMemcpyAsync(ord_hci.data(), colidx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                 c->stream2));
+            int64_t *hrp = (int64_t *)(c->ord_pin + ob);
+            int32_t *hci = (int32_t *)(c->ord_pin + ob + ((size_t)n + 1) * 8);
+            CK(cudaMemcpyAsync(hrp, rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream2));
+            if (nnz) CK(cudaMemcpyAsync(hci, colidx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream2));
             CK(cudaStreamSynchronize(c->stream2));
-            rp_h = ord_hrp.data();
-            ci_h = ord_hci.data();
+            rp_h = hrp;
+            ci_h = hci;
           }
-          ord_host.resize((size_t)n * 6);  // posrec (4 per position) | hgt | pos
-          const gsofa::OrderShape shape = gsofa::height_order(
-              n, rp_h, ci_h, ord_host.data() + 4 * n, ord_host.data() + 5 * n, ord_host.data());
+          auto now_ms = [] {
+            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
+                .count();
+          };
+          const double t_ord = now_ms();
+          const gsofa::OrderShape shape = gsofa::height_order(n, rp_h, ci_h, ord_host + 4 * n, ord_host + 5 * n,
+                                                              ord_host, c->ord_scratch);
+          if (std::getenv("GSOFA_TIMELINE"))
+            std::fprintf(stderr, "[timeline] host height order %.3f ms\n", now_ms() - t_ord);
           if (auto_order) {
             // AUTO: height order when the last row's id-order chain (about
             // |L(n-1,:)| threshold steps) is far longer than the tree is
@@ -1455,8 +1474,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
             o.schedule = use_h ? GSOFA_SCHEDULE_HEIGHT : GSOFA_SCHEDULE_THRESHOLD;
           }
           if (sp.hmode)
-            CK(cudaMemcpyAsync(c->ord_buf, ord_host.data(), ord_host.size() * 4,
-                               cudaMemcpyHostToDevice, c->stream2));
+            CK(cudaMemcpyAsync(c->ord_buf, ord_host, (size_t)n * 6 * 4, cudaMemcpyHostToDevice, c->stream2));
         }
         // the solo kernel's first tasks are static per CTA, so every CTA of
         // its grid must be able to become resident: AUTO may have switched
@@ -2022,43 +2040,17 @@ int gsofa_partition_rows(int64_t n, const int64_t *rowptr, const int32_t *colidx
       set_detail("bad rowptr at row %lld", (long long)i);
       return GSOFA_EBADCSR;
     }
-  // transpose pattern (for the symmetrised A + A^T)
-  std::vector<int64_t> tp(n + 1, 0);
-  std::vector<int32_t> ti(std::max<int64_t>(nnz, 1));
-  for (int64_t e = 0; e < nnz; ++e) {
-    const int32_t cix = colidx[e];
-    if (cix < 0 || cix >= n) {
-      set_detail("column out of range");
-      return GSOFA_EBADCSR;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+      const int32_t cix = colidx[e];
+      if (cix < 0 || cix >= n || (e > rowptr[i] && cix <= colidx[e - 1])) {
+        set_detail("column out of range or not strictly increasing in row %lld", (long long)i);
+        return GSOFA_EBADCSR;
+      }
     }
-    ++tp[cix + 1];
-  }
-  for (int64_t i = 0; i < n; ++i) tp[i + 1] += tp[i];
-  {
-    std::vector<int64_t> cur(tp.begin(), tp.end() - 1);
-    for (int64_t i = 0; i < n; ++i)
-      for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) ti[cur[colidx[e]]++] = (int32_t)i;
-  }
-  // elimination tree of A + A^T (Liu, with path compression)
-  std::vector<int32_t> parent(n, -1), anc(n, -1);
-  auto visit = [&](int32_t i, int32_t k) {
-    int32_t r = k;
-    while (anc[r] != -1 && anc[r] != i) {
-      const int32_t t = anc[r];
-      anc[r] = i;
-      r = t;
-    }
-    if (anc[r] == -1) {
-      anc[r] = i;
-      parent[r] = i;
-    }
-  };
-  for (int32_t i = 0; i < n; ++i) {
-    for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e)
-      if (colidx[e] < i) visit(i, colidx[e]);
-    for (int64_t e = tp[i]; e < tp[i + 1]; ++e)
-      if (ti[e] < i) visit(i, ti[e]);
-  }
+  // elimination tree of A + A^T (Liu, with path compression; order.cu)
+  std::vector<int32_t> parent(n, -1);
+  gsofa::etree_sym(n, rowptr, colidx, parent.data(), nullptr);
   // work(s) ~ sum of out-degrees over the subtree of s (vertices reachable from
   // s through smaller ids are inside it; work grows with s)
   std::vector<double> w(n);
@@ -2078,6 +2070,48 @@ int gsofa_partition_rows(int64_t n, const int64_t *rowptr, const int32_t *colidx
     bounds[p] = s;
   }
   bounds[nparts] = n;
+  return GSOFA_OK;
+}
+
+// ----------------------------------------------------- height order (A2)
+int gsofa_height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *parent,
+                       int32_t *hgt, int32_t *pos, int64_t *height, int64_t *last_row_chain) {
+  if (n <= 0 || n >= (int64_t(1) << 31) || !rowptr || !colidx) {
+    set_detail("bad arguments to gsofa_height_order");
+    return GSOFA_EINVAL;
+  }
+  if (is_device_ptr(rowptr) || is_device_ptr(colidx)) {
+    set_detail("gsofa_height_order takes host pointers");
+    return GSOFA_EINVAL;
+  }
+  const int64_t nnz = rowptr[n];
+  if (rowptr[0] != 0 || nnz < 0 || nnz >= (int64_t(1) << 31)) {
+    set_detail("bad rowptr (rowptr[0] != 0 or nnz out of range)");
+    return GSOFA_EBADCSR;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    if (rowptr[i + 1] < rowptr[i] || rowptr[i + 1] > nnz) {
+      set_detail("bad rowptr at row %lld", (long long)i);
+      return GSOFA_EBADCSR;
+    }
+    for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+      const int32_t cix = colidx[e];
+      if (cix < 0 || cix >= n || (e > rowptr[i] && cix <= colidx[e - 1])) {
+        set_detail("column out of range or not strictly increasing in row %lld", (long long)i);
+        return GSOFA_EBADCSR;
+      }
+    }
+  }
+  std::vector<int32_t> buf((size_t)n * 6);
+  gsofa::OrderScratch *sc = gsofa::order_scratch_new();
+  const gsofa::OrderShape sh =
+      gsofa::height_order(n, rowptr, colidx, buf.data() + 4 * n, buf.data() + 5 * n, buf.data(), sc);
+  if (parent) std::memcpy(parent, gsofa::order_scratch_parent(sc), (size_t)n * 4);
+  gsofa::order_scratch_free(sc);
+  if (hgt) std::memcpy(hgt, buf.data() + 4 * n, (size_t)n * 4);
+  if (pos) std::memcpy(pos, buf.data() + 5 * n, (size_t)n * 4);
+  if (height) *height = sh.height;
+  if (last_row_chain) *last_row_chain = sh.last_row_chain;
   return GSOFA_OK;
 }
 

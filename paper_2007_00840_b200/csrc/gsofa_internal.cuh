@@ -169,8 +169,13 @@ struct OrderShape {
 };
 // etree heights, positions (sorted by (height, id)) and per position
 // {vertex, rowptr, rowptr + 1, segment end} (int4 as four int32)
+// scratch (transpose, tree, split) reused across calls; nullptr: per call
+struct OrderScratch;
+OrderScratch *order_scratch_new();
+void order_scratch_free(OrderScratch *s);
+const int32_t *order_scratch_parent(const OrderScratch *s);  // the tree of the last pass
 OrderShape height_order(int64_t n, const int64_t *rowptr, const int32_t *colidx, int32_t *hgt,
-                        int32_t *pos, int32_t *posrec);
+                        int32_t *pos, int32_t *posrec, OrderScratch *scratch = nullptr);
 cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st);
 cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st);
 cudaError_t launch_gather(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,

@@ -192,6 +192,22 @@ pass20() {
   for tr in 0 448; do r=$(GSOFA_TEAM_ROWS=$tr timeout 300 python scripts/probe.py --config C4 --reps 3 --rows 1584915:1585478 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "C4 hub rank team_rows=$tr $r"; done
 }
 
+pass21() {
+  # team-kernel parity failure (C2_20, all rows on teams): deterministic?; the rest of the
+  # suite; parallel host height order (C4 timeline, 1 vs all host threads, hub rank)
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  nproc
+  for i in 1 2; do timeout 600 python -m pytest tests -m gpu -q -k "team_kernel" 2>&1 | tail -4; done
+  timeout 2400 python -m pytest tests -m gpu -q -k "not team_kernel" > gpurun_out/p21_tests.log 2>&1; echo "pytest rc=$?"; tail -4 gpurun_out/p21_tests.log
+  for t in 1 0; do
+    if [ "$t" = "0" ]; then unset GSOFA_HOST_THREADS; else export GSOFA_HOST_THREADS=$t; fi
+    echo "== C4 host threads=$t"; GSOFA_TIMELINE=1 timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep\|height order" | tail -3
+    echo "== C4 hub rank host threads=$t"; timeout 300 python scripts/probe.py --config C4 --reps 3 --rows 1584915:1585478 2>&1 | grep "^rep 2"
+  done
+  unset GSOFA_HOST_THREADS
+  timeout 900 python scripts/scaling_emulation.py --config C4 --gpus 8 --out gpurun_out/p21_scal_C4.json 2>&1 | tail -3
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -212,5 +228,6 @@ case "${1:-}" in
   18) pass18 ;;
   19) pass19 ;;
   20) pass20 ;;
+  21) pass21 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac
