@@ -106,7 +106,6 @@ struct gsofa_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;  // heavy-group kernel runs here, concurrently
-  cudaStream_t stream3 = nullptr;  // team kernel (height order), concurrently
   int64_t budget = 0;        // requested budget (0 = auto)
   // arena (one cudaMalloc, carved in fixed regions)
   char *arena = nullptr;
@@ -154,10 +153,6 @@ struct gsofa_context {
   // ELL copy of the adjacency (solo kernel, id order, rows <= 8 entries)
   int32_t *ell = nullptr;
   size_t ell_cap = 0;
-  // team kernel slots (solo layout, one per team CTA); all zero at rest
-  uint32_t *team_ws = nullptr;
-  size_t team_words = 0;     // allocated words
-  uint64_t team_sig = 0;     // layout the slots were zeroed for
   HostBlock *hpool = nullptr;  // pinned storage reused by host-side results
   // external frontier (FIFO queue overflow) in mapped pinned host memory,
   // grow-only; spill_dev is its device address
@@ -522,7 +517,6 @@ int gsofa_context_create(int32_t device, int64_t mem_budget_bytes, gsofa_context
     return cuda_fail(e, "cudaStreamCreate");
   }
   e = cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     cudaStreamDestroy(c->stream);
     delete c;
@@ -575,8 +569,6 @@ void gsofa_context_destroy(gsofa_context *c) {
   host_block_release(c->hpool);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->stream2) cudaStreamDestroy(c->stream2);
-  if (c->stream3) cudaStreamDestroy(c->stream3);
-  if (c->team_ws) cudaFree(c->team_ws);
   delete c;
 }
 
@@ -1293,7 +1285,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     unsigned long long *failed_need = cursor + 1;
     // qcount: [0] group_ctr, [1] nfailed, [2] hq_head, [3] hq_tail, [4] done,
     // [5] solo_ctr, [6..7] task_ctr, [8] live lockstep CTAs
-    // [9] team task counter
+    // [9] unused
     CK(cudaMemsetAsync(c->qcount, 0, 40, st));
     CK(cudaMemsetAsync(c->totals, 0, 16, st));
     gsofa::StreamParams sp;
@@ -1329,9 +1321,6 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.group_trace = nullptr;
     sp.src_trace = nullptr;
     sp.ell = nullptr;
-    sp.team_ws = nullptr;
-    sp.team_ctr = nullptr;
-    sp.team_tasks = 0;
     sp.task_base = 0;
     const char *src_trace_path = std::getenv("GSOFA_SRC_TRACE");  // dev: per-source trace dump
     if (src_trace_path) {
@@ -1484,53 +1473,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
         const int64_t hres =
             gsofa::stream_max_blocks(c->device, plan.Vmax, 1, sp.hmode ? ord_npos : 0, sp.wide);
         if (hres > 0) hgrid = std::min<int64_t>(hgrid, hres);
-        // team kernel (height order): the heaviest pre-enqueued groups run
-        // one source per 16-warp CTA; the solo kernel's tasks start after them
-        sp.team_ws = nullptr;
-        sp.team_ctr = c->qcount + 9;
-        sp.team_tasks = 0;
         sp.task_base = 0;
-        if (sp.hmode && sp.solo_top > 0 && sp.solo_ring >= 64) {
-          // dev A/B (GSOFA_TEAM_ROWS): measured slower on C4 (0.42 s ->
-          // 0.83 s with 448 team rows: a hub source's steps are too narrow
-          // for 16 warps, so a team runs one source about as fast as one
-          // warp while the solo kernel runs all of them at once;
-          // profiles/r2/team_ab.txt) -- off by default
-          int64_t trows = 0;
-          if (const char *e = std::getenv("GSOFA_TEAM_ROWS")) trows = atoll(e);
-          const int64_t tg = std::min<int64_t>(sp.solo_top, ceil_div(std::max<int64_t>(trows, 0), 32));
-          if (tg > 0) {
-            const size_t words = (size_t)c->sms * gsofa::team_slot_words(sp);
-            const uint64_t sig = ((uint64_t)plan.hws_words << 20) ^ (uint64_t)plan.Vmax ^
-                                 ((uint64_t)n << 40);
-            if (c->team_words < words) {
-              if (c->team_ws) cudaFree(c->team_ws);
-              c->team_ws = nullptr;
-              c->team_words = 0;
-              CK(cudaMalloc((void **)&c->team_ws, words * 4));
-              c->team_words = words;
-              c->team_sig = 0;
-            }
-            if (c->team_sig != sig) {  // rings of another layout may sit under bitmaps
-              CK(cudaMemsetAsync(c->team_ws, 0, words * 4, c->stream2));
-              c->team_sig = sig;
-            }
-            sp.team_ws = c->team_ws;
-            sp.team_tasks = tg * 32;
-            sp.task_base = tg * 32;
-            cudaEvent_t et, ec;
-            CK(cudaEventCreateWithFlags(&et, cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&ec, cudaEventDisableTiming));
-            CK(cudaEventRecord(et, c->stream2));  // after the order upload / zeroing
-            CK(cudaStreamWaitEvent(c->stream3, et, 0));
-            CK(gsofa::launch_team(sp, c->sms, c->stream3));
-            CK(cudaEventRecord(ec, c->stream3));
-            CK(cudaStreamWaitEvent(st, ec, 0));
-            cudaEventDestroy(et);
-            cudaEventDestroy(ec);
-            ++launches;
-          }
-        }
         CK(gsofa::launch_solo(sp, (int)hgrid, c->stream2));
         CK(cudaEventRecord(eb, c->stream2));
         CK(cudaStreamWaitEvent(st, eb, 0));
@@ -1875,9 +1818,6 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     res->stats.first_visits = (int64_t)hs[8];
     res->stats.source_expansions = (int64_t)hs[9];
     res->stats.frontier_spilled = (int64_t)hs[10];
-    if (std::getenv("GSOFA_TEAM_DEBUG") && hs[13])
-      std::fprintf(stderr, "[team] per-step pairs: busiest warp %llu, all warps %llu -> balance %.2f of 16\n",
-                   (unsigned long long)hs[12], (unsigned long long)hs[13], (double)hs[13] / (double)hs[12]);
     res->stats.batches = nbatches;
     res->stats.max_batch = maxC;
     res->stats.kernel_launches = launches;

@@ -135,13 +135,7 @@ struct StreamParams {
   const int32_t *hgt;        // [n] etree height of a vertex
   const int32_t *pos;        // [n] vertex -> position
   const int32_t *ell;        // [8 n] ELL adjacency (id order, rows <= 8 entries), or NULL
-  // team kernel (height order): the first team_tasks source tasks of the
-  // solo queue, one source per 16-warp CTA on its own slot of team_ws; the
-  // solo kernel's tasks start at task_base
-  uint32_t *team_ws;
-  unsigned int *team_ctr;
-  long long team_tasks;
-  long long task_base;
+  long long task_base;  // the solo kernel's first task (queue entry 32 x task_base)
   // solo slot layout: word offsets of its arrays (solo_layout)
   uint32_t so_pend, so_thr, so_rsum, so_tsum, so_is, so_isum, so_queue;
 };
@@ -273,8 +267,6 @@ cudaError_t launch_supernode_scatter(const int32_t *flags, const int32_t *pos, c
 
 // ELL copy of the adjacency for the solo kernel's id order (rows <= 8
 // entries): ell[8 v + j] = j-th neighbour of v, -1 padded
-cudaError_t launch_team(const StreamParams &p, int grid, cudaStream_t st);
-size_t team_slot_words(const StreamParams &p);  // words per team slot
 cudaError_t launch_ell_build(const int32_t *rowptr, const int32_t *colidx, int32_t n, int32_t *ell,
                              cudaStream_t st);
 

@@ -749,34 +749,16 @@ __device__ __forceinline__ void solo_push(const StreamParams &p, const SoloSlot 
   }
 }
 
-// CTA-shared work queue of a team (team kernel): entries[i] = vertex + 1 (0 =
-// not written yet / consumed); every vertex is queued at most once per
-// source (its reached bit), so indices never wrap within a source.
-struct TeamQ {
-  uint32_t *entries;
-  unsigned int *qt;  // shared memory: next index to fill
-};
-
-__device__ __forceinline__ void team_push(const TeamQ &tq, bool push, int wk, int lane) {
-  const uint32_t pb = __ballot_sync(kFull, push);
-  if (!pb) return;
-  unsigned int base = 0;
-  if (lane == 0) base = atomicAdd(tq.qt, (unsigned int)__popc(pb));
-  base = __shfl_sync(kFull, base, 0);
-  if (push) __stcg(tq.entries + base + __popc(pb & lanemask_lt()), (uint32_t)wk + 1u);
-}
-
 // expand the closure items u (one per lane, -1 = none; beg/end = adjacency)
 // of the current step t of source s.  Thresholds are kept at their bitmap
 // position: the vertex id (id order) or pos(w) (height order, loaded for
 // each new fill).
-template <bool kH, int kB, bool kC = false, bool kT = false>
+template <bool kH, int kB, bool kC = false>
 __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlot &sl,
                                             SoloWarpSmem &sw, SoloPF *pf, int wb, SoloQueue &Q,
                                             int s, const SoloStep &t, int u, int beg, int end,
                                             int us, int lane, uint32_t *win, uint32_t *ring,
-                                            int rmask, uint2 *rc = nullptr,
-                                            const TeamQ *tq = nullptr) {
+                                            int rmask, uint2 *rc = nullptr) {
   constexpr bool kPF = kB > 1 && kAdjPrefetch;  // us: this lane's prefetch slot (-1: none)
   const int deg = u >= 0 ? end - beg : 0;
   // fast path (every threshold's level 0, most closure levels of a chain):
@@ -899,8 +881,7 @@ __device__ __forceinline__ void solo_expand(const StreamParams &p, const SoloSlo
           push = true;  // maxId(w) = T, not in the structure: continue with T
         }
       }
-      if constexpr (kT) team_push(*tq, push, wk, lane);  // the team's shared queue
-      else solo_push<kPF>(p, sl, sw, pf, Q, push, wk, rb[k], re[k], lane, ring, rmask);
+      solo_push<kPF>(p, sl, sw, pf, Q, push, wk, rb[k], re[k], lane, ring, rmask);
     }
   }
 }
@@ -1415,271 +1396,6 @@ __global__ void __launch_bounds__(kSoloWarps * 32, kB == 1 ? 48 / kSoloWarps : 3
 }
 
 
-// ---------------------------------------------------------------- team kernel
-// Height order only (order.cu).  The heaviest sources of a hub pattern (C4's
-// hub rows, ordered last) are chains of at most tree-height steps whose steps
-// hold many same-height thresholds with DISJOINT closures.  A team of
-// kTeamWarps warps (one CTA, one source at a time, its own solo-layout slot)
-// deals every step's threshold words -- every threshold of one height, the
-// whole segment of positions, found through the summary -- to its warps
-// (threshold bits are read from the global bitmap: a team has no window);
-// each warp closes its
-// thresholds' closures with its own worklist (shared memory, then its own
-// ring of solo_ring entries past the slot's solo layout -- a 1/kTeamWarps
-// share of one ring overflowed constantly on hub closures and every overflow
-// rescans pend, 9x slower on C4 -- then the shared pend bitmap, reloaded by
-// claiming whole words); the CTA meets at a barrier before the next step.
-// Fills found inside the source's 32-word threshold window go to the CTA's
-// shared window, the others to the global threshold bitmap.  The team takes
-// the first team_tasks source tasks of the solo queue (the pre-enqueued top
-// groups); the solo kernel starts after them (task_base).
-// Measured slower than the solo kernel on C4's hub rows (0.42 -> 0.83 s at
-// 448 team rows; profiles/r2/team_ab.txt): their height steps are too narrow
-// to occupy 16 warps.  Off by default (GSOFA_TEAM_ROWS enables it).
-constexpr int kTeamWarps = 16;
-
-struct TeamCtl {
-  uint32_t win[32];  // (unused window of solo_expand's signature)
-  int P, wb, lim, h, tmin, tmax;
-  long long task;
-  unsigned int maxw, sumw;  // dev balance statistics of the current step
-  unsigned int qh, qt;      // the team queue: next index to take / to fill
-  unsigned int idle;        // warps of the team with nothing to do
-};
-
-__device__ __forceinline__ void team_source(const StreamParams &p, const SoloSlot &sl, int s,
-                                            int warp, int lane, SoloWarpSmem &sw, TeamCtl &ctl) {
-  const int tbw = (p.n + 31) >> 5;  // threshold positions over [0, n)
-  TeamQ tq;
-  tq.entries = sl.base + p.hws_words;  // n entries past the solo layout
-  tq.qt = &ctl.qt;
-  // seed: the warps share the neighbour list of s
-  const int beg = __ldg(p.rowptr + s), end = __ldg(p.rowptr + s + 1);
-  for (int j0 = beg + 32 * warp; j0 < end; j0 += 32 * kTeamWarps) {
-    const int j = j0 + lane;
-    const int w = j < end ? __ldg(p.colidx + j) : s;
-    if (w == s) continue;
-    const uint32_t bw = vbit(w);
-    if (atomicOr(SL_IS + (w >> 5), bw) == 0u) red_sum(SL_ISUM, w);
-    if (w < s) {
-      if (atomicOr(SL_REACHED + (w >> 5), bw) == 0u) red_sum(SL_RSUM, w);
-      const int q = __ldg(p.pos + w);
-      atomicOr(SL_THR + (q >> 5), vbit(q));  // RED
-      red_sum(SL_TSUM, q);
-    }
-  }
-  fence_gpu();
-  if (warp == 0 && lane == 0) {
-    ctl.P = -1;
-    ctl.maxw = ctl.sumw = 0u;
-    ctl.qh = ctl.qt = 0u;
-  }
-  __syncthreads();
-  // no shared window: every fill goes to the global threshold bitmap (a
-  // window base far below any position sends solo_expand there)
-  const int wb = -(1 << 29);
-  SoloQueue Q = {0, 0, 0, 0, false, 0};  // (unused: the team queue replaces it)
-  for (;;) {
-    if (warp == 0) {
-      // the next step: EVERY threshold of height h = height(P), i.e. the
-      // set bits of the whole segment [P, seg_end(h)) of positions -- they
-      // are final (fills are ancestors: strictly greater height)
-      const int T0 = ctl.P < 0 ? -1 : ctl.lim - 1;
-      const int P = solo_scan_next(SL_THR, SL_TSUM, tbw, T0, lane);
-      if (lane == 0) {
-        ctl.P = P;
-        ctl.idle = 0u;
-        if (P != INT_MAX) {
-          const int4 r = __ldg(p.posrec + P);
-          ctl.lim = r.w;
-          ctl.h = __ldg(p.hgt + r.x);
-          ctl.tmin = INT_MAX;
-          ctl.tmax = -1;
-          sw.steps += 1;
-        }
-      }
-    }
-    __syncthreads();
-    const int P = ctl.P;
-    if (P == INT_MAX) break;
-    const int lim = ctl.lim;
-    int tmin = INT_MAX, tmax = -1;
-    // the segment's threshold words, by summary word (32 words each) dealt
-    // round-robin to the warps; the thresholds go to the team queue
-    const int w0 = P >> 5, w1 = (lim - 1) >> 5;
-    const unsigned int q0 = ctl.qt;  // (the step's first queue index)
-    for (int si = (w0 >> 5) + warp; si <= (w1 >> 5); si += kTeamWarps) {
-      const uint32_t sm = __ldcg(SL_TSUM + si);
-      const int wi = (si << 5) + lane;
-      uint32_t x = ((sm >> lane) & 1u) && wi >= w0 && wi <= w1 ? __ldcg(SL_THR + wi) : 0u;
-      if (wi == w0) x &= kFull << (P & 31);
-      if (wi == w1 && (lim & 31)) x &= (1u << (lim & 31)) - 1u;
-      for (;;) {
-        const bool has = x != 0u;
-        if (!__ballot_sync(kFull, has)) break;
-        int v = -1;
-        if (has) {
-          const int b = __ffs(x) - 1;
-          x &= x - 1u;
-          v = __ldg(p.posrec + (wi << 5) + b).x;
-          tmin = min(tmin, v);
-          tmax = max(tmax, v);
-        }
-        team_push(tq, has, v, lane);
-      }
-    }
-    tmin = __reduce_min_sync(kFull, tmin);
-    tmax = __reduce_max_sync(kFull, tmax);
-    if (lane == 0 && tmax >= 0) {
-      atomicMin(&ctl.tmin, tmin);
-      atomicMax(&ctl.tmax, tmax);
-    }
-    __syncthreads();
-    SoloStep t;
-    t.tmin = ctl.tmin;
-    t.tmax = ctl.tmax;
-    t.h = ctl.h;
-    const unsigned int nthr = ctl.qt - q0;  // the step's own thresholds (counted at staging)
-    const uint32_t pairs0 = sw.pairs;        // (dev balance statistics)
-    // cooperative closure: warps take up to 32 queued items at a time; the
-    // step ends when every warp is idle and nothing is queued.  A warp leaves
-    // the idle count BEFORE it claims, so an all-idle count proves that no
-    // claimed item is still being expanded.
-    bool idle = false;
-    for (;;) {
-      if (!idle) {
-        unsigned int k = 0, cnt = 0;
-        if (lane == 0) {
-          for (;;) {
-            const unsigned int h = *(volatile unsigned int *)&ctl.qh;
-            const unsigned int tt = *(volatile unsigned int *)&ctl.qt;
-            if (h >= tt) break;
-            const unsigned int c = min(32u, tt - h);
-            if (atomicCAS(&ctl.qh, h, h + c) == h) {
-              k = h;
-              cnt = c;
-              break;
-            }
-          }
-        }
-        k = __shfl_sync(kFull, k, 0);
-        cnt = __shfl_sync(kFull, cnt, 0);
-        if (cnt) {
-          int u = -1, ub = 0, ue = 0;
-          if (lane < (int)cnt) {
-            uint32_t v;
-            while ((v = __ldcg(tq.entries + k + lane)) == 0u) {
-            }  // its producer is writing it
-            __stcg(tq.entries + k + lane, 0u);
-            u = (int)v - 1;
-            ub = __ldg(p.rowptr + u);
-            ue = __ldg(p.rowptr + u + 1);
-          }
-          solo_expand<true, 1, false, true>(p, sl, sw, nullptr, wb, Q, s, t, u, ub, ue, -1, lane,
-                                            ctl.win, nullptr, 0, nullptr, &tq);
-          __syncwarp();
-          continue;
-        }
-        if (lane == 0) atomicAdd(&ctl.idle, 1u);
-        idle = true;
-      }
-      int go = 0;  // 1: work appeared, 2: the step is done
-      if (lane == 0) {
-        if (*(volatile unsigned int *)&ctl.idle == (unsigned int)kTeamWarps &&
-            *(volatile unsigned int *)&ctl.qh >= *(volatile unsigned int *)&ctl.qt)
-          go = 2;
-        else if (*(volatile unsigned int *)&ctl.qh < *(volatile unsigned int *)&ctl.qt)
-          go = 1;
-        if (go == 1) atomicSub(&ctl.idle, 1u);
-        if (go == 0) __nanosleep(100);
-      }
-      go = __shfl_sync(kFull, go, 0);
-      if (go == 2) break;
-      if (go == 1) idle = false;
-    }
-    if (lane == 0) {
-      if (warp == 0) sw.fv += ctl.qt - q0 - nthr;  // closure members (first visits below s)
-      const uint32_t mine = sw.pairs - pairs0;    // this warp's (item, neighbour) pairs in the step
-      atomicMax(&ctl.maxw, mine);
-      atomicAdd(&ctl.sumw, mine);
-    }
-    fence_gpu();  // this warp's REDs (fills, thresholds) before the next step's scan
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      // dev: sum over steps of the busiest warp's pairs vs of all pairs / warps
-      atomicAdd(p.stats + 12, (unsigned long long)ctl.maxw);
-      atomicAdd(p.stats + 13, (unsigned long long)ctl.sumw);
-      ctl.maxw = ctl.sumw = 0u;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kTeamWarps * 32, 1) team_kernel(StreamParams p) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ SoloWarpSmem s_sw[kTeamWarps];
-  __shared__ TeamCtl ctl;
-  SoloWarpSmem &sw = s_sw[warp];
-  // team slot: the solo layout, then the team queue (one entry per vertex)
-  const SoloSlot sl =
-      SoloSlot{p.team_ws + (size_t)blockIdx.x * (p.hws_words + (((size_t)p.n + 31) & ~(size_t)31))};
-  const int Vs = (int)(p.so_tsum - p.so_rsum), Ts = (int)(p.so_is - p.so_tsum);
-  if (lane == 0) sw.items = sw.pairs = sw.levels = sw.steps = sw.fv = 0u;
-  for (;;) {
-    if (threadIdx.x == 0) ctl.task = (long long)atomicAdd(p.team_ctr, 1u);
-    __syncthreads();
-    const long long k = ctl.task;
-    if (k >= p.team_tasks) break;
-    const int g = *(volatile int *)(p.hq + (k >> 5));  // pre-enqueued before the launch
-    const int r = 32 * g + (int)(k & 31);
-    if (r < p.nrows) {
-      const int s = p.map.row(r);
-      team_source(p, sl, s, warp, lane, sw, ctl);
-      fence_gpu();
-      __syncthreads();
-      if (warp == 0) solo_stage_row(p, sl, s, r, g, lane, sw);
-      __syncthreads();
-      // reset the touched reached | pend words and (height order) the global
-      // threshold words, split over the warps
-      for (int i0 = 32 * warp; i0 < Vs; i0 += 32 * kTeamWarps) {
-        const int i = i0 + lane;
-        uint32_t x = i < Vs ? __ldcg(SL_RSUM + i) : 0u;
-        if (x) SL_RSUM[i] = 0u;
-        while (x) {
-          const int b = __ffs(x) - 1;
-          x &= x - 1u;
-          const int wi = (i << 5) + b;
-          SL_REACHED[wi] = 0u;
-          SL_PEND[wi] = 0u;
-        }
-      }
-      for (int i0 = 32 * warp; i0 < Ts; i0 += 32 * kTeamWarps) {
-        const int i = i0 + lane;
-        uint32_t x = i < Ts ? __ldcg(SL_TSUM + i) : 0u;
-        if (x) SL_TSUM[i] = 0u;
-        while (x) {
-          const int b = __ffs(x) - 1;
-          x &= x - 1u;
-          SL_THR[(i << 5) + b] = 0u;
-        }
-      }
-      __threadfence();
-      __syncthreads();
-      if (lane == 0) {
-        atomicAdd(p.stats + 0, (unsigned long long)sw.items);
-        atomicAdd(p.stats + 1, (unsigned long long)sw.pairs);
-        atomicAdd(p.stats + 4, (unsigned long long)sw.pairs);
-        atomicAdd(p.stats + 2, (unsigned long long)sw.levels);
-        atomicAdd(p.stats + 3, (unsigned long long)sw.steps);
-        atomicAdd(p.stats + 8, (unsigned long long)sw.fv);
-        atomicAdd(p.stats + 9, (unsigned long long)sw.items);
-        sw.items = sw.pairs = sw.levels = sw.steps = sw.fv = 0u;
-      }
-      if (threadIdx.x == 0) atomicAdd(p.done, 1u);
-    }
-    __syncthreads();
-  }
-}
-
 // copies each staged row into the final CSR arrays (warp per row)
 __global__ void gather_kernel(const int32_t *stage, const int64_t *row_off, const int32_t *row_nL,
                               const int64_t *L_rowptr, const int64_t *U_rowptr, int rows,
@@ -1842,16 +1558,6 @@ cudaError_t launch_solo(const StreamParams &p, int grid, cudaStream_t st) {
       solo_kernel<false, 1, false, true><<<grid, kSoloWarps * 32, 0, st>>>(p);
     else solo_kernel<false, 1><<<grid, kSoloWarps * 32, 0, st>>>(p);
   }
-  return cudaGetLastError();
-}
-
-size_t team_slot_words(const StreamParams &p) {  // (as team_kernel computes it)
-  return p.hws_words + (((size_t)p.n + 31) & ~(size_t)31);
-}
-
-cudaError_t launch_team(const StreamParams &p, int grid, cudaStream_t st) {
-  if (grid <= 0 || p.team_tasks <= 0) return cudaSuccess;
-  team_kernel<<<grid, kTeamWarps * 32, 0, st>>>(p);
   return cudaGetLastError();
 }
 

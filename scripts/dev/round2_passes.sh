@@ -182,22 +182,11 @@ pass19() {
   time (timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/p19_ref.json 2> gpurun_out/p19_ref.log); tail -c 300 gpurun_out/p19_ref.json
 }
 
-pass20() {
-  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
-  timeout 600 python -m pytest tests -m gpu -q -x -k "team" 2>&1 | tail -2
-  for tr in 0 448 1024; do
-    r=$(GSOFA_TEAM_ROWS=$tr timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
-    echo "C4 team_rows=$tr $r"
-  done
-  for tr in 0 448; do r=$(GSOFA_TEAM_ROWS=$tr timeout 300 python scripts/probe.py --config C4 --reps 3 --rows 1584915:1585478 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "C4 hub rank team_rows=$tr $r"; done
-}
-
 pass21() {
-  # team-kernel parity failure (C2_20, all rows on teams): deterministic?; the rest of the
-  # suite; parallel host height order (C4 timeline, 1 vs all host threads, hub rank)
+  # (the team-kernel reruns of this pass were green twice; that kernel is removed since)
+  # the suite; parallel host height order (C4 timeline, 1 vs all host threads, hub rank)
   python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
   nproc
-  for i in 1 2; do timeout 600 python -m pytest tests -m gpu -q -k "team_kernel" 2>&1 | tail -4; done
   timeout 2400 python -m pytest tests -m gpu -q -k "not team_kernel" > gpurun_out/p21_tests.log 2>&1; echo "pytest rc=$?"; tail -4 gpurun_out/p21_tests.log
   for t in 1 0; do
     if [ "$t" = "0" ]; then unset GSOFA_HOST_THREADS; else export GSOFA_HOST_THREADS=$t; fi
@@ -227,7 +216,6 @@ case "${1:-}" in
   17) pass17 ;;
   18) pass18 ;;
   19) pass19 ;;
-  20) pass20 ;;
   21) pass21 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac

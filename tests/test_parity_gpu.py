@@ -820,29 +820,6 @@ def test_solo_ell_path(case, ell, monkeypatch):
     assert_full_equal(got, oracle.symbolic(rp, ci), f"{case} ell={ell}")
 
 
-# ------------------------- team kernel (height order, 16 warps per source) --
-
-@pytest.mark.parametrize("rows", ["0", "32", "448", "100000"])
-@pytest.mark.parametrize("case", ["C4_70", "C5_16", "C2_20", "rand"])
-def test_team_kernel(case, rows, monkeypatch):
-    """Height order, dev path (off by default): the heaviest pre-enqueued groups run on the team kernel
-    (one source per 16-warp CTA, step thresholds dealt to the warps) -- none,
-    one group, the default share, or every pre-enqueued group; the result
-    equals the oracle."""
-    monkeypatch.setenv("GSOFA_TEAM_ROWS", rows)
-    if case == "rand":
-        rp, ci = gen.random_graph(2500, 0.004, seed=91)
-    else:
-        name, scale = case.split("_")
-        rp, ci = gen.config(name, int(scale))
-    c = g.Context(0)
-    try:
-        got = run(rp, ci, c, schedule="height")
-    finally:
-        c.close()
-    assert_full_equal(got, oracle.symbolic(rp, ci), f"{case} team rows={rows}")
-
-
 @pytest.mark.parametrize("case", ["C2_24", "C5_20", "rand"])
 def test_solo_reached_cache(case, monkeypatch):
     """Dev variant (off by default): the per-warp reached-word cache skips
