@@ -197,6 +197,23 @@ pass21() {
   timeout 900 python scripts/scaling_emulation.py --config C4 --gpus 8 --out gpurun_out/p21_scal_C4.json 2>&1 | tail -3
 }
 
+pass22() {
+  # chain shape (kB = 8, 16 warps/SM): parity, then A/B against the latency shape on the
+  # chain-bound ranges (C4 hub rank and its neighbours, C5 top range), full C4, C4 8-way
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 1200 python -m pytest tests -m gpu -q -x -k "solo_shapes or auto_chain or auto_threshold" 2>&1 | tail -2
+  for rows in 1584915:1585478 1584351:1584915 1583754:1584351; do for w in 1 2; do
+    r=$(GSOFA_SOLO_WIDE=$w timeout 300 python scripts/probe.py --config C4 --reps 3 --rows $rows 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C4 rows $rows wide=$w $r"
+  done; done
+  for rows in 2092230:2097152 2087297:2092230; do for w in 0 1 2; do
+    r=$(GSOFA_SOLO_WIDE=$w timeout 300 python scripts/probe.py --config C5 --reps 2 --rows $rows 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C5 rows $rows wide=$w $r"
+  done; done
+  echo "== C4 full auto"; timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep 2"
+  timeout 900 python scripts/scaling_emulation.py --config C4 --gpus 8 --out gpurun_out/p22_scal_C4.json 2>&1 | tail -3
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -217,5 +234,6 @@ case "${1:-}" in
   18) pass18 ;;
   19) pass19 ;;
   21) pass21 ;;
+  22) pass22 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac
