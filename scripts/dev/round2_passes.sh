@@ -214,6 +214,20 @@ pass22() {
   timeout 900 python scripts/scaling_emulation.py --config C4 --gpus 8 --out gpurun_out/p22_scal_C4.json 2>&1 | tail -3
 }
 
+pass23() {
+  # C5 8-way with the top separator (the last 16,384 rows) split into four 4,096-row ranks:
+  # each fits one wave of the latency shape (32 warps x 148 SMs = 4,736 slots); bulk ranges
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for rows in 2080768:2084864 2084864:2088960 2088960:2093056 2093056:2097152; do for w in 0 1; do
+    r=$(GSOFA_SOLO_WIDE=$w timeout 300 python scripts/probe.py --config C5 --reps 2 --rows $rows 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C5 rows $rows wide=$w $r"
+  done; done
+  for rows in 0:781266 781266:1045051 1045051:1562531 1045051:1600000 1045051:1650000 1562531:2080768 1600000:2080768 1650000:2080768; do
+    r=$(timeout 300 python scripts/probe.py --config C5 --reps 2 --rows $rows 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C5 rows $rows auto $r"
+  done
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -235,5 +249,6 @@ case "${1:-}" in
   19) pass19 ;;
   21) pass21 ;;
   22) pass22 ;;
+  23) pass23 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac

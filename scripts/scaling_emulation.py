@@ -39,6 +39,10 @@ ap.add_argument("--mode", default="ranges", choices=["ranges", "interleave", "st
 ap.add_argument("--blocks-per-rank", type=int, default=4)
 ap.add_argument("--unit", type=int, default=128)
 ap.add_argument("--out", default=None)
+ap.add_argument("--bounds", type=int, nargs="+", default=None,
+                help="explicit range bounds (ranges mode, one N = len - 1) instead of the partition")
+ap.add_argument("--skip-full", action="store_true", help="reuse --full-ms instead of timing 1 GPU")
+ap.add_argument("--full-ms", type=float, default=None)
 a = ap.parse_args()
 
 rp, ci = gen.config(a.config)
@@ -75,7 +79,10 @@ def timed(rb, re, il=None):
     return best, fill
 
 
-full_ms, full_fill = timed(0, n)
+if a.skip_full:
+    full_ms, full_fill = a.full_ms, None
+else:
+    full_ms, full_fill = timed(0, n)
 print(f"{a.config}: 1 GPU {full_ms:.1f} ms, fill {full_fill}", flush=True)
 report = {"config": a.config, "n": n, "one_gpu_ms": full_ms, "fill": full_fill, "mode": a.mode,
           "unit": a.unit if a.mode == "interleave" else None, "runs": []}
@@ -108,6 +115,9 @@ for N in a.gpus:
                                "max_ms": mx, "speedup": full_ms / mx})
         continue
     bounds = gd.partition(rp, ci, N) if a.mode == "ranges" else np.array([0, n])
+    if a.bounds is not None:
+        bounds = np.array(a.bounds, dtype=np.int64)
+        N = bounds.size - 1
     per = []
     fills = 0
     for r in range(N):
@@ -117,7 +127,7 @@ for N in a.gpus:
             ms, f = timed(0, n, (N, r, a.unit))
         per.append(ms)
         fills += f
-    assert fills == full_fill
+    assert full_fill is None or fills == full_fill
     mx = max(per)
     print(f"  N={N}: ranges {list(map(int, bounds))}\n        ms {[round(x, 1) for x in per]} -> max {mx:.1f} ms, "
           f"speedup {full_ms / mx:.2f}x, efficiency {full_ms / mx / N:.2f}", flush=True)
