@@ -263,10 +263,12 @@ bool make_plan(int schedule, int64_t n, int64_t rows, int64_t vb_max, int64_t cm
 // sources").
 // npos > 0: height order (threshold bitmaps over npos positions, order.cu)
 bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int device, Plan &p,
-                      int64_t npos, bool wide) {
-  // the lockstep kernel runs id order (its slots do not depend on npos)
-  if (gsofa::stream_smem_bytes(Vmax, 0) > 200 * 1024) return false;
-  const size_t ws = gsofa::stream_ws_words(Vmax, 0), isw = gsofa::stream_is_words(n);
+                      int64_t npos, bool wide, bool lock_h = false, int lw = 16) {
+  // the lockstep kernel runs id order (its slots do not depend on npos), or
+  // height order alone (lock_h: threshold bits over npos positions, no solo)
+  const int64_t lnpos = lock_h ? npos : 0;
+  if (gsofa::stream_smem_bytes(Vmax, lnpos) > 200 * 1024) return false;
+  const size_t ws = gsofa::stream_ws_words(Vmax, lnpos), isw = gsofa::stream_is_words(n);
   const size_t hws = gsofa::solo_ws_words(Vmax, n, npos);
   const int64_t spc = gsofa::solo_warps_per_cta();
   const size_t per_light = (ws + isw) * 4, per_heavy = hws * 4 * (size_t)spc;  // per solo CTA
@@ -276,7 +278,7 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const int64_t ngroups = ceil_div(rows, 32);
   const int64_t wpc = gsofa::stream_warps_per_cta();  // lockstep slots (warps) per CTA
-  const int64_t res_light = gsofa::stream_max_blocks(device, Vmax, 0, npos, wide) * wpc;
+  const int64_t res_light = gsofa::stream_max_blocks(device, Vmax, 0, npos, wide, lock_h, lw) * wpc;
   const int64_t res_heavy = gsofa::stream_max_blocks(device, Vmax, 1, npos, wide);
   if (res_light < 1) return false;
   // solo CTAs: one per SM is resident next to the lockstep CTAs from the
@@ -289,6 +291,7 @@ bool make_plan_stream(int64_t n, int64_t rows, int64_t Vmax, int64_t budget, int
   (void)res_heavy;
   if (const char *e = std::getenv("GSOFA_SOLO_CTAS")) heavy = std::min<int64_t>(heavy, atoll(e));
   heavy = std::max<int64_t>(0, std::min<int64_t>(heavy, (int64_t)(((size_t)budget - fixed) / 2 / per_heavy)));
+  if (lock_h) heavy = 0;  // every group runs lockstep in height order
   int64_t light = heavy > 0 ? (int64_t)sms * gsofa::stream_light_per_sm_with_solo(device, Vmax, npos, wide) * wpc
                             : res_light;
   if (res_heavy < 1) heavy = 0;
@@ -996,6 +999,46 @@ int gsofa_supernode_stitch(gsofa_result *r, const gsofa_tail *prev, gsofa_tail *
   return GSOFA_OK;
 }
 
+// A2 host pass (order.cu): the elimination tree of A + A^T, heights and
+// (height, id) positions into the context's pinned block (posrec | hgt | pos,
+// 6n int32), from host inputs or a host copy of device inputs (made on s).
+static cudaError_t host_height_order(gsofa_context *c, int64_t n, int64_t nnz, bool in_dev,
+                                     const int64_t *rowptr, const int32_t *colidx, cudaStream_t s,
+                                     gsofa::OrderShape *shape) {
+  const size_t ob = ((size_t)n * 6 * 4 + 15) & ~(size_t)15;
+  const size_t need = ob + (in_dev ? ((size_t)n + 1) * 8 + (size_t)std::max<int64_t>(nnz, 1) * 4 : 0);
+  cudaError_t e;
+  if (c->ord_pin_cap < need) {
+    if (c->ord_pin) cudaFreeHost(c->ord_pin);
+    c->ord_pin = nullptr;
+    c->ord_pin_cap = 0;
+    if ((e = cudaMallocHost((void **)&c->ord_pin, need)) != cudaSuccess) return e;
+    c->ord_pin_cap = need;
+  }
+  if (!c->ord_scratch) c->ord_scratch = gsofa::order_scratch_new();
+  int32_t *ord_host = (int32_t *)c->ord_pin;
+  const int64_t *rp_h = rowptr;
+  const int32_t *ci_h = colidx;
+  if (in_dev) {
+    int64_t *hrp = (int64_t *)(c->ord_pin + ob);
+    int32_t *hci = (int32_t *)(c->ord_pin + ob + ((size_t)n + 1) * 8);
+    if ((e = cudaMemcpyAsync(hrp, rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return e;
+    if (nnz && (e = cudaMemcpyAsync(hci, colidx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    rp_h = hrp;
+    ci_h = hci;
+  }
+  auto now_ms = [] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t0 = now_ms();
+  *shape = gsofa::height_order(n, rp_h, ci_h, ord_host + 4 * n, ord_host + 5 * n, ord_host, c->ord_scratch);
+  if (std::getenv("GSOFA_TIMELINE")) std::fprintf(stderr, "[timeline] host height order %.3f ms\n", now_ms() - t0);
+  return cudaSuccess;
+}
+
 int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const int32_t *colidx,
                    const gsofa_opts *opts_in, gsofa_result **out) {
   if (!out) {
@@ -1089,8 +1132,15 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   unsigned int maxdeg = 0;  // largest row of A (validation pass)
   int64_t ord_npos = 0;  // > 0: height order possible (threshold bitmaps sized for n positions)
   bool auto_order = false;  // AUTO: pick the threshold order from the tree's shape
-  // solo kernel shape: dev knob for now
-  const bool solo_wide = std::getenv("GSOFA_SOLO_WIDE") && atoi(std::getenv("GSOFA_SOLO_WIDE")) != 0;
+  bool lock_h = false;      // height order in the lockstep kernel (no solo kernel)
+  int lock_w = 16;          // ... its warps per CTA
+  // solo kernel shape: the latency shape (4 pair batches in
+  // flight, 32 warps/SM) when the call's sources fit one wave of its slots --
+  // the chain-bound ranks of a multi-GPU split (C2's top ranks: 61 -> 57 ms;
+  // two waves of long chains lose: C5's 4,922-row top range 645 -> 860 ms);
+  // GSOFA_SOLO_WIDE=0/1 forces a shape (dev A/B)
+  const bool solo_wide = std::getenv("GSOFA_SOLO_WIDE") ? atoi(std::getenv("GSOFA_SOLO_WIDE")) != 0
+                                                        : rows <= 32 * (int64_t)std::max(c->sms, 1);
 
   CK(cudaSetDevice(c->device));
   e_start = ev();
@@ -1173,6 +1223,33 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   if (o.schedule == GSOFA_SCHEDULE_HEIGHT || auto_order) {
     ord_npos = n;
     if ((rc = grow_device(&c->ord_buf, &c->ord_cap, (size_t)n * 6, st)) != GSOFA_OK) goto fail;
+    if (!std::getenv("GSOFA_HEIGHT_SOLO")) {
+      // height order in the LOCKSTEP kernel (default): a group's steps are the
+      // union of its sources' heights (<= the tree height), and the 32 hub /
+      // separator sources of a group share their closures (C4's top groups:
+      // 10-15x fewer pairs than 32 solo sources, union steps ~ one source's),
+      // so every group runs lockstep and no solo kernel is launched.  The tree
+      // is needed before the launch: computed here, on the host.
+      // GSOFA_HEIGHT_SOLO=1 keeps the solo kernel's height order (dev A/B).
+      gsofa::OrderShape shape;
+      CK(host_height_order(c, n, nnz, in_dev, rowptr, colidx, st, &shape));
+      bool use_h = true;
+      if (auto_order) {
+        // AUTO: height order when the last row's id-order chain (about
+        // |L(n-1,:)| threshold steps) is far longer than the tree is high
+        // (C4's hub rows: 577k vs 4.2k; 3D grids keep id order)
+        use_h = shape.last_row_chain > 4 * shape.height;
+        o.schedule = use_h ? GSOFA_SCHEDULE_HEIGHT : GSOFA_SCHEDULE_THRESHOLD;
+        auto_order = false;
+      }
+      if (use_h) {
+        lock_h = true;
+        lock_w = gsofa::lock_warps(ceil_div(rows, 32), c->sms);
+        CK(cudaMemcpyAsync(c->ord_buf, c->ord_pin, (size_t)n * 6 * 4, cudaMemcpyHostToDevice, st));
+      } else {
+        ord_npos = 0;
+      }
+    }
   }
   // ---------------------------------------------------- plan + arena
   {
@@ -1180,7 +1257,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
         o.max_concurrent ? o.max_concurrent : 65536;  // FIFO: one batch when it fits (C3 -6% vs 16k)
     const int64_t budget_req = o.mem_budget_bytes ? o.mem_budget_bytes : c->budget;
     int64_t key[7] = {o.schedule, n, rb, re ^ ((int64_t)rmap.q << 32) ^ ((int64_t)rmap.N << 40),
-                      budget_req, cmax_req, ord_npos * 2 + solo_wide};
+                      budget_req, cmax_req, ord_npos * 256 + lock_w * 4 + solo_wide * 2 + lock_h};
     bool ok = true;
     if (std::equal(key, key + 7, c->plan_key)) {
       plan = c->plan_cache;
@@ -1191,7 +1268,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       ok = o.schedule == GSOFA_SCHEDULE_FIFO
                ? make_plan(o.schedule, n, rows, vb_max, cmax_req, budget, plan)
                : make_plan_stream(n, rows, std::min<int64_t>(n, re), budget, c->device, plan,
-                                  ord_npos, solo_wide);
+                                  ord_npos, solo_wide, lock_h, lock_w);
       if (!ok && auto_fifo) {
         // AUTO picked FIFO but its smallest batch does not fit: threshold
         // order needs far less memory per source (no maxId labels)
@@ -1358,7 +1435,9 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     sp.light_slots = (int32_t)plan.light;
     sp.abort_cycles = 0;
     gsofa::solo_layout(plan.Vmax, n, ord_npos, &sp);
-    sp.hmode = o.schedule == GSOFA_SCHEDULE_HEIGHT;  // AUTO: decided at the solo launch
+    sp.hmode = o.schedule == GSOFA_SCHEDULE_HEIGHT && !lock_h;  // AUTO: decided at the solo launch
+    sp.lmode = lock_h;
+    sp.lwarps = lock_w;
     sp.wide = solo_wide;
     sp.nnz = nnz;
     sp.npos = (int32_t)ord_npos;
@@ -1420,37 +1499,9 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
           // (height, id) positions on the host (order.cu; SURVEY §8(a) A2,
           // O(nnz alpha)), while the lockstep kernel -- id order, no tree
           // needed -- runs; then up to the solo kernel's stream
-          const size_t ob = ((size_t)n * 6 * 4 + 15) & ~(size_t)15;  // posrec | hgt | pos
-          const size_t need = ob + (in_dev ? ((size_t)n + 1) * 8 + (size_t)std::max<int64_t>(nnz, 1) * 4 : 0);
-          if (c->ord_pin_cap < need) {
-            if (c->ord_pin) cudaFreeHost(c->ord_pin);
-            c->ord_pin = nullptr;
-            c->ord_pin_cap = 0;
-            CK(cudaMallocHost((void **)&c->ord_pin, need));
-            c->ord_pin_cap = need;
-          }
-          if (!c->ord_scratch) c->ord_scratch = gsofa::order_scratch_new();
+          gsofa::OrderShape shape;
+          CK(host_height_order(c, n, nnz, in_dev, rowptr, colidx, c->stream2, &shape));
           int32_t *ord_host = (int32_t *)c->ord_pin;
-          const int64_t *rp_h = rowptr;
-          const int32_t *ci_h = colidx;
-          if (in_dev) {
-            int64_t *hrp = (int64_t *)(c->ord_pin + ob);
-            int32_t *hci = (int32_t *)(c->ord_pin + ob + ((size_t)n + 1) * 8);
-            CK(cudaMemcpyAsync(hrp, rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream2));
-            if (nnz) CK(cudaMemcpyAsync(hci, colidx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream2));
-            CK(cudaStreamSynchronize(c->stream2));
-            rp_h = hrp;
-            ci_h = hci;
-          }
-          auto now_ms = [] {
-            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
-                .count();
-          };
-          const double t_ord = now_ms();
-          const gsofa::OrderShape shape = gsofa::height_order(n, rp_h, ci_h, ord_host + 4 * n, ord_host + 5 * n,
-                                                              ord_host, c->ord_scratch);
-          if (std::getenv("GSOFA_TIMELINE"))
-            std::fprintf(stderr, "[timeline] host height order %.3f ms\n", now_ms() - t_ord);
           if (auto_order) {
             // AUTO: height order when the last row's id-order chain (about
             // |L(n-1,:)| threshold steps) is far longer than the tree is
@@ -1459,7 +1510,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
             // step.  The chain-bound pattern also takes the latency shape.
             const bool use_h = shape.last_row_chain > 4 * shape.height;
             sp.hmode = use_h;
-            if (!std::getenv("GSOFA_SOLO_WIDE")) sp.wide = use_h;
+            if (!std::getenv("GSOFA_SOLO_WIDE")) sp.wide = use_h || solo_wide;
             o.schedule = use_h ? GSOFA_SCHEDULE_HEIGHT : GSOFA_SCHEDULE_THRESHOLD;
           }
           if (sp.hmode)

@@ -127,6 +127,8 @@ struct StreamParams {
   // height (all same-height thresholds of the window per step); threshold
   // bitmaps then indexed by position (vertices sorted by (height, id), npos = n)
   int32_t hmode;
+  int32_t lmode;             // lockstep kernel: 0 = id order, 1 = height order (no solo kernel)
+  int32_t lwarps;            // warps per lockstep CTA in height order (lock_warps)
   int32_t npos;
   int32_t wide;              // solo kernel shape: 0 = throughput (48 warps/SM), 1 = latency (4 batches)
   int64_t nnz;               // entries of colidx (the latency shape's bulk copies stay inside)
@@ -141,7 +143,10 @@ struct StreamParams {
 };
 size_t stream_ws_words(int64_t Vmax, int64_t npos);
 size_t stream_is_words(int64_t n);
-int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos, bool wide);
+// lock_h: the lockstep kernel in height order (heavy = 0; its slots then hold npos threshold bits)
+int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos, bool wide, bool lock_h = false,
+                      int lw = 16);
+int lock_warps(int64_t groups, int sms);  // warps per lockstep CTA in height order
 int stream_heavy_ratio();  // warps of a solo CTA / warps of a lockstep CTA
 int stream_warps_per_cta();  // lockstep slots (one group per warp) per CTA
 size_t solo_ws_words(int64_t Vmax, int64_t n, int64_t npos);  // per solo slot (one warp, one source)

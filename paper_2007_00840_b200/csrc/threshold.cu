@@ -109,9 +109,14 @@ constexpr int kBatch = 4;  // 32-pair batches whose atomics a warp keeps in flig
 // pend mask (enqueue test); both are issued for kBatch*32 pairs before any
 // result is used.  Every other update is a RED, published by fence_gpu()
 // before the next barrier.
+// Height order (kH, lockstep): the step is every threshold of one etree
+// height h (ids tmin = T .. tmax, union over the group's sources); a newly
+// reached w < source is a fill iff w > tmax, or w > tmin and height(w) > h
+// (order.cu), and its threshold bit sits at its position pos(w).
+template <bool kH = false>
 __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, int s0g, int T,
                                        int u, uint32_t *nq, int *nqn, int *minfill, int lane,
-                                       Counters &c) {
+                                       Counters &c, int tmax = 0, int hh = 0) {
   const int32_t *__restrict__ rowptr = p.rowptr;
   const int32_t *__restrict__ colidx = p.colidx;
   int beg = 0, deg = 0;
@@ -172,15 +177,17 @@ __device__ __forceinline__ void expand(const StreamParams &p, const Slot &sl, in
       push[k] = false;
       po[k] = kFull;
       if (nw) {
-        if (w[k] > T) {
+        const bool fill = kH ? (w[k] > tmax || (w[k] > T && __ldg(p.hgt + w[k]) > hh)) : w[k] > T;
+        if (fill) {
           // newMaxId T < w: (src, w) is a fill of L (R4); w proposes newMaxId
-          // = w later, as a threshold
+          // = w later, as a threshold (at its bitmap position q)
+          const int q = kH ? __ldg(p.pos + w[k]) : w[k];
           atomicOr(sl.is + w[k], nw);                                           // RED
           atomicOr(sl.isum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));          // RED
           atomicOr(sl.state + 2 * w[k] + 1, nw);                                // RED
-          atomicOr(sl.thr + (w[k] >> 5), 1u << (w[k] & 31));                    // RED
-          atomicOr(sl.tsum + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));          // smem
-          atomicMin(minfill, w[k]);                                             // smem
+          atomicOr(sl.thr + (q >> 5), 1u << (q & 31));                          // RED
+          atomicOr(sl.tsum + (q >> 10), 1u << ((q >> 5) & 31));                // smem
+          atomicMin(minfill, q);                                                // smem
         } else {
           // w < T: maxId(w) = T, not in the structure: continue with T
           po[k] = atomicOr(sl.state + 2 * w[k] + 1, nw);
@@ -319,12 +326,19 @@ __device__ __forceinline__ void stage_rows(const StreamParams &p, uint32_t *is, 
 // Lockstep kernel: the 32 sources of a group share frontier items (one bit
 // each); a group that runs longer than p.abort_cycles is abandoned -- its
 // slot is cleaned -- and handed to the solo kernel through the heavy queue.
-__global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParams p) {
-  constexpr int kWarps = kLightWarps;
+// kH: etree-height order (order.cu) -- a step takes every threshold of one
+// height (the group's union: the whole segment of positions), so a group is
+// at most tree-height steps long and the 32 sources of hub / separator groups
+// share their closures (C4); the threshold bitmap is indexed by position.
+// kW warps per CTA: 4 in id order; height order takes 16 by default (one
+// group's step spreads over more warps: a hub group is one CTA's work)
+template <bool kH, int kW = kLightWarps>
+__global__ void __launch_bounds__(kW * 32, kW == 4 ? 8 : (kW == 16 ? 2 : 1)) stream_kernel(StreamParams p) {
+  constexpr int kWarps = kW;
   constexpr int kThreads = kWarps * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   const int n = p.n, Vmax = p.Vmax;
-  const int tbw_max = (Vmax + 31) >> 5;
+  const int tbw_max = kH ? (p.npos + 31) >> 5 : (Vmax + 31) >> 5;
   const int rsw = (Vmax + 1023) >> 10;
   Slot sl;
   const size_t slot = blockIdx.x;
@@ -343,6 +357,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
   __shared__ long long s_rowoff[32];
   __shared__ int s_nL[32];
   __shared__ int s_ok, s_abort;
+  __shared__ int s_hs[4];  // kH step: segment end, height, tmin, tmax
   Counters c = {0, 0, 0, 0, 0, 0, 0, 0u};
   // live lockstep CTAs: while any runs, it may still abandon a group to the
   // solo kernel's queue (idle solo warps wait only as long as that can happen)
@@ -374,7 +389,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
     const int s0g = p.map.row(32 * g);  // the group's 32 rows are consecutive
     const int nsrc = min(32, p.nrows - 32 * g);
     const int Vb = min(n, s0g + nsrc);  // maxId only below the largest source
-    const int tbw = (Vb + 31) >> 5;
+    const int tbw = kH ? tbw_max : (Vb + 31) >> 5;
     for (int i = tid; i < ((tbw + 31) >> 5); i += kThreads) s_tsum[i] = 0u;
     __syncthreads();
 
@@ -394,8 +409,9 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
           atomicOr(sl.state + 2 * w, bit);                            // RED
           atomicOr(sl.rsum + (w >> 10), 1u << ((w >> 5) & 31));       // RED
           atomicOr(sl.state + 2 * w + 1, bit);                        // RED
-          atomicOr(sl.thr + (w >> 5), 1u << (w & 31));                // RED
-          atomicOr(sl.tsum + (w >> 10), 1u << ((w >> 5) & 31));       // smem
+          const int q = kH ? __ldg(p.pos + w) : w;                    // bitmap position
+          atomicOr(sl.thr + (q >> 5), 1u << (q & 31));                // RED
+          atomicOr(sl.tsum + (q >> 10), 1u << ((q >> 5) & 31));       // smem
         }
       }
     }
@@ -420,15 +436,71 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
         s_scan[(step + 2) % 3] = INT_MAX;
         s_minfill[(step + 2) % 3] = INT_MAX;
       }
-      // level 0: warp 0 expands T itself; warp 1 finds the next threshold
-      // above T in parallel (new fills of this step go to s_minfill[nx3])
-      if (warp == 0) {
-        expand(p, sl, s0g, T, lane == 0 ? T : -1, sl.list1, &s_qn[1], &s_minfill[nx3], lane, c);
-      } else if (warp == 1) {
-        const int nt = scan_next(sl.thr, sl.tsum, tbw, T, lane);
-        if (lane == 0) s_scan[nx3] = nt;
+      int tmin = T, tmax = 0, hh = 0;
+      if (kH) {
+        // the step: every threshold of height h = height(T), positions
+        // [T, seg_end(h)) -- all final (fills are ancestors: greater height);
+        // their vertices become the first level's items (list1)
+        if (tid == 0) {
+          const int4 r = __ldg(p.posrec + T);
+          s_hs[0] = r.w;
+          s_hs[1] = __ldg(p.hgt + r.x);
+          s_hs[2] = INT_MAX;
+          s_hs[3] = -1;
+        }
+        __syncthreads();
+        const int lim = s_hs[0];
+        const int w0 = T >> 5, w1 = (lim - 1) >> 5;
+        int tmn = INT_MAX, tmx = -1;
+        for (int si = (w0 >> 5) + warp; si <= (w1 >> 5); si += kWarps) {
+          const int wi = (si << 5) + lane;
+          uint32_t x = ((sl.tsum[si] >> lane) & 1u) && wi >= w0 && wi <= w1 ? __ldcg(sl.thr + wi) : 0u;
+          if (wi == w0) x &= kFull << (T & 31);
+          if (wi == w1 && (lim & 31)) x &= (1u << (lim & 31)) - 1u;
+          for (;;) {
+            const bool has = x != 0u;
+            const uint32_t hb = __ballot_sync(kFull, has);
+            if (!hb) break;
+            int v = -1;
+            if (has) {
+              const int b = __ffs(x) - 1;
+              x &= x - 1u;
+              v = __ldg(&p.posrec[(wi << 5) + b].x);
+              tmn = min(tmn, v);
+              tmx = max(tmx, v);
+            }
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&s_qn[1], __popc(hb));
+            base = __shfl_sync(kFull, base, 0);
+            if (has) sl.list1[base + __popc(hb & lanemask_lt())] = (uint32_t)v;
+          }
+        }
+        tmn = __reduce_min_sync(kFull, tmn);
+        tmx = __reduce_max_sync(kFull, tmx);
+        if (lane == 0 && tmx >= 0) {
+          atomicMin(&s_hs[2], tmn);
+          atomicMax(&s_hs[3], tmx);
+        }
+        __syncthreads();
+        // the next threshold past the segment (this step's fills: s_minfill[nx3])
+        if (warp == 0) {
+          const int nt = scan_next(sl.thr, sl.tsum, tbw, lim - 1, lane);
+          if (lane == 0) s_scan[nx3] = nt;
+        }
+        tmin = s_hs[2];
+        tmax = s_hs[3];
+        hh = s_hs[1];
+      } else {
+        // level 0: warp 0 expands T itself; warp 1 finds the next threshold
+        // above T in parallel (new fills of this step go to s_minfill[nx3])
+        if (warp == 0) {
+          expand(p, sl, s0g, T, lane == 0 ? T : -1, sl.list1, &s_qn[1], &s_minfill[nx3], lane, c);
+        } else if (warp == 1) {
+          const int nt = scan_next(sl.thr, sl.tsum, tbw, T, lane);
+          if (lane == 0) s_scan[nx3] = nt;
+        }
+        __syncthreads();
       }
-      __syncthreads();
       c.levels += 1;
       // closure levels: every item has newMaxId T.  Levels only consume
       // returning atomics (reached, pend pushes); the REDs of this step
@@ -447,7 +519,7 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
         c.levels += 1;
         for (int b0 = warp * 32; b0 < qn; b0 += kThreads) {
           const int u = (b0 + lane < qn) ? (int)cq[b0 + lane] : -1;
-          expand(p, sl, s0g, T, u, nq, &s_qn[nxt], &s_minfill[nx3], lane, c);
+          expand<kH>(p, sl, s0g, tmin, u, nq, &s_qn[nxt], &s_minfill[nx3], lane, c, tmax, hh);
         }
         __syncthreads();
       }
@@ -473,8 +545,13 @@ __global__ void __launch_bounds__(kLightWarps * 32, 8) stream_kernel(StreamParam
           x &= x - 1u;
           const int line = (i << 5) + b;
           reinterpret_cast<uint2 *>(sl.state)[(line << 5) + lane] = make_uint2(0u, 0u);
-          if (lane == 0) sl.thr[line] = 0u;
+          if (!kH && lane == 0) sl.thr[line] = 0u;
         }
+      }
+      if (kH) {
+        // threshold words sit at positions: the shared summary lists them
+        for (int i = warp; i < ((tbw + 31) >> 5); i += kWarps)
+          if ((sl.tsum[i] >> lane) & 1u) sl.thr[(i << 5) + lane] = 0u;
       }
     }
     // the clears above are plain stores; the next group's atomics on the same
@@ -1431,7 +1508,26 @@ size_t stream_smem_bytes(int64_t Vmax, int64_t npos) {
 }
 
 // kernel instances of the two threshold orders (kH = height order)
-const void *stream_fn(bool) { return (const void *)stream_kernel; }  // id order only
+// warps per lockstep CTA in height order: 32 for calls of few groups (a hub
+// group is one CTA's work: C4's hub rank 324 -> 238 ms vs 16 warps), else 16
+// (more groups in flight: the full C4 371 vs 410 ms); GSOFA_LOCK_WARPS = 4 /
+// 16 / 32 forces it (dev A/B)
+int lock_warps(int64_t groups, int sms) {
+  if (const char *e = std::getenv("GSOFA_LOCK_WARPS")) {
+    const int w = atoi(e);
+    if (w == 4 || w == 16 || w == 32) return w;
+  }
+  return groups <= 16 * (int64_t)sms ? 32 : 16;
+}
+const void *stream_fn(bool h, int lw) {
+  if (!h) return (const void *)stream_kernel<false>;
+  switch (lw) {
+    case 4: return (const void *)stream_kernel<true, 4>;
+    case 32: return (const void *)stream_kernel<true, 32>;
+    default: return (const void *)stream_kernel<true, 16>;
+  }
+}
+
 const void *solo_fn(bool h, bool wide) {
   if (wide) return h ? (const void *)solo_kernel<true, 4> : (const void *)solo_kernel<false, 4>;
   return h ? (const void *)solo_kernel<true, 1> : (const void *)solo_kernel<false, 1>;
@@ -1440,11 +1536,11 @@ const void *solo_fn(bool h, bool wide) {
 // dynamic shared memory of the solo kernel: the latency shape's prefetch slots
 size_t solo_dyn_smem(bool wide) { return wide && kAdjPrefetch ? sizeof(SoloPF) * kSoloWarps : 0; }
 
-int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos, bool wide) {
+int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos, bool wide, bool lock_h, int lw) {
   int sms = 0, per = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
   cudaError_t e;
-  const bool h = npos > 0;
+  const bool h = heavy ? npos > 0 : lock_h;
   if (heavy) {
     const size_t dyn = solo_dyn_smem(wide);
     if (dyn && cudaFuncSetAttribute(solo_fn(h, wide), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1452,12 +1548,12 @@ int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos, bool wi
       return 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solo_fn(h, wide), kSoloWarps * 32, dyn);
   } else {
-    const size_t smem = stream_smem_bytes(Vmax, 0);  // the lockstep kernel runs id order
+    const size_t smem = stream_smem_bytes(Vmax, lock_h ? npos : 0);  // lockstep: id or height order
     if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(stream_fn(h), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaFuncSetAttribute(stream_fn(h, lw), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
       return 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_fn(h), kLightWarps * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_fn(h, lw), (h ? lw : kLightWarps) * 32, smem);
   }
   if (e != cudaSuccess) return 0;
   return sms * per;
@@ -1472,7 +1568,7 @@ int stream_light_per_sm_with_solo(int device, int64_t Vmax, int64_t npos, bool w
   cudaFuncAttributes fs, fl;
   const bool h = npos > 0;
   if (cudaFuncGetAttributes(&fs, solo_fn(h, wide)) != cudaSuccess ||
-      cudaFuncGetAttributes(&fl, stream_fn(h)) != cudaSuccess)
+      cudaFuncGetAttributes(&fl, stream_fn(false, kLightWarps)) != cudaSuccess)  // next to a solo CTA: id order
     return 0;
   int regs = 0, warps = 0, smem_sm = 0;
   cudaDeviceGetAttribute(&regs, cudaDevAttrMaxRegistersPerMultiprocessor, device);
@@ -1530,13 +1626,21 @@ int solo_warps_per_cta() { return kSoloWarps; }
 
 cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st) {
   if (grid <= 0) return cudaSuccess;
-  const size_t smem = stream_smem_bytes(p.Vmax, 0);
+  const bool h = p.lmode != 0;
+  const size_t smem = stream_smem_bytes(p.Vmax, h ? p.npos : 0);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(stream_fn(p.hmode), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(stream_fn(h, p.lwarps), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  stream_kernel<<<grid, kLightWarps * 32, smem, st>>>(p);
+  if (!h) {
+    stream_kernel<false><<<grid, kLightWarps * 32, smem, st>>>(p);
+  } else {
+    switch (p.lwarps) {
+      case 4: stream_kernel<true, 4><<<grid, 4 * 32, smem, st>>>(p); break;
+      case 32: stream_kernel<true, 32><<<grid, 32 * 32, smem, st>>>(p); break;
+      default: stream_kernel<true, 16><<<grid, 16 * 32, smem, st>>>(p); break;
+    }
+  }
   return cudaGetLastError();
 }
 

@@ -228,6 +228,70 @@ pass23() {
   done
 }
 
+pass24() {
+  # latency shape for calls with few rows (<= one wave of its 4,736 slots): C2's chain-bound
+  # ranks of the 2/4/8-way splits, throughput vs latency shape
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for rows in 256702:258564 258564:259763 259763:260956 260956:262144 257226:259905 259905:262144 257226:262144; do for w in 0 1; do
+    r=$(GSOFA_SOLO_WIDE=$w timeout 300 python scripts/probe.py --config C2 --reps 3 --rows $rows 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C2 rows $rows wide=$w $r"
+  done; done
+}
+
+pass25() {
+  # AUTO latency shape for one-wave calls: smoke, full suite, C2/C5 emulation, bench (C5) +
+  # reference arm + ncu launch list of the bench command
+  python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/p25_smoke.log 2>&1; tail -1 gpurun_out/p25_smoke.log
+  timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/p25_tests.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/p25_tests.log
+  timeout 900 python scripts/scaling_emulation.py --config C2 --gpus 2 4 8 --out gpurun_out/p25_scal_C2.json 2>&1 | tail -7
+  timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/p25_bench.json 2> gpurun_out/p25_bench.log; tail -c 600 gpurun_out/p25_bench.json
+  timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/p25_ref.json 2> gpurun_out/p25_ref.log; tail -c 300 gpurun_out/p25_ref.json
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/p25_launches_C5.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/p25_ncu_bench.log 2>&1; echo "ncu rc=$?"
+  timeout 900 python scripts/scaling_emulation.py --config C5 --gpus 2 4 8 --out gpurun_out/p25_scal_C5.json 2>&1 | tail -7
+}
+
+pass26() {
+  # height order in the lockstep kernel (union of the group's same-height thresholds per
+  # step; no solo kernel): parity, then C4 A/B against the solo kernel's height order
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 1500 python -m pytest tests -m gpu -q -x -k "height or random_graphs or config_shapes or paper_example or solo_shapes or auto_threshold or auto_schedule" 2>&1 | tail -3
+  for hs in 0 1; do
+    if [ "$hs" = "1" ]; then export GSOFA_HEIGHT_SOLO=1; else unset GSOFA_HEIGHT_SOLO; fi
+    echo "== C4 full height_solo=$hs"; GSOFA_TIMELINE=1 timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep" | tail -2
+    for rows in 1584915:1585478 1584351:1584915 1583754:1584351 1532558:1583754; do
+      r=$(timeout 300 python scripts/probe.py --config C4 --reps 3 --rows $rows 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+      echo "C4 rows $rows height_solo=$hs $r"
+    done
+  done
+  unset GSOFA_HEIGHT_SOLO
+  timeout 900 python scripts/scaling_emulation.py --config C4 --gpus 2 4 8 --out gpurun_out/p26_scal_C4.json 2>&1 | tail -7
+}
+
+pass27() {
+  # lockstep height order with 16 / 32 warps per CTA (a hub group is one CTA's work)
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 900 python -m pytest tests -m gpu -q -x -k "lockstep_height or height_order_hub or auto_threshold" 2>&1 | tail -2
+  GSOFA_LOCK_WARPS=32 timeout 900 python -m pytest tests -m gpu -q -x -k "lockstep_height" 2>&1 | tail -2
+  for lw in 16 32; do
+    export GSOFA_LOCK_WARPS=$lw
+    echo "== C4 full lock_warps=$lw"; timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep 2"
+    for rows in 1584915:1585478 1584351:1584915 1583754:1584351 1532558:1583754 0:438521; do
+      r=$(timeout 300 python scripts/probe.py --config C4 --reps 3 --rows $rows 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+      echo "C4 rows $rows lock_warps=$lw $r"
+    done
+  done
+  unset GSOFA_LOCK_WARPS
+}
+
+pass28() {
+  # lockstep height order by default (warps per CTA by call size): full suite, C4 timeline, C4 emulation
+  python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/p28_smoke.log 2>&1; tail -1 gpurun_out/p28_smoke.log
+  timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/p28_tests.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/p28_tests.log
+  echo "== C4 full"; GSOFA_TIMELINE=1 timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep 2\|height order" | tail -2
+  timeout 900 python scripts/scaling_emulation.py --config C4 --gpus 2 4 8 --out gpurun_out/p28_scal_C4.json 2>&1 | tail -7
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -250,5 +314,10 @@ case "${1:-}" in
   21) pass21 ;;
   22) pass22 ;;
   23) pass23 ;;
+  24) pass24 ;;
+  25) pass25 ;;
+  26) pass26 ;;
+  27) pass27 ;;
+  28) pass28 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac

@@ -574,6 +574,7 @@ def test_solo_shapes(schedule, wide, monkeypatch):
     all groups), repeated on one context: the oracle's result each time."""
     monkeypatch.setenv("GSOFA_SOLO_WIDE", wide)
     monkeypatch.setenv("GSOFA_ABORT_MS", "0.00001")
+    monkeypatch.setenv("GSOFA_HEIGHT_SOLO", "1")  # height order in the solo kernel
     cases = [gen.config("C4", 60), gen.config("C5", 14), gen.config("C2", 16), gen.config("C3", 2000)]
     wants = [oracle.symbolic(rp, ci) for rp, ci in cases]
     with g.Context(0) as c:
@@ -602,6 +603,40 @@ def test_auto_threshold_order_full(ctx, name, want):
     r.free()
     assert sched == want
     assert_full_equal(got, oracle.symbolic(rp, ci), tag=name)
+
+
+@pytest.mark.parametrize("solo", ["0", "1"])
+def test_height_order_hub_rows(ctx, solo, monkeypatch):
+    """Height order on a call holding only C4's hub rows (the top rank of an
+    8-way split): in the lockstep kernel (default; the group's sources share
+    their closures) and in the solo kernel (GSOFA_HEIGHT_SOLO=1); bit-exact
+    against the oracle on those rows."""
+    if solo == "1":
+        monkeypatch.setenv("GSOFA_HEIGHT_SOLO", "1")
+    rp, ci = gen.config("C4")
+    n = rp.size - 1
+    rb = n - 563
+    got = run(rp, ci, ctx, row_begin=rb, row_end=n, schedule="height")
+    want = oracle.symbolic(rp, ci, row_begin=rb, row_end=n)
+    assert_full_equal(got, want, tag=f"C4 hub rows solo={solo}")
+    for k in ("nnz_L", "nnz_U", "nsuper", "fill_count"):
+        assert got[k] == want[k], k
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_lockstep_height_random(ctx, seed):
+    """Lockstep height order (the group's union of same-height thresholds per
+    step) on random patterns with hubs and on small configs, several groups,
+    with and without a tight budget: the oracle's result."""
+    rng = np.random.default_rng(700 + seed)
+    n = int(rng.integers(200, 3000))
+    rp, ci = gen.random_graph(n, float(rng.uniform(0.001, 0.02)), seed=int(rng.integers(1 << 30)))
+    want = oracle.symbolic(rp, ci)
+    assert_full_equal(run(rp, ci, ctx, schedule="height"), want, tag=f"random n={n}")
+    assert_full_equal(run(rp, ci, ctx, schedule="height", max_concurrent=32), want, tag=f"random C=32 n={n}")
+    for name, scale in (("C4", 40 + 10 * seed), ("C2", 10 + seed), ("C5", 8 + seed)):
+        rp, ci = gen.config(name, scale)
+        assert_full_equal(run(rp, ci, ctx, schedule="height"), oracle.symbolic(rp, ci), tag=f"{name}_{scale}")
 
 
 @pytest.mark.parametrize("name,scale,rb", [("C5", 14, 0), ("C4", 60, 777), ("C1", None, 0)])
