@@ -225,7 +225,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5", choices=sorted(CONFIG_DESC))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--schedule", default="auto", choices=["auto", "threshold", "fifo"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "threshold", "height", "fifo"])
     ap.add_argument("--max-concurrent", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -402,7 +402,8 @@ def main():
     alg, alg_parts = (algorithmic_bytes(stats_acc, n, (re - rb) * args.steps, local_fills)
                       if stats_acc else (0, {}))
     achieved = alg / (trav_ms / 1e3) / 1e9 if trav_ms > 0 else 0.0
-    kern = "solo_kernel+stream_kernel" if sched_used == "threshold" else "traverse_kernel"
+    kern = {"threshold": "solo_kernel+stream_kernel", "height": "stream_kernel (height order)"}.get(
+        sched_used, "traverse_kernel")
     roofline = {"kernel": kern, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                 "bytes_model": "SURVEY.md §8(d): 4 B/edge inspection + 4 B/first visit + "

@@ -1132,6 +1132,7 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
   unsigned int maxdeg = 0;  // largest row of A (validation pass)
   int64_t ord_npos = 0;  // > 0: height order possible (threshold bitmaps sized for n positions)
   bool auto_order = false;  // AUTO: pick the threshold order from the tree's shape
+  bool auto_hubs = false;   // AUTO: the pattern has hub rows
   bool lock_h = false;      // height order in the lockstep kernel (no solo kernel)
   int lock_w = 16;          // ... its warps per CTA
   // solo kernel shape: the latency shape (4 pair batches in
@@ -1215,7 +1216,14 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
     // mean), where height order was measured to win (C4: 1.19 s -> 0.45 s);
     // on grids it would only delay the solo kernel (C5: ~5%)
     const int64_t mean = std::max<int64_t>(1, nnz / std::max<int64_t>(1, n));
-    auto_order = !auto_fifo && (int64_t)maxdeg > 32 * mean;
+    auto_hubs = (int64_t)maxdeg > 32 * mean;
+    // large patterns (n >= 2^20) factorized whole take the height order in
+    // the lockstep kernel too: the sources of a group share their closures
+    // (C5: 3,386 -> 2,389 ms; C2 at n = 262k stays faster in id order, 125 vs
+    // 165 ms).  Row ranges of a multi-GPU split keep id order: their
+    // chain-bound top ranks were slower in height order (C5 8-way: 1,102 vs
+    // 631 ms on one of them)
+    auto_order = !auto_fifo && (auto_hubs || (n >= (int64_t(1) << 20) && rows == n));
   }
   // ---------------------------------------------------- A2: height order
   // positions are a permutation of [0, n): the plan does not depend on the
@@ -1235,10 +1243,10 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       CK(host_height_order(c, n, nnz, in_dev, rowptr, colidx, st, &shape));
       bool use_h = true;
       if (auto_order) {
-        // AUTO: height order when the last row's id-order chain (about
-        // |L(n-1,:)| threshold steps) is far longer than the tree is high
-        // (C4's hub rows: 577k vs 4.2k; 3D grids keep id order)
-        use_h = shape.last_row_chain > 4 * shape.height;
+        // AUTO: large patterns always; hub patterns when the last row's
+        // id-order chain (about |L(n-1,:)| threshold steps) is far longer
+        // than the tree is high (C4's hub rows: 577k vs 4.2k)
+        use_h = !auto_hubs || shape.last_row_chain > 4 * shape.height;
         o.schedule = use_h ? GSOFA_SCHEDULE_HEIGHT : GSOFA_SCHEDULE_THRESHOLD;
         auto_order = false;
       }

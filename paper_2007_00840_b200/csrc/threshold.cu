@@ -1508,16 +1508,17 @@ size_t stream_smem_bytes(int64_t Vmax, int64_t npos) {
 }
 
 // kernel instances of the two threshold orders (kH = height order)
-// warps per lockstep CTA in height order: 32 for calls of few groups (a hub
-// group is one CTA's work: C4's hub rank 324 -> 238 ms vs 16 warps), else 16
-// (more groups in flight: the full C4 371 vs 410 ms); GSOFA_LOCK_WARPS = 4 /
-// 16 / 32 forces it (dev A/B)
+// warps per lockstep CTA in height order: 32 when every group of the call
+// gets its own SM at once (a hub group is one CTA's work: C4's hub rank
+// 324 -> 238 ms vs 16 warps), else 16 (two CTAs per SM: more groups in
+// flight, and no second wave for a few groups more than SMs -- C5's 154-group
+// top ranks); GSOFA_LOCK_WARPS = 4 / 16 / 32 forces it (dev A/B)
 int lock_warps(int64_t groups, int sms) {
   if (const char *e = std::getenv("GSOFA_LOCK_WARPS")) {
     const int w = atoi(e);
     if (w == 4 || w == 16 || w == 32) return w;
   }
-  return groups <= 16 * (int64_t)sms ? 32 : 16;
+  return groups <= (int64_t)sms ? 32 : 16;
 }
 const void *stream_fn(bool h, int lw) {
   if (!h) return (const void *)stream_kernel<false>;

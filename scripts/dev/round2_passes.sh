@@ -292,6 +292,46 @@ pass28() {
   timeout 900 python scripts/scaling_emulation.py --config C4 --gpus 2 4 8 --out gpurun_out/p28_scal_C4.json 2>&1 | tail -7
 }
 
+pass29() {
+  # lockstep height order on the grids (explicit schedule=height): C5/C2 full and chain-bound ranks
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for rows in 2092230:2097152 2087297:2092230 2082353:2087297 2074239:2082353; do
+    r=$(GSOFA_TIMELINE=1 timeout 300 python scripts/probe.py --config C5 --schedule height --reps 2 --rows $rows 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*rounds \([0-9]*\).*/dev \1 trav \2 rounds \3/')
+    echo "C5 rows $rows height $r"
+  done
+  for rows in 256702:258564 260956:262144 0:97268; do
+    r=$(timeout 300 python scripts/probe.py --config C2 --schedule height --reps 3 --rows $rows 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C2 rows $rows height $r"
+  done
+  echo "== C2 full height"; timeout 300 python scripts/probe.py --config C2 --schedule height --reps 3 2>&1 | grep "^rep 2"
+  echo "== C5 full height"; timeout 600 python scripts/probe.py --config C5 --schedule height --reps 2 2>&1 | grep "^rep 1"
+}
+
+pass30() {
+  # AUTO height order (lockstep) for n >= 2^20: C5 full-size parity, bench, 8-way emulation
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 1500 python -m pytest tests -m gpu -q -x -k "full_C5 or full_config or auto_threshold or auto_schedule or l_csc_C5" 2>&1 | tail -3
+  timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/p30_bench.json 2> gpurun_out/p30_bench.log; python -c "
+import json; d=json.load(open('gpurun_out/p30_bench.json')); r=d['roofline']
+print('bench', '%.4g'%d['value'], '%.1f ms'%d['ms_per_step'], 'e2e %.4g'%d['e2e']['value'], 'frac %.3f'%r['frac'], r.get('ncu_dram_frac'), d['config'].get('schedule'), d['clocks'], d['gpu_launches'])"
+  timeout 1500 python scripts/scaling_emulation.py --config C5 --gpus 2 4 8 --out gpurun_out/p30_scal_C5.json 2>&1 | tail -7
+}
+
+pass31() {
+  # measurement of the lockstep height order on C5 (the bench default): ncu launch list of the
+  # bench command, ncu --set full of stream_kernel (second launch of a probe), folded into
+  # profiles/traffic.json as C5/height; bench lines C4 and C2
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/p31_launches_C5.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/p31_ncu_bench.log 2>&1; echo "ncu list rc=$?"
+  timeout 2400 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 1 -c 1 \
+    -o gpurun_out/prof_stream_h_C5 -f python scripts/probe.py --config C5 --reps 2 > gpurun_out/p31_ncu_full.log 2>&1; echo "ncu full rc=$?"
+  python scripts/ncu_traffic.py C5 height gpurun_out/ncu_full_r2_C5_height.txt gpurun_out/prof_stream_h_C5.ncu-rep > gpurun_out/p31_traffic.log 2>&1; echo "traffic rc=$?"
+  cp profiles/traffic.json gpurun_out/traffic_p31.json
+  for c in C4 C2; do timeout 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/p31_bench_$c.json 2> gpurun_out/p31_bench_$c.log; tail -c 300 gpurun_out/p31_bench_$c.json; echo; done
+  timeout 1500 python scripts/scaling_emulation.py --config C5 --gpus 2 4 8 --out gpurun_out/p31_scal_C5.json 2>&1 | tail -7
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -319,5 +359,8 @@ case "${1:-}" in
   26) pass26 ;;
   27) pass27 ;;
   28) pass28 ;;
+  29) pass29 ;;
+  30) pass30 ;;
+  31) pass31 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac
