@@ -1252,7 +1252,8 @@ int gsofa_symbolic(gsofa_context *ctx, int64_t n, const int64_t *rowptr, const i
       }
       if (use_h) {
         lock_h = true;
-        lock_w = gsofa::lock_warps(ceil_div(rows, 32), c->sms);
+        const int64_t mean = std::max<int64_t>(1, nnz / std::max<int64_t>(1, n));
+        lock_w = gsofa::lock_warps(ceil_div(rows, 32), c->sms, (int64_t)maxdeg > 32 * mean);
         CK(cudaMemcpyAsync(c->ord_buf, c->ord_pin, (size_t)n * 6 * 4, cudaMemcpyHostToDevice, st));
       } else {
         ord_npos = 0;

@@ -146,7 +146,7 @@ size_t stream_is_words(int64_t n);
 // lock_h: the lockstep kernel in height order (heavy = 0; its slots then hold npos threshold bits)
 int stream_max_blocks(int device, int64_t Vmax, int heavy, int64_t npos, bool wide, bool lock_h = false,
                       int lw = 16);
-int lock_warps(int64_t groups, int sms);  // warps per lockstep CTA in height order
+int lock_warps(int64_t groups, int sms, bool hubs);  // warps per lockstep CTA in height order
 int stream_heavy_ratio();  // warps of a solo CTA / warps of a lockstep CTA
 int stream_warps_per_cta();  // lockstep slots (one group per warp) per CTA
 size_t solo_ws_words(int64_t Vmax, int64_t n, int64_t npos);  // per solo slot (one warp, one source)

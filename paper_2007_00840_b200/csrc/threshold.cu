@@ -333,7 +333,7 @@ __device__ __forceinline__ void stage_rows(const StreamParams &p, uint32_t *is, 
 // kW warps per CTA: 4 in id order; height order takes 16 by default (one
 // group's step spreads over more warps: a hub group is one CTA's work)
 template <bool kH, int kW = kLightWarps>
-__global__ void __launch_bounds__(kW * 32, kW == 4 ? 8 : (kW == 16 ? 2 : 1)) stream_kernel(StreamParams p) {
+__global__ void __launch_bounds__(kW * 32, 32 / kW) stream_kernel(StreamParams p) {
   constexpr int kWarps = kW;
   constexpr int kThreads = kWarps * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kW * 32, kW == 4 ? 8 : (kW == 16 ? 2 : 1)) str
   extern __shared__ uint32_t s_tsum[];  // [(tbw_max + 31) / 32]
   sl.tsum = s_tsum;
 
-  __shared__ int s_g, s_qn[2], s_scan[3], s_minfill[3];
+  __shared__ int s_g, s_qn[3], s_scan[3], s_minfill[3];
   __shared__ uint32_t s_cnt[kWarps][2][32];
   __shared__ long long s_rowoff[32];
   __shared__ int s_nL[32];
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kW * 32, kW == 4 ? 8 : (kW == 16 ? 2 : 1)) str
       }
       s_g = gg;
       s_abort = 0;
-      s_qn[0] = s_qn[1] = 0;
+      s_qn[0] = s_qn[1] = s_qn[2] = 0;
       for (int i = 0; i < 3; ++i) s_scan[i] = s_minfill[i] = INT_MAX;
     }
     __syncthreads();
@@ -505,21 +505,26 @@ __global__ void __launch_bounds__(kW * 32, kW == 4 ? 8 : (kW == 16 ? 2 : 1)) str
       // closure levels: every item has newMaxId T.  Levels only consume
       // returning atomics (reached, pend pushes); the REDs of this step
       // (fill pend / thr / is) are published before the next step's barrier.
+      // One barrier per level: the item counts rotate over three words --
+      // level l reads count l % 3, pushes into (l + 1) % 3 and clears
+      // (l + 2) % 3, which every thread read at level l - 1 before its
+      // barrier; the lists alternate (a level's barrier orders the reads of
+      // one list before the next level's writes into it).
       for (int lvl = 1;; ++lvl) {
-        const int cur = lvl & 1, nxt = cur ^ 1;
-        const int qn = s_qn[cur];
+        const int cur = lvl & 1;
+        const int qn = s_qn[lvl % 3];
         if (qn == 0) {
           fence_gpu();
+          if (tid == 0) s_qn[0] = s_qn[1] = s_qn[2] = 0;  // (ordered by the next step's barrier)
           break;
         }
         const uint32_t *cq = cur ? sl.list1 : sl.list0;
         uint32_t *nq = cur ? sl.list0 : sl.list1;
-        __syncthreads();
-        if (tid == 0) s_qn[cur] = 0;
+        if (tid == 0) s_qn[(lvl + 2) % 3] = 0;
         c.levels += 1;
         for (int b0 = warp * 32; b0 < qn; b0 += kThreads) {
           const int u = (b0 + lane < qn) ? (int)cq[b0 + lane] : -1;
-          expand<kH>(p, sl, s0g, tmin, u, nq, &s_qn[nxt], &s_minfill[nx3], lane, c, tmax, hh);
+          expand<kH>(p, sl, s0g, tmin, u, nq, &s_qn[(lvl + 1) % 3], &s_minfill[nx3], lane, c, tmax, hh);
         }
         __syncthreads();
       }
@@ -1510,20 +1515,23 @@ size_t stream_smem_bytes(int64_t Vmax, int64_t npos) {
 // kernel instances of the two threshold orders (kH = height order)
 // warps per lockstep CTA in height order: 32 when every group of the call
 // gets its own SM at once (a hub group is one CTA's work: C4's hub rank
-// 324 -> 238 ms vs 16 warps), else 16 (two CTAs per SM: more groups in
-// flight, and no second wave for a few groups more than SMs -- C5's 154-group
-// top ranks); GSOFA_LOCK_WARPS = 4 / 16 / 32 forces it (dev A/B)
-int lock_warps(int64_t groups, int sms) {
+// 324 -> 238 ms vs 16 warps); else 16 for hub patterns (C4 whole: 368 ms vs
+// 556 with 8 warps -- its hub groups are long) and 8 otherwise (more groups
+// in flight: C5 2,260 vs 2,369 ms with 16, 3,816 with 4, 3,687 with 32);
+// GSOFA_LOCK_WARPS = 4 / 8 / 16 / 32 forces it (dev A/B)
+int lock_warps(int64_t groups, int sms, bool hubs) {
   if (const char *e = std::getenv("GSOFA_LOCK_WARPS")) {
     const int w = atoi(e);
-    if (w == 4 || w == 16 || w == 32) return w;
+    if (w == 4 || w == 8 || w == 16 || w == 32) return w;
   }
-  return groups <= (int64_t)sms ? 32 : 16;
+  if (groups <= (int64_t)sms) return 32;
+  return hubs ? 16 : 8;
 }
 const void *stream_fn(bool h, int lw) {
   if (!h) return (const void *)stream_kernel<false>;
   switch (lw) {
     case 4: return (const void *)stream_kernel<true, 4>;
+    case 8: return (const void *)stream_kernel<true, 8>;
     case 32: return (const void *)stream_kernel<true, 32>;
     default: return (const void *)stream_kernel<true, 16>;
   }
@@ -1638,6 +1646,7 @@ cudaError_t launch_stream(const StreamParams &p, int grid, cudaStream_t st) {
   } else {
     switch (p.lwarps) {
       case 4: stream_kernel<true, 4><<<grid, 4 * 32, smem, st>>>(p); break;
+      case 8: stream_kernel<true, 8><<<grid, 8 * 32, smem, st>>>(p); break;
       case 32: stream_kernel<true, 32><<<grid, 32 * 32, smem, st>>>(p); break;
       default: stream_kernel<true, 16><<<grid, 16 * 32, smem, st>>>(p); break;
     }

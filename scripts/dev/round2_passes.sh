@@ -332,6 +332,58 @@ pass31() {
   timeout 1500 python scripts/scaling_emulation.py --config C5 --gpus 2 4 8 --out gpurun_out/p31_scal_C5.json 2>&1 | tail -7
 }
 
+pass32() {
+  # lockstep height order: warps per CTA on the grids (C5 whole: AUTO; C2: schedule=height)
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for lw in 4 16 32; do
+    r=$(GSOFA_LOCK_WARPS=$lw timeout 600 python scripts/probe.py --config C5 --reps 2 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C5 lock_warps=$lw $r"
+    r=$(GSOFA_LOCK_WARPS=$lw timeout 300 python scripts/probe.py --config C2 --schedule height --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C2 height lock_warps=$lw $r"
+  done
+}
+
+pass33() {
+  # one barrier per lockstep level (three rotating item counts): parity and timings
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 1500 python -m pytest tests -m gpu -q -x -k "lockstep_height or height_order_hub or random_graphs or config_shapes or full_config or stream_paths or overflow or budget" 2>&1 | tail -2
+  echo "== C5"; timeout 600 python scripts/probe.py --config C5 --reps 2 2>&1 | grep "^rep 1"
+  echo "== C4"; timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep 2"
+  echo "== C2"; timeout 300 python scripts/probe.py --config C2 --reps 3 2>&1 | grep "^rep 2"
+  echo "== C2 height"; timeout 300 python scripts/probe.py --config C2 --schedule height --reps 3 2>&1 | grep "^rep 2"
+  r=$(timeout 300 python scripts/probe.py --config C4 --reps 3 --rows 1584915:1585478 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "C4 hub rank $r"
+}
+
+pass34() {
+  # lockstep height order, 8 vs 16 warps per CTA on C5 (whole) and C4
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for lw in 8 16; do
+    r=$(GSOFA_LOCK_WARPS=$lw timeout 600 python scripts/probe.py --config C5 --reps 2 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C5 lock_warps=$lw $r"
+    r=$(GSOFA_LOCK_WARPS=$lw timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C4 lock_warps=$lw $r"
+  done
+  GSOFA_LOCK_WARPS=8 timeout 900 python -m pytest tests -m gpu -q -x -k "lockstep_height" 2>&1 | tail -1
+}
+
+pass35() {
+  # final verification: smoke, full suite, bench (C5) + reference arm, ncu launch list, ncu --set full
+  # of the dominant kernel folded into profiles/traffic.json, C4 bench line, C5/C4 emulation
+  python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/p35_smoke.log 2>&1; tail -1 gpurun_out/p35_smoke.log
+  timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/p35_tests.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/p35_tests.log
+  timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/p35_bench.json 2> gpurun_out/p35_bench.log; tail -c 400 gpurun_out/p35_bench.json; echo
+  timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/p35_ref.json 2> gpurun_out/p35_ref.log; tail -c 200 gpurun_out/p35_ref.json; echo
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/p35_launches_C5.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/p35_ncu_bench.log 2>&1; echo "ncu list rc=$?"
+  timeout 2400 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 1 -c 1 \
+    -o gpurun_out/prof_stream_h8_C5 -f python scripts/probe.py --config C5 --reps 2 > gpurun_out/p35_ncu_full.log 2>&1; echo "ncu full rc=$?"
+  python scripts/ncu_traffic.py C5 height gpurun_out/ncu_full_r2_C5_height8.txt gpurun_out/prof_stream_h8_C5.ncu-rep > gpurun_out/p35_traffic.log 2>&1; echo "traffic rc=$?"
+  cp profiles/traffic.json gpurun_out/traffic_p35.json
+  timeout 900 python bench.py --config C4 --steps 5 --warmup 3 > gpurun_out/p35_bench_C4.json 2> gpurun_out/p35_bench_C4.log; tail -c 200 gpurun_out/p35_bench_C4.json; echo
+  timeout 1500 python scripts/scaling_emulation.py --config C5 --gpus 2 4 8 --out gpurun_out/p35_scal_C5.json 2>&1 | tail -7
+  timeout 900 python scripts/scaling_emulation.py --config C4 --gpus 2 4 8 --out gpurun_out/p35_scal_C4.json 2>&1 | tail -7
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -362,5 +414,9 @@ case "${1:-}" in
   29) pass29 ;;
   30) pass30 ;;
   31) pass31 ;;
+  32) pass32 ;;
+  33) pass33 ;;
+  34) pass34 ;;
+  35) pass35 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac
