@@ -384,6 +384,17 @@ pass35() {
   timeout 900 python scripts/scaling_emulation.py --config C4 --gpus 2 4 8 --out gpurun_out/p35_scal_C4.json 2>&1 | tail -7
 }
 
+pass36() {
+  # dev A/B: the heaviest groups on a 16-warp lockstep kernel, the rest on 4-warp CTAs (C5 whole)
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  GSOFA_SPLIT_TOP=5 timeout 900 python -m pytest tests -m gpu -q -x -k "lockstep_height" 2>&1 | tail -1
+  for k in 148 296 592; do
+    r=$(GSOFA_SPLIT_TOP=$k timeout 600 python scripts/probe.py --config C5 --reps 2 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C5 split_top=$k $r"
+  done
+  r=$(timeout 600 python scripts/probe.py --config C5 --reps 2 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "C5 default $r"
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -418,5 +429,6 @@ case "${1:-}" in
   33) pass33 ;;
   34) pass34 ;;
   35) pass35 ;;
+  36) pass36 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac
