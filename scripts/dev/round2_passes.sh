@@ -395,6 +395,17 @@ pass36() {
   r=$(timeout 600 python scripts/probe.py --config C5 --reps 2 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "C5 default $r"
 }
 
+pass37() {
+  # height order (lockstep, 8-warp CTAs / 32 when groups <= SMs) on every rank range of the
+  # C5 2/4/8-way splits, against the id order
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for rows in 0:781266 781266:1045051 1045051:1562531 1562531:2074239 2074239:2082353 2082353:2087297 2087297:2092230 2092230:2097152 \
+              0:1046157 1046157:2076464 2076464:2087915 2087915:2097152 0:2076464 2076464:2097152; do
+    r=$(timeout 600 python scripts/probe.py --config C5 --schedule height --reps 2 --rows $rows 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C5 rows $rows height $r"
+  done
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -430,5 +441,6 @@ case "${1:-}" in
   34) pass34 ;;
   35) pass35 ;;
   36) pass36 ;;
+  37) pass37 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac
