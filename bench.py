@@ -434,8 +434,12 @@ def main():
         if dur > 0:
             roofline["ncu_dram_gbs"] = tot_b / dur / 1e9
             roofline["ncu_dram_frac"] = roofline["ncu_dram_gbs"] / peak
-        roofline["limiter"] = ("latency of dependent L2 atomics (ncu: long-scoreboard stalls "
-                               "dominate, DRAM well below peak; see roofline.ncu)")
+        roofline["limiter"] = (
+            "per-level CTA barriers of the lockstep groups over latency-bound closure levels (ncu: "
+            "barrier stalls dominate, then long scoreboard; DRAM well below peak; see roofline.ncu)"
+            if sched_used == "height" else
+            "latency of dependent L2 atomics (ncu: long-scoreboard stalls dominate, DRAM well below "
+            "peak; see roofline.ncu)")
     # the unit operation of the traversal is a random 4-byte atomic (one per
     # (item, neighbour) pair); its ceiling on this GPU was measured with
     # scripts/atomics_bench.cu (profiles/atomic_peak.json)

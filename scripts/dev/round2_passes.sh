@@ -406,6 +406,19 @@ pass37() {
   done
 }
 
+pass38() {
+  # lockstep height order on C2 / C3 with the final CTA rule (8 warps), and CTA sizes
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for c in C2 C3; do
+    for lw in 8 16; do
+      r=$(GSOFA_LOCK_WARPS=$lw timeout 300 python scripts/probe.py --config $c --schedule height --reps 3 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+      echo "$c height lock_warps=$lw $r"
+    done
+    r=$(timeout 300 python scripts/probe.py --config $c --reps 3 2>&1 | grep "^rep 2" | sed 's/.*\[\([a-z]*\)\].*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/\1 dev \2 trav \3/')
+    echo "$c auto $r"
+  done
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -442,5 +455,6 @@ case "${1:-}" in
   35) pass35 ;;
   36) pass36 ;;
   37) pass37 ;;
+  38) pass38 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac
