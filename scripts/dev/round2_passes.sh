@@ -419,6 +419,17 @@ pass38() {
   done
 }
 
+pass39() {
+  # dev A/B: the heaviest groups on a 16-warp lockstep kernel, the rest on 8-warp CTAs (C5 whole)
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  GSOFA_SPLIT_TOP=5 timeout 900 python -m pytest tests -m gpu -q -x -k "lockstep_height" 2>&1 | tail -1
+  for k in 148 296 512; do
+    r=$(GSOFA_SPLIT_TOP=$k timeout 600 python scripts/probe.py --config C5 --reps 2 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/')
+    echo "C5 split_top=$k (16w top, 8w bulk) $r"
+  done
+  r=$(timeout 600 python scripts/probe.py --config C5 --reps 2 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "C5 default $r"
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -456,5 +467,6 @@ case "${1:-}" in
   36) pass36 ;;
   37) pass37 ;;
   38) pass38 ;;
+  39) pass39 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac
