@@ -430,6 +430,13 @@ pass39() {
   r=$(timeout 600 python scripts/probe.py --config C5 --reps 2 2>&1 | grep "^rep 1" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "C5 default $r"
 }
 
+pass40() {
+  # HEAD check: smoke, full GPU suite, default bench line
+  python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/p40_smoke.log 2>&1; tail -1 gpurun_out/p40_smoke.log
+  timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/p40_tests.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/p40_tests.log
+  timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/p40_bench.json 2> gpurun_out/p40_bench.log; tail -c 300 gpurun_out/p40_bench.json; echo
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -468,5 +475,6 @@ case "${1:-}" in
   37) pass37 ;;
   38) pass38 ;;
   39) pass39 ;;
+  40) pass40 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac
