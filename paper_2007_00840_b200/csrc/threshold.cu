@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(kW * 32, 32 / kW) stream_kernel(StreamParams p
   __shared__ int s_nL[32];
   __shared__ int s_ok, s_abort;
   __shared__ int s_hs[4];  // kH step: segment end, height, tmin, tmax
+  __shared__ int s_nx[3];  // kH: the scanned next threshold, its segment end and height
   Counters c = {0, 0, 0, 0, 0, 0, 0, 0u};
   // live lockstep CTAs: while any runs, it may still abandon a group to the
   // solo kernel's queue (idle solo warps wait only as long as that can happen)
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(kW * 32, 32 / kW) stream_kernel(StreamParams p
       s_g = gg;
       s_abort = 0;
       s_qn[0] = s_qn[1] = s_qn[2] = 0;
+      s_nx[0] = -1;
       for (int i = 0; i < 3; ++i) s_scan[i] = s_minfill[i] = INT_MAX;
     }
     __syncthreads();
@@ -430,6 +432,24 @@ __global__ void __launch_bounds__(kW * 32, 32 / kW) stream_kernel(StreamParams p
       if (T == INT_MAX) break;
       c.steps += 1;
       if (tid == 0) s_abort = p.abort_cycles > 0 && clock64() - t_start > p.abort_cycles;
+      if (kH && tid == 0) {
+        // the step: every threshold of height h = height(T), positions
+        // [T, seg_end(h)); its record was usually prefetched with the scan
+        // that found T (s_nx), else loaded now
+        int lim, h;
+        if (T == s_nx[0]) {
+          lim = s_nx[1];
+          h = s_nx[2];
+        } else {
+          const int4 r = __ldg(p.posrec + T);
+          lim = r.w;
+          h = __ldg(p.hgt + r.x);
+        }
+        s_hs[0] = lim;
+        s_hs[1] = h;
+        s_hs[2] = INT_MAX;
+        s_hs[3] = -1;
+      }
       __syncthreads();  // all threads are done with the previous step's s_qn / T
       if (s_abort) break;
       if (tid == 0) {
@@ -438,17 +458,8 @@ __global__ void __launch_bounds__(kW * 32, 32 / kW) stream_kernel(StreamParams p
       }
       int tmin = T, tmax = 0, hh = 0;
       if (kH) {
-        // the step: every threshold of height h = height(T), positions
-        // [T, seg_end(h)) -- all final (fills are ancestors: greater height);
-        // their vertices become the first level's items (list1)
-        if (tid == 0) {
-          const int4 r = __ldg(p.posrec + T);
-          s_hs[0] = r.w;
-          s_hs[1] = __ldg(p.hgt + r.x);
-          s_hs[2] = INT_MAX;
-          s_hs[3] = -1;
-        }
-        __syncthreads();
+        // the step's thresholds (positions [T, lim), all final: fills are
+        // ancestors, of greater height) become the first level's items (list1)
         const int lim = s_hs[0];
         const int w0 = T >> 5, w1 = (lim - 1) >> 5;
         int tmn = INT_MAX, tmx = -1;
@@ -483,9 +494,19 @@ __global__ void __launch_bounds__(kW * 32, 32 / kW) stream_kernel(StreamParams p
         }
         __syncthreads();
         // the next threshold past the segment (this step's fills: s_minfill[nx3])
-        if (warp == 0) {
+        // and its record, by the last warp (the one a small first level
+        // leaves idle)
+        if (warp == kWarps - 1) {
           const int nt = scan_next(sl.thr, sl.tsum, tbw, lim - 1, lane);
-          if (lane == 0) s_scan[nx3] = nt;
+          if (lane == 0) {
+            s_scan[nx3] = nt;
+            if (nt != INT_MAX) {
+              const int4 r = __ldg(p.posrec + nt);
+              s_nx[1] = r.w;
+              s_nx[2] = __ldg(p.hgt + r.x);
+            }
+            s_nx[0] = nt;
+          }
         }
         tmin = s_hs[2];
         tmax = s_hs[3];

@@ -437,6 +437,18 @@ pass40() {
   timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/p40_bench.json 2> gpurun_out/p40_bench.log; tail -c 300 gpurun_out/p40_bench.json; echo
 }
 
+pass41() {
+  # lockstep height: the next step's record prefetched by the scanning (last) warp, one barrier
+  # less per step: parity and timings
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  timeout 1500 python -m pytest tests -m gpu -q -x -k "lockstep_height or height_order_hub or auto_threshold or full_C5 or random_graphs" 2>&1 | tail -1
+  for i in 1 2; do
+    echo "== C5"; timeout 600 python scripts/probe.py --config C5 --reps 2 2>&1 | grep "^rep 1"
+    echo "== C4"; timeout 300 python scripts/probe.py --config C4 --reps 3 2>&1 | grep "^rep 2"
+  done
+  r=$(timeout 300 python scripts/probe.py --config C4 --reps 3 --rows 1584915:1585478 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "C4 hub rank $r"
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -476,5 +488,6 @@ case "${1:-}" in
   38) pass38 ;;
   39) pass39 ;;
   40) pass40 ;;
+  41) pass41 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac
