@@ -449,6 +449,12 @@ pass41() {
   r=$(timeout 300 python scripts/probe.py --config C4 --reps 3 --rows 1584915:1585478 2>&1 | grep "^rep 2" | sed 's/.*dev \([0-9.]*\) ms  trav \([0-9.]*\).*/dev \1 trav \2/'); echo "C4 hub rank $r"
 }
 
+pass42() {
+  # 8-warp lockstep CTAs at 3 per SM (no register spills) vs 4 per SM: C5 whole
+  python -c "from paper_2007_00840_b200.build import build; build()" > /dev/null 2>&1
+  for i in 1 2; do echo "== C5"; timeout 600 python scripts/probe.py --config C5 --reps 2 2>&1 | grep "^rep 1"; done
+}
+
 case "${1:-}" in
   1) pass1 ;;
   2) pass2 ;;
@@ -489,5 +495,6 @@ case "${1:-}" in
   39) pass39 ;;
   40) pass40 ;;
   41) pass41 ;;
+  42) pass42 ;;
   *) echo "usage: $0 PASS_NUMBER"; exit 2 ;;
 esac
